@@ -1,0 +1,222 @@
+/*
+ * tetray_b200.h -- C ABI of libtetray_b200.so, the B200-native replacement
+ * for the tetray render hot path (arXiv 1908.01906 reference).
+ *
+ * The reference's only FFI on this path is the numba call
+ *   _kernels.render_frame(<49 positional args>)      pkg/src/tetray/_kernels.py:312-322
+ * assembled by render()                              pkg/src/tetray/render.py:183-193
+ * plus the batched point query
+ *   _kernels.field_at_many(pts, <mesh args>)         pkg/src/tetray/_kernels.py:157-170
+ * and the host-side producers of its inputs (mesh.py:246-260, partitions.py:73-128,
+ * traversal.py:82-99, transfer.py:95-167).  This header replaces each of them;
+ * the mapping is given per entry point.  All entry points return 0 on success
+ * and a nonzero TR_E* code on failure, with tr_last_error() describing it; they
+ * never abort.  No torch types appear here: device buffers are plain pointers
+ * (owned by the caller -- in the Python host layer, torch tensors).
+ *
+ * Device data layout:
+ *   TrTetRecord[T]   128 B/tet: inverse edge matrix, origin, 4 field values
+ *   TrPNode[]        64 B BVH2 nodes over padded tet boxes, f32 child boxes
+ *   TrPLeaf[]        32 B leaf headers: exclusive box + id range
+ *   uint32 leaf ids  ascending per leaf (lowest-index-first scan)
+ *   TrBNode[]        112 B BVH2 nodes over partition boxes, f64 child boxes
+ */
+#ifndef TETRAY_B200_H
+#define TETRAY_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TR_OK 0
+#define TR_EINVAL 1   /* bad argument */
+#define TR_ECUDA 2    /* CUDA runtime error */
+#define TR_ENOMEM 3   /* host allocation failure */
+#define TR_ESTATE 4   /* object in the wrong state */
+
+/* ------------------------------------------------------------ layouts */
+
+/* One tetrahedron, 128 B (one L2 line).  inv/orig are the reference's
+ * MeshSampler.tet_inv / tet_orig (mesh.py:251-254) bit for bit; f[i] is
+ * field[tets[t,i]] for vertex-centered data, f[0] = field[t] for cell data. */
+typedef struct TrTetRecord {
+    double inv[9];
+    double orig[3];
+    double f[4];
+} TrTetRecord;
+
+/* Point-location BVH2 node: both child boxes (f32, rounded outward from the
+ * f64 padded tet boxes of mesh.py:248-250), child links and the minimum tet
+ * id below each child.  child >= 0: node index; child < 0: leaf ~child;
+ * child == INT32_MIN: no child. */
+typedef struct TrPNode {
+    float lo0[3], hi0[3], lo1[3], hi1[3];
+    int32_t child[2];
+    uint32_t minid[2];
+} TrPNode;
+
+/* Leaf header.  ex_lo/ex_hi: the leaf's EXCLUSIVE box (rounded inward to
+ * f32): no other leaf's box meets its interior, so a point strictly inside
+ * it can only be contained by this leaf's tets. */
+typedef struct TrPLeaf {
+    float ex_lo[3], ex_hi[3];
+    uint32_t start, count;
+} TrPLeaf;
+
+/* Partition BVH2 node: f64 child boxes (exact unions of partition boxes,
+ * so node pruning is conservative for the exact f64 slab test).
+ * child >= 0: node; child < 0: partition ~child; INT32_MIN: none. */
+typedef struct TrBNode {
+    double box[2][6]; /* per child: lo x,y,z then hi x,y,z (48 B, 16-B aligned) */
+    int32_t child[2];
+    int32_t pad[2];
+} TrBNode;
+
+/* ------------------------------------------------- host-side builders */
+/* Opaque host object holding variable-size build results. */
+typedef struct TrHostBuf TrHostBuf;
+
+/* KD partitions, replacing partitions.build_partitions (partitions.py:73-128)
+ * with the reference's exact split/median/straddle/leaf semantics.
+ * Result arrays via tr_kd_* getters below. */
+int tr_kd_build(int64_t n_vertices, const double *vertices, int64_t n_tets, const int64_t *tets,
+                const double *field, int32_t centering, const double *mesh_lo,
+                const double *mesh_hi, int64_t max_leaf_elements, int64_t max_depth,
+                TrHostBuf **out);
+/* sizes: [0] = n_parts, [1] = total element ids */
+int tr_kd_sizes(const TrHostBuf *kd, int64_t *sizes2);
+/* offsets[n_parts+1], ids[total], leaf_lo/hi[n_parts*3] (KD leaf boxes),
+ * lo/hi[n_parts*3] (refined bounds, partitions.py:61-70), vrange[n_parts*2] */
+int tr_kd_copy(const TrHostBuf *kd, int64_t *offsets, int64_t *ids, double *leaf_lo,
+               double *leaf_hi, double *lo, double *hi, double *vrange);
+
+/* Point-location BVH over padded tet boxes (replaces MeshSampler's BVH,
+ * mesh.py:248-250 / bvh.py:41-98; any conservative structure gives the
+ * reference's lowest-index result). */
+int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, int32_t leaf_max,
+                  TrHostBuf **out);
+/* sizes: [0] = nodes, [1] = leaves, [2] = leaf ids */
+int tr_pbvh_sizes(const TrHostBuf *b, int64_t *sizes3);
+int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids);
+
+/* Partition BVH (replaces traversal.build_partition_bvh, traversal.py:82-91). */
+int tr_bbvh_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out);
+int tr_bbvh_sizes(const TrHostBuf *b, int64_t *n_nodes);
+int tr_bbvh_copy(const TrHostBuf *b, TrBNode *nodes);
+/* Per-epoch subtree activity: out[node] bit c = child c reaches an active partition. */
+int tr_bbvh_activity(const TrHostBuf *b, const uint8_t *active, uint8_t *out);
+/* Same from a node array (no host object needed). */
+int tr_bnodes_activity(int64_t n_nodes, const TrBNode *nodes, const uint8_t *active,
+                       uint8_t *out);
+
+void tr_host_free(TrHostBuf *b);
+
+/* Pack tet records (host, OpenMP). inv/orig exactly as MeshSampler computes them. */
+int tr_pack_tets(int64_t n_tets, const int64_t *tets, const double *tet_orig,
+                 const double *tet_inv, const double *field, int32_t centering,
+                 TrTetRecord *out);
+
+/* Transfer-function partition metadata (transfer.py:95-141): per partition
+ * max opacity, raw variance (numpy reduction order reproduced), normalized
+ * sigma, active flag. */
+int tr_tf_meta(int64_t n_parts, const double *vrange, const double *tf_table, int64_t n_tf,
+               double tf_lo, double tf_hi, double *max_opacity, double *raw_variance,
+               double *sigma, uint8_t *active);
+
+/* step_size (K:20-22) per partition on the host with glibc pow, so adaptive
+ * steps are bit-identical to the reference's. */
+int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out);
+double tr_step_size(double s1, double s2, double p, double sigma);
+double tr_opacity_correction(double alpha, double s, double s1);
+
+/* ------------------------------------------------- device entry points */
+
+/* Device-resident scene (device pointers, owned by the caller). */
+typedef struct TrDeviceScene {
+    const TrTetRecord *tets;
+    const TrPNode *pnodes;
+    const TrPLeaf *pleaves;
+    const uint32_t *pleaf_ids;
+    int64_t n_tets, n_pnodes, n_pleaves;
+    int32_t centering;
+    int32_t pad0;
+    const TrBNode *bnodes;
+    const double *part_lo; /* (P,3) refined partition bounds */
+    const double *part_hi;
+    int64_t n_parts, n_bnodes;
+    double mesh_lo[3], mesh_hi[3];
+} TrDeviceScene;
+
+/* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
+typedef struct TrEpoch {
+    const uint8_t *active;       /* (P,) */
+    const uint8_t *bnode_active; /* (n_bnodes,) from tr_bbvh_activity */
+    const double *step;          /* (P,) host step_size; only read in mode 2 */
+    const double *tf_table;      /* (n_tf, 4) */
+    int64_t n_tf;
+    double tf_lo, tf_hi;
+} TrEpoch;
+
+/* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
+typedef struct TrFrame {
+    double cam_pos[3], cam_right[3], cam_up[3], cam_fwd[3];
+    double tan_half, aspect;
+    int64_t width, height;
+    int32_t jitter, mode; /* mode: 0 reference, 1 skip, 2 skip-adaptive (R:27) */
+    double s1, term, eps;
+    double bg[4];
+    int32_t track_ppart;
+    int32_t shard_rank, shard_count; /* pixel tiles t with t % count == rank */
+    int32_t compact;                 /* 1: write tile-major compact slots (multi-GPU) */
+    int32_t flags;                   /* TR_FLAG_* */
+    int32_t pad0;
+} TrFrame;
+
+#define TR_FLAG_NO_LEAF_HINT 1 /* disable the exclusive-leaf shortcut (testing) */
+
+/* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)
+ * i64, visited (H,W) i32.  Compact layout: slot-major 8x4 pixel tiles.
+ * ppart (P,) u64 and totals[2] = {sum samples, sum visited} are ACCUMULATED
+ * (zero them first); work[1] is scratch, zeroed by the call. */
+typedef struct TrOutputs {
+    double *rgba;
+    int64_t *samples;
+    int32_t *visited;
+    uint64_t *ppart;
+    uint64_t *totals;
+    uint32_t *work;
+} TrOutputs;
+
+/* Replaces _kernels.render_frame (K:312-398). stream: cudaStream_t. */
+int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                    const TrOutputs *out, void *stream);
+
+/* Replaces _kernels.field_at_many (K:157-170): pts (n,3) f64 device;
+ * found (n,) u8, vals (n,) f64, tet (n,) i64 (may be NULL) device. */
+int tr_field_at_many(const TrDeviceScene *scene, int64_t n, const double *pts, uint8_t *found,
+                     double *vals, int64_t *tet, void *stream);
+
+/* Multi-GPU merge: scatter gathered compact tiles (count ranks, slot-major)
+ * into the image layout. */
+int tr_scatter_tiles(int64_t width, int64_t height, int32_t shard_count,
+                     const double *src_rgba, const int64_t *src_samples,
+                     const int32_t *src_visited, int64_t slots_per_rank, double *rgba,
+                     int64_t *samples, int32_t *visited, void *stream);
+
+/* Number of tiles (8x4 pixels) of a frame and slots per rank. */
+int64_t tr_num_tiles(int64_t width, int64_t height);
+int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t shard_count);
+
+/* Launch statistics of the last tr_render_frame on this thread:
+ * [0] kernels launched, [1] grid blocks, [2] threads per block. */
+int tr_last_launch(int64_t *out3);
+
+const char *tr_last_error(void);
+int tr_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,703 @@
+// host_build.cpp -- native host-side producers of the device-resident scene.
+//
+// These replace the reference's Python scene-build steps whose outputs feed
+// the hot path:
+//   * KD partitions            partitions.py:73-128  (exact semantics, ids in DFS order)
+//   * point-location BVH       mesh.py:246-250, bvh.py:41-98 (own design: BVH2,
+//                              cube-preserving splits, exclusive leaf boxes)
+//   * partition BVH            traversal.py:82-91 (own design: BVH2, f64 boxes)
+//   * TF partition metadata    transfer.py:95-141 (numpy reduction order reproduced)
+//   * adaptive step sizes      _kernels.py:20-22 (glibc pow, bit-identical)
+//   * tet record packing       mesh.py:251-254 arrays -> 128 B records
+#include <algorithm>
+#include <array>
+#include <cfloat>
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "tetray_b200.h"
+#include "tr_internal.h"
+
+struct TrHostBuf {
+    virtual ~TrHostBuf() {}
+};
+
+namespace {
+
+// ------------------------------------------------------------ float rounding
+inline float f32_down(double x) {
+    float f = (float)x;
+    if ((double)f > x) f = std::nextafter(f, -INFINITY);
+    return f;
+}
+inline float f32_up(double x) {
+    float f = (float)x;
+    if ((double)f < x) f = std::nextafter(f, INFINITY);
+    return f;
+}
+
+// ============================================================ KD partitions
+struct KdBuf : TrHostBuf {
+    std::vector<int64_t> offsets{0};
+    std::vector<int64_t> ids;
+    std::vector<double> leaf_lo, leaf_hi, lo, hi, vrange;
+};
+
+struct KdCtx {
+    const double *V;
+    const int64_t *tets;
+    int64_t max_leaf, max_depth;
+    std::vector<double> blo, bhi, cen;  // (T,3) tet boxes and centroids
+    std::vector<double> emin, emax;     // per-element value range
+    KdBuf *out;
+};
+
+// np.median of vals (partitions.py:105): odd n -> middle, even n -> (a+b)/2.
+double np_median(std::vector<double> &v) {
+    size_t n = v.size(), k = n / 2;
+    std::nth_element(v.begin(), v.begin() + k, v.end());
+    double b = v[k];
+    if (n % 2 == 1) return b;
+    double a = *std::max_element(v.begin(), v.begin() + k);
+    return (a + b) / 2.0;
+}
+
+void kd_emit(KdCtx &C, std::vector<int64_t> &ids, const double *nlo, const double *nhi) {
+    // partitions.py:88-97: sorted ids, value range, bounds refined to the
+    // box of the contained elements' vertices intersected with the leaf box.
+    std::sort(ids.begin(), ids.end());
+    KdBuf &O = *C.out;
+    double vmin = INFINITY, vmax = -INFINITY;
+    double plo[3] = {INFINITY, INFINITY, INFINITY}, phi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t t : ids) {
+        vmin = std::min(vmin, C.emin[t]);
+        vmax = std::max(vmax, C.emax[t]);
+        for (int a = 0; a < 3; ++a) {
+            plo[a] = std::min(plo[a], C.blo[3 * t + a]);
+            phi[a] = std::max(phi[a], C.bhi[3 * t + a]);
+        }
+    }
+    for (int a = 0; a < 3; ++a) {
+        O.leaf_lo.push_back(nlo[a]);
+        O.leaf_hi.push_back(nhi[a]);
+        O.lo.push_back(std::max(plo[a], nlo[a]));
+        O.hi.push_back(std::min(phi[a], nhi[a]));
+    }
+    O.vrange.push_back(vmin);
+    O.vrange.push_back(vmax);
+    O.ids.insert(O.ids.end(), ids.begin(), ids.end());
+    O.offsets.push_back((int64_t)O.ids.size());
+}
+
+void kd_split(KdCtx &C, std::vector<int64_t> ids, const double *nlo, const double *nhi,
+              int64_t depth) {
+    const int64_t n = (int64_t)ids.size();
+    if (n <= C.max_leaf || depth >= C.max_depth) {
+        kd_emit(C, ids, nlo, nhi);
+        return;
+    }
+    // np.argmax: first longest node axis
+    int axis = 0;
+    double ext = nhi[0] - nlo[0];
+    for (int a = 1; a < 3; ++a)
+        if (nhi[a] - nlo[a] > ext) { ext = nhi[a] - nlo[a]; axis = a; }
+    std::vector<double> vals(n);
+    for (int64_t i = 0; i < n; ++i) vals[i] = C.cen[3 * ids[i] + axis];
+    const double m = np_median(vals);
+    std::vector<int64_t> left, right, flat;
+    left.reserve(n / 2 + 16);
+    right.reserve(n / 2 + 16);
+    for (int64_t t : ids) {
+        bool l = C.blo[3 * t + axis] < m, r = C.bhi[3 * t + axis] > m;
+        if (l) left.push_back(t);
+        if (r) right.push_back(t);
+        if (!l && !r) flat.push_back(t);  // flat on the plane -> right (closed) side
+    }
+    if (!flat.empty()) {
+        std::vector<int64_t> merged(right.size() + flat.size());
+        std::merge(right.begin(), right.end(), flat.begin(), flat.end(), merged.begin());
+        right.swap(merged);
+    }
+    if (((int64_t)left.size() == n && (int64_t)right.size() == n) || left.empty() ||
+        right.empty()) {
+        kd_emit(C, ids, nlo, nhi);
+        return;
+    }
+    std::vector<int64_t>().swap(ids);
+    double lhi[3] = {nhi[0], nhi[1], nhi[2]}, rlo[3] = {nlo[0], nlo[1], nlo[2]};
+    lhi[axis] = m;
+    rlo[axis] = m;
+    kd_split(C, std::move(left), nlo, lhi, depth + 1);
+    kd_split(C, std::move(right), rlo, nhi, depth + 1);
+}
+
+// ====================================================== point-location BVH
+struct PBuf : TrHostBuf {
+    std::vector<TrPNode> nodes;
+    std::vector<TrPLeaf> leaves;
+    std::vector<uint32_t> ids;
+    std::vector<std::array<double, 6>> leaf_box;  // exact f64 union boxes
+};
+
+constexpr int32_t CHILD_NONE = INT32_MIN;
+
+struct PRef {
+    int32_t child;
+    uint32_t minid;
+    double lo[3], hi[3];
+};
+
+struct PCtx {
+    const double *lo, *hi;
+    std::vector<double> key;  // box centres
+    std::vector<uint32_t> idx;
+    int leaf_max;
+    PBuf *out;
+};
+
+PRef p_make_leaf(PCtx &C, int64_t b, int64_t e) {
+    PBuf &O = *C.out;
+    std::sort(C.idx.begin() + b, C.idx.begin() + e);
+    TrPLeaf L;
+    L.start = (uint32_t)O.ids.size();
+    L.count = (uint32_t)(e - b);
+    PRef r;
+    for (int a = 0; a < 3; ++a) { r.lo[a] = INFINITY; r.hi[a] = -INFINITY; }
+    for (int64_t k = b; k < e; ++k) {
+        uint32_t t = C.idx[k];
+        O.ids.push_back(t);
+        for (int a = 0; a < 3; ++a) {
+            r.lo[a] = std::min(r.lo[a], C.lo[3 * (size_t)t + a]);
+            r.hi[a] = std::max(r.hi[a], C.hi[3 * (size_t)t + a]);
+        }
+    }
+    for (int a = 0; a < 3; ++a) { L.ex_lo[a] = 1.0f; L.ex_hi[a] = 0.0f; }  // filled later
+    O.leaves.push_back(L);
+    O.leaf_box.push_back({r.lo[0], r.lo[1], r.lo[2], r.hi[0], r.hi[1], r.hi[2]});
+    r.child = ~(int32_t)(O.leaves.size() - 1);
+    r.minid = C.idx[b];
+    return r;
+}
+
+void p_set_child(TrPNode &N, int c, const PRef &r) {
+    float *lo = c == 0 ? N.lo0 : N.lo1, *hi = c == 0 ? N.hi0 : N.hi1;
+    for (int a = 0; a < 3; ++a) { lo[a] = f32_down(r.lo[a]); hi[a] = f32_up(r.hi[a]); }
+    N.child[c] = r.child;
+    N.minid[c] = r.minid;
+}
+
+PRef p_build(PCtx &C, int64_t b, int64_t e) {
+    const int64_t n = e - b;
+    if (n <= C.leaf_max) return p_make_leaf(C, b, e);
+    double klo[3] = {INFINITY, INFINITY, INFINITY}, khi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = b; k < e; ++k)
+        for (int a = 0; a < 3; ++a) {
+            double v = C.key[3 * (size_t)C.idx[k] + a];
+            klo[a] = std::min(klo[a], v);
+            khi[a] = std::max(khi[a], v);
+        }
+    int order[3] = {0, 1, 2};
+    std::sort(order, order + 3, [&](int x, int y) { return khi[x] - klo[x] > khi[y] - klo[y]; });
+    int64_t split = -1;
+    for (int oi = 0; oi < 3 && split < 0; ++oi) {
+        int a = order[oi];
+        if (!(khi[a] > klo[a])) continue;
+        auto key = [&](uint32_t t) { return C.key[3 * (size_t)t + a]; };
+        int64_t mid = b + n / 2;
+        std::nth_element(C.idx.begin() + b, C.idx.begin() + mid, C.idx.begin() + e,
+                         [&](uint32_t x, uint32_t y) { return key(x) < key(y) || (key(x) == key(y) && x < y); });
+        double v = key(C.idx[mid]);
+        // three-way partition so boxes with equal centres (e.g. the 5 tets of
+        // one cube) never straddle a split
+        auto p1 = std::partition(C.idx.begin() + b, C.idx.begin() + e, [&](uint32_t t) { return key(t) < v; });
+        auto p2 = std::partition(p1, C.idx.begin() + e, [&](uint32_t t) { return key(t) == v; });
+        int64_t s1 = p1 - C.idx.begin(), s2 = p2 - C.idx.begin();
+        int64_t best = -1;
+        for (int64_t s : {s1, s2})
+            if (s > b && s < e && (best < 0 || std::llabs(s - mid) < std::llabs(best - mid))) best = s;
+        split = best;
+    }
+    if (split < 0) {
+        if (n <= 64) return p_make_leaf(C, b, e);
+        split = b + n / 2;  // identical centres everywhere: force a split
+    }
+    const size_t ni = C.out->nodes.size();
+    C.out->nodes.push_back(TrPNode{});
+    PRef l = p_build(C, b, split);
+    PRef r = p_build(C, split, e);
+    TrPNode &N = C.out->nodes[ni];
+    p_set_child(N, 0, l);
+    p_set_child(N, 1, r);
+    PRef me;
+    me.child = (int32_t)ni;
+    me.minid = std::min(l.minid, r.minid);
+    for (int a = 0; a < 3; ++a) { me.lo[a] = std::min(l.lo[a], r.lo[a]); me.hi[a] = std::max(l.hi[a], r.hi[a]); }
+    return me;
+}
+
+inline bool boxes_meet(const double *a, const double *b) {  // closed boxes [lo(3), hi(3)]
+    for (int k = 0; k < 3; ++k)
+        if (a[k] > b[3 + k] || b[k] > a[3 + k]) return false;
+    return true;
+}
+
+// Exclusive box of every leaf: its box minus (greedy axis cuts) every other
+// leaf box that meets it.  Rounded inward to f32 and tested with strict
+// inequalities, a point inside it lies in no other leaf's box.
+void p_exclusive_boxes(PBuf &O) {
+    const int64_t nl = (int64_t)O.leaves.size();
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t L = 0; L < nl; ++L) {
+        const double *B = O.leaf_box[L].data();
+        double E[6];
+        std::memcpy(E, B, sizeof E);
+        int32_t stack[128];
+        int sp = 0;
+        stack[sp++] = 0;
+        while (sp > 0) {
+            const TrPNode &N = O.nodes[stack[--sp]];
+            for (int c = 0; c < 2; ++c) {
+                int32_t ch = N.child[c];
+                if (ch == CHILD_NONE) continue;
+                const float *lo = c == 0 ? N.lo0 : N.lo1, *hi = c == 0 ? N.hi0 : N.hi1;
+                double cb[6] = {lo[0], lo[1], lo[2], hi[0], hi[1], hi[2]};
+                if (!boxes_meet(cb, B)) continue;
+                if (ch >= 0) { stack[sp++] = ch; continue; }
+                int64_t M = ~ch;
+                if (M == L) continue;
+                const double *Mb = O.leaf_box[M].data();
+                if (!boxes_meet(Mb, E)) continue;
+                // candidate cuts: keep the part of E below Mb.lo[a] or above Mb.hi[a]
+                double best_vol = -1.0, cut_val = 0.0;
+                int cut_axis = -1, cut_side = 0;
+                for (int a = 0; a < 3; ++a) {
+                    for (int side = 0; side < 2; ++side) {
+                        double nlo = E[a], nhi = E[3 + a];
+                        if (side == 0) { if (!(Mb[a] > E[a])) continue; nhi = Mb[a]; }
+                        else { if (!(Mb[3 + a] < E[3 + a])) continue; nlo = Mb[3 + a]; }
+                        double vol = 1.0;
+                        for (int q = 0; q < 3; ++q) {
+                            double lo_q = q == a ? nlo : E[q], hi_q = q == a ? nhi : E[3 + q];
+                            vol *= std::max(0.0, hi_q - lo_q);
+                        }
+                        if (vol > best_vol) { best_vol = vol; cut_axis = a; cut_side = side; cut_val = side == 0 ? nhi : nlo; }
+                    }
+                }
+                if (cut_axis < 0) {  // Mb covers E: nothing exclusive is left
+                    E[0] = 1.0; E[3] = 0.0;
+                    sp = 0;
+                    break;
+                }
+                if (cut_side == 0) E[3 + cut_axis] = cut_val; else E[cut_axis] = cut_val;
+            }
+        }
+        TrPLeaf &LF = O.leaves[L];
+        for (int a = 0; a < 3; ++a) {
+            LF.ex_lo[a] = f32_up(E[a]);
+            LF.ex_hi[a] = f32_down(E[3 + a]);
+        }
+        if (!(E[0] <= E[3])) { LF.ex_lo[0] = 1.0f; LF.ex_hi[0] = 0.0f; }
+    }
+}
+
+// ============================================================ partition BVH
+struct BBuf : TrHostBuf {
+    std::vector<TrBNode> nodes;
+};
+
+struct BRef {
+    int32_t child;
+    double lo[3], hi[3];
+};
+
+BRef b_build(BBuf &O, const double *lo, const double *hi, std::vector<int32_t> &idx, int64_t b,
+             int64_t e) {
+    if (e - b == 1) {
+        BRef r;
+        r.child = ~idx[b];
+        for (int a = 0; a < 3; ++a) { r.lo[a] = lo[3 * idx[b] + a]; r.hi[a] = hi[3 * idx[b] + a]; }
+        return r;
+    }
+    double clo[3] = {INFINITY, INFINITY, INFINITY}, chi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int64_t k = b; k < e; ++k)
+        for (int a = 0; a < 3; ++a) {
+            double c = 0.5 * (lo[3 * idx[k] + a] + hi[3 * idx[k] + a]);
+            clo[a] = std::min(clo[a], c);
+            chi[a] = std::max(chi[a], c);
+        }
+    int axis = 0;
+    for (int a = 1; a < 3; ++a)
+        if (chi[a] - clo[a] > chi[axis] - clo[axis]) axis = a;
+    int64_t mid = b + (e - b) / 2;
+    std::nth_element(idx.begin() + b, idx.begin() + mid, idx.begin() + e, [&](int32_t x, int32_t y) {
+        double cx = lo[3 * x + axis] + hi[3 * x + axis], cy = lo[3 * y + axis] + hi[3 * y + axis];
+        return cx < cy || (cx == cy && x < y);
+    });
+    size_t ni = O.nodes.size();
+    O.nodes.push_back(TrBNode{});
+    BRef l = b_build(O, lo, hi, idx, b, mid);
+    BRef r = b_build(O, lo, hi, idx, mid, e);
+    TrBNode &N = O.nodes[ni];
+    const BRef *cs[2] = {&l, &r};
+    BRef me;
+    me.child = (int32_t)ni;
+    for (int a = 0; a < 3; ++a) { me.lo[a] = INFINITY; me.hi[a] = -INFINITY; }
+    for (int c = 0; c < 2; ++c) {
+        N.child[c] = cs[c]->child;
+        for (int a = 0; a < 3; ++a) {
+            N.box[c][a] = cs[c]->lo[a];
+            N.box[c][3 + a] = cs[c]->hi[a];
+            me.lo[a] = std::min(me.lo[a], cs[c]->lo[a]);
+            me.hi[a] = std::max(me.hi[a], cs[c]->hi[a]);
+        }
+    }
+    return me;
+}
+
+// ============================================================ TF metadata
+// numpy's pairwise summation of a contiguous float64 vector (add.reduce).
+double np_pairwise_sum(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise_sum(a, n2) + np_pairwise_sum(a + n2, n - n2);
+}
+
+void tf_lookup(const double *T, int64_t n, double lo, double hi, double v, double *rgba) {
+    tr_tf_sample_host(T, n, lo, hi, v, rgba);
+}
+
+}  // namespace
+
+// Shared with the device code's host-side checks: K:74-90 on the host.
+void tr_tf_sample_host(const double *T, int64_t n, double lo, double hi, double v, double *rgba) {
+    double u = (v - lo) / (hi - lo) * (double)(n - 1);
+    if (u <= 0.0) { std::memcpy(rgba, T, 32); return; }
+    if (u >= (double)(n - 1)) { std::memcpy(rgba, T + 4 * (n - 1), 32); return; }
+    int64_t j = (int64_t)std::floor(u);
+    double f = u - (double)j;
+    for (int c = 0; c < 4; ++c) rgba[c] = T[4 * j + c] + f * (T[4 * (j + 1) + c] - T[4 * j + c]);
+}
+
+extern "C" {
+
+int tr_kd_build(int64_t n_vertices, const double *vertices, int64_t n_tets, const int64_t *tets,
+                const double *field, int32_t centering, const double *mesh_lo,
+                const double *mesh_hi, int64_t max_leaf_elements, int64_t max_depth,
+                TrHostBuf **out) {
+    if (!out || !vertices || !tets || !field || n_tets <= 0 || max_leaf_elements < 1 ||
+        max_depth < 1)
+        return tr_fail(TR_EINVAL, "tr_kd_build: invalid arguments");
+    try {
+        KdBuf *K = new KdBuf();
+        KdCtx C;
+        C.V = vertices;
+        C.tets = tets;
+        C.max_leaf = max_leaf_elements;
+        C.max_depth = max_depth;
+        C.out = K;
+        C.blo.resize(3 * n_tets);
+        C.bhi.resize(3 * n_tets);
+        C.cen.resize(3 * n_tets);
+        C.emin.resize(n_tets);
+        C.emax.resize(n_tets);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < n_tets; ++t) {
+            const int64_t *tv = tets + 4 * t;
+            for (int a = 0; a < 3; ++a) {
+                double v0 = vertices[3 * tv[0] + a], v1 = vertices[3 * tv[1] + a];
+                double v2 = vertices[3 * tv[2] + a], v3 = vertices[3 * tv[3] + a];
+                C.blo[3 * t + a] = std::min(std::min(v0, v1), std::min(v2, v3));
+                C.bhi[3 * t + a] = std::max(std::max(v0, v1), std::max(v2, v3));
+                C.cen[3 * t + a] = (((v0 + v1) + v2) + v3) / 4.0;  // mesh.vertices[tets].mean(axis=1)
+            }
+            if (centering == 0) {
+                double f0 = field[tv[0]], f1 = field[tv[1]], f2 = field[tv[2]], f3 = field[tv[3]];
+                C.emin[t] = std::min(std::min(f0, f1), std::min(f2, f3));
+                C.emax[t] = std::max(std::max(f0, f1), std::max(f2, f3));
+            } else {
+                C.emin[t] = C.emax[t] = field[t];
+            }
+        }
+        std::vector<int64_t> all(n_tets);
+        for (int64_t t = 0; t < n_tets; ++t) all[t] = t;
+        kd_split(C, std::move(all), mesh_lo, mesh_hi, 0);
+        *out = K;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_kd_build: out of host memory");
+    }
+}
+
+int tr_kd_sizes(const TrHostBuf *b, int64_t *sizes2) {
+    auto K = dynamic_cast<const KdBuf *>(b);
+    if (!K || !sizes2) return tr_fail(TR_EINVAL, "tr_kd_sizes: not a KD result");
+    sizes2[0] = (int64_t)K->offsets.size() - 1;
+    sizes2[1] = (int64_t)K->ids.size();
+    return TR_OK;
+}
+
+int tr_kd_copy(const TrHostBuf *b, int64_t *offsets, int64_t *ids, double *leaf_lo,
+               double *leaf_hi, double *lo, double *hi, double *vrange) {
+    auto K = dynamic_cast<const KdBuf *>(b);
+    if (!K) return tr_fail(TR_EINVAL, "tr_kd_copy: not a KD result");
+    auto cp = [](void *dst, const auto &v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    cp(offsets, K->offsets);
+    cp(ids, K->ids);
+    cp(leaf_lo, K->leaf_lo);
+    cp(leaf_hi, K->leaf_hi);
+    cp(lo, K->lo);
+    cp(hi, K->hi);
+    cp(vrange, K->vrange);
+    return TR_OK;
+}
+
+int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, int32_t leaf_max,
+                  TrHostBuf **out) {
+    if (!out || n_tets <= 0 || n_tets >= (int64_t)INT32_MAX || leaf_max < 1 || leaf_max > 64)
+        return tr_fail(TR_EINVAL, "tr_pbvh_build: invalid arguments");
+    try {
+        PBuf *O = new PBuf();
+        PCtx C;
+        C.lo = box_lo;
+        C.hi = box_hi;
+        C.leaf_max = leaf_max;
+        C.out = O;
+        C.key.resize(3 * (size_t)n_tets);
+        C.idx.resize(n_tets);
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < n_tets; ++t) {
+            C.idx[t] = (uint32_t)t;
+            for (int a = 0; a < 3; ++a) C.key[3 * t + a] = 0.5 * (box_lo[3 * t + a] + box_hi[3 * t + a]);
+        }
+        O->nodes.reserve(2 * (size_t)n_tets / 4 + 4);
+        PRef root = p_build(C, 0, n_tets);  // an internal root lands at index 0
+        if (root.child < 0) {  // whole mesh is one leaf: root node with one child
+            TrPNode N{};
+            p_set_child(N, 0, root);
+            for (int a = 0; a < 3; ++a) { N.lo1[a] = 1.0f; N.hi1[a] = 0.0f; }
+            N.child[1] = CHILD_NONE;
+            N.minid[1] = UINT32_MAX;
+            O->nodes.push_back(N);
+        }
+        p_exclusive_boxes(*O);
+        *out = O;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_pbvh_build: out of host memory");
+    }
+}
+
+int tr_pbvh_sizes(const TrHostBuf *b, int64_t *s) {
+    auto P = dynamic_cast<const PBuf *>(b);
+    if (!P || !s) return tr_fail(TR_EINVAL, "tr_pbvh_sizes: not a point BVH");
+    s[0] = (int64_t)P->nodes.size();
+    s[1] = (int64_t)P->leaves.size();
+    s[2] = (int64_t)P->ids.size();
+    return TR_OK;
+}
+
+int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids) {
+    auto P = dynamic_cast<const PBuf *>(b);
+    if (!P) return tr_fail(TR_EINVAL, "tr_pbvh_copy: not a point BVH");
+    if (nodes) std::memcpy(nodes, P->nodes.data(), P->nodes.size() * sizeof(TrPNode));
+    if (leaves) std::memcpy(leaves, P->leaves.data(), P->leaves.size() * sizeof(TrPLeaf));
+    if (ids) std::memcpy(ids, P->ids.data(), P->ids.size() * sizeof(uint32_t));
+    return TR_OK;
+}
+
+int tr_bbvh_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out) {
+    if (!out || n_parts <= 0 || n_parts >= (int64_t)INT32_MAX)
+        return tr_fail(TR_EINVAL, "tr_bbvh_build: invalid arguments");
+    try {
+        BBuf *O = new BBuf();
+        std::vector<int32_t> idx(n_parts);
+        for (int64_t i = 0; i < n_parts; ++i) idx[i] = (int32_t)i;
+        if (n_parts == 1) {
+            TrBNode N{};
+            N.child[0] = ~0;
+            N.child[1] = CHILD_NONE;
+            for (int a = 0; a < 3; ++a) {
+                N.box[0][a] = lo[a]; N.box[0][3 + a] = hi[a];
+                N.box[1][a] = 1.0; N.box[1][3 + a] = 0.0;
+            }
+            O->nodes.push_back(N);
+        } else {
+            b_build(*O, lo, hi, idx, 0, n_parts);
+        }
+        *out = O;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_bbvh_build: out of host memory");
+    }
+}
+
+int tr_bbvh_sizes(const TrHostBuf *b, int64_t *n) {
+    auto B = dynamic_cast<const BBuf *>(b);
+    if (!B || !n) return tr_fail(TR_EINVAL, "tr_bbvh_sizes: not a partition BVH");
+    *n = (int64_t)B->nodes.size();
+    return TR_OK;
+}
+
+int tr_bbvh_copy(const TrHostBuf *b, TrBNode *nodes) {
+    auto B = dynamic_cast<const BBuf *>(b);
+    if (!B || !nodes) return tr_fail(TR_EINVAL, "tr_bbvh_copy: not a partition BVH");
+    std::memcpy(nodes, B->nodes.data(), B->nodes.size() * sizeof(TrBNode));
+    return TR_OK;
+}
+
+int tr_bnodes_activity(int64_t n_nodes, const TrBNode *nodes, const uint8_t *active,
+                       uint8_t *out) {
+    if (!nodes || !active || !out || n_nodes <= 0)
+        return tr_fail(TR_EINVAL, "tr_bnodes_activity: invalid arguments");
+    // children always have larger indices than their parent (pre-order build)
+    for (int64_t i = n_nodes - 1; i >= 0; --i) {
+        uint8_t bits = 0;
+        for (int c = 0; c < 2; ++c) {
+            int32_t ch = nodes[i].child[c];
+            bool any = false;
+            if (ch == CHILD_NONE) any = false;
+            else if (ch < 0) any = active[~ch] != 0;
+            else any = out[ch] != 0;
+            if (any) bits |= (uint8_t)(1u << c);
+        }
+        out[i] = bits;
+    }
+    return TR_OK;
+}
+
+int tr_bbvh_activity(const TrHostBuf *b, const uint8_t *active, uint8_t *out) {
+    auto B = dynamic_cast<const BBuf *>(b);
+    if (!B) return tr_fail(TR_EINVAL, "tr_bbvh_activity: not a partition BVH");
+    return tr_bnodes_activity((int64_t)B->nodes.size(), B->nodes.data(), active, out);
+}
+
+void tr_host_free(TrHostBuf *b) { delete b; }
+
+int tr_pack_tets(int64_t n_tets, const int64_t *tets, const double *tet_orig,
+                 const double *tet_inv, const double *field, int32_t centering,
+                 TrTetRecord *out) {
+    if (n_tets <= 0 || !tets || !tet_orig || !tet_inv || !field || !out)
+        return tr_fail(TR_EINVAL, "tr_pack_tets: invalid arguments");
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n_tets; ++t) {
+        TrTetRecord &R = out[t];
+        std::memcpy(R.inv, tet_inv + 9 * t, 72);
+        std::memcpy(R.orig, tet_orig + 3 * t, 24);
+        if (centering == 0) {
+            for (int i = 0; i < 4; ++i) R.f[i] = field[tets[4 * t + i]];
+        } else {
+            R.f[0] = field[t];
+            R.f[1] = R.f[2] = R.f[3] = 0.0;
+        }
+    }
+    return TR_OK;
+}
+
+int tr_tf_meta(int64_t n_parts, const double *vrange, const double *T, int64_t n, double lo,
+               double hi, double *max_opacity, double *raw_variance, double *sigma,
+               uint8_t *active) {
+    if (n_parts <= 0 || !vrange || !T || n < 2 || !(lo < hi))
+        return tr_fail(TR_EINVAL, "tr_tf_meta: invalid arguments");
+    std::vector<double> raw(n_parts), mop(n_parts);
+    int err = 0;
+#pragma omp parallel
+    {
+        std::vector<double> rows, W, D;
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t p = 0; p < n_parts; ++p) {
+            // transfer.py:_overlapping_colors: interpolated ends + table rows inside
+            double rmin = vrange[2 * p], rmax = vrange[2 * p + 1];
+            if (rmin > rmax) { err = 1; continue; }
+            double u_min = (rmin - lo) / (hi - lo) * (double)(n - 1);
+            double u_max = (rmax - lo) / (hi - lo) * (double)(n - 1);
+            // Python int(floor(.)) semantics, clamped so the cast cannot overflow
+            double fl = std::min(std::max(std::floor(u_min), -2.0), (double)n + 2.0);
+            double cl = std::min(std::max(std::ceil(u_max), -2.0), (double)n + 2.0);
+            int64_t j0 = std::max((int64_t)fl + 1, (int64_t)0);
+            int64_t j1 = std::min((int64_t)cl - 1, n - 1);
+            rows.clear();
+            double c[4];
+            tf_lookup(T, n, lo, hi, rmin, c);
+            rows.insert(rows.end(), c, c + 4);
+            for (int64_t j = j0; j <= j1; ++j) rows.insert(rows.end(), T + 4 * j, T + 4 * j + 4);
+            tf_lookup(T, n, lo, hi, rmax, c);
+            rows.insert(rows.end(), c, c + 4);
+            const int64_t k = (int64_t)rows.size() / 4;
+            // compute_partition_meta: opacity-weighted RGB, axis-0 mean
+            // (sequential), per-row squared distance (sequential over 3),
+            // mean over rows (numpy pairwise sum)
+            W.resize(3 * k);
+            double amax = -INFINITY;
+            for (int64_t i = 0; i < k; ++i) {
+                double a = rows[4 * i + 3];
+                amax = (a > amax) ? a : amax;
+                for (int q = 0; q < 3; ++q) W[3 * i + q] = rows[4 * i + q] * a;
+            }
+            double mean[3];
+            for (int q = 0; q < 3; ++q) {
+                double s = W[q];
+                for (int64_t i = 1; i < k; ++i) s += W[3 * i + q];
+                mean[q] = s / (double)k;
+            }
+            D.resize(k);
+            for (int64_t i = 0; i < k; ++i) {
+                double d0 = W[3 * i] - mean[0], d1 = W[3 * i + 1] - mean[1], d2 = W[3 * i + 2] - mean[2];
+                D[i] = ((d0 * d0) + (d1 * d1)) + (d2 * d2);
+            }
+            raw[p] = np_pairwise_sum(D.data(), k) / (double)k;
+            mop[p] = amax;
+        }
+    }
+    if (err) return tr_fail(TR_EINVAL, "tr_tf_meta: invalid value range (min > max)");
+    // normalize_variances (transfer.py:127-141)
+    double vmin = raw[0], vmax = raw[0];
+    for (int64_t p = 1; p < n_parts; ++p) { vmin = std::min(vmin, raw[p]); vmax = std::max(vmax, raw[p]); }
+    for (int64_t p = 0; p < n_parts; ++p) {
+        double s = (vmax == vmin) ? 1.0 : (raw[p] - vmin) / (vmax - vmin);
+        if (sigma) sigma[p] = s;
+        if (max_opacity) max_opacity[p] = mop[p];
+        if (raw_variance) raw_variance[p] = raw[p];
+        if (active) active[p] = mop[p] > 0.0 ? 1 : 0;
+    }
+    return TR_OK;
+}
+
+double tr_step_size(double s1, double s2, double p, double sigma) {
+    double m = (1.0 < sigma) ? 1.0 : sigma;  // Python min(sigma, 1.0)
+    double v = s1 + (s2 - s1) * std::pow(std::fabs(m - 1.0), p);
+    return (s1 > v) ? s1 : v;  // Python max(v, s1)
+}
+
+double tr_opacity_correction(double alpha, double s, double s1) {
+    return 1.0 - std::pow(1.0 - alpha, s / s1);
+}
+
+int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out) {
+    if (n < 0 || (n > 0 && (!sigma || !out))) return tr_fail(TR_EINVAL, "tr_step_sizes: invalid arguments");
+    for (int64_t i = 0; i < n; ++i) out[i] = tr_step_size(s1, s2, p, sigma[i]);
+    return TR_OK;
+}
+
+}  // extern "C"

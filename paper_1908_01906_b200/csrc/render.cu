@@ -1,0 +1,693 @@
+// render.cu -- sm_100a kernels of the tetray hot path.
+//
+//   tr_render_frame   replaces _kernels.render_frame   (pkg/src/tetray/_kernels.py:312-398)
+//   tr_field_at_many  replaces _kernels.field_at_many  (K:157-170)
+//   tr_scatter_tiles  multi-GPU merge of disjoint pixel tiles
+//
+// Arithmetic contract: every fp64 expression is
+// evaluated in the reference's (Python left-to-right) order and this file is
+// compiled with -fmad=false, so no multiply-add is contracted; / and sqrt
+// are IEEE round-to-nearest.  Results are therefore bit-identical to the
+// numba reference, except glibc pow in skip-adaptive mode.
+//
+// Structure:
+//   * persistent CTAs; each warp pulls 8x4 pixel tiles from an atomic queue
+//     (ray lengths vary 0..~300 samples, so static grids load-imbalance)
+//   * partition traversal: exact next_interval over a BVH2 with f64 child
+//     boxes, subtree-activity bits per metadata epoch prune transparent space
+//   * point location: per-ray "exclusive leaf" shortcut -- a point strictly
+//     inside the current leaf's exclusive box can only be in that leaf's tets,
+//     which are scanned in ascending id order (first hit = lowest index, the
+//     reference's tie rule K:119); otherwise a full min-id-pruned BVH descent
+//   * per-partition sample histogram privatised per CTA in shared memory,
+//     merged with 64-bit integer atomics (exact, order independent)
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+
+#include "tetray_b200.h"
+#include "tr_internal.h"
+
+namespace {
+
+constexpr double BARY_TOL = 1e-9;  // K:15
+constexpr int TILE_W = 8, TILE_H = 4;
+constexpr int PSTACK = 64;
+constexpr int BSTACK = 64;
+constexpr int BLOCK = 256;
+constexpr int32_t CHILD_NONE = INT32_MIN;
+constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
+
+struct RayD {
+    double ox, oy, oz, dx, dy, dz;
+    double ix, iy, iz;  // 1/d per axis (valid where d != 0), K:36
+    bool nx, ny, nz;    // d != 0
+};
+
+// K:30-71.  Returns false on a miss of the zero-direction kind ((1, 0)).
+__device__ __forceinline__ void slab(const RayD &r, const double *lo, const double *hi,
+                                     double &t0, double &t1) {
+    t0 = -INFINITY;
+    t1 = INFINITY;
+    if (r.nx) {
+        double a = (lo[0] - r.ox) * r.ix, b = (hi[0] - r.ox) * r.ix;
+        if (a > b) { double t = a; a = b; b = t; }
+        if (a > t0) t0 = a;
+        if (b < t1) t1 = b;
+    } else if (r.ox < lo[0] || r.ox > hi[0]) { t0 = 1.0; t1 = 0.0; return; }
+    if (r.ny) {
+        double a = (lo[1] - r.oy) * r.iy, b = (hi[1] - r.oy) * r.iy;
+        if (a > b) { double t = a; a = b; b = t; }
+        if (a > t0) t0 = a;
+        if (b < t1) t1 = b;
+    } else if (r.oy < lo[1] || r.oy > hi[1]) { t0 = 1.0; t1 = 0.0; return; }
+    if (r.nz) {
+        double a = (lo[2] - r.oz) * r.iz, b = (hi[2] - r.oz) * r.iz;
+        if (a > b) { double t = a; a = b; b = t; }
+        if (a > t0) t0 = a;
+        if (b < t1) t1 = b;
+    } else if (r.oz < lo[2] || r.oz > hi[2]) { t0 = 1.0; t1 = 0.0; return; }
+}
+
+// ------------------------------------------------------------ point location
+
+struct PQuery {  // a point with f32 round-down / round-up copies for conservative box tests
+    double x, y, z;
+    float xd, yd, zd, xu, yu, zu;
+};
+
+__device__ __forceinline__ PQuery make_query(double x, double y, double z) {
+    PQuery q;
+    q.x = x; q.y = y; q.z = z;
+    q.xd = __double2float_rd(x); q.yd = __double2float_rd(y); q.zd = __double2float_rd(z);
+    q.xu = __double2float_ru(x); q.yu = __double2float_ru(y); q.zu = __double2float_ru(z);
+    return q;
+}
+
+// conservative: true whenever the exact point lies in the closed box
+__device__ __forceinline__ bool in_box(const PQuery &q, float lx, float ly, float lz, float hx,
+                                       float hy, float hz) {
+    return !(q.xu < lx) && !(q.xd > hx) && !(q.yu < ly) && !(q.yd > hy) && !(q.zu < lz) &&
+           !(q.zd > hz);
+}
+
+// strict and exact-safe: true only if the exact point is strictly inside
+__device__ __forceinline__ bool strictly_in(const PQuery &q, const float *lo, const float *hi) {
+    return q.xd > lo[0] && q.xu < hi[0] && q.yd > lo[1] && q.yu < hi[1] && q.zd > lo[2] &&
+           q.zu < hi[2];
+}
+
+// K:121-128: barycentrics of q in tet t; true if all >= -BARY_TOL.
+__device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, uint32_t t,
+                                          const PQuery &q, double l[4]) {
+    const double2 *r = reinterpret_cast<const double2 *>(recs + t);
+    const double2 a0 = __ldg(r + 0), a1 = __ldg(r + 1), a2 = __ldg(r + 2);
+    const double2 a3 = __ldg(r + 3), a4 = __ldg(r + 4), a5 = __ldg(r + 5);
+    const double qx = q.x - a4.y, qy = q.y - a5.x, qz = q.z - a5.y;
+    const double l1 = a0.x * qx + a0.y * qy + a1.x * qz;
+    const double l2 = a1.y * qx + a2.x * qy + a2.y * qz;
+    const double l3 = a3.x * qx + a3.y * qy + a4.x * qz;
+    const double l0 = 1.0 - l1 - l2 - l3;
+    l[0] = l0; l[1] = l1; l[2] = l2; l[3] = l3;
+    return l0 >= -BARY_TOL && l1 >= -BARY_TOL && l2 >= -BARY_TOL && l3 >= -BARY_TOL;
+}
+
+struct SceneK {  // kernel copy of TrDeviceScene
+    const TrTetRecord *__restrict__ tets;
+    const TrPNode *__restrict__ pnodes;
+    const TrPLeaf *__restrict__ pleaves;
+    const uint32_t *__restrict__ pleaf_ids;
+    const TrBNode *__restrict__ bnodes;
+    int32_t centering;
+    double mesh_lo[3], mesh_hi[3];
+};
+
+// Scan one leaf's ids (ascending) for the first tet below `best` containing q.
+__device__ __forceinline__ void scan_leaf(const SceneK &S, uint32_t start, uint32_t count,
+                                          const PQuery &q, uint32_t &best, double l[4]) {
+    for (uint32_t k = start; k < start + count; ++k) {
+        const uint32_t t = __ldg(S.pleaf_ids + k);
+        if (t >= best) break;
+        double lt[4];
+        if (bary_test(S.tets, t, q, lt)) {
+            best = t;
+            l[0] = lt[0]; l[1] = lt[1]; l[2] = lt[2]; l[3] = lt[3];
+            break;
+        }
+    }
+}
+
+// Full descent: lowest-index tet containing q (K:93-136 semantics), pruning
+// subtrees whose minimum id cannot beat the best so far.  Returns the tet id
+// (UINT32_MAX if none) and the leaf it was found in.
+__device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], int32_t &leaf_out) {
+    uint32_t best = UINT32_MAX;
+    int32_t best_leaf = -1;
+    int32_t st_node[PSTACK];
+    uint32_t st_min[PSTACK];
+    int sp = 0;
+    int32_t node = 0;
+    while (true) {
+        const float4 *np = reinterpret_cast<const float4 *>(S.pnodes + node);
+        const float4 A = __ldg(np + 0), B = __ldg(np + 1), C = __ldg(np + 2);
+        const int4 D = __ldg(reinterpret_cast<const int4 *>(np + 3));
+        const int32_t c0 = D.x, c1 = D.y;
+        const uint32_t m0 = (uint32_t)D.z, m1 = (uint32_t)D.w;
+        bool h0 = m0 < best && in_box(q, A.x, A.y, A.z, A.w, B.x, B.y);
+        bool h1 = m1 < best && in_box(q, B.z, B.w, C.x, C.y, C.z, C.w);
+        if (h0 && c0 < 0) {
+            const uint32_t before = best;
+            const TrPLeaf *lf = S.pleaves + (~c0);
+            scan_leaf(S, __ldg(&lf->start), __ldg(&lf->count), q, best, l);
+            if (best != before) best_leaf = ~c0;
+            h0 = false;
+        }
+        if (h1 && c1 < 0 && c1 != CHILD_NONE) {
+            const uint32_t before = best;
+            const TrPLeaf *lf = S.pleaves + (~c1);
+            scan_leaf(S, __ldg(&lf->start), __ldg(&lf->count), q, best, l);
+            if (best != before) best_leaf = ~c1;
+            h1 = false;
+        }
+        h0 = h0 && m0 < best;
+        h1 = h1 && c1 != CHILD_NONE && m1 < best;
+        if (h0 && h1) {
+            // descend into the lower-min-id child first, defer the other
+            if (m0 <= m1) { node = c0; st_node[sp] = c1; st_min[sp] = m1; }
+            else { node = c1; st_node[sp] = c0; st_min[sp] = m0; }
+            ++sp;
+            continue;
+        }
+        if (h0) { node = c0; continue; }
+        if (h1) { node = c1; continue; }
+        bool found = false;
+        while (sp > 0) {
+            --sp;
+            if (st_min[sp] < best) { node = st_node[sp]; found = true; break; }
+        }
+        if (!found) break;
+    }
+    leaf_out = best_leaf;
+    return best;
+}
+
+struct LeafHint {  // the ray's current leaf: exclusive box + id range, in registers
+    float lo[3], hi[3];
+    uint32_t start, count;
+    bool valid;
+};
+
+__device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHint &h) {
+    const float4 *p = reinterpret_cast<const float4 *>(S.pleaves + leaf);
+    const float4 a = __ldg(p), b = __ldg(p + 1);
+    h.lo[0] = a.x; h.lo[1] = a.y; h.lo[2] = a.z;
+    h.hi[0] = a.w; h.hi[1] = b.x; h.hi[2] = b.y;
+    h.start = __float_as_uint(b.z);
+    h.count = __float_as_uint(b.w);
+    h.valid = true;
+}
+
+// K:139-154.  `hint` carries the exclusive-leaf shortcut between samples of a ray.
+__device__ __forceinline__ bool field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
+                                         bool use_hint, double &v, uint32_t &tet) {
+    double l[4];
+    uint32_t t = UINT32_MAX;
+    if (use_hint && hint.valid && strictly_in(q, hint.lo, hint.hi)) {
+        scan_leaf(S, hint.start, hint.count, q, t, l);
+    } else {
+        int32_t leaf;
+        t = locate_full(S, q, l, leaf);
+        if (use_hint && leaf >= 0) load_hint(S, leaf, hint);
+    }
+    tet = t;
+    if (t == UINT32_MAX) { v = 0.0; return false; }
+    const double2 *r = reinterpret_cast<const double2 *>(S.tets + t);
+    if (S.centering == 0) {
+        const double2 f01 = __ldg(r + 6), f23 = __ldg(r + 7);
+        v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
+    } else {
+        v = __ldg(r + 6).x;
+    }
+    return true;
+}
+
+// K:74-90
+__device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t n, double lo,
+                                          double hi, double v, double c[4]) {
+    const double u = (v - lo) / (hi - lo) * (double)(n - 1);
+    const double2 *t2 = reinterpret_cast<const double2 *>(T);
+    if (u <= 0.0) {
+        const double2 x = __ldg(t2), y = __ldg(t2 + 1);
+        c[0] = x.x; c[1] = x.y; c[2] = y.x; c[3] = y.y;
+        return;
+    }
+    if (u >= (double)(n - 1)) {
+        const double2 x = __ldg(t2 + 2 * (n - 1)), y = __ldg(t2 + 2 * (n - 1) + 1);
+        c[0] = x.x; c[1] = x.y; c[2] = y.x; c[3] = y.y;
+        return;
+    }
+    const int64_t j = (int64_t)floor(u);
+    const double f = u - (double)j;
+    const double2 a0 = __ldg(t2 + 2 * j), a1 = __ldg(t2 + 2 * j + 1);
+    const double2 b0 = __ldg(t2 + 2 * j + 2), b1 = __ldg(t2 + 2 * j + 3);
+    c[0] = a0.x + f * (b0.x - a0.x);
+    c[1] = a0.y + f * (b0.y - a0.y);
+    c[2] = a1.x + f * (b1.x - a1.x);
+    c[3] = a1.y + f * (b1.y - a1.y);
+}
+
+struct EpochK {
+    const uint8_t *__restrict__ active;
+    const uint8_t *__restrict__ bnode_active;
+    const double *__restrict__ step;
+    const double *__restrict__ tf;
+    int64_t n_tf;
+    double tf_lo, tf_hi;
+};
+
+struct Acc {
+    double r, g, b, a;
+};
+
+// K:262-297.  Returns samples taken; sets `terminated`.
+__device__ int64_t march_range(const SceneK &S, const EpochK &E, const RayD &ray, double t0,
+                               double t1, double step, double s1, double term, double phase,
+                               LeafHint &hint, bool use_hint, Acc &acc, bool &terminated) {
+    const double e = step / s1;  // opacity_correction's exponent (K:27)
+    const bool unit = (e == 1.0);
+    int64_t samples = 0;
+    terminated = false;
+    for (int64_t k = 0;; ++k) {
+        const double t = t0 + ((double)k + phase) * step;
+        if (k > 0 && t >= t1) break;
+        samples += 1;
+        const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy, ray.oz + t * ray.dz);
+        double v;
+        uint32_t tet;
+        if (field_at(S, q, hint, use_hint, v, tet)) {
+            double c[4];
+            tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+            const double x = 1.0 - c[3];
+            const double ca = 1.0 - (unit ? x : pow(x, e));  // glibc pow(x, 1) == x
+            const double w = (1.0 - acc.a) * ca;
+            acc.r += w * c[0];
+            acc.g += w * c[1];
+            acc.b += w * c[2];
+            acc.a += w;
+            if (acc.a >= term) { terminated = true; break; }
+        }
+    }
+    return samples;
+}
+
+// K:173-230: first active partition interval, lexicographic min (clamped
+// t_enter, pid) among partitions with t_exit > t_min + excl_eps.
+__device__ int32_t next_interval(const SceneK &S, const EpochK &E, const RayD &ray, double t_min,
+                                 double excl_eps, int32_t excl_id, double &ra, double &rb) {
+    int32_t best_id = -1;
+    double best_a = INFINITY, best_b = INFINITY;
+    const double thr = t_min + excl_eps;
+    int32_t st_node[BSTACK];
+    double st_a[BSTACK];
+    int sp = 0;
+    int32_t node = 0;
+    double node_a = -INFINITY;
+    while (true) {
+        if (node_a <= best_a) {
+            const TrBNode *N = S.bnodes + node;
+            const uint32_t act = __ldg(E.bnode_active + node);
+            const int2 ch = __ldg(reinterpret_cast<const int2 *>(&N->child[0]));
+            int32_t push_n[2];
+            double push_a[2];
+            int np = 0;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int32_t child = c == 0 ? ch.x : ch.y;
+                if (!((act >> c) & 1u)) continue;  // CHILD_NONE has a clear bit
+                const double2 *bp = reinterpret_cast<const double2 *>(&N->box[c][0]);
+                const double2 b0 = __ldg(bp), b1 = __ldg(bp + 1), b2 = __ldg(bp + 2);
+                const double lo[3] = {b0.x, b0.y, b1.x}, hi[3] = {b1.y, b2.x, b2.y};
+                double a, b;
+                slab(ray, lo, hi, a, b);
+                if (a > b) continue;
+                if (b <= thr) continue;
+                const double a_cl = (a > t_min) ? a : t_min;
+                if (a_cl >= INFINITY) continue;  // t_max = inf (K:366)
+                if (a_cl > best_a) continue;
+                if (child < 0) {
+                    const int32_t pid = ~child;
+                    if (pid == excl_id) continue;
+                    if (a_cl < best_a || (a_cl == best_a && pid < best_id)) {
+                        best_id = pid;
+                        best_a = a_cl;
+                        best_b = b;
+                    }
+                } else {
+                    push_n[np] = child;
+                    push_a[np] = a_cl;
+                    ++np;
+                }
+            }
+            if (np == 2) {  // visit the nearer child first
+                const int near = push_a[1] < push_a[0] ? 1 : 0;
+                st_node[sp] = push_n[1 - near];
+                st_a[sp] = push_a[1 - near];
+                ++sp;
+                node = push_n[near];
+                node_a = push_a[near];
+                continue;
+            }
+            if (np == 1) { node = push_n[0]; node_a = push_a[0]; continue; }
+        }
+        if (sp == 0) break;
+        --sp;
+        node = st_node[sp];
+        node_a = st_a[sp];
+    }
+    ra = best_a;
+    rb = best_b;
+    return best_id;
+}
+
+// K:300-309 with numba's 64-bit integer promotion.
+__device__ __forceinline__ double hash01(int64_t ix, int64_t iy) {
+    uint64_t h = ((uint64_t)(uint32_t)ix * 73856093ull) ^ ((uint64_t)(uint32_t)iy * 19349663ull);
+    h = (h ^ 61ull) ^ (h >> 16);
+    h = h * 9ull;
+    h = h ^ (h >> 4);
+    h = h * 0x27D4EB2Dull;
+    h = h ^ (h >> 15);
+    return __ull2double_rn(h) / 4294967296.0;
+}
+
+struct FrameK {
+    TrFrame f;
+    int64_t tiles_x, n_tiles, my_tiles;
+    int32_t n_parts;
+    int32_t hist_smem;
+};
+
+__global__ void __launch_bounds__(BLOCK, 2)
+render_frame_kernel(SceneK S, EpochK E, FrameK F, TrOutputs O) {
+    extern __shared__ unsigned long long hist[];  // [n_parts] when F.hist_smem
+    __shared__ unsigned long long red[2][BLOCK / 32];
+    const TrFrame &fr = F.f;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool track = fr.track_ppart && fr.mode != 0;
+    if (track && F.hist_smem)
+        for (int i = threadIdx.x; i < F.n_parts; i += BLOCK) hist[i] = 0ull;
+    __syncthreads();
+    const bool use_hint = !(fr.flags & TR_FLAG_NO_LEAF_HINT);
+    unsigned long long my_samples = 0, my_visited = 0;
+
+    while (true) {
+        int64_t j = 0;
+        if (lane == 0) j = (int64_t)atomicAdd(O.work, 1u);
+        j = __shfl_sync(0xffffffffu, j, 0);
+        if (j >= F.my_tiles) break;
+        const int64_t tile = (int64_t)fr.shard_rank + (int64_t)fr.shard_count * j;
+        const int64_t ix = (tile % F.tiles_x) * TILE_W + (lane % TILE_W);
+        const int64_t iy = (tile / F.tiles_x) * TILE_H + (lane / TILE_W);
+        if (ix >= fr.width || iy >= fr.height) continue;
+
+        // ---- ray generation, K:330-340 (left-to-right, no contraction)
+        const double sx = (((double)ix + 0.5) / (double)fr.width) * 2.0 - 1.0;
+        const double sy = 1.0 - (((double)iy + 0.5) / (double)fr.height) * 2.0;
+        double dx = fr.cam_fwd[0] + sx * fr.aspect * fr.tan_half * fr.cam_right[0] + sy * fr.tan_half * fr.cam_up[0];
+        double dy = fr.cam_fwd[1] + sx * fr.aspect * fr.tan_half * fr.cam_right[1] + sy * fr.tan_half * fr.cam_up[1];
+        double dz = fr.cam_fwd[2] + sx * fr.aspect * fr.tan_half * fr.cam_right[2] + sy * fr.tan_half * fr.cam_up[2];
+        const double dn = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+        dx *= dn; dy *= dn; dz *= dn;
+        RayD ray;
+        ray.ox = fr.cam_pos[0]; ray.oy = fr.cam_pos[1]; ray.oz = fr.cam_pos[2];
+        ray.dx = dx; ray.dy = dy; ray.dz = dz;
+        ray.nx = dx != 0.0; ray.ny = dy != 0.0; ray.nz = dz != 0.0;
+        ray.ix = ray.nx ? 1.0 / dx : 0.0;
+        ray.iy = ray.ny ? 1.0 / dy : 0.0;
+        ray.iz = ray.nz ? 1.0 / dz : 0.0;
+        const double phase = fr.jitter ? hash01(ix, iy) : 0.5;
+
+        Acc acc = {0.0, 0.0, 0.0, 0.0};
+        int64_t samples = 0;
+        int32_t visited = 0;
+        LeafHint hint;
+        hint.valid = false;
+        bool terminated;
+        if (fr.mode == 0) {  // K:346-359
+            double a, b;
+            slab(ray, S.mesh_lo, S.mesh_hi, a, b);
+            const double t0 = (a > 0.0) ? a : 0.0;
+            if (a <= b && b - t0 >= fr.eps)
+                samples = march_range(S, E, ray, t0, b, fr.s1, fr.s1, fr.term, phase, hint, use_hint,
+                                      acc, terminated);
+        } else {  // K:360-391
+            double t_min = 0.0;
+            int32_t last = -1;
+            while (true) {
+                const double excl = (last < 0) ? 0.0 : fr.eps;
+                double a, b;
+                const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
+                if (pid < 0) break;
+                visited += 1;
+                terminated = false;
+                if (b - a >= fr.eps) {
+                    const double s = (fr.mode == 2) ? __ldg(E.step + pid) : fr.s1;
+                    const int64_t ns = march_range(S, E, ray, a, b, s, fr.s1, fr.term, phase, hint,
+                                                   use_hint, acc, terminated);
+                    samples += ns;
+                    if (track && ns) {
+                        if (F.hist_smem) atomicAdd(&hist[pid], (unsigned long long)ns);
+                        else atomicAdd((unsigned long long *)O.ppart + pid, (unsigned long long)ns);
+                    }
+                }
+                if (terminated) break;
+                t_min = b - fr.eps;
+                last = pid;
+            }
+        }
+        // K:393-398
+        const double r = acc.r + (1.0 - acc.a) * fr.bg[0];
+        const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
+        const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
+        const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
+        const int64_t o = fr.compact ? j * (TILE_W * TILE_H) + lane : iy * fr.width + ix;
+        double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * o);
+        px[0] = make_double2(r, g);
+        px[1] = make_double2(bl, al);
+        O.samples[o] = samples;
+        O.visited[o] = visited;
+        my_samples += (unsigned long long)samples;
+        my_visited += (unsigned long long)visited;
+    }
+    // block reduction of the frame totals (R:198-201) and histogram merge
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
+        my_visited += __shfl_xor_sync(0xffffffffu, my_visited, off);
+    }
+    if (lane == 0) { red[0][warp] = my_samples; red[1][warp] = my_visited; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0, v = 0;
+        for (int w = 0; w < BLOCK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
+        if (s) atomicAdd((unsigned long long *)O.totals, s);
+        if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
+    }
+    if (track && F.hist_smem)
+        for (int i = threadIdx.x; i < F.n_parts; i += BLOCK)
+            if (hist[i]) atomicAdd((unsigned long long *)O.ppart + i, hist[i]);
+}
+
+__global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restrict__ pts,
+                                     uint8_t *found, double *vals, int64_t *tet) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const PQuery q = make_query(pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+        LeafHint h;
+        h.valid = false;
+        double v;
+        uint32_t t;
+        const bool f = field_at(S, q, h, false, v, t);
+        found[i] = f ? 1 : 0;
+        vals[i] = v;
+        if (tet) tet[i] = f ? (int64_t)t : -1;
+    }
+}
+
+__global__ void scatter_tiles_kernel(int64_t width, int64_t height, int64_t tiles_x,
+                                     int64_t n_tiles, int32_t count, int64_t slots,
+                                     const double *__restrict__ src_rgba,
+                                     const int64_t *__restrict__ src_samples,
+                                     const int32_t *__restrict__ src_visited, double *rgba,
+                                     int64_t *samples, int32_t *visited) {
+    const int64_t total = (int64_t)count * slots * (TILE_W * TILE_H);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t lane = i % (TILE_W * TILE_H);
+        const int64_t slot = (i / (TILE_W * TILE_H)) % slots;
+        const int64_t rank = i / (TILE_W * TILE_H * slots);
+        const int64_t tile = rank + (int64_t)count * slot;
+        if (tile >= n_tiles) continue;
+        const int64_t ix = (tile % tiles_x) * TILE_W + lane % TILE_W;
+        const int64_t iy = (tile / tiles_x) * TILE_H + lane / TILE_W;
+        if (ix >= width || iy >= height) continue;
+        const int64_t o = iy * width + ix;
+        const double2 *s = reinterpret_cast<const double2 *>(src_rgba + 4 * i);
+        double2 *d = reinterpret_cast<double2 *>(rgba + 4 * o);
+        d[0] = s[0];
+        d[1] = s[1];
+        samples[o] = src_samples[i];
+        visited[o] = src_visited[i];
+    }
+}
+
+thread_local int64_t g_last_launch[3] = {0, 0, 0};
+
+int cuda_fail(cudaError_t e, const char *where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+    return tr_fail(TR_ECUDA, m.c_str());
+}
+
+SceneK make_scene(const TrDeviceScene *s) {
+    SceneK S;
+    S.tets = s->tets;
+    S.pnodes = s->pnodes;
+    S.pleaves = s->pleaves;
+    S.pleaf_ids = s->pleaf_ids;
+    S.bnodes = s->bnodes;
+    S.centering = s->centering;
+    for (int a = 0; a < 3; ++a) { S.mesh_lo[a] = s->mesh_lo[a]; S.mesh_hi[a] = s->mesh_hi[a]; }
+    return S;
+}
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t tr_num_tiles(int64_t width, int64_t height) {
+    return ((width + TILE_W - 1) / TILE_W) * ((height + TILE_H - 1) / TILE_H);
+}
+
+int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t count) {
+    if (count < 1) return 0;
+    return (tr_num_tiles(width, height) + count - 1) / count;
+}
+
+int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                    const TrOutputs *out, void *stream) {
+    if (!scene || !epoch || !frame || !out)
+        return tr_fail(TR_EINVAL, "tr_render_frame: null argument");
+    if (frame->width < 1 || frame->height < 1 || frame->mode < 0 || frame->mode > 2 ||
+        frame->shard_count < 1 || frame->shard_rank < 0 || frame->shard_rank >= frame->shard_count)
+        return tr_fail(TR_EINVAL, "tr_render_frame: invalid frame");
+    if (!scene->tets || !scene->pnodes || !scene->pleaves || !scene->pleaf_ids || !out->rgba ||
+        !out->samples || !out->visited || !out->totals || !out->work || !epoch->tf_table ||
+        epoch->n_tf < 2)
+        return tr_fail(TR_EINVAL, "tr_render_frame: missing buffer");
+    if (frame->mode != 0 && (!scene->bnodes || !epoch->active || !epoch->bnode_active ||
+                             (frame->mode == 2 && !epoch->step)))
+        return tr_fail(TR_EINVAL, "tr_render_frame: missing partition buffers");
+    if (frame->track_ppart && frame->mode != 0 && !out->ppart)
+        return tr_fail(TR_EINVAL, "tr_render_frame: missing ppart buffer");
+    cudaStream_t st = (cudaStream_t)stream;
+    SceneK S = make_scene(scene);
+    EpochK E;
+    E.active = epoch->active;
+    E.bnode_active = epoch->bnode_active;
+    E.step = epoch->step;
+    E.tf = epoch->tf_table;
+    E.n_tf = epoch->n_tf;
+    E.tf_lo = epoch->tf_lo;
+    E.tf_hi = epoch->tf_hi;
+    FrameK F;
+    F.f = *frame;
+    F.tiles_x = (frame->width + TILE_W - 1) / TILE_W;
+    F.n_tiles = tr_num_tiles(frame->width, frame->height);
+    F.my_tiles = (F.n_tiles - frame->shard_rank + frame->shard_count - 1) / frame->shard_count;
+    if (F.my_tiles < 0) F.my_tiles = 0;
+    F.n_parts = (int32_t)scene->n_parts;
+    const bool track = frame->track_ppart && frame->mode != 0;
+    F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX) ? 1 : 0;
+    const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
+    cudaError_t e;
+    if (smem > 48 * 1024) {
+        e = cudaFuncSetAttribute(render_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
+    }
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_frame_kernel, BLOCK, smem);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+    if (per_sm < 1) per_sm = 1;
+    int64_t warps_needed = F.my_tiles;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    const int64_t grid_need = (warps_needed + BLOCK / 32 - 1) / (BLOCK / 32);
+    if (grid > grid_need) grid = grid_need;
+    if (grid < 1) grid = 1;
+    e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
+    render_frame_kernel<<<(unsigned)grid, BLOCK, smem, st>>>(S, E, F, *out);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "render_frame_kernel launch");
+    g_last_launch[0] = 1;
+    g_last_launch[1] = grid;
+    g_last_launch[2] = BLOCK;
+    return TR_OK;
+}
+
+int tr_field_at_many(const TrDeviceScene *scene, int64_t n, const double *pts, uint8_t *found,
+                     double *vals, int64_t *tet, void *stream) {
+    if (!scene || n < 0 || (n > 0 && (!pts || !found || !vals)))
+        return tr_fail(TR_EINVAL, "tr_field_at_many: invalid arguments");
+    if (n == 0) return TR_OK;
+    SceneK S = make_scene(scene);
+    int64_t grid = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    field_at_many_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(S, n, pts, found, vals, tet);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "field_at_many_kernel launch");
+    return TR_OK;
+}
+
+int tr_scatter_tiles(int64_t width, int64_t height, int32_t count, const double *src_rgba,
+                     const int64_t *src_samples, const int32_t *src_visited,
+                     int64_t slots_per_rank, double *rgba, int64_t *samples, int32_t *visited,
+                     void *stream) {
+    if (width < 1 || height < 1 || count < 1 || slots_per_rank < 0 || !src_rgba || !src_samples ||
+        !src_visited || !rgba || !samples || !visited)
+        return tr_fail(TR_EINVAL, "tr_scatter_tiles: invalid arguments");
+    const int64_t total = (int64_t)count * slots_per_rank * TILE_W * TILE_H;
+    if (total == 0) return TR_OK;
+    int64_t grid = (total + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 16;
+    if (grid > cap) grid = cap;
+    scatter_tiles_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(
+        width, height, (width + TILE_W - 1) / TILE_W, tr_num_tiles(width, height), count,
+        slots_per_rank, src_rgba, src_samples, src_visited, rgba, samples, visited);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "scatter_tiles_kernel launch");
+    return TR_OK;
+}
+
+int tr_last_launch(int64_t *out3) {
+    if (!out3) return tr_fail(TR_EINVAL, "tr_last_launch: null");
+    for (int i = 0; i < 3; ++i) out3[i] = g_last_launch[i];
+    return TR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,8 @@
+// tr_internal.h -- shared helpers of libtetray_b200 (not part of the C ABI).
+#pragma once
+#include <cstdint>
+
+// Record an error message for tr_last_error() and return code.
+int tr_fail(int code, const char *msg);
+// K:74-90 on the host (used by the TF-metadata restatement).
+void tr_tf_sample_host(const double *T, int64_t n, double lo, double hi, double v, double *rgba);

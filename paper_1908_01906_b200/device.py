@@ -1,0 +1,359 @@
+"""Device-resident dataset, metadata epochs and frame launches.
+
+Layout in HBM, all owned by torch tensors:
+  tets       TrTetRecord[T]     128 B/tet  (inv 72 B | orig 24 B | field x4 32 B)
+  pnodes     TrPNode[]          64 B BVH2 nodes over padded tet boxes (f32, outward)
+  pleaves    TrPLeaf[]          32 B: exclusive box (f32, inward) + id range
+  pleaf_ids  uint32[]           ascending per leaf
+  bnodes     TrBNode[]          112 B BVH2 nodes over partition boxes (f64)
+  epoch      one buffer per (active, sigma, tf) snapshot and (s1, s2, p):
+             step f64[P] | tf f64[n,4] | active u8[P] | node activity u8[M]
+
+The scene is uploaded once per (sampler, partition BVH) pair and cached;
+transfer-function edits only create a new epoch (never touch geometry),
+mirroring the reference's TF decoupling (transfer.py:144-167, A7).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+import threading
+import time
+import weakref
+from collections import OrderedDict
+from typing import Optional
+
+import numpy as np
+
+from . import _lib
+from .mesh import BOX_PAD_REL
+
+_CACHE_ATTR = "_b200_device_cache"
+_LEAF_MAX = 8
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def resolve_device(device=None):
+    torch = _torch()
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: the B200 render path has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise RuntimeError(f"device {device} is not a CUDA device (no CPU fallback)")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+def _upload(arr: np.ndarray, device):
+    torch = _torch()
+    raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
+    return torch.from_numpy(raw.copy()).to(device)
+
+
+def _padded_boxes(scene) -> tuple[np.ndarray, np.ndarray]:
+    sampler = scene.sampler
+    if hasattr(sampler, "padded_boxes"):
+        return sampler.padded_boxes()
+    mesh = scene.mesh  # a tetray Scene: same rule as mesh.py:248-250
+    lo, hi = mesh.tet_aabbs()
+    pad = BOX_PAD_REL * max(mesh.bounds.diagonal(), 1e-30)
+    return lo - pad, hi + pad
+
+
+def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEAF_MAX):
+    L = _lib.lib()
+    box_lo = np.ascontiguousarray(box_lo, dtype=np.float64)
+    box_hi = np.ascontiguousarray(box_hi, dtype=np.float64)
+    h = C.c_void_p()
+    _lib.check(L.tr_pbvh_build(len(box_lo), _lib.ptr(box_lo, C.c_double),
+                               _lib.ptr(box_hi, C.c_double), leaf_max, C.byref(h)), "tr_pbvh_build")
+    try:
+        sz = np.zeros(3, np.int64)
+        _lib.check(L.tr_pbvh_sizes(h, _lib.ptr(sz, C.c_int64)), "tr_pbvh_sizes")
+        nodes = np.zeros(int(sz[0]), dtype=_lib.PNODE_DTYPE)
+        leaves = np.zeros(int(sz[1]), dtype=_lib.PLEAF_DTYPE)
+        ids = np.zeros(int(sz[2]), dtype=np.uint32)
+        _lib.check(L.tr_pbvh_copy(h, _lib.vptr(nodes), _lib.vptr(leaves), _lib.vptr(ids)),
+                   "tr_pbvh_copy")
+    finally:
+        L.tr_host_free(h)
+    return nodes, leaves, ids
+
+
+def pack_tet_records(mesh, sampler) -> np.ndarray:
+    rec = np.empty(mesh.n_tets, dtype=_lib.TET_RECORD_DTYPE)
+    orig = np.ascontiguousarray(sampler.tet_orig, dtype=np.float64)
+    inv = np.ascontiguousarray(sampler.tet_inv, dtype=np.float64)
+    tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+    fld = np.ascontiguousarray(mesh.field, dtype=np.float64)
+    _lib.check(_lib.lib().tr_pack_tets(mesh.n_tets, _lib.ptr(tets, C.c_int64),
+                                       _lib.ptr(orig, C.c_double), _lib.ptr(inv, C.c_double),
+                                       _lib.ptr(fld, C.c_double), int(mesh.centering),
+                                       _lib.vptr(rec)), "tr_pack_tets")
+    return rec
+
+
+class Epoch:
+    """One uploaded (active, step, tf) snapshot."""
+
+    def __init__(self, dev: "DeviceScene", meta_state, params):
+        torch = _torch()
+        active, sigma, tf = meta_state
+        self.meta_state = meta_state  # pins the tuple so its id stays unique
+        P = dev.n_parts
+        act = np.ascontiguousarray(active, dtype=np.uint8).reshape(-1)
+        sig = np.ascontiguousarray(sigma, dtype=np.float64).reshape(-1)
+        if len(act) != P or len(sig) != P:
+            raise ValueError(f"metadata epoch has {len(act)} partitions, scene has {P}")
+        step = np.empty(P)
+        _lib.check(_lib.lib().tr_step_sizes(P, _lib.ptr(sig, C.c_double), float(params.s1),
+                                            float(params.s2), float(params.p),
+                                            _lib.ptr(step, C.c_double)), "tr_step_sizes")
+        bact = np.empty(dev.n_bnodes, dtype=np.uint8)
+        _lib.check(_lib.lib().tr_bnodes_activity(dev.n_bnodes, _lib.vptr(dev.bnodes_host),
+                                                 _lib.ptr(act, C.c_uint8), _lib.ptr(bact, C.c_uint8)),
+                   "tr_bnodes_activity")
+        table = np.ascontiguousarray(tf.table, dtype=np.float64)
+        self.n_tf = int(table.shape[0])
+        self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
+        o_tf = 8 * P
+        o_act = o_tf + table.nbytes
+        o_bact = o_act + P
+        nbytes = (o_bact + dev.n_bnodes + 15) // 16 * 16
+        host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        hv[:o_tf] = step.view(np.uint8)
+        hv[o_tf:o_act] = table.view(np.uint8).reshape(-1)
+        hv[o_act:o_bact] = act
+        hv[o_bact:o_bact + dev.n_bnodes] = bact
+        self.h2d_bytes = nbytes
+        self.host = host
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev.device)
+        self.buf.copy_(host, non_blocking=True)
+        base = self.buf.data_ptr()
+        self.desc = _lib.TrEpoch(active=base + o_act, bnode_active=base + o_bact, step=base,
+                                 tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
+                                 tf_hi=self.tf_hi)
+        self.step_host = step
+
+
+class FrameBuffers:
+    """Device outputs of one frame shape, reused across frames."""
+
+    def __init__(self, dev: "DeviceScene", width: int, height: int, compact_slots: int = 0):
+        torch = _torch()
+        d = dev.device
+        n = compact_slots * 32 if compact_slots else width * height
+        self.rgba = torch.empty((n, 4), dtype=torch.float64, device=d)
+        self.samples = torch.empty(n, dtype=torch.int64, device=d)
+        self.visited = torch.empty(n, dtype=torch.int32, device=d)
+        # [totals(2) | work(1) | ppart(P)] zeroed with one fill per frame
+        self.counters = torch.empty(3 + dev.n_parts, dtype=torch.int64, device=d)
+        self.start = torch.cuda.Event(enable_timing=True)
+        self.end = torch.cuda.Event(enable_timing=True)
+
+    def outputs(self) -> _lib.TrOutputs:
+        c = self.counters.data_ptr()
+        return _lib.TrOutputs(rgba=self.rgba.data_ptr(), samples=self.samples.data_ptr(),
+                              visited=self.visited.data_ptr(), ppart=c + 24, totals=c,
+                              work=c + 16)
+
+
+class DeviceScene:
+    """The scene's geometry in HBM plus its epoch and output caches."""
+
+    def __init__(self, scene, device):
+        torch = _torch()
+        self.device = device
+        self.lock = threading.Lock()
+        mesh, sampler = scene.mesh, scene.sampler
+        with torch.cuda.device(device):
+            t0 = time.perf_counter()
+            rec = pack_tet_records(mesh, sampler)
+            lo, hi = _padded_boxes(scene)
+            pnodes, pleaves, pids = build_point_bvh(lo, hi)
+            part_lo = np.ascontiguousarray(scene.bvh.box_lo, dtype=np.float64)
+            part_hi = np.ascontiguousarray(scene.bvh.box_hi, dtype=np.float64)
+            bnodes = getattr(scene.bvh, "nodes", None)
+            if not (isinstance(bnodes, np.ndarray) and bnodes.dtype == _lib.BNODE_DTYPE):
+                from .traversal import build_bvh_over_boxes
+                bnodes = build_bvh_over_boxes(part_lo, part_hi)
+            self.build_s = time.perf_counter() - t0
+            self.bnodes_host = np.ascontiguousarray(bnodes)
+            self.n_parts = int(part_lo.shape[0])
+            self.n_bnodes = int(len(bnodes))
+            self.n_tets = int(mesh.n_tets)
+            self.pnodes_host, self.pleaves_host = pnodes, pleaves
+            self.t_tets = _upload(rec, device)
+            self.t_pnodes = _upload(pnodes, device)
+            self.t_pleaves = _upload(pleaves, device)
+            self.t_pids = _upload(pids, device)
+            self.t_bnodes = _upload(bnodes, device)
+            self.t_plo = _upload(part_lo, device)
+            self.t_phi = _upload(part_hi, device)
+            torch.cuda.synchronize(device)
+        self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
+                                                      self.t_pids, self.t_bnodes, self.t_plo,
+                                                      self.t_phi))
+        self.desc = _lib.TrDeviceScene(
+            tets=self.t_tets.data_ptr(), pnodes=self.t_pnodes.data_ptr(),
+            pleaves=self.t_pleaves.data_ptr(), pleaf_ids=self.t_pids.data_ptr(),
+            n_tets=self.n_tets, n_pnodes=len(pnodes), n_pleaves=len(pleaves),
+            centering=int(mesh.centering), bnodes=self.t_bnodes.data_ptr(),
+            part_lo=self.t_plo.data_ptr(), part_hi=self.t_phi.data_ptr(), n_parts=self.n_parts,
+            n_bnodes=self.n_bnodes,
+            mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi))
+        self._epochs: OrderedDict = OrderedDict()
+        self._frames: dict = {}
+
+    # ---------------------------------------------------------------- epochs
+    def epoch(self, meta_state, params) -> Epoch:
+        key = (id(meta_state), float(params.s1), float(params.s2), float(params.p))
+        ep = self._epochs.get(key)
+        if ep is None or ep.meta_state is not meta_state:
+            ep = Epoch(self, meta_state, params)
+            self._epochs[key] = ep
+            while len(self._epochs) > 8:
+                self._epochs.popitem(last=False)
+        else:
+            self._epochs.move_to_end(key)
+        return ep
+
+    def frame_buffers(self, width: int, height: int, compact_slots: int = 0) -> FrameBuffers:
+        key = (width, height, compact_slots)
+        fb = self._frames.get(key)
+        if fb is None:
+            fb = self._frames[key] = FrameBuffers(self, width, height, compact_slots)
+        return fb
+
+    # ---------------------------------------------------------------- frames
+    def frame_desc(self, scene, camera, mode: int, params, jitter: bool, track: bool,
+                   flags: int = 0, shard_rank: int = 0, shard_count: int = 1,
+                   compact: bool = False) -> _lib.TrFrame:
+        right, up, fwd = camera.basis()
+        w, h = int(camera.width), int(camera.height)
+        bg = np.asarray(scene.background, dtype=np.float64).reshape(4)
+        D3 = C.c_double * 3
+        return _lib.TrFrame(
+            cam_pos=D3(*camera.position), cam_right=D3(*right), cam_up=D3(*up), cam_fwd=D3(*fwd),
+            tan_half=math.tan(math.radians(camera.fov_y_deg) / 2.0), aspect=w / h,
+            width=w, height=h, jitter=1 if jitter else 0, mode=mode, s1=float(params.s1),
+            term=float(params.termination_opacity),
+            eps=float(scene.traversal_config.epsilon), bg=(C.c_double * 4)(*bg),
+            track_ppart=1 if track else 0, shard_rank=shard_rank, shard_count=shard_count,
+            compact=1 if compact else 0, flags=flags)
+
+    def launch(self, frame: _lib.TrFrame, epoch: Epoch, fb: FrameBuffers, stream) -> None:
+        fb.counters.zero_()
+        out = fb.outputs()
+        fb.start.record(stream)
+        _lib.check(_lib.lib().tr_render_frame(C.byref(self.desc), C.byref(epoch.desc),
+                                              C.byref(frame), C.byref(out),
+                                              C.c_void_p(stream.cuda_stream)), "tr_render_frame")
+        fb.end.record(stream)
+
+    def render(self, scene, camera, mode: int, params, *, jitter: bool, track: bool,
+               flags: int = 0):
+        from .render import Framebuffer, RenderStats
+        torch = _torch()
+        w, h = int(camera.width), int(camera.height)
+        with self.lock, torch.cuda.device(self.device):
+            t0 = time.perf_counter()
+            stream = torch.cuda.current_stream(self.device)
+            meta = scene.meta_state()
+            ep = self.epoch(meta, params)
+            frame = self.frame_desc(scene, camera, mode, params, jitter, track, flags)
+            fb = self.frame_buffers(w, h)
+            self.launch(frame, ep, fb, stream)
+            rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
+            samp_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
+            cnt_h = torch.empty(3 + self.n_parts, dtype=torch.int64, pin_memory=True)
+            rgba_h.view(-1, 4).copy_(fb.rgba, non_blocking=True)
+            samp_h.view(-1).copy_(fb.samples, non_blocking=True)
+            cnt_h.copy_(fb.counters, non_blocking=True)
+            stream.synchronize()
+            wall_ms = (time.perf_counter() - t0) * 1000.0
+            dev_ms = fb.start.elapsed_time(fb.end)
+        cnt = cnt_h.numpy()
+        rgba = rgba_h.numpy()
+        samples = samp_h.numpy()
+        fbuf = Framebuffer(width=w, height=h, rgba=rgba, samples=samples,
+                           background=np.asarray(scene.background, dtype=np.float64).copy())
+        stats = RenderStats(
+            total_samples=int(cnt[0]), wall_ms=wall_ms,
+            partitions_visited_mean=float(np.float64(cnt[1]) / np.float64(w * h)),
+            per_partition_samples=cnt[3:].copy() if track else None,
+            samples=samples, device_ms=float(dev_ms), gpu_launches=1)
+        return fbuf, stats
+
+
+def device_scene_for(scene, device=None) -> DeviceScene:
+    """Cached DeviceScene of `scene` (rebuilt if its sampler or BVH changed)."""
+    device = resolve_device(device)
+    cache = getattr(scene, _CACHE_ATTR, None)
+    if cache is None:
+        cache = {}
+        try:
+            object.__setattr__(scene, _CACHE_ATTR, cache)
+        except AttributeError:
+            cache = _GLOBAL_CACHE.setdefault(id(scene), {})
+    key = (str(device), id(scene.sampler), id(scene.bvh))
+    ent = cache.get(key)
+    if ent is None or ent[0]() is not scene.sampler or ent[1]() is not scene.bvh:
+        for k in [k for k in cache if k[0] == str(device)]:
+            del cache[k]
+        dev = DeviceScene(scene, device)
+        cache[key] = (weakref.ref(scene.sampler), weakref.ref(scene.bvh), dev)
+        return dev
+    return ent[2]
+
+
+_GLOBAL_CACHE: dict = {}
+
+
+class _SamplerScene:
+    """Adapter so a bare MeshSampler can be made device-resident for point
+    queries (no partitions needed: a single dummy partition)."""
+
+    def __init__(self, sampler):
+        from .traversal import PartitionBVH, build_bvh_over_boxes
+        self.sampler = sampler
+        self.mesh = sampler.mesh
+        lo = sampler.mesh.bounds.lo.reshape(1, 3).copy()
+        hi = sampler.mesh.bounds.hi.reshape(1, 3).copy()
+        self.bvh = PartitionBVH(box_lo=lo, box_hi=hi, nodes=build_bvh_over_boxes(lo, hi))
+
+
+def sample_points(sampler, points, device=None):
+    """Batched point query on the GPU: (found u8->bool, value f64, tet id i64)."""
+    torch = _torch()
+    device = resolve_device(device)
+    holder = sampler._device if hasattr(sampler, "_device") else {}
+    dev = holder.get(str(device))
+    if dev is None:
+        dev = DeviceScene(_SamplerScene(sampler), device)
+        if hasattr(sampler, "_device"):
+            sampler._device[str(device)] = dev
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    n = len(pts)
+    with torch.cuda.device(device):
+        stream = torch.cuda.current_stream(device)
+        p_d = torch.from_numpy(pts).to(device, non_blocking=False)
+        found = torch.empty(n, dtype=torch.uint8, device=device)
+        vals = torch.empty(n, dtype=torch.float64, device=device)
+        tet = torch.empty(n, dtype=torch.int64, device=device)
+        _lib.check(_lib.lib().tr_field_at_many(C.byref(dev.desc), n, C.c_void_p(p_d.data_ptr()),
+                                               C.c_void_p(found.data_ptr()),
+                                               C.c_void_p(vals.data_ptr()),
+                                               C.c_void_p(tet.data_ptr()),
+                                               C.c_void_p(stream.cuda_stream)), "tr_field_at_many")
+        out = (found.cpu().numpy().astype(bool), vals.cpu().numpy(), tet.cpu().numpy())
+    return out
