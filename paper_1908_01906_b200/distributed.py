@@ -1,0 +1,193 @@
+"""Multi-GPU frame rendering: one process per GPU, the scene
+replicated in every GPU's HBM, the frame's 8x4 pixel tiles interleaved over
+the ranks (tile t -> rank t % world, slot t // world), so long and short rays
+spread evenly.  The merge is exactly the frame's data dependencies:
+
+  * disjoint pixel tiles   -> NCCL all-gather of each rank's compact slots,
+                              then tr_scatter_tiles into image layout
+  * mergeable aggregates   -> NCCL all-reduce (int64 sum) of
+                              [total samples, visited sum, per-partition samples]
+
+Integer sums are order independent and tiles are disjoint, so an N-GPU frame
+is bit-identical to the 1-GPU frame (tests/test_distributed.py checks the
+host-side logic with gloo on CPU; tests/test_parity_gpu.py the kernels).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+
+import numpy as np
+
+from . import _lib
+
+TILE_W, TILE_H = 8, 4
+TILE_PIXELS = TILE_W * TILE_H
+
+
+def num_tiles(width: int, height: int) -> int:
+    return ((width + TILE_W - 1) // TILE_W) * ((height + TILE_H - 1) // TILE_H)
+
+
+def slots_per_rank(width: int, height: int, world: int) -> int:
+    return (num_tiles(width, height) + world - 1) // world
+
+
+def tile_owner(tile: int, world: int) -> tuple[int, int]:
+    """(rank, slot) of a tile under the interleaved assignment."""
+    return tile % world, tile // world
+
+
+def tile_pixels(tile: int, width: int):
+    """(ix, iy) of the 32 lanes of a tile (lane = 8*row + col)."""
+    tiles_x = (width + TILE_W - 1) // TILE_W
+    lane = np.arange(TILE_PIXELS)
+    ix = (tile % tiles_x) * TILE_W + lane % TILE_W
+    iy = (tile // tiles_x) * TILE_H + lane // TILE_W
+    return ix, iy
+
+
+def scatter_tiles_host(width, height, world, slots, rgba_all, samples_all, visited_all):
+    """numpy statement of tr_scatter_tiles (used by the CPU/gloo tests to
+    check the merge plumbing; the product calls the CUDA kernel)."""
+    rgba = np.zeros((height * width, 4))
+    samples = np.zeros(height * width, np.int64)
+    visited = np.zeros(height * width, np.int32)
+    n = num_tiles(width, height)
+    for r in range(world):
+        for s in range(slots):
+            t = r + world * s
+            if t >= n:
+                continue
+            ix, iy = tile_pixels(t, width)
+            ok = (ix < width) & (iy < height)
+            src = (r * slots + s) * TILE_PIXELS + np.arange(TILE_PIXELS)
+            dst = iy * width + ix
+            rgba[dst[ok]] = rgba_all[src[ok]]
+            samples[dst[ok]] = samples_all[src[ok]]
+            visited[dst[ok]] = visited_all[src[ok]]
+    return rgba.reshape(height, width, 4), samples.reshape(height, width), \
+        visited.reshape(height, width)
+
+
+def merge_partials(rank_rgba, rank_samples, rank_visited, rank_counters, world, width, height,
+                   all_gather, all_reduce, scatter):
+    """The collective part of a sharded frame, with the transport injected
+    (torch.distributed NCCL on GPU, gloo in the CPU tests).  Returns the
+    image-layout rgba/samples/visited and the summed counters."""
+    g_rgba = all_gather(rank_rgba)
+    g_samples = all_gather(rank_samples)
+    g_visited = all_gather(rank_visited)
+    counters = all_reduce(rank_counters)
+    slots = slots_per_rank(width, height, world)
+    return (*scatter(width, height, world, slots, g_rgba, g_samples, g_visited), counters)
+
+
+class ShardedFrame:
+    """One frame's launch plan on one rank: epoch, frame descriptor, buffers
+    and (world > 1) the NCCL merge.  world == 1 renders straight into the
+    image layout with no collective."""
+
+    def __init__(self, dscene, scene, camera, mode_id: int, params, *, track: bool, rank: int = 0,
+                 world: int = 1, flags: int = 0, jitter: bool = False):
+        import torch
+        self.torch = torch
+        self.dscene = dscene
+        self.scene, self.camera, self.params = scene, camera, params
+        self.world, self.rank = world, rank
+        self.w, self.h = int(camera.width), int(camera.height)
+        self.compact = world > 1
+        self.slots = slots_per_rank(self.w, self.h, world) if self.compact else 0
+        self.epoch = dscene.epoch(scene.meta_state(), params)
+        self.frame = dscene.frame_desc(scene, camera, mode_id, params, jitter, track, flags,
+                                       shard_rank=rank, shard_count=world, compact=self.compact)
+        self.fb = dscene.frame_buffers(self.w, self.h, compact_slots=self.slots)
+        dev = dscene.device
+        if self.compact:
+            n = world * self.slots * TILE_PIXELS
+            self.g_rgba = torch.empty((n, 4), dtype=torch.float64, device=dev)
+            self.g_samples = torch.empty(n, dtype=torch.int64, device=dev)
+            self.g_visited = torch.empty(n, dtype=torch.int32, device=dev)
+            self.rgba = torch.empty((self.h * self.w, 4), dtype=torch.float64, device=dev)
+            self.samples = torch.empty(self.h * self.w, dtype=torch.int64, device=dev)
+            self.visited = torch.empty(self.h * self.w, dtype=torch.int32, device=dev)
+            self.local = torch.empty(2, dtype=torch.int64, device=dev)
+        else:
+            self.rgba, self.samples, self.visited = self.fb.rgba, self.fb.samples, self.fb.visited
+            self.local = None
+
+    def launches_per_step(self) -> int:
+        return 2 if self.compact else 1
+
+    def run(self, stream, kernel_events=None):
+        fb = self.fb
+        fb.counters.zero_()
+        if kernel_events is not None:
+            kernel_events[0].record(stream)
+        _lib.check(_lib.lib().tr_render_frame(C.byref(self.dscene.desc), C.byref(self.epoch.desc),
+                                              C.byref(self.frame), C.byref(fb.outputs()),
+                                              C.c_void_p(stream.cuda_stream)), "tr_render_frame")
+        if kernel_events is not None:
+            kernel_events[1].record(stream)
+        if self.compact:
+            import torch.distributed as dist
+            self.local.copy_(fb.counters[:2])
+            dist.all_gather_into_tensor(self.g_rgba, fb.rgba)
+            dist.all_gather_into_tensor(self.g_samples, fb.samples)
+            dist.all_gather_into_tensor(self.g_visited, fb.visited)
+            dist.all_reduce(fb.counters)
+            _lib.check(_lib.lib().tr_scatter_tiles(
+                self.w, self.h, self.world, C.c_void_p(self.g_rgba.data_ptr()),
+                C.c_void_p(self.g_samples.data_ptr()), C.c_void_p(self.g_visited.data_ptr()),
+                self.slots, C.c_void_p(self.rgba.data_ptr()), C.c_void_p(self.samples.data_ptr()),
+                C.c_void_p(self.visited.data_ptr()), C.c_void_p(stream.cuda_stream)),
+                "tr_scatter_tiles")
+
+    def total_samples(self) -> int:
+        return int(self.fb.counters[0].item())
+
+    def local_samples(self) -> int:
+        if self.compact:
+            return int(self.local[0].item())
+        return int(self.fb.counters[0].item())
+
+    def local_pixels(self) -> int:
+        if not self.compact:
+            return self.w * self.h
+        n = num_tiles(self.w, self.h)
+        mine = len(range(self.rank, n, self.world))
+        return min(mine * TILE_PIXELS, self.w * self.h)
+
+    def host_outputs(self):
+        """(rgba (H,W,4), samples (H,W), counters) on the host."""
+        return (self.rgba.view(self.h, self.w, 4).cpu().numpy(),
+                self.samples.view(self.h, self.w).cpu().numpy(),
+                self.fb.counters.cpu().numpy())
+
+
+def bench_e2e_sharded(runner: ShardedFrame, steps: int, rank: int, world: int) -> dict:
+    """End-to-end sharded frames: epoch re-upload (H2D) each step, image
+    read back (D2H) on rank 0; wall clock, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    dev = runner.dscene.device
+    stream = torch.cuda.current_stream(dev)
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        runner.dscene._epochs.clear()
+        runner.epoch = runner.dscene.epoch(runner.scene.meta_state(), runner.params)
+        runner.run(stream)
+        if rank == 0:
+            rgba = runner.rgba.cpu()
+            samples = runner.samples.cpu()
+        else:
+            torch.cuda.synchronize(dev)
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+    total = runner.total_samples()
+    d2h = (runner.w * runner.h * 40 + 8 * runner.fb.counters.numel()) if rank == 0 else 0
+    return {"value": total * steps / float(dt[0]), "unit": "samples/s",
+            "h2d_bytes_per_step": int(runner.epoch.h2d_bytes), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": float(dt[0]) * 1000.0 / steps}

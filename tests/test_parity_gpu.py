@@ -1,0 +1,167 @@
+"""GPU parity: the sm_100a render path against the oracle and the reference's
+own fixtures, through the public render() API (C ABI underneath).
+
+Bar: samples / visited / per-partition counts bit-exact in
+every mode; rgba bit-exact in reference and skip modes.  skip-adaptive
+computes (1-a)^(s/s1) with CUDA's pow instead of glibc's, so rgba there is
+held to RGBA_RTOL and sample counts may differ only where a one-ulp change
+flips `acc_a >= term` (counted and bounded below).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import cases as C
+
+pytestmark = pytest.mark.gpu
+
+RGBA_RTOL = 1e-12     # skip-adaptive colour tolerance (pow is not glibc's)
+MAX_FLIP_PIXELS = 2   # pixels whose sample count may differ in skip-adaptive
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def B(built_lib):
+    import paper_1908_01906_b200 as B
+    return B
+
+
+_SCENES = {}
+
+
+def scene_of(B, recipe):
+    if recipe not in _SCENES:
+        from oracle.oracle import OracleScene
+        sc = C.build_scene(B, recipe)
+        _SCENES[recipe] = (sc, OracleScene(sc))
+    return _SCENES[recipe]
+
+
+def _compare(fb, st, ref, mode, golden_rec=None):
+    rgba, samples, visited, ppart = ref
+    exact = mode != "skip-adaptive"
+    n_flip = int((fb.samples != samples).sum())
+    if exact:
+        assert n_flip == 0
+        assert np.array_equal(fb.rgba, rgba), "rgba not bit-identical"
+        if golden_rec is not None:
+            assert sha(fb.rgba) == golden_rec["rgba"]
+            assert sha(fb.samples) == golden_rec["samples"]
+    else:
+        assert n_flip <= MAX_FLIP_PIXELS
+        ok = fb.samples == samples
+        np.testing.assert_allclose(fb.rgba[ok], rgba[ok], rtol=RGBA_RTOL, atol=1e-15)
+    if n_flip == 0:
+        assert st.total_samples == int(samples.sum())
+        assert st.partitions_visited_mean == float(visited.mean())
+        if ppart is None:
+            assert st.per_partition_samples is None
+        else:
+            assert np.array_equal(st.per_partition_samples, ppart)
+    if golden_rec is not None and n_flip == 0:
+        assert st.total_samples == golden_rec["total_samples"]
+        assert st.partitions_visited_mean == golden_rec["partitions_visited_mean"]
+
+
+@pytest.mark.parametrize("cid,recipe,modes,jitter", C.FRAME_CASES, ids=[c[0] for c in C.FRAME_CASES])
+def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitter):
+    sc, orc = scene_of(B, recipe)
+    cam, par = C.camera(B, recipe), C.params(B, recipe)
+    for mode in modes:
+        ref = orc.render(cam, mode, par, jitter=jitter)
+        for flags in (0, 1):  # with and without the exclusive-leaf shortcut
+            fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
+            _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
+
+
+@pytest.mark.parametrize("mode", ["reference", "skip", "skip-adaptive"])
+def test_radial59_benchmark_scene(B, golden, mode):
+    """BASELINE config 2 (1.03M tets, 4,040 active partitions) at 512^2."""
+    sc, orc = scene_of(B, "radial59")
+    cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
+    fb, st = B.render(sc, cam, mode, par)
+    g = golden["frames"][f"radial59/{mode}"]
+    if mode != "skip-adaptive":
+        assert sha(fb.rgba) == g["rgba"]
+        assert sha(fb.samples) == g["samples"]
+        assert st.total_samples == g["total_samples"]
+        assert st.partitions_visited_mean == g["partitions_visited_mean"]
+        if g["ppart"] is not None:
+            assert sha(st.per_partition_samples) == g["ppart"]
+    else:
+        ref = orc.render(cam, mode, par)
+        _compare(fb, st, ref, mode)
+
+
+def test_field_at_many_matches_reference_points(B):
+    fx = np.load(C.GOLDEN / "reference_points.npz")
+    for recipe in ("golden_radial4", "radial16", "voidcell", "sinus"):
+        sc, _ = scene_of(B, recipe)
+        pts = fx[f"{recipe}/pts"]
+        tet, vals = sc.sampler.locate_many(pts)
+        found, vals2 = sc.sampler.sample_many(pts)
+        assert np.array_equal(tet, fx[f"{recipe}/tet"]), recipe
+        assert np.array_equal(found, fx[f"{recipe}/found"]), recipe
+        assert np.array_equal(vals, fx[f"{recipe}/vals"]), recipe
+        assert np.array_equal(vals2, vals)
+
+
+def test_render_is_deterministic_and_reuses_device_scene(B):
+    sc, _ = scene_of(B, "radial16")
+    cam, par = C.camera(B, "radial16", scale=0.25), C.params(B, "radial16")
+    a = B.render(sc, cam, "skip-adaptive", par)
+    b = B.render(sc, cam, "skip-adaptive", par)
+    assert np.array_equal(a[0].rgba, b[0].rgba)
+    assert np.array_equal(a[0].samples, b[0].samples)
+    assert np.array_equal(a[1].per_partition_samples, b[1].per_partition_samples)
+    assert a[1].per_partition_samples.sum() == a[1].total_samples
+    assert getattr(sc, "_b200_device_cache")
+
+
+def test_tf_edit_changes_epoch_not_geometry(B):
+    sc, orc = scene_of(B, "golden_radial4")
+    cam, par = C.camera(B, "golden_radial4"), C.params(B, "golden_radial4")
+    from paper_1908_01906_b200.device import device_scene_for
+    dev = device_scene_for(sc)
+    tf0 = sc.tf
+    try:
+        sc.set_transfer_function(B.TransferFunction.constant([1, 0, 0, 0.0], domain=(0.0, 3.5)))
+        for mode in ("skip", "skip-adaptive"):
+            fb, st = B.render(sc, cam, mode, par)
+            assert st.total_samples == 0
+            assert np.array_equal(fb.rgba, np.broadcast_to(sc.background, fb.rgba.shape))
+        assert device_scene_for(sc) is dev
+    finally:
+        sc.set_transfer_function(tf0)
+    fb, st = B.render(sc, cam, "skip", par)
+    ref = orc.render(cam, "skip", par)
+    assert np.array_equal(fb.rgba, ref[0])
+
+
+def test_render_validation_before_device_work(B):
+    sc, _ = scene_of(B, "golden_radial4")
+    cam, par = C.camera(B, "golden_radial4"), C.params(B, "golden_radial4")
+    with pytest.raises(ValueError):
+        B.render(sc, cam, "turbo", par)
+
+
+def test_reference_scene_object_is_accepted(B):
+    """render() duck-types: a scene assembled from reference-named attributes
+    (no package Scene class) renders identically."""
+    sc, orc = scene_of(B, "conftest48")
+
+    class Foreign:
+        pass
+
+    f = Foreign()
+    for k in ("mesh", "sampler", "partitions", "bvh", "tf", "traversal_config", "background"):
+        setattr(f, k, getattr(sc, k))
+    f.meta_state = sc.meta_state
+    cam, par = C.camera(B, "conftest48"), C.params(B, "conftest48")
+    fb, _ = B.render(f, cam, "skip", par)
+    assert np.array_equal(fb.rgba, orc.render(cam, "skip", par)[0])
