@@ -179,7 +179,7 @@ typedef struct TrFrame {
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)
  * i64, visited (H,W) i32.  Compact layout: slot-major 8x4 pixel tiles.
  * ppart (P,) u64 and totals[2] = {sum samples, sum visited} are ACCUMULATED
- * (zero them first); work[1] is scratch, zeroed by the call. */
+ * (zero them first); work[1] is a queue counter, zeroed by the call. */
 typedef struct TrOutputs {
     double *rgba;
     int64_t *samples;
@@ -187,7 +187,12 @@ typedef struct TrOutputs {
     uint64_t *ppart;
     uint64_t *totals;
     uint32_t *work;
+    void *scratch;          /* interval lists (modes 1, 2); size via tr_scratch_bytes */
+    int64_t scratch_bytes;  /* smaller than a frame's need => the frame runs in ray chunks */
 } TrOutputs;
+
+/* Scratch bytes for n_rays rays in one chunk (pass W*H rounded up to 32). */
+int64_t tr_scratch_bytes(int64_t n_rays);
 
 /* Replaces _kernels.render_frame (K:312-398). stream: cudaStream_t. */
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,

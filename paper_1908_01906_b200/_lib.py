@@ -58,6 +58,7 @@ class TrOutputs(C.Structure):
     _fields_ = [
         ("rgba", C.c_void_p), ("samples", C.c_void_p), ("visited", C.c_void_p),
         ("ppart", C.c_void_p), ("totals", C.c_void_p), ("work", C.c_void_p),
+        ("scratch", C.c_void_p), ("scratch_bytes", C.c_int64),
     ]
 
 
@@ -101,6 +102,7 @@ _SIGNATURES = [
                                    C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                    C.c_void_p]),
     ("tr_num_tiles", C.c_int64, [C.c_int64, C.c_int64]),
+    ("tr_scratch_bytes", C.c_int64, [C.c_int64]),
     ("tr_slots_per_rank", C.c_int64, [C.c_int64, C.c_int64, C.c_int32]),
     ("tr_last_launch", C.c_int, [c_i64p]),
     ("tr_last_error", C.c_char_p, []),

@@ -10,17 +10,22 @@
 // are IEEE round-to-nearest.  Results are therefore bit-identical to the
 // numba reference, except glibc pow in skip-adaptive mode.
 //
-// Structure:
-//   * persistent CTAs; each warp pulls 8x4 pixel tiles from an atomic queue
-//     (ray lengths vary 0..~300 samples, so static grids load-imbalance)
-//   * partition traversal: exact next_interval over a BVH2 with f64 child
-//     boxes, subtree-activity bits per metadata epoch prune transparent space
-//   * point location: per-ray "exclusive leaf" shortcut -- a point strictly
-//     inside the current leaf's exclusive box can only be in that leaf's tets,
-//     which are scanned in ascending id order (first hit = lowest index, the
-//     reference's tie rule K:119); otherwise a full min-id-pruned BVH descent
-//   * per-partition sample histogram privatised per CTA in shared memory,
-//     merged with 64-bit integer atomics (exact, order independent)
+// A frame is two kernels per ray chunk:
+//   trace_intervals_kernel  one thread per ray, 8x4 pixel tiles per warp: the
+//       exact front-to-back partition-interval sequence (K:360-391 calling
+//       next_interval K:173-230) over a BVH2 with f64 child boxes, pruned by
+//       per-epoch subtree activity bits; up to IV_CAP intervals per ray go to
+//       a scratch list, longer rays resume next_interval inline later.
+//   march_kernel  persistent CTAs with PER-LANE RAY REFILL: a lane whose ray
+//       finishes immediately takes the next ray from a warp-aggregated atomic
+//       queue, so rays of very different length (0..~300 samples) never idle
+//       a warp.  Each sample locates its tet through the ray's current
+//       "exclusive leaf" (a point strictly inside it can only lie in that
+//       leaf's tets, scanned in ascending id order: first hit = lowest index,
+//       the reference's tie rule K:119) or, failing that, a full
+//       min-id-pruned BVH descent; then TF, opacity correction, compositing.
+//   The per-partition histogram is privatised per CTA in shared memory and
+//   merged with 64-bit integer atomics (exact, order independent).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -37,9 +42,13 @@ constexpr double BARY_TOL = 1e-9;  // K:15
 constexpr int TILE_W = 8, TILE_H = 4;
 constexpr int PSTACK = 64;
 constexpr int BSTACK = 64;
-constexpr int BLOCK = 256;
+constexpr int MARCH_BLOCK = 256;
+constexpr int TRACE_BLOCK = 128;
+constexpr int IV_CAP = 16;           // intervals per ray kept in the scratch list
+constexpr int SAMPLE_BATCH = 4;      // samples per lane per scheduling round
 constexpr int32_t CHILD_NONE = INT32_MIN;
 constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
+constexpr unsigned FULL = 0xffffffffu;
 
 struct RayD {
     double ox, oy, oz, dx, dy, dz;
@@ -47,7 +56,7 @@ struct RayD {
     bool nx, ny, nz;    // d != 0
 };
 
-// K:30-71.  Returns false on a miss of the zero-direction kind ((1, 0)).
+// K:30-71 (a zero-direction miss returns (1, 0)).
 __device__ __forceinline__ void slab(const RayD &r, const double *lo, const double *hi,
                                      double &t0, double &t1) {
     t0 = -INFINITY;
@@ -100,10 +109,10 @@ __device__ __forceinline__ bool strictly_in(const PQuery &q, const float *lo, co
            q.zu < hi[2];
 }
 
-// K:121-128: barycentrics of q in tet t; true if all >= -BARY_TOL.
-__device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, uint32_t t,
+// K:121-128: barycentrics of q in record k; true if all >= -BARY_TOL.
+__device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, uint32_t k,
                                           const PQuery &q, double l[4]) {
-    const double2 *r = reinterpret_cast<const double2 *>(recs + t);
+    const double2 *r = reinterpret_cast<const double2 *>(recs + k);
     const double2 a0 = __ldg(r + 0), a1 = __ldg(r + 1), a2 = __ldg(r + 2);
     const double2 a3 = __ldg(r + 3), a4 = __ldg(r + 4), a5 = __ldg(r + 5);
     const double qx = q.x - a4.y, qy = q.y - a5.x, qz = q.z - a5.y;
@@ -116,7 +125,7 @@ __device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, 
 }
 
 struct SceneK {  // kernel copy of TrDeviceScene
-    const TrTetRecord *__restrict__ tets;
+    const TrTetRecord *__restrict__ tets;   // in LEAF order: record k holds tet pleaf_ids[k]
     const TrPNode *__restrict__ pnodes;
     const TrPLeaf *__restrict__ pleaves;
     const uint32_t *__restrict__ pleaf_ids;
@@ -125,15 +134,34 @@ struct SceneK {  // kernel copy of TrDeviceScene
     double mesh_lo[3], mesh_hi[3];
 };
 
-// Scan one leaf's ids (ascending) for the first tet below `best` containing q.
-__device__ __forceinline__ void scan_leaf(const SceneK &S, uint32_t start, uint32_t count,
-                                          const PQuery &q, uint32_t &best, double l[4]) {
+// Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
+// ascending id order, so the first one containing q is the lowest index.
+// Tested two at a time so both records' loads are in flight together.
+__device__ __forceinline__ uint32_t scan_leaf_first(const SceneK &S, uint32_t start,
+                                                    uint32_t count, const PQuery &q, double l[4]) {
+    const uint32_t end = start + count;
+    for (uint32_t k = start; k < end; k += 2) {
+        double la[4], lb[4];
+        const bool pa = bary_test(S.tets, k, q, la);
+        const bool has_b = k + 1 < end;
+        const bool pb = bary_test(S.tets, has_b ? k + 1 : k, q, lb) && has_b;
+        if (pa) { l[0] = la[0]; l[1] = la[1]; l[2] = la[2]; l[3] = la[3]; return k; }
+        if (pb) { l[0] = lb[0]; l[1] = lb[1]; l[2] = lb[2]; l[3] = lb[3]; return k + 1; }
+    }
+    return UINT32_MAX;
+}
+
+// Full-descent leaf scan: ids ascending; stop at the first id >= best.
+__device__ __forceinline__ void scan_leaf_ids(const SceneK &S, uint32_t start, uint32_t count,
+                                              const PQuery &q, uint32_t &best, uint32_t &best_pos,
+                                              double l[4]) {
     for (uint32_t k = start; k < start + count; ++k) {
         const uint32_t t = __ldg(S.pleaf_ids + k);
         if (t >= best) break;
         double lt[4];
-        if (bary_test(S.tets, t, q, lt)) {
+        if (bary_test(S.tets, k, q, lt)) {
             best = t;
+            best_pos = k;
             l[0] = lt[0]; l[1] = lt[1]; l[2] = lt[2]; l[3] = lt[3];
             break;
         }
@@ -141,10 +169,10 @@ __device__ __forceinline__ void scan_leaf(const SceneK &S, uint32_t start, uint3
 }
 
 // Full descent: lowest-index tet containing q (K:93-136 semantics), pruning
-// subtrees whose minimum id cannot beat the best so far.  Returns the tet id
-// (UINT32_MAX if none) and the leaf it was found in.
+// subtrees whose minimum id cannot beat the best so far.  Returns the record
+// position (UINT32_MAX if none) and the leaf it was found in.
 __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], int32_t &leaf_out) {
-    uint32_t best = UINT32_MAX;
+    uint32_t best = UINT32_MAX, best_pos = UINT32_MAX;
     int32_t best_leaf = -1;
     int32_t st_node[PSTACK];
     uint32_t st_min[PSTACK];
@@ -157,23 +185,23 @@ __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], i
         const int32_t c0 = D.x, c1 = D.y;
         const uint32_t m0 = (uint32_t)D.z, m1 = (uint32_t)D.w;
         bool h0 = m0 < best && in_box(q, A.x, A.y, A.z, A.w, B.x, B.y);
-        bool h1 = m1 < best && in_box(q, B.z, B.w, C.x, C.y, C.z, C.w);
+        bool h1 = c1 != CHILD_NONE && m1 < best && in_box(q, B.z, B.w, C.x, C.y, C.z, C.w);
         if (h0 && c0 < 0) {
             const uint32_t before = best;
             const TrPLeaf *lf = S.pleaves + (~c0);
-            scan_leaf(S, __ldg(&lf->start), __ldg(&lf->count), q, best, l);
+            scan_leaf_ids(S, __ldg(&lf->start), __ldg(&lf->count), q, best, best_pos, l);
             if (best != before) best_leaf = ~c0;
             h0 = false;
         }
-        if (h1 && c1 < 0 && c1 != CHILD_NONE) {
+        if (h1 && c1 < 0) {
             const uint32_t before = best;
             const TrPLeaf *lf = S.pleaves + (~c1);
-            scan_leaf(S, __ldg(&lf->start), __ldg(&lf->count), q, best, l);
+            scan_leaf_ids(S, __ldg(&lf->start), __ldg(&lf->count), q, best, best_pos, l);
             if (best != before) best_leaf = ~c1;
             h1 = false;
         }
         h0 = h0 && m0 < best;
-        h1 = h1 && c1 != CHILD_NONE && m1 < best;
+        h1 = h1 && m1 < best;
         if (h0 && h1) {
             // descend into the lower-min-id child first, defer the other
             if (m0 <= m1) { node = c0; st_node[sp] = c1; st_min[sp] = m1; }
@@ -191,10 +219,10 @@ __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], i
         if (!found) break;
     }
     leaf_out = best_leaf;
-    return best;
+    return best_pos;
 }
 
-struct LeafHint {  // the ray's current leaf: exclusive box + id range, in registers
+struct LeafHint {  // the ray's current leaf: exclusive box + record range, in registers
     float lo[3], hi[3];
     uint32_t start, count;
     bool valid;
@@ -210,28 +238,27 @@ __device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHin
     h.valid = true;
 }
 
-// K:139-154.  `hint` carries the exclusive-leaf shortcut between samples of a ray.
-__device__ __forceinline__ bool field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
-                                         bool use_hint, double &v, uint32_t &tet) {
+// K:139-154.  Returns the record position (UINT32_MAX: outside every tet).
+__device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
+                                             bool use_hint, double &v) {
     double l[4];
-    uint32_t t = UINT32_MAX;
+    uint32_t pos;
     if (use_hint && hint.valid && strictly_in(q, hint.lo, hint.hi)) {
-        scan_leaf(S, hint.start, hint.count, q, t, l);
+        pos = scan_leaf_first(S, hint.start, hint.count, q, l);
     } else {
         int32_t leaf;
-        t = locate_full(S, q, l, leaf);
+        pos = locate_full(S, q, l, leaf);
         if (use_hint && leaf >= 0) load_hint(S, leaf, hint);
     }
-    tet = t;
-    if (t == UINT32_MAX) { v = 0.0; return false; }
-    const double2 *r = reinterpret_cast<const double2 *>(S.tets + t);
+    if (pos == UINT32_MAX) { v = 0.0; return pos; }
+    const double2 *r = reinterpret_cast<const double2 *>(S.tets + pos);
     if (S.centering == 0) {
         const double2 f01 = __ldg(r + 6), f23 = __ldg(r + 7);
         v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
     } else {
         v = __ldg(r + 6).x;
     }
-    return true;
+    return pos;
 }
 
 // K:74-90
@@ -239,19 +266,15 @@ __device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t 
                                           double hi, double v, double c[4]) {
     const double u = (v - lo) / (hi - lo) * (double)(n - 1);
     const double2 *t2 = reinterpret_cast<const double2 *>(T);
-    if (u <= 0.0) {
-        const double2 x = __ldg(t2), y = __ldg(t2 + 1);
-        c[0] = x.x; c[1] = x.y; c[2] = y.x; c[3] = y.y;
-        return;
-    }
-    if (u >= (double)(n - 1)) {
-        const double2 x = __ldg(t2 + 2 * (n - 1)), y = __ldg(t2 + 2 * (n - 1) + 1);
-        c[0] = x.x; c[1] = x.y; c[2] = y.x; c[3] = y.y;
-        return;
-    }
-    const int64_t j = (int64_t)floor(u);
-    const double f = u - (double)j;
+    int64_t j;
+    double f;
+    bool interp = true;
+    if (u <= 0.0) { j = 0; interp = false; }
+    else if (u >= (double)(n - 1)) { j = n - 1; interp = false; }
+    else { j = (int64_t)floor(u); }
     const double2 a0 = __ldg(t2 + 2 * j), a1 = __ldg(t2 + 2 * j + 1);
+    if (!interp) { c[0] = a0.x; c[1] = a0.y; c[2] = a1.x; c[3] = a1.y; return; }
+    f = u - (double)j;
     const double2 b0 = __ldg(t2 + 2 * j + 2), b1 = __ldg(t2 + 2 * j + 3);
     c[0] = a0.x + f * (b0.x - a0.x);
     c[1] = a0.y + f * (b0.y - a0.y);
@@ -271,37 +294,6 @@ struct EpochK {
 struct Acc {
     double r, g, b, a;
 };
-
-// K:262-297.  Returns samples taken; sets `terminated`.
-__device__ int64_t march_range(const SceneK &S, const EpochK &E, const RayD &ray, double t0,
-                               double t1, double step, double s1, double term, double phase,
-                               LeafHint &hint, bool use_hint, Acc &acc, bool &terminated) {
-    const double e = step / s1;  // opacity_correction's exponent (K:27)
-    const bool unit = (e == 1.0);
-    int64_t samples = 0;
-    terminated = false;
-    for (int64_t k = 0;; ++k) {
-        const double t = t0 + ((double)k + phase) * step;
-        if (k > 0 && t >= t1) break;
-        samples += 1;
-        const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy, ray.oz + t * ray.dz);
-        double v;
-        uint32_t tet;
-        if (field_at(S, q, hint, use_hint, v, tet)) {
-            double c[4];
-            tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
-            const double x = 1.0 - c[3];
-            const double ca = 1.0 - (unit ? x : pow(x, e));  // glibc pow(x, 1) == x
-            const double w = (1.0 - acc.a) * ca;
-            acc.r += w * c[0];
-            acc.g += w * c[1];
-            acc.b += w * c[2];
-            acc.a += w;
-            if (acc.a >= term) { terminated = true; break; }
-        }
-    }
-    return samples;
-}
 
 // K:173-230: first active partition interval, lexicographic min (clamped
 // t_enter, pid) among partitions with t_exit > t_min + excl_eps.
@@ -383,121 +375,284 @@ __device__ __forceinline__ double hash01(int64_t ix, int64_t iy) {
     return __ull2double_rn(h) / 4294967296.0;
 }
 
+
 struct FrameK {
     TrFrame f;
     int64_t tiles_x, n_tiles, my_tiles;
+    int64_t ray_begin, n_rays;   // this chunk: rays [ray_begin, ray_begin + n_rays) in tile order
     int32_t n_parts;
     int32_t hist_smem;
 };
 
-__global__ void __launch_bounds__(BLOCK, 2)
-render_frame_kernel(SceneK S, EpochK E, FrameK F, TrOutputs O) {
+struct IvBuf {                   // per-chunk scratch interval lists, interval-major
+    int32_t *pid;                // [IV_CAP][n_rays]
+    double *a, *b;               // [IV_CAP][n_rays]
+    uint32_t *cnt;               // [n_rays]: count | 0x80000000 if the ray has more
+};
+
+struct Pixel {
+    int64_t ix, iy, out;
+    bool valid;
+};
+
+// chunk-local ray index -> pixel (8x4 tiles, tile t of rank r is slot t/count)
+__device__ __forceinline__ Pixel ray_pixel(const FrameK &F, int64_t rr) {
+    const TrFrame &fr = F.f;
+    const int64_t g = F.ray_begin + rr;
+    const int64_t j = g >> 5;
+    const int lane = (int)(g & 31);
+    const int64_t tile = (int64_t)fr.shard_rank + (int64_t)fr.shard_count * j;
+    Pixel p;
+    p.ix = (tile % F.tiles_x) * TILE_W + (lane % TILE_W);
+    p.iy = (tile / F.tiles_x) * TILE_H + (lane / TILE_W);
+    p.valid = j < F.my_tiles && p.ix < fr.width && p.iy < fr.height;
+    p.out = fr.compact ? g : p.iy * fr.width + p.ix;
+    return p;
+}
+
+// K:330-339 (left-to-right evaluation, no contraction)
+__device__ __forceinline__ RayD make_ray(const TrFrame &fr, int64_t ix, int64_t iy) {
+    const double sx = (((double)ix + 0.5) / (double)fr.width) * 2.0 - 1.0;
+    const double sy = 1.0 - (((double)iy + 0.5) / (double)fr.height) * 2.0;
+    double dx = fr.cam_fwd[0] + sx * fr.aspect * fr.tan_half * fr.cam_right[0] + sy * fr.tan_half * fr.cam_up[0];
+    double dy = fr.cam_fwd[1] + sx * fr.aspect * fr.tan_half * fr.cam_right[1] + sy * fr.tan_half * fr.cam_up[1];
+    double dz = fr.cam_fwd[2] + sx * fr.aspect * fr.tan_half * fr.cam_right[2] + sy * fr.tan_half * fr.cam_up[2];
+    const double dn = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
+    dx *= dn; dy *= dn; dz *= dn;
+    RayD ray;
+    ray.ox = fr.cam_pos[0]; ray.oy = fr.cam_pos[1]; ray.oz = fr.cam_pos[2];
+    ray.dx = dx; ray.dy = dy; ray.dz = dz;
+    ray.nx = dx != 0.0; ray.ny = dy != 0.0; ray.nz = dz != 0.0;
+    ray.ix = ray.nx ? 1.0 / dx : 0.0;
+    ray.iy = ray.ny ? 1.0 / dy : 0.0;
+    ray.iz = ray.nz ? 1.0 / dz : 0.0;
+    return ray;
+}
+
+// Phase 1: the exact interval sequence of every ray of the chunk (K:360-391
+// minus the marching).  Intervals past an early termination are computed but
+// never consumed, so counts and `visited` still follow the reference.
+__global__ void __launch_bounds__(TRACE_BLOCK)
+trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
+    const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
+    if (rr >= F.n_rays) return;
+    const Pixel px = ray_pixel(F, rr);
+    uint32_t n = 0;
+    if (px.valid) {
+        const RayD ray = make_ray(F.f, px.ix, px.iy);
+        double t_min = 0.0;
+        int32_t last = -1;
+        while (true) {
+            const double excl = (last < 0) ? 0.0 : F.f.eps;
+            double a, b;
+            const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
+            if (pid < 0) break;
+            if (n == IV_CAP) { n |= 0x80000000u; break; }  // resume inline in the march
+            iv.pid[(int64_t)n * F.n_rays + rr] = pid;
+            iv.a[(int64_t)n * F.n_rays + rr] = a;
+            iv.b[(int64_t)n * F.n_rays + rr] = b;
+            ++n;
+            t_min = b - F.f.eps;
+            last = pid;
+        }
+    }
+    iv.cnt[rr] = n;
+}
+
+enum : int { ST_IDLE = 0, ST_NEED = 1, ST_MARCH = 2 };
+
+// Phase 2: front-to-back compositing with per-lane ray refill.
+__global__ void __launch_bounds__(MARCH_BLOCK, 2)
+march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     extern __shared__ unsigned long long hist[];  // [n_parts] when F.hist_smem
-    __shared__ unsigned long long red[2][BLOCK / 32];
+    __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool track = fr.track_ppart && fr.mode != 0;
     if (track && F.hist_smem)
-        for (int i = threadIdx.x; i < F.n_parts; i += BLOCK) hist[i] = 0ull;
+        for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK) hist[i] = 0ull;
     __syncthreads();
     const bool use_hint = !(fr.flags & TR_FLAG_NO_LEAF_HINT);
+    const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long my_samples = 0, my_visited = 0;
 
+    int state = ST_IDLE;
+    bool exhausted = false;
+    int64_t rr = 0, out = 0;
+    RayD ray;
+    double phase = 0.5;
+    Acc acc = {0.0, 0.0, 0.0, 0.0};
+    int64_t samples = 0;
+    int32_t visited = 0;
+    double t_min = 0.0;
+    int32_t last = -1;
+    uint32_t iv_i = 0, iv_n = 0;
+    bool iv_more = false;
+    int32_t pid = -1;
+    double t0 = 0.0, t1 = 0.0, step = 0.0, e = 1.0;
+    bool unit = true;
+    int64_t k = 0, ns = 0;
+    LeafHint hint;
+    hint.valid = false;
+    bool has_ray = false;  // a started ray whose pixel is not written yet
+
     while (true) {
-        int64_t j = 0;
-        if (lane == 0) j = (int64_t)atomicAdd(O.work, 1u);
-        j = __shfl_sync(0xffffffffu, j, 0);
-        if (j >= F.my_tiles) break;
-        const int64_t tile = (int64_t)fr.shard_rank + (int64_t)fr.shard_count * j;
-        const int64_t ix = (tile % F.tiles_x) * TILE_W + (lane % TILE_W);
-        const int64_t iy = (tile / F.tiles_x) * TILE_H + (lane / TILE_W);
-        if (ix >= fr.width || iy >= fr.height) continue;
-
-        // ---- ray generation, K:330-340 (left-to-right, no contraction)
-        const double sx = (((double)ix + 0.5) / (double)fr.width) * 2.0 - 1.0;
-        const double sy = 1.0 - (((double)iy + 0.5) / (double)fr.height) * 2.0;
-        double dx = fr.cam_fwd[0] + sx * fr.aspect * fr.tan_half * fr.cam_right[0] + sy * fr.tan_half * fr.cam_up[0];
-        double dy = fr.cam_fwd[1] + sx * fr.aspect * fr.tan_half * fr.cam_right[1] + sy * fr.tan_half * fr.cam_up[1];
-        double dz = fr.cam_fwd[2] + sx * fr.aspect * fr.tan_half * fr.cam_right[2] + sy * fr.tan_half * fr.cam_up[2];
-        const double dn = 1.0 / sqrt(dx * dx + dy * dy + dz * dz);
-        dx *= dn; dy *= dn; dz *= dn;
-        RayD ray;
-        ray.ox = fr.cam_pos[0]; ray.oy = fr.cam_pos[1]; ray.oz = fr.cam_pos[2];
-        ray.dx = dx; ray.dy = dy; ray.dz = dz;
-        ray.nx = dx != 0.0; ray.ny = dy != 0.0; ray.nz = dz != 0.0;
-        ray.ix = ray.nx ? 1.0 / dx : 0.0;
-        ray.iy = ray.ny ? 1.0 / dy : 0.0;
-        ray.iz = ray.nz ? 1.0 / dz : 0.0;
-        const double phase = fr.jitter ? hash01(ix, iy) : 0.5;
-
-        Acc acc = {0.0, 0.0, 0.0, 0.0};
-        int64_t samples = 0;
-        int32_t visited = 0;
-        LeafHint hint;
-        hint.valid = false;
-        bool terminated;
-        if (fr.mode == 0) {  // K:346-359
-            double a, b;
-            slab(ray, S.mesh_lo, S.mesh_hi, a, b);
-            const double t0 = (a > 0.0) ? a : 0.0;
-            if (a <= b && b - t0 >= fr.eps)
-                samples = march_range(S, E, ray, t0, b, fr.s1, fr.s1, fr.term, phase, hint, use_hint,
-                                      acc, terminated);
-        } else {  // K:360-391
-            double t_min = 0.0;
-            int32_t last = -1;
-            while (true) {
-                const double excl = (last < 0) ? 0.0 : fr.eps;
-                double a, b;
-                const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
-                if (pid < 0) break;
-                visited += 1;
-                terminated = false;
-                if (b - a >= fr.eps) {
-                    const double s = (fr.mode == 2) ? __ldg(E.step + pid) : fr.s1;
-                    const int64_t ns = march_range(S, E, ray, a, b, s, fr.s1, fr.term, phase, hint,
-                                                   use_hint, acc, terminated);
-                    samples += ns;
-                    if (track && ns) {
-                        if (F.hist_smem) atomicAdd(&hist[pid], (unsigned long long)ns);
-                        else atomicAdd((unsigned long long *)O.ppart + pid, (unsigned long long)ns);
+        // ---- refill idle lanes from the chunk's ray queue
+        const bool want = state == ST_IDLE && !exhausted;
+        const unsigned m = __ballot_sync(FULL, want);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(O.work, (unsigned)__popc(m));
+            base = __shfl_sync(FULL, base, leader);
+            if (want) {
+                rr = (int64_t)base + __popc(m & lt_mask);
+                if (rr >= F.n_rays) {
+                    exhausted = true;
+                } else {
+                    const Pixel px = ray_pixel(F, rr);
+                    if (px.valid) {
+                        has_ray = true;
+                        out = px.out;
+                        ray = make_ray(fr, px.ix, px.iy);
+                        phase = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
+                        acc.r = acc.g = acc.b = acc.a = 0.0;
+                        samples = 0;
+                        visited = 0;
+                        hint.valid = false;
+                        if (fr.mode == 0) {  // K:346-353: one interval, the mesh box
+                            double a, b;
+                            slab(ray, S.mesh_lo, S.mesh_hi, a, b);
+                            const double ta = (a > 0.0) ? a : 0.0;
+                            if (a <= b && b - ta >= fr.eps) {
+                                pid = -1; t0 = ta; t1 = b; step = fr.s1; e = fr.s1 / fr.s1;
+                                unit = e == 1.0; k = 0; ns = 0;
+                                state = ST_MARCH;
+                            } else {
+                                state = ST_NEED;  // finishes below with no interval
+                                iv_n = 0; iv_i = 0; iv_more = false;
+                            }
+                        } else {
+                            t_min = 0.0;
+                            last = -1;
+                            const uint32_t c = iv.cnt[rr];
+                            iv_n = c & 0x7fffffffu;
+                            iv_more = (c >> 31) != 0;
+                            iv_i = 0;
+                            state = ST_NEED;
+                        }
                     }
                 }
-                if (terminated) break;
-                t_min = b - fr.eps;
-                last = pid;
             }
         }
-        // K:393-398
-        const double r = acc.r + (1.0 - acc.a) * fr.bg[0];
-        const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
-        const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
-        const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
-        const int64_t o = fr.compact ? j * (TILE_W * TILE_H) + lane : iy * fr.width + ix;
-        double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * o);
-        px[0] = make_double2(r, g);
-        px[1] = make_double2(bl, al);
-        O.samples[o] = samples;
-        O.visited[o] = visited;
-        my_samples += (unsigned long long)samples;
-        my_visited += (unsigned long long)visited;
+        if (__all_sync(FULL, exhausted)) break;
+
+        // ---- next interval (K:363-378): from the list, or inline past its end
+        if (state == ST_NEED) {
+            while (true) {
+                int32_t p = -1;
+                double a = 0.0, b = 0.0;
+                if (iv_i < iv_n) {
+                    const int64_t o = (int64_t)iv_i * F.n_rays + rr;
+                    p = iv.pid[o];
+                    a = iv.a[o];
+                    b = iv.b[o];
+                    ++iv_i;
+                } else if (iv_more) {
+                    p = next_interval(S, E, ray, t_min, (last < 0) ? 0.0 : fr.eps, last, a, b);
+                }
+                if (p < 0) {
+                    state = ST_IDLE;  // ray done
+                    break;
+                }
+                visited += 1;
+                if (b - a >= fr.eps) {
+                    pid = p; t0 = a; t1 = b;
+                    step = (fr.mode == 2) ? __ldg(E.step + p) : fr.s1;
+                    e = step / fr.s1;
+                    unit = e == 1.0;
+                    k = 0;
+                    ns = 0;
+                    state = ST_MARCH;
+                    break;
+                }
+                t_min = b - fr.eps;  // degenerate interval: visited, not marched
+                last = p;
+            }
+        }
+
+        // ---- up to SAMPLE_BATCH samples of the current interval (K:276-296)
+        bool terminated = false, ended = false;
+        if (state == ST_MARCH) {
+#pragma unroll 1
+            for (int s = 0; s < SAMPLE_BATCH; ++s) {
+                const double t = t0 + ((double)k + phase) * step;
+                if (k > 0 && t >= t1) { ended = true; break; }
+                samples += 1;
+                ns += 1;
+                const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy,
+                                            ray.oz + t * ray.dz);
+                double v;
+                if (field_at(S, q, hint, use_hint, v) != UINT32_MAX) {
+                    double c[4];
+                    tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+                    const double x = 1.0 - c[3];
+                    const double ca = 1.0 - (unit ? x : pow(x, e));  // glibc pow(x, 1) == x
+                    const double w = (1.0 - acc.a) * ca;
+                    acc.r += w * c[0];
+                    acc.g += w * c[1];
+                    acc.b += w * c[2];
+                    acc.a += w;
+                    if (acc.a >= fr.term) { terminated = true; ended = true; ++k; break; }
+                }
+                ++k;
+            }
+        }
+        if (ended) {
+            if (track && ns) {
+                if (F.hist_smem) atomicAdd(&hist[pid], (unsigned long long)ns);
+                else atomicAdd((unsigned long long *)O.ppart + pid, (unsigned long long)ns);
+            }
+            if (terminated || fr.mode == 0) {
+                state = ST_IDLE;
+            } else {
+                t_min = t1 - fr.eps;
+                last = pid;
+                state = ST_NEED;
+            }
+        }
+        // ---- a finished ray writes its pixel (K:393-398)
+        if (has_ray && state == ST_IDLE) {
+            has_ray = false;
+            const double r = acc.r + (1.0 - acc.a) * fr.bg[0];
+            const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
+            const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
+            const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
+            double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * out);
+            px[0] = make_double2(r, g);
+            px[1] = make_double2(bl, al);
+            O.samples[out] = samples;
+            O.visited[out] = visited;
+            my_samples += (unsigned long long)samples;
+            my_visited += (unsigned long long)visited;
+        }
     }
     // block reduction of the frame totals (R:198-201) and histogram merge
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
-        my_samples += __shfl_xor_sync(0xffffffffu, my_samples, off);
-        my_visited += __shfl_xor_sync(0xffffffffu, my_visited, off);
+        my_samples += __shfl_xor_sync(FULL, my_samples, off);
+        my_visited += __shfl_xor_sync(FULL, my_visited, off);
     }
     if (lane == 0) { red[0][warp] = my_samples; red[1][warp] = my_visited; }
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long s = 0, v = 0;
-        for (int w = 0; w < BLOCK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
+        for (int w = 0; w < MARCH_BLOCK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
         if (s) atomicAdd((unsigned long long *)O.totals, s);
         if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
     }
     if (track && F.hist_smem)
-        for (int i = threadIdx.x; i < F.n_parts; i += BLOCK)
+        for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK)
             if (hist[i]) atomicAdd((unsigned long long *)O.ppart + i, hist[i]);
 }
 
@@ -509,11 +664,10 @@ __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restri
         LeafHint h;
         h.valid = false;
         double v;
-        uint32_t t;
-        const bool f = field_at(S, q, h, false, v, t);
-        found[i] = f ? 1 : 0;
+        const uint32_t pos = field_at(S, q, h, false, v);
+        found[i] = pos != UINT32_MAX ? 1 : 0;
         vals[i] = v;
-        if (tet) tet[i] = f ? (int64_t)t : -1;
+        if (tet) tet[i] = pos != UINT32_MAX ? (int64_t)__ldg(S.pleaf_ids + pos) : -1;
     }
 }
 
@@ -574,6 +728,8 @@ int sm_count() {
     return n;
 }
 
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * (4 + 8 + 8) + 4;
+
 }  // namespace
 
 extern "C" {
@@ -585,6 +741,10 @@ int64_t tr_num_tiles(int64_t width, int64_t height) {
 int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t count) {
     if (count < 1) return 0;
     return (tr_num_tiles(width, height) + count - 1) / count;
+}
+
+int64_t tr_scratch_bytes(int64_t n_rays) {
+    return n_rays * IV_BYTES_PER_RAY + 1024;
 }
 
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
@@ -622,30 +782,59 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     F.n_parts = (int32_t)scene->n_parts;
     const bool track = frame->track_ppart && frame->mode != 0;
     F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX) ? 1 : 0;
+    const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
+    // ray chunk = what the scratch interval lists can hold
+    int64_t chunk = total_rays;
+    if (frame->mode != 0) {
+        if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + 1024)
+            return tr_fail(TR_EINVAL, "tr_render_frame: scratch buffer too small");
+        chunk = (out->scratch_bytes - 1024) / IV_BYTES_PER_RAY / 32 * 32;
+        if (chunk > total_rays) chunk = total_rays;
+        if (chunk < 32) chunk = 32;
+    }
     const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
     cudaError_t e;
     if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(render_frame_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        e = cudaFuncSetAttribute(march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, render_frame_kernel, BLOCK, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, MARCH_BLOCK, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
-    int64_t warps_needed = F.my_tiles;
-    int64_t grid = (int64_t)sm_count() * per_sm;
-    const int64_t grid_need = (warps_needed + BLOCK / 32 - 1) / (BLOCK / 32);
-    if (grid > grid_need) grid = grid_need;
-    if (grid < 1) grid = 1;
-    e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
-    render_frame_kernel<<<(unsigned)grid, BLOCK, smem, st>>>(S, E, F, *out);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_fail(e, "render_frame_kernel launch");
-    g_last_launch[0] = 1;
-    g_last_launch[1] = grid;
-    g_last_launch[2] = BLOCK;
+    int64_t launches = 0, march_grid = 0;
+    for (int64_t r0 = 0; r0 < total_rays; r0 += chunk) {
+        F.ray_begin = r0;
+        F.n_rays = (total_rays - r0 < chunk) ? total_rays - r0 : chunk;
+        IvBuf iv;
+        char *base = reinterpret_cast<char *>(out->scratch);
+        iv.b = reinterpret_cast<double *>(base);
+        iv.a = iv.b + (int64_t)IV_CAP * F.n_rays;
+        iv.pid = reinterpret_cast<int32_t *>(iv.a + (int64_t)IV_CAP * F.n_rays);
+        iv.cnt = reinterpret_cast<uint32_t *>(iv.pid + (int64_t)IV_CAP * F.n_rays);
+        e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
+        if (frame->mode != 0) {
+            const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
+            trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
+            ++launches;
+        }
+        int64_t grid = (int64_t)sm_count() * per_sm;
+        const int64_t need = (F.n_rays + MARCH_BLOCK - 1) / MARCH_BLOCK;
+        if (grid > need) grid = need;
+        if (grid < 1) grid = 1;
+        march_kernel<<<(unsigned)grid, MARCH_BLOCK, smem, st>>>(S, E, F, iv, *out);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
+        ++launches;
+        march_grid = grid;
+    }
+    g_last_launch[0] = launches;
+    g_last_launch[1] = march_grid;
+    g_last_launch[2] = MARCH_BLOCK;
     return TR_OK;
 }
 

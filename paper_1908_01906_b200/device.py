@@ -1,11 +1,13 @@
 """Device-resident dataset, metadata epochs and frame launches.
 
 Layout in HBM, all owned by torch tensors:
-  tets       TrTetRecord[T]     128 B/tet  (inv 72 B | orig 24 B | field x4 32 B)
+  tets       TrTetRecord[T]     128 B/tet  (inv 72 B | orig 24 B | field x4 32 B),
+                                in point-BVH leaf order
   pnodes     TrPNode[]          64 B BVH2 nodes over padded tet boxes (f32, outward)
   pleaves    TrPLeaf[]          32 B: exclusive box (f32, inward) + id range
   pleaf_ids  uint32[]           ascending per leaf
   bnodes     TrBNode[]          112 B BVH2 nodes over partition boxes (f64)
+  scratch    per-ray interval lists of a ray chunk (IV_CAP x 20 B + 4 B per ray)
   epoch      one buffer per (active, sigma, tf) snapshot and (s1, s2, p):
              step f64[P] | tf f64[n,4] | active u8[P] | node activity u8[M]
 
@@ -124,15 +126,18 @@ class Epoch:
         table = np.ascontiguousarray(tf.table, dtype=np.float64)
         self.n_tf = int(table.shape[0])
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
-        o_tf = 8 * P
-        o_act = o_tf + table.nbytes
-        o_bact = o_act + P
-        nbytes = (o_bact + dev.n_bnodes + 15) // 16 * 16
+        def a64(x):  # 64-B aligned sections (the kernel reads the TF with 16-B loads)
+            return (x + 63) // 64 * 64
+        o_tf = a64(8 * P)
+        o_act = a64(o_tf + table.nbytes)
+        o_bact = a64(o_act + P)
+        nbytes = a64(o_bact + dev.n_bnodes)
         host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
-        hv[:o_tf] = step.view(np.uint8)
-        hv[o_tf:o_act] = table.view(np.uint8).reshape(-1)
-        hv[o_act:o_bact] = act
+        hv[:] = 0
+        hv[:8 * P] = step.view(np.uint8)
+        hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
+        hv[o_act:o_act + P] = act
         hv[o_bact:o_bact + dev.n_bnodes] = bact
         self.h2d_bytes = nbytes
         self.host = host
@@ -157,6 +162,10 @@ class FrameBuffers:
         self.visited = torch.empty(n, dtype=torch.int32, device=d)
         # [totals(2) | work(1) | ppart(P)] zeroed with one fill per frame
         self.counters = torch.empty(3 + dev.n_parts, dtype=torch.int64, device=d)
+        # interval lists of one ray chunk (<= 1M rays; larger frames run in chunks)
+        rays = ((n + 31) // 32) * 32
+        self.scratch_bytes = int(_lib.lib().tr_scratch_bytes(min(rays, 1 << 20)))
+        self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device=d)
         self.start = torch.cuda.Event(enable_timing=True)
         self.end = torch.cuda.Event(enable_timing=True)
 
@@ -164,7 +173,8 @@ class FrameBuffers:
         c = self.counters.data_ptr()
         return _lib.TrOutputs(rgba=self.rgba.data_ptr(), samples=self.samples.data_ptr(),
                               visited=self.visited.data_ptr(), ppart=c + 24, totals=c,
-                              work=c + 16)
+                              work=c + 16, scratch=self.scratch.data_ptr(),
+                              scratch_bytes=self.scratch_bytes)
 
 
 class DeviceScene:
@@ -192,7 +202,9 @@ class DeviceScene:
             self.n_bnodes = int(len(bnodes))
             self.n_tets = int(mesh.n_tets)
             self.pnodes_host, self.pleaves_host = pnodes, pleaves
-            self.t_tets = _upload(rec, device)
+            # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
+            # reads consecutive 128-B lines with no id indirection
+            self.t_tets = _upload(rec[pids], device)
             self.t_pnodes = _upload(pnodes, device)
             self.t_pleaves = _upload(pleaves, device)
             self.t_pids = _upload(pids, device)
