@@ -97,9 +97,13 @@ int tr_kd_copy(const TrHostBuf *kd, int64_t *offsets, int64_t *ids, double *leaf
  * reference's lowest-index result). */
 int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, int32_t leaf_max,
                   TrHostBuf **out);
-/* sizes: [0] = nodes, [1] = leaves, [2] = leaf ids */
-int tr_pbvh_sizes(const TrHostBuf *b, int64_t *sizes3);
+/* sizes: [0] = nodes, [1] = leaves, [2] = leaf ids, [3] = grid cells */
+int tr_pbvh_sizes(const TrHostBuf *b, int64_t *sizes4);
 int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids);
+/* Uniform-grid leaf index: cell (x,y,z) -> leaf whose exclusive box covers
+ * most of it (-1: none).  cell = floor((p - org) * scale), row-major x,y,z. */
+int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
+                 int32_t *cells);
 
 /* Partition BVH (replaces traversal.build_partition_bvh, traversal.py:82-91). */
 int tr_bbvh_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out);
@@ -147,6 +151,10 @@ typedef struct TrDeviceScene {
     const double *part_hi;
     int64_t n_parts, n_bnodes;
     double mesh_lo[3], mesh_hi[3];
+    const int32_t *pgrid;  /* tr_pbvh_grid cells */
+    int32_t gdim[3];
+    int32_t pad1;
+    double gorg[3], gscale[3];
 } TrDeviceScene;
 
 /* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
@@ -174,7 +182,8 @@ typedef struct TrFrame {
     int32_t pad0;
 } TrFrame;
 
-#define TR_FLAG_NO_LEAF_HINT 1 /* disable the exclusive-leaf shortcut (testing) */
+#define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
+#define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)
  * i64, visited (H,W) i32.  Compact layout: slot-major 8x4 pixel tiles.

@@ -29,6 +29,8 @@ class TrDeviceScene(C.Structure):
         ("bnodes", C.c_void_p), ("part_lo", C.c_void_p), ("part_hi", C.c_void_p),
         ("n_parts", C.c_int64), ("n_bnodes", C.c_int64),
         ("mesh_lo", C.c_double * 3), ("mesh_hi", C.c_double * 3),
+        ("pgrid", C.c_void_p), ("gdim", C.c_int32 * 3), ("pad1", C.c_int32),
+        ("gorg", C.c_double * 3), ("gscale", C.c_double * 3),
     ]
 
 
@@ -71,6 +73,7 @@ PLEAF_DTYPE = np.dtype([("ex_lo", "<f4", 3), ("ex_hi", "<f4", 3), ("start", "<u4
 BNODE_DTYPE = np.dtype([("box", "<f8", (2, 6)), ("child", "<i4", 2), ("pad", "<i4", 2)])
 
 TR_FLAG_NO_LEAF_HINT = 1
+TR_FLAG_NO_GRID = 2
 CHILD_NONE = -2**31
 
 # (name, restype, argtypes) for every symbol include/tetray_b200.h declares
@@ -82,6 +85,7 @@ _SIGNATURES = [
     ("tr_pbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("tr_pbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_pbvh_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_pbvh_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p]),
     ("tr_bbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.POINTER(C.c_void_p)]),
     ("tr_bbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_bbvh_copy", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -142,6 +142,10 @@ struct PBuf : TrHostBuf {
     std::vector<TrPLeaf> leaves;
     std::vector<uint32_t> ids;
     std::vector<std::array<double, 6>> leaf_box;  // exact f64 union boxes
+    // uniform grid of leaf candidates (a hint only: the exclusive box proves it)
+    std::vector<int32_t> grid;
+    int32_t gdim[3] = {1, 1, 1};
+    double gorg[3] = {0, 0, 0}, gscale[3] = {1, 1, 1};
 };
 
 constexpr int32_t CHILD_NONE = INT32_MIN;
@@ -302,6 +306,57 @@ void p_exclusive_boxes(PBuf &O) {
             LF.ex_hi[a] = f32_down(E[3 + a]);
         }
         if (!(E[0] <= E[3])) { LF.ex_lo[0] = 1.0f; LF.ex_hi[0] = 0.0f; }
+    }
+}
+
+// Uniform grid over the leaves: each cell names the leaf whose exclusive box
+// covers most of it.  Sized for about one leaf per cell.
+void p_build_grid(PBuf &O) {
+    const int64_t nl = (int64_t)O.leaves.size();
+    double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (const auto &b : O.leaf_box)
+        for (int a = 0; a < 3; ++a) { lo[a] = std::min(lo[a], b[a]); hi[a] = std::max(hi[a], b[3 + a]); }
+    double ext[3], vol = 1.0;
+    for (int a = 0; a < 3; ++a) { ext[a] = std::max(hi[a] - lo[a], 1e-300); vol *= ext[a]; }
+    const double side = std::cbrt(vol / (double)std::max<int64_t>(nl, 1));
+    int64_t cells = 1;
+    for (int a = 0; a < 3; ++a) {
+        double d = std::ceil(ext[a] / side);
+        O.gdim[a] = (int32_t)std::min(std::max(d, 1.0), 2048.0);
+        cells *= O.gdim[a];
+        O.gorg[a] = lo[a];
+        O.gscale[a] = (double)O.gdim[a] / ext[a];
+    }
+    O.grid.assign((size_t)cells, -1);
+    std::vector<double> best((size_t)cells, 0.0);
+    for (int64_t L = 0; L < nl; ++L) {
+        const TrPLeaf &lf = O.leaves[L];
+        double e0[3], e1[3];
+        bool ok = true;
+        for (int a = 0; a < 3; ++a) {
+            e0[a] = lf.ex_lo[a];
+            e1[a] = lf.ex_hi[a];
+            ok = ok && e0[a] < e1[a];
+        }
+        if (!ok) continue;
+        int64_t c0[3], c1[3];
+        for (int a = 0; a < 3; ++a) {
+            c0[a] = std::min<int64_t>(std::max<int64_t>((int64_t)std::floor((e0[a] - O.gorg[a]) * O.gscale[a]), 0), O.gdim[a] - 1);
+            c1[a] = std::min<int64_t>(std::max<int64_t>((int64_t)std::floor((e1[a] - O.gorg[a]) * O.gscale[a]), 0), O.gdim[a] - 1);
+        }
+        for (int64_t x = c0[0]; x <= c1[0]; ++x)
+            for (int64_t y = c0[1]; y <= c1[1]; ++y)
+                for (int64_t z = c0[2]; z <= c1[2]; ++z) {
+                    const int64_t c[3] = {x, y, z};
+                    double ov = 1.0;
+                    for (int a = 0; a < 3; ++a) {
+                        double cl = O.gorg[a] + (double)c[a] / O.gscale[a];
+                        double ch = O.gorg[a] + (double)(c[a] + 1) / O.gscale[a];
+                        ov *= std::max(0.0, std::min(e1[a], ch) - std::max(e0[a], cl));
+                    }
+                    const size_t ci = (size_t)((x * O.gdim[1] + y) * O.gdim[2] + z);
+                    if (ov > best[ci]) { best[ci] = ov; O.grid[ci] = (int32_t)L; }
+                }
     }
 }
 
@@ -502,6 +557,7 @@ int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, in
             O->nodes.push_back(N);
         }
         p_exclusive_boxes(*O);
+        p_build_grid(*O);
         *out = O;
         return TR_OK;
     } catch (const std::bad_alloc &) {
@@ -515,6 +571,20 @@ int tr_pbvh_sizes(const TrHostBuf *b, int64_t *s) {
     s[0] = (int64_t)P->nodes.size();
     s[1] = (int64_t)P->leaves.size();
     s[2] = (int64_t)P->ids.size();
+    s[3] = (int64_t)P->grid.size();
+    return TR_OK;
+}
+
+int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
+                 int32_t *cells) {
+    auto P = dynamic_cast<const PBuf *>(b);
+    if (!P) return tr_fail(TR_EINVAL, "tr_pbvh_grid: not a point BVH");
+    for (int a = 0; a < 3; ++a) {
+        if (dims3) dims3[a] = P->gdim[a];
+        if (org3) org3[a] = P->gorg[a];
+        if (scale3) scale3[a] = P->gscale[a];
+    }
+    if (cells) std::memcpy(cells, P->grid.data(), P->grid.size() * sizeof(int32_t));
     return TR_OK;
 }
 

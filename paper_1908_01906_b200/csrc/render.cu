@@ -46,6 +46,7 @@ constexpr int MARCH_BLOCK = 256;
 constexpr int TRACE_BLOCK = 128;
 constexpr int IV_CAP = 16;           // intervals per ray kept in the scratch list
 constexpr int SAMPLE_BATCH = 4;      // samples per lane per scheduling round
+constexpr int N_BUCKETS = 64;        // ray-cost buckets (4 per octave) for longest-first order
 constexpr int32_t CHILD_NONE = INT32_MIN;
 constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
 constexpr unsigned FULL = 0xffffffffu;
@@ -130,7 +131,10 @@ struct SceneK {  // kernel copy of TrDeviceScene
     const TrPLeaf *__restrict__ pleaves;
     const uint32_t *__restrict__ pleaf_ids;
     const TrBNode *__restrict__ bnodes;
+    const int32_t *__restrict__ pgrid;      // uniform-grid leaf candidates
+    int32_t gdim[3];
     int32_t centering;
+    double gorg[3], gscale[3];
     double mesh_lo[3], mesh_hi[3];
 };
 
@@ -238,14 +242,42 @@ __device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHin
     h.valid = true;
 }
 
+// Grid candidate leaf of q (-1: outside the grid or an empty cell).  Only a
+// hint: the caller accepts it after proving q strictly inside its exclusive box.
+__device__ __forceinline__ int32_t grid_leaf(const SceneK &S, const PQuery &q) {
+    const double fx = (q.x - S.gorg[0]) * S.gscale[0];
+    const double fy = (q.y - S.gorg[1]) * S.gscale[1];
+    const double fz = (q.z - S.gorg[2]) * S.gscale[2];
+    if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0)) return -1;
+    const int64_t cx = (int64_t)fx, cy = (int64_t)fy, cz = (int64_t)fz;
+    if (cx >= S.gdim[0] || cy >= S.gdim[1] || cz >= S.gdim[2]) return -1;
+    return __ldg(S.pgrid + (cx * S.gdim[1] + cy) * S.gdim[2] + cz);
+}
+
 // K:139-154.  Returns the record position (UINT32_MAX: outside every tet).
+// Order: the ray's current exclusive leaf (registers), the grid's candidate
+// leaf, else the full descent.  All three return the lowest containing index.
 __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
-                                             bool use_hint, double &v) {
+                                             bool use_hint, bool use_grid, double &v) {
     double l[4];
     uint32_t pos;
+    bool done = false;
     if (use_hint && hint.valid && strictly_in(q, hint.lo, hint.hi)) {
         pos = scan_leaf_first(S, hint.start, hint.count, q, l);
-    } else {
+        done = true;
+    } else if (use_grid) {
+        const int32_t gl = grid_leaf(S, q);
+        if (gl >= 0) {
+            LeafHint h;
+            load_hint(S, gl, h);
+            if (strictly_in(q, h.lo, h.hi)) {
+                pos = scan_leaf_first(S, h.start, h.count, q, l);
+                if (use_hint) hint = h;
+                done = true;
+            }
+        }
+    }
+    if (!done) {
         int32_t leaf;
         pos = locate_full(S, q, l, leaf);
         if (use_hint && leaf >= 0) load_hint(S, leaf, hint);
@@ -387,8 +419,16 @@ struct FrameK {
 struct IvBuf {                   // per-chunk scratch interval lists, interval-major
     int32_t *pid;                // [IV_CAP][n_rays]
     double *a, *b;               // [IV_CAP][n_rays]
-    uint32_t *cnt;               // [n_rays]: count | 0x80000000 if the ray has more
+    uint32_t *cnt;               // [n_rays]: count | cost bucket << 16 | 0x80000000 if more
+    uint32_t *order;             // [n_rays]: ray ids, most expensive first
+    uint32_t *hist, *cursor;     // [N_BUCKETS] each
 };
+
+__device__ __forceinline__ uint32_t cost_bucket(double cost) {
+    if (!(cost > 0.0)) return 0;
+    const int b = (int)(4.0f * __log2f((float)cost + 1.0f));
+    return (uint32_t)(b < N_BUCKETS - 1 ? b : N_BUCKETS - 1);
+}
 
 struct Pixel {
     int64_t ix, iy, out;
@@ -431,32 +471,78 @@ __device__ __forceinline__ RayD make_ray(const TrFrame &fr, int64_t ix, int64_t 
 
 // Phase 1: the exact interval sequence of every ray of the chunk (K:360-391
 // minus the marching).  Intervals past an early termination are computed but
-// never consumed, so counts and `visited` still follow the reference.
+// never consumed, so counts and `visited` still follow the reference.  Each
+// ray also gets a cost bucket (~log of its sample count) for longest-first
+// scheduling of the march.
 __global__ void __launch_bounds__(TRACE_BLOCK)
 trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
     const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
-    if (rr >= F.n_rays) return;
-    const Pixel px = ray_pixel(F, rr);
-    uint32_t n = 0;
-    if (px.valid) {
-        const RayD ray = make_ray(F.f, px.ix, px.iy);
-        double t_min = 0.0;
-        int32_t last = -1;
-        while (true) {
-            const double excl = (last < 0) ? 0.0 : F.f.eps;
-            double a, b;
-            const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
-            if (pid < 0) break;
-            if (n == IV_CAP) { n |= 0x80000000u; break; }  // resume inline in the march
-            iv.pid[(int64_t)n * F.n_rays + rr] = pid;
-            iv.a[(int64_t)n * F.n_rays + rr] = a;
-            iv.b[(int64_t)n * F.n_rays + rr] = b;
-            ++n;
-            t_min = b - F.f.eps;
-            last = pid;
+    uint32_t n = 0, bucket = 0;
+    if (rr < F.n_rays) {
+        const Pixel px = ray_pixel(F, rr);
+        if (px.valid) {
+            const RayD ray = make_ray(F.f, px.ix, px.iy);
+            double cost = 0.0;
+            if (F.f.mode == 0) {
+                double a, b;
+                slab(ray, S.mesh_lo, S.mesh_hi, a, b);
+                const double ta = (a > 0.0) ? a : 0.0;
+                if (a <= b && b - ta >= F.f.eps) cost = (b - ta) / F.f.s1 + 1.0;
+            } else {
+                double t_min = 0.0;
+                int32_t last = -1;
+                while (true) {
+                    const double excl = (last < 0) ? 0.0 : F.f.eps;
+                    double a, b;
+                    const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
+                    if (pid < 0) break;
+                    if (n == IV_CAP) { n |= 0x80000000u; cost += 4.0 * IV_CAP; break; }
+                    iv.pid[(int64_t)n * F.n_rays + rr] = pid;
+                    iv.a[(int64_t)n * F.n_rays + rr] = a;
+                    iv.b[(int64_t)n * F.n_rays + rr] = b;
+                    ++n;
+                    if (b - a >= F.f.eps)
+                        cost += (b - a) / ((F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1) + 1.0;
+                    t_min = b - F.f.eps;
+                    last = pid;
+                }
+            }
+            bucket = cost_bucket(cost);
         }
+        iv.cnt[rr] = n | (bucket << 16);
     }
-    iv.cnt[rr] = n;
+    // warp-aggregated bucket histogram
+    const bool valid = rr < F.n_rays;
+    const unsigned vm = __ballot_sync(FULL, valid);
+    if (valid) {
+        const unsigned peers = __match_any_sync(vm, bucket);
+        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
+    }
+}
+
+// Rays of the chunk sorted into descending cost buckets (order within a
+// bucket is arbitrary; outputs do not depend on it).
+__global__ void __launch_bounds__(TRACE_BLOCK)
+order_rays_kernel(FrameK F, IvBuf iv) {
+    __shared__ uint32_t start[N_BUCKETS];
+    if (threadIdx.x < N_BUCKETS) {
+        uint32_t s = 0;
+        for (int b = N_BUCKETS - 1; b > (int)threadIdx.x; --b) s += iv.hist[b];
+        start[threadIdx.x] = s;
+    }
+    __syncthreads();
+    const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
+    const bool valid = rr < F.n_rays;
+    const unsigned vm = __ballot_sync(FULL, valid);
+    if (!valid) return;
+    const uint32_t bucket = (iv.cnt[rr] >> 16) & 0xffu;
+    const unsigned peers = __match_any_sync(vm, bucket);
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(iv.cursor + bucket, (unsigned)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    iv.order[start[bucket] + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)rr;
 }
 
 enum : int { ST_IDLE = 0, ST_NEED = 1, ST_MARCH = 2 };
@@ -473,6 +559,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK) hist[i] = 0ull;
     __syncthreads();
     const bool use_hint = !(fr.flags & TR_FLAG_NO_LEAF_HINT);
+    const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
     const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long my_samples = 0, my_visited = 0;
 
@@ -506,10 +593,11 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             if (lane == leader) base = atomicAdd(O.work, (unsigned)__popc(m));
             base = __shfl_sync(FULL, base, leader);
             if (want) {
-                rr = (int64_t)base + __popc(m & lt_mask);
-                if (rr >= F.n_rays) {
+                const int64_t qpos = (int64_t)base + __popc(m & lt_mask);
+                if (qpos >= F.n_rays) {
                     exhausted = true;
                 } else {
+                    rr = (int64_t)iv.order[qpos];
                     const Pixel px = ray_pixel(F, rr);
                     if (px.valid) {
                         has_ray = true;
@@ -536,7 +624,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                             t_min = 0.0;
                             last = -1;
                             const uint32_t c = iv.cnt[rr];
-                            iv_n = c & 0x7fffffffu;
+                            iv_n = c & 0xffffu;
                             iv_more = (c >> 31) != 0;
                             iv_i = 0;
                             state = ST_NEED;
@@ -593,7 +681,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy,
                                             ray.oz + t * ray.dz);
                 double v;
-                if (field_at(S, q, hint, use_hint, v) != UINT32_MAX) {
+                if (field_at(S, q, hint, use_hint, use_grid, v) != UINT32_MAX) {
                     double c[4];
                     tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
                     const double x = 1.0 - c[3];
@@ -664,7 +752,7 @@ __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restri
         LeafHint h;
         h.valid = false;
         double v;
-        const uint32_t pos = field_at(S, q, h, false, v);
+        const uint32_t pos = field_at(S, q, h, false, true, v);
         found[i] = pos != UINT32_MAX ? 1 : 0;
         vals[i] = v;
         if (tet) tet[i] = pos != UINT32_MAX ? (int64_t)__ldg(S.pleaf_ids + pos) : -1;
@@ -712,7 +800,13 @@ SceneK make_scene(const TrDeviceScene *s) {
     S.pleaves = s->pleaves;
     S.pleaf_ids = s->pleaf_ids;
     S.bnodes = s->bnodes;
+    S.pgrid = s->pgrid;
     S.centering = s->centering;
+    for (int a = 0; a < 3; ++a) {
+        S.gdim[a] = s->gdim[a];
+        S.gorg[a] = s->gorg[a];
+        S.gscale[a] = s->gscale[a];
+    }
     for (int a = 0; a < 3; ++a) { S.mesh_lo[a] = s->mesh_lo[a]; S.mesh_hi[a] = s->mesh_hi[a]; }
     return S;
 }
@@ -728,7 +822,8 @@ int sm_count() {
     return n;
 }
 
-constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * (4 + 8 + 8) + 4;
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * (4 + 8 + 8) + 4 + 4;
+constexpr int64_t IV_FIXED_BYTES = 1024;
 
 }  // namespace
 
@@ -744,7 +839,7 @@ int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t count) {
 }
 
 int64_t tr_scratch_bytes(int64_t n_rays) {
-    return n_rays * IV_BYTES_PER_RAY + 1024;
+    return n_rays * IV_BYTES_PER_RAY + IV_FIXED_BYTES;
 }
 
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
@@ -784,14 +879,11 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX) ? 1 : 0;
     const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
     // ray chunk = what the scratch interval lists can hold
-    int64_t chunk = total_rays;
-    if (frame->mode != 0) {
-        if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + 1024)
-            return tr_fail(TR_EINVAL, "tr_render_frame: scratch buffer too small");
-        chunk = (out->scratch_bytes - 1024) / IV_BYTES_PER_RAY / 32 * 32;
-        if (chunk > total_rays) chunk = total_rays;
-        if (chunk < 32) chunk = 32;
-    }
+    if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + IV_FIXED_BYTES)
+        return tr_fail(TR_EINVAL, "tr_render_frame: scratch buffer too small");
+    int64_t chunk = (out->scratch_bytes - IV_FIXED_BYTES) / IV_BYTES_PER_RAY / 32 * 32;
+    if (chunk > total_rays) chunk = total_rays;
+    if (chunk < 32) chunk = 32;
     const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
     cudaError_t e;
     if (smem > 48 * 1024) {
@@ -809,19 +901,25 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         F.n_rays = (total_rays - r0 < chunk) ? total_rays - r0 : chunk;
         IvBuf iv;
         char *base = reinterpret_cast<char *>(out->scratch);
-        iv.b = reinterpret_cast<double *>(base);
+        iv.hist = reinterpret_cast<uint32_t *>(base);
+        iv.cursor = iv.hist + N_BUCKETS;
+        iv.b = reinterpret_cast<double *>(base + IV_FIXED_BYTES);
         iv.a = iv.b + (int64_t)IV_CAP * F.n_rays;
         iv.pid = reinterpret_cast<int32_t *>(iv.a + (int64_t)IV_CAP * F.n_rays);
         iv.cnt = reinterpret_cast<uint32_t *>(iv.pid + (int64_t)IV_CAP * F.n_rays);
+        iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
-        if (frame->mode != 0) {
-            const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
-            trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv);
-            e = cudaGetLastError();
-            if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
-            ++launches;
-        }
+        e = cudaMemsetAsync(iv.hist, 0, 2 * N_BUCKETS * sizeof(uint32_t), st);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
+        const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
+        trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
+        order_rays_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(F, iv);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_fail(e, "order_rays_kernel launch");
+        launches += 2;
         int64_t grid = (int64_t)sm_count() * per_sm;
         const int64_t need = (F.n_rays + MARCH_BLOCK - 1) / MARCH_BLOCK;
         if (grid > need) grid = need;

@@ -70,6 +70,13 @@ def _padded_boxes(scene) -> tuple[np.ndarray, np.ndarray]:
     return lo - pad, hi + pad
 
 
+class PointGrid:
+    """Uniform-grid leaf index of the point BVH (tr_pbvh_grid)."""
+
+    def __init__(self, dims, org, scale, cells):
+        self.dims, self.org, self.scale, self.cells = dims, org, scale, cells
+
+
 def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEAF_MAX):
     L = _lib.lib()
     box_lo = np.ascontiguousarray(box_lo, dtype=np.float64)
@@ -78,16 +85,21 @@ def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEA
     _lib.check(L.tr_pbvh_build(len(box_lo), _lib.ptr(box_lo, C.c_double),
                                _lib.ptr(box_hi, C.c_double), leaf_max, C.byref(h)), "tr_pbvh_build")
     try:
-        sz = np.zeros(3, np.int64)
+        sz = np.zeros(4, np.int64)
         _lib.check(L.tr_pbvh_sizes(h, _lib.ptr(sz, C.c_int64)), "tr_pbvh_sizes")
         nodes = np.zeros(int(sz[0]), dtype=_lib.PNODE_DTYPE)
         leaves = np.zeros(int(sz[1]), dtype=_lib.PLEAF_DTYPE)
         ids = np.zeros(int(sz[2]), dtype=np.uint32)
         _lib.check(L.tr_pbvh_copy(h, _lib.vptr(nodes), _lib.vptr(leaves), _lib.vptr(ids)),
                    "tr_pbvh_copy")
+        grid = PointGrid(np.zeros(3, np.int32), np.zeros(3), np.zeros(3),
+                         np.zeros(int(sz[3]), np.int32))
+        _lib.check(L.tr_pbvh_grid(h, _lib.vptr(grid.dims), _lib.ptr(grid.org, C.c_double),
+                                  _lib.ptr(grid.scale, C.c_double), _lib.vptr(grid.cells)),
+                   "tr_pbvh_grid")
     finally:
         L.tr_host_free(h)
-    return nodes, leaves, ids
+    return nodes, leaves, ids, grid
 
 
 def pack_tet_records(mesh, sampler) -> np.ndarray:
@@ -189,7 +201,7 @@ class DeviceScene:
             t0 = time.perf_counter()
             rec = pack_tet_records(mesh, sampler)
             lo, hi = _padded_boxes(scene)
-            pnodes, pleaves, pids = build_point_bvh(lo, hi)
+            pnodes, pleaves, pids, grid = build_point_bvh(lo, hi)
             part_lo = np.ascontiguousarray(scene.bvh.box_lo, dtype=np.float64)
             part_hi = np.ascontiguousarray(scene.bvh.box_hi, dtype=np.float64)
             bnodes = getattr(scene.bvh, "nodes", None)
@@ -211,10 +223,12 @@ class DeviceScene:
             self.t_bnodes = _upload(bnodes, device)
             self.t_plo = _upload(part_lo, device)
             self.t_phi = _upload(part_hi, device)
+            self.t_grid = _upload(grid.cells, device)
+            self.grid = grid
             torch.cuda.synchronize(device)
         self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
                                                       self.t_pids, self.t_bnodes, self.t_plo,
-                                                      self.t_phi))
+                                                      self.t_phi, self.t_grid))
         self.desc = _lib.TrDeviceScene(
             tets=self.t_tets.data_ptr(), pnodes=self.t_pnodes.data_ptr(),
             pleaves=self.t_pleaves.data_ptr(), pleaf_ids=self.t_pids.data_ptr(),
@@ -222,7 +236,9 @@ class DeviceScene:
             centering=int(mesh.centering), bnodes=self.t_bnodes.data_ptr(),
             part_lo=self.t_plo.data_ptr(), part_hi=self.t_phi.data_ptr(), n_parts=self.n_parts,
             n_bnodes=self.n_bnodes,
-            mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi))
+            mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi),
+            pgrid=self.t_grid.data_ptr(), gdim=(C.c_int32 * 3)(*grid.dims),
+            gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale))
         self._epochs: OrderedDict = OrderedDict()
         self._frames: dict = {}
 

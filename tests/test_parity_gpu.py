@@ -74,7 +74,7 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     for mode in modes:
         ref = orc.render(cam, mode, par, jitter=jitter)
-        for flags in (0, 1):  # with and without the exclusive-leaf shortcut
+        for flags in (0, 1, 2, 3):  # with and without the leaf shortcut and the grid
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 

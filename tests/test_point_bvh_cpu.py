@@ -70,7 +70,7 @@ def test_exclusive_leaf_and_full_descent_agree_with_reference(B, recipe):
     from paper_1908_01906_b200.device import _padded_boxes, build_point_bvh
     sc = C.build_scene(B, recipe)
     lo, hi = _padded_boxes(sc)
-    nodes, leaves, ids = build_point_bvh(lo, hi)
+    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
     # (1) f32 child boxes contain the f64 padded boxes of everything below
     for n in nodes:
         for c, (blo, bhi) in enumerate(((n["lo0"], n["hi0"]), (n["lo1"], n["hi1"]))):
@@ -102,7 +102,7 @@ def test_exclusive_boxes_are_disjoint_from_other_leaf_boxes(B):
     from paper_1908_01906_b200.device import _padded_boxes, build_point_bvh
     sc = C.build_scene(B, "sinus")
     lo, hi = _padded_boxes(sc)
-    nodes, leaves, ids = build_point_bvh(lo, hi)
+    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
     boxes = []
     for lf in leaves:
         t = ids[lf["start"]:lf["start"] + lf["count"]]
