@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--flags", type=lambda x: int(x, 0), default=0,
+                    help="TR_FLAG_* bits (tuning experiments; bits 8-11 = log2 group size)")
     return ap.parse_args()
 
 
@@ -227,7 +229,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
     runner = D.ShardedFrame(dscene, scene, cam, mode_id, par, track=track,
-                            rank=rank if world > 1 else 0, world=world)
+                            rank=rank if world > 1 else 0, world=world, flags=args.flags)
     # warm-up
     for _ in range(args.warmup):
         runner.run(stream)

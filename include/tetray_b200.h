@@ -184,6 +184,7 @@ typedef struct TrFrame {
 
 #define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
+/* flags bits 8-11: log2 of the lanes that march one ray together (0 = 8) */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)
  * i64, visited (H,W) i32.  Compact layout: slot-major 8x4 pixel tiles.

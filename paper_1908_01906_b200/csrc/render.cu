@@ -10,20 +10,22 @@
 // are IEEE round-to-nearest.  Results are therefore bit-identical to the
 // numba reference, except glibc pow in skip-adaptive mode.
 //
-// A frame is two kernels per ray chunk:
+// A frame is three kernels per ray chunk:
 //   trace_intervals_kernel  one thread per ray, 8x4 pixel tiles per warp: the
 //       exact front-to-back partition-interval sequence (K:360-391 calling
 //       next_interval K:173-230) over a BVH2 with f64 child boxes, pruned by
-//       per-epoch subtree activity bits; up to IV_CAP intervals per ray go to
-//       a scratch list, longer rays resume next_interval inline later.
-//   march_kernel  persistent CTAs with PER-LANE RAY REFILL: a lane whose ray
-//       finishes immediately takes the next ray from a warp-aggregated atomic
-//       queue, so rays of very different length (0..~300 samples) never idle
-//       a warp.  Each sample locates its tet through the ray's current
-//       "exclusive leaf" (a point strictly inside it can only lie in that
-//       leaf's tets, scanned in ascending id order: first hit = lowest index,
-//       the reference's tie rule K:119) or, failing that, a full
-//       min-id-pruned BVH descent; then TF, opacity correction, compositing.
+//       per-epoch subtree activity bits, kept as partition ids; rays with
+//       nothing to march are finished here, the rest get a cost bucket.
+//   order_rays_kernel  marching rays sorted into descending cost buckets
+//       (longest first, so the frame does not end on one long ray).
+//   march_group_kernel<G>  persistent CTAs; G lanes march ONE ray: each lane
+//       shades one consecutive sample (interval and k derived exactly from
+//       the list), then the group composites the G results in sample order
+//       with the exact early-termination rule.  Point location: uniform-grid
+//       candidate leaf proved by its exclusive box (a point strictly inside
+//       it can only lie in that leaf's tets, scanned in ascending id order:
+//       first hit = lowest index, the reference's tie rule K:119), else a
+//       full min-id-pruned BVH descent.
 //   The per-partition histogram is privatised per CTA in shared memory and
 //   merged with 64-bit integer atomics (exact, order independent).
 #include <cuda_runtime.h>
@@ -44,8 +46,7 @@ constexpr int PSTACK = 64;
 constexpr int BSTACK = 64;
 constexpr int MARCH_BLOCK = 256;
 constexpr int TRACE_BLOCK = 128;
-constexpr int IV_CAP = 16;           // intervals per ray kept in the scratch list
-constexpr int SAMPLE_BATCH = 4;      // samples per lane per scheduling round
+constexpr int IV_CAP = 64;           // partition ids per ray kept in the scratch list
 constexpr int N_BUCKETS = 64;        // ray-cost buckets (4 per octave) for longest-first order
 constexpr int32_t CHILD_NONE = INT32_MIN;
 constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
@@ -131,6 +132,8 @@ struct SceneK {  // kernel copy of TrDeviceScene
     const TrPLeaf *__restrict__ pleaves;
     const uint32_t *__restrict__ pleaf_ids;
     const TrBNode *__restrict__ bnodes;
+    const double *__restrict__ part_lo;     // (P,3) partition boxes (next_interval's leaf boxes)
+    const double *__restrict__ part_hi;
     const int32_t *__restrict__ pgrid;      // uniform-grid leaf candidates
     int32_t gdim[3];
     int32_t centering;
@@ -416,18 +419,18 @@ struct FrameK {
     int32_t hist_smem;
 };
 
-struct IvBuf {                   // per-chunk scratch interval lists, interval-major
+struct IvBuf {                   // per-chunk scratch, interval-major lists of partition ids
     int32_t *pid;                // [IV_CAP][n_rays]
-    double *a, *b;               // [IV_CAP][n_rays]
-    uint32_t *cnt;               // [n_rays]: count | cost bucket << 16 | 0x80000000 if more
-    uint32_t *order;             // [n_rays]: ray ids, most expensive first
-    uint32_t *hist, *cursor;     // [N_BUCKETS] each
+    uint32_t *cnt;               // [n_rays]: n | bucket << 16 | 0x80000000 if more than IV_CAP
+    uint32_t *order;             // marching rays, most expensive first
+    uint32_t *hist, *cursor;     // [N_BUCKETS] each; bucket 0 = nothing to march
+    unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
 };
 
 __device__ __forceinline__ uint32_t cost_bucket(double cost) {
     if (!(cost > 0.0)) return 0;
     const int b = (int)(4.0f * __log2f((float)cost + 1.0f));
-    return (uint32_t)(b < N_BUCKETS - 1 ? b : N_BUCKETS - 1);
+    return (uint32_t)(b < 1 ? 1 : (b < N_BUCKETS - 1 ? b : N_BUCKETS - 1));
 }
 
 struct Pixel {
@@ -469,20 +472,50 @@ __device__ __forceinline__ RayD make_ray(const TrFrame &fr, int64_t ix, int64_t 
     return ray;
 }
 
-// Phase 1: the exact interval sequence of every ray of the chunk (K:360-391
-// minus the marching).  Intervals past an early termination are computed but
-// never consumed, so counts and `visited` still follow the reference.  Each
-// ray also gets a cost bucket (~log of its sample count) for longest-first
-// scheduling of the march.
+// Samples march_range takes on [a, b): k = 0 always, then every k >= 1 with
+// t_k = a + (k + phase) * step < b (K:277-280).  fl(a + fl(fl(k + phase) *
+// step)) is monotone in k, so the count is the first k >= 1 with t_k >= b,
+// found from the real-valued estimate and corrected with the exact expression.
+__device__ __forceinline__ int64_t interval_samples(double a, double b, double step,
+                                                    double phase) {
+    const double est = ceil((b - a) / step - phase);
+    int64_t k = (est > 1.0) ? (int64_t)fmin(est, 4.0e15) : 1;
+    while (k > 1 && a + ((double)(k - 1) + phase) * step >= b) --k;
+    while (a + ((double)k + phase) * step < b) ++k;
+    return k;
+}
+
+__device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &O, int64_t out,
+                                            const Acc &acc, int64_t samples, int32_t visited) {
+    const double r = acc.r + (1.0 - acc.a) * fr.bg[0];  // K:393-396
+    const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
+    const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
+    const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
+    double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * out);
+    px[0] = make_double2(r, g);
+    px[1] = make_double2(bl, al);
+    O.samples[out] = samples;
+    O.visited[out] = visited;
+}
+
+// Phase 1 (one thread per ray, 8x4 pixel tiles per warp): the exact
+// partition-interval sequence (K:360-391 calling next_interval K:173-230),
+// stored as partition ids; the clamped (t_enter, t_exit) are recomputed
+// bit-identically in phase 2.  Rays with nothing to march (no hit, or only
+// degenerate intervals) are finished here; the others get a cost bucket
+// (~4 log2 of their sample count) for longest-first scheduling.
 __global__ void __launch_bounds__(TRACE_BLOCK)
-trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
+trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
     uint32_t n = 0, bucket = 0;
-    if (rr < F.n_rays) {
+    unsigned long long vis_done = 0;
+    const bool in_chunk = rr < F.n_rays;
+    if (in_chunk) {
         const Pixel px = ray_pixel(F, rr);
         if (px.valid) {
             const RayD ray = make_ray(F.f, px.ix, px.iy);
             double cost = 0.0;
+            bool more = false;
             if (F.f.mode == 0) {
                 double a, b;
                 slab(ray, S.mesh_lo, S.mesh_hi, a, b);
@@ -496,10 +529,8 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
                     double a, b;
                     const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
                     if (pid < 0) break;
-                    if (n == IV_CAP) { n |= 0x80000000u; cost += 4.0 * IV_CAP; break; }
+                    if (n == IV_CAP) { more = true; cost += 4.0 * IV_CAP; break; }
                     iv.pid[(int64_t)n * F.n_rays + rr] = pid;
-                    iv.a[(int64_t)n * F.n_rays + rr] = a;
-                    iv.b[(int64_t)n * F.n_rays + rr] = b;
                     ++n;
                     if (b - a >= F.f.eps)
                         cost += (b - a) / ((F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1) + 1.0;
@@ -507,20 +538,29 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
                     last = pid;
                 }
             }
-            bucket = cost_bucket(cost);
+            if (cost > 0.0) {
+                bucket = cost_bucket(cost);
+            } else {  // nothing to march: background, `visited` = every interval returned
+                const Acc zero = {0.0, 0.0, 0.0, 0.0};
+                write_pixel(F.f, O, px.out, zero, 0, (int32_t)n);
+                vis_done = n;
+            }
+            iv.cnt[rr] = n | (bucket << 16) | (more ? 0x80000000u : 0u);
+        } else {
+            iv.cnt[rr] = 0;
         }
-        iv.cnt[rr] = n | (bucket << 16);
     }
-    // warp-aggregated bucket histogram
-    const bool valid = rr < F.n_rays;
-    const unsigned vm = __ballot_sync(FULL, valid);
-    if (valid) {
+    const unsigned vm = __ballot_sync(FULL, in_chunk);
+    if (in_chunk) {
         const unsigned peers = __match_any_sync(vm, bucket);
         if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
     }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) vis_done += __shfl_xor_sync(FULL, vis_done, off);
+    if ((threadIdx.x & 31) == 0 && vis_done) atomicAdd(iv.totals + 1, vis_done);
 }
 
-// Rays of the chunk sorted into descending cost buckets (order within a
+// Marching rays of the chunk in descending cost buckets (order inside a
 // bucket is arbitrary; outputs do not depend on it).
 __global__ void __launch_bounds__(TRACE_BLOCK)
 order_rays_kernel(FrameK F, IvBuf iv) {
@@ -532,10 +572,10 @@ order_rays_kernel(FrameK F, IvBuf iv) {
     }
     __syncthreads();
     const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
-    const bool valid = rr < F.n_rays;
+    const uint32_t bucket = rr < F.n_rays ? (iv.cnt[rr] >> 16) & 0xffu : 0u;
+    const bool valid = bucket != 0;
     const unsigned vm = __ballot_sync(FULL, valid);
     if (!valid) return;
-    const uint32_t bucket = (iv.cnt[rr] >> 16) & 0xffu;
     const unsigned peers = __match_any_sync(vm, bucket);
     const int lane = threadIdx.x & 31;
     const int leader = __ffs(peers) - 1;
@@ -545,184 +585,273 @@ order_rays_kernel(FrameK F, IvBuf iv) {
     iv.order[start[bucket] + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)rr;
 }
 
-enum : int { ST_IDLE = 0, ST_NEED = 1, ST_MARCH = 2 };
-
-// Phase 2: front-to-back compositing with per-lane ray refill.
+// Phase 2: G lanes march one ray together.  Per round each lane of the
+// group takes one consecutive sample of the ray (across interval borders:
+// the window is the next G intervals of the list), locates and shades it
+// independently, then the group composites the G results in sample order
+// with the exact early-termination rule (K:285-295).  Lanes whose group has
+// no ray take part in the collectives with empty windows.
+template <int G>
 __global__ void __launch_bounds__(MARCH_BLOCK, 2)
-march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
+march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
+    static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
     extern __shared__ unsigned long long hist[];  // [n_parts] when F.hist_smem
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
+    __shared__ double shade[MARCH_BLOCK][5];      // per-lane sample result: ca, r, g, b, (found)
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane % G;                   // lane in group
+    const int gbase = lane - j;               // first lane of my group
     const bool track = fr.track_ppart && fr.mode != 0;
     if (track && F.hist_smem)
         for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK) hist[i] = 0ull;
     __syncthreads();
-    const bool use_hint = !(fr.flags & TR_FLAG_NO_LEAF_HINT);
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
-    const unsigned lt_mask = (1u << lane) - 1u;
+    uint32_t n_queue = 0;
+    for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
 
-    int state = ST_IDLE;
-    bool exhausted = false;
+    // group-uniform ray state
+    bool active = false, exhausted = false;
     int64_t rr = 0, out = 0;
     RayD ray;
     double phase = 0.5;
     Acc acc = {0.0, 0.0, 0.0, 0.0};
     int64_t samples = 0;
     int32_t visited = 0;
-    double t_min = 0.0;
-    int32_t last = -1;
-    uint32_t iv_i = 0, iv_n = 0;
-    bool iv_more = false;
-    int32_t pid = -1;
-    double t0 = 0.0, t1 = 0.0, step = 0.0, e = 1.0;
-    bool unit = true;
-    int64_t k = 0, ns = 0;
-    LeafHint hint;
-    hint.valid = false;
-    bool has_ray = false;  // a started ray whose pixel is not written yet
+    int32_t i_cur = 0, iv_n = 0, last_pid = -1;
+    bool more = false;
+    int64_t k_cur = 0;
+    double tmin_c = 0.0;
+    int32_t ov_pid = -1;                       // inline interval past the list
+    double ov_a = 0.0, ov_b = 0.0;
+    double m0_a = 0.0, m0_b = 0.0;             // reference mode's single interval
 
     while (true) {
-        // ---- refill idle lanes from the chunk's ray queue
-        const bool want = state == ST_IDLE && !exhausted;
-        const unsigned m = __ballot_sync(FULL, want);
-        if (m) {
-            const int leader = __ffs(m) - 1;
+        // ---- refill: one queue slot per group that needs a ray
+        const bool want = !active && !exhausted;
+        const unsigned lm = __ballot_sync(FULL, want && j == 0);
+        if (lm) {
+            const int leader = __ffs(lm) - 1;
             unsigned base = 0;
-            if (lane == leader) base = atomicAdd(O.work, (unsigned)__popc(m));
+            if (lane == leader) base = atomicAdd(O.work, (unsigned)__popc(lm));
             base = __shfl_sync(FULL, base, leader);
+            const unsigned qpos = base + __popc(lm & ((1u << gbase) - 1u));
             if (want) {
-                const int64_t qpos = (int64_t)base + __popc(m & lt_mask);
-                if (qpos >= F.n_rays) {
+                if (qpos >= n_queue) {
                     exhausted = true;
                 } else {
                     rr = (int64_t)iv.order[qpos];
                     const Pixel px = ray_pixel(F, rr);
-                    if (px.valid) {
-                        has_ray = true;
-                        out = px.out;
-                        ray = make_ray(fr, px.ix, px.iy);
-                        phase = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
-                        acc.r = acc.g = acc.b = acc.a = 0.0;
-                        samples = 0;
-                        visited = 0;
-                        hint.valid = false;
-                        if (fr.mode == 0) {  // K:346-353: one interval, the mesh box
-                            double a, b;
-                            slab(ray, S.mesh_lo, S.mesh_hi, a, b);
-                            const double ta = (a > 0.0) ? a : 0.0;
-                            if (a <= b && b - ta >= fr.eps) {
-                                pid = -1; t0 = ta; t1 = b; step = fr.s1; e = fr.s1 / fr.s1;
-                                unit = e == 1.0; k = 0; ns = 0;
-                                state = ST_MARCH;
-                            } else {
-                                state = ST_NEED;  // finishes below with no interval
-                                iv_n = 0; iv_i = 0; iv_more = false;
-                            }
-                        } else {
-                            t_min = 0.0;
-                            last = -1;
-                            const uint32_t c = iv.cnt[rr];
-                            iv_n = c & 0xffffu;
-                            iv_more = (c >> 31) != 0;
-                            iv_i = 0;
-                            state = ST_NEED;
-                        }
+                    out = px.out;
+                    ray = make_ray(fr, px.ix, px.iy);
+                    phase = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
+                    acc.r = acc.g = acc.b = acc.a = 0.0;
+                    samples = 0;
+                    visited = 0;
+                    i_cur = 0;
+                    k_cur = 0;
+                    tmin_c = 0.0;
+                    last_pid = -1;
+                    ov_pid = -1;
+                    const uint32_t c = iv.cnt[rr];
+                    iv_n = (int32_t)(c & 0xffffu);
+                    more = (c >> 31) != 0;
+                    if (fr.mode == 0) {  // K:346-353: the mesh box is the one interval
+                        double a0, b0;
+                        slab(ray, S.mesh_lo, S.mesh_hi, a0, b0);
+                        m0_a = (a0 > 0.0) ? a0 : 0.0;
+                        m0_b = b0;
+                        iv_n = 1;
                     }
+                    active = true;
                 }
             }
         }
         if (__all_sync(FULL, exhausted)) break;
 
-        // ---- next interval (K:363-378): from the list, or inline past its end
-        if (state == ST_NEED) {
-            while (true) {
-                int32_t p = -1;
-                double a = 0.0, b = 0.0;
-                if (iv_i < iv_n) {
-                    const int64_t o = (int64_t)iv_i * F.n_rays + rr;
-                    p = iv.pid[o];
-                    a = iv.a[o];
-                    b = iv.b[o];
-                    ++iv_i;
-                } else if (iv_more) {
-                    p = next_interval(S, E, ray, t_min, (last < 0) ? 0.0 : fr.eps, last, a, b);
+        // ---- past the stored list (rare): next_interval inline, one interval per window
+        const bool inline_iv = active && fr.mode != 0 && i_cur >= iv_n;
+        if (inline_iv && ov_pid < 0 && more && j == 0) {
+            double a0, b0;
+            ov_pid = next_interval(S, E, ray, tmin_c, (last_pid < 0) ? 0.0 : fr.eps, last_pid,
+                                   a0, b0);
+            ov_a = a0;
+            ov_b = b0;
+        }
+        ov_pid = __shfl_sync(FULL, ov_pid, gbase);
+        ov_a = __shfl_sync(FULL, ov_a, gbase);
+        ov_b = __shfl_sync(FULL, ov_b, gbase);
+        if (inline_iv && ov_pid < 0) more = false;
+
+        // ---- the window: intervals i_cur .. i_cur+G-1, one per lane
+        int32_t pid = -1;
+        double a = 0.0, b = 0.0, step = fr.s1;
+        bool valid = false;
+        if (active) {
+            if (fr.mode == 0) {
+                valid = (j == 0) && i_cur < 1;
+                a = m0_a;
+                b = m0_b;
+            } else if (inline_iv) {
+                valid = (j == 0) && ov_pid >= 0;
+                pid = ov_pid;
+                a = ov_a;
+                b = ov_b;
+            } else {
+                const int32_t ii = i_cur + j;
+                valid = ii < iv_n;
+                if (valid) {
+                    pid = iv.pid[(int64_t)ii * F.n_rays + rr];
+                    // next_interval's slab of the partition box (bit-identical)
+                    const double lo[3] = {__ldg(S.part_lo + 3 * pid), __ldg(S.part_lo + 3 * pid + 1),
+                                          __ldg(S.part_lo + 3 * pid + 2)};
+                    const double hi[3] = {__ldg(S.part_hi + 3 * pid), __ldg(S.part_hi + 3 * pid + 1),
+                                          __ldg(S.part_hi + 3 * pid + 2)};
+                    slab(ray, lo, hi, a, b);
                 }
-                if (p < 0) {
-                    state = ST_IDLE;  // ray done
-                    break;
-                }
-                visited += 1;
-                if (b - a >= fr.eps) {
-                    pid = p; t0 = a; t1 = b;
-                    step = (fr.mode == 2) ? __ldg(E.step + p) : fr.s1;
-                    e = step / fr.s1;
-                    unit = e == 1.0;
-                    k = 0;
-                    ns = 0;
-                    state = ST_MARCH;
-                    break;
-                }
-                t_min = b - fr.eps;  // degenerate interval: visited, not marched
-                last = p;
             }
+        }
+        // list intervals: t_min = previous exit - eps, entry clamped to it (K:200, K:390)
+        const double prev_b = __shfl_up_sync(FULL, b, 1, G);
+        const int32_t prev_pid = __shfl_up_sync(FULL, pid, 1, G);
+        if (valid && fr.mode != 0 && !inline_iv) {
+            const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
+            a = (a > tmin_j) ? a : tmin_j;
+        }
+        if (valid && fr.mode == 2) step = __ldg(E.step + pid);
+        const bool marchable = valid && (b - a >= fr.eps);
+        const int64_t n_i = marchable ? interval_samples(a, b, step, phase) : 0;
+        int64_t rem = n_i - ((j == 0) ? k_cur : 0);
+        if (rem < 0) rem = 0;
+        int64_t incl = rem;  // inclusive scan of remaining samples over the window
+#pragma unroll
+        for (int d = 1; d < G; d <<= 1) {
+            const int64_t y = __shfl_up_sync(FULL, incl, d, G);
+            if (j >= d) incl += y;
+        }
+        const int64_t R = __shfl_sync(FULL, incl, gbase + G - 1);
+        const unsigned vbits = (__ballot_sync(FULL, valid) >> gbase) &
+                               ((G == 32) ? FULL : ((1u << G) - 1u));
+        const int nvalid = __popc(vbits);
+        // my sample is the j-th of the round: owner = first window lane with incl > j
+        int owner = G;
+        int64_t own_incl = 0, own_rem = 0;
+#pragma unroll
+        for (int l = G - 1; l >= 0; --l) {
+            const int64_t x = __shfl_sync(FULL, incl, gbase + l);
+            const int64_t y = __shfl_sync(FULL, rem, gbase + l);
+            if (x > j) { owner = l; own_incl = x; own_rem = y; }
+        }
+        const bool has = active && (int64_t)j < R;
+        const int src = gbase + (owner < G ? owner : 0);
+        const double sa = __shfl_sync(FULL, a, src);
+        const double sstep = __shfl_sync(FULL, step, src);
+        const int32_t spid = __shfl_sync(FULL, pid, src);
+        const int64_t sfirst = own_incl - own_rem;  // round index of the owner's first sample
+        const int64_t sk = (int64_t)j - sfirst + ((owner == 0) ? k_cur : 0);
+
+        // ---- shade my sample (K:277-290)
+        double ca = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, found = 0.0;
+        if (has) {
+            const double t = sa + ((double)sk + phase) * sstep;
+            const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy, ray.oz + t * ray.dz);
+            LeafHint h;
+            h.valid = false;
+            double v;
+            if (field_at(S, q, h, false, use_grid, v) != UINT32_MAX) {
+                double c[4];
+                tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+                const double e = sstep / fr.s1;
+                const double x = 1.0 - c[3];
+                ca = 1.0 - ((e == 1.0) ? x : pow(x, e));  // glibc pow(x, 1) == x
+                cr = c[0]; cg = c[1]; cb = c[2];
+                found = 1.0;
+            }
+        }
+        double *mine = shade[threadIdx.x];
+        mine[0] = ca; mine[1] = cr; mine[2] = cg; mine[3] = cb; mine[4] = found;
+        __syncwarp();
+
+        // ---- composite the round in sample order (K:285-295).  A sample
+        // outside every tet has ca = c = 0, which leaves acc bit-unchanged;
+        // termination is only tested after a found sample, as in K:285-295.
+        const int cnt = (int)((R < G) ? R : G);
+        int taken = cnt;
+        bool term = false;
+        if (active) {
+            const double(*grp)[5] = shade + (threadIdx.x - j);
+            for (int m = 0; m < cnt; ++m) {
+                const double w = (1.0 - acc.a) * grp[m][0];
+                acc.r += w * grp[m][1];
+                acc.g += w * grp[m][2];
+                acc.b += w * grp[m][3];
+                acc.a += w;
+                if (grp[m][4] != 0.0 && acc.a >= fr.term) { taken = m + 1; term = true; break; }
+            }
+        }
+        __syncwarp();
+        // per-partition samples: the first taken sample of each interval's run adds the run
+        if (track && has && (int64_t)j < taken && (int64_t)j == sfirst) {
+            const int64_t c = ((own_incl < taken) ? own_incl : (int64_t)taken) - (int64_t)j;
+            if (F.hist_smem) atomicAdd(&hist[spid], (unsigned long long)c);
+            else atomicAdd((unsigned long long *)O.ppart + spid, (unsigned long long)c);
         }
 
-        // ---- up to SAMPLE_BATCH samples of the current interval (K:276-296)
-        bool terminated = false, ended = false;
-        if (state == ST_MARCH) {
-#pragma unroll 1
-            for (int s = 0; s < SAMPLE_BATCH; ++s) {
-                const double t = t0 + ((double)k + phase) * step;
-                if (k > 0 && t >= t1) { ended = true; break; }
-                samples += 1;
-                ns += 1;
-                const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy,
-                                            ray.oz + t * ray.dz);
-                double v;
-                if (field_at(S, q, hint, use_hint, use_grid, v) != UINT32_MAX) {
-                    double c[4];
-                    tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
-                    const double x = 1.0 - c[3];
-                    const double ca = 1.0 - (unit ? x : pow(x, e));  // glibc pow(x, 1) == x
-                    const double w = (1.0 - acc.a) * ca;
-                    acc.r += w * c[0];
-                    acc.g += w * c[1];
-                    acc.b += w * c[2];
-                    acc.a += w;
-                    if (acc.a >= fr.term) { terminated = true; ended = true; ++k; break; }
+        // ---- advance the group's cursor (all shuffles before any divergence)
+        const int lastj = (taken > 0) ? taken - 1 : 0;
+        const int own_last = __shfl_sync(FULL, owner, gbase + lastj);
+        const int64_t k_last = __shfl_sync(FULL, sk, gbase + lastj);
+        const int ol = (own_last < G) ? own_last : 0;
+        const double b_before_own = __shfl_sync(FULL, prev_b, gbase + ol);
+        const int32_t pid_before_own = __shfl_sync(FULL, prev_pid, gbase + ol);
+        const int lv = (nvalid > 0) ? nvalid - 1 : 0;
+        const double b_lastvalid = __shfl_sync(FULL, b, gbase + lv);
+        const int32_t pid_lastvalid = __shfl_sync(FULL, pid, gbase + lv);
+        if (active) {
+            samples += taken;
+            bool done = false;
+            if (term) {  // K:388-389: the terminating interval is the last one visited
+                if (fr.mode != 0) visited += own_last + 1;
+                done = true;
+            } else if (R > G) {  // interval own_last continues in the next round
+                if (fr.mode != 0 && !inline_iv && own_last > 0) {
+                    visited += own_last;
+                    i_cur += own_last;
+                    tmin_c = b_before_own - fr.eps;
+                    last_pid = pid_before_own;
                 }
-                ++k;
+                k_cur = k_last + 1;
+            } else if (fr.mode == 0) {  // the single interval is done
+                done = true;
+            } else if (inline_iv) {
+                if (ov_pid < 0) {
+                    done = true;
+                } else {
+                    visited += 1;
+                    tmin_c = ov_b - fr.eps;
+                    last_pid = ov_pid;
+                    ov_pid = -1;
+                    k_cur = 0;
+                }
+            } else {  // every interval of the window is consumed
+                visited += nvalid;
+                i_cur += nvalid;
+                k_cur = 0;
+                if (nvalid > 0) {
+                    tmin_c = b_lastvalid - fr.eps;
+                    last_pid = pid_lastvalid;
+                }
+                done = (i_cur >= iv_n) && !more;
             }
-        }
-        if (ended) {
-            if (track && ns) {
-                if (F.hist_smem) atomicAdd(&hist[pid], (unsigned long long)ns);
-                else atomicAdd((unsigned long long *)O.ppart + pid, (unsigned long long)ns);
+            if (done) {
+                if (j == 0) {
+                    write_pixel(fr, O, out, acc, samples, visited);
+                    my_samples += (unsigned long long)samples;
+                    my_visited += (unsigned long long)visited;
+                }
+                active = false;
             }
-            if (terminated || fr.mode == 0) {
-                state = ST_IDLE;
-            } else {
-                t_min = t1 - fr.eps;
-                last = pid;
-                state = ST_NEED;
-            }
-        }
-        // ---- a finished ray writes its pixel (K:393-398)
-        if (has_ray && state == ST_IDLE) {
-            has_ray = false;
-            const double r = acc.r + (1.0 - acc.a) * fr.bg[0];
-            const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
-            const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
-            const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
-            double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * out);
-            px[0] = make_double2(r, g);
-            px[1] = make_double2(bl, al);
-            O.samples[out] = samples;
-            O.visited[out] = visited;
-            my_samples += (unsigned long long)samples;
-            my_visited += (unsigned long long)visited;
         }
     }
     // block reduction of the frame totals (R:198-201) and histogram merge
@@ -801,6 +930,8 @@ SceneK make_scene(const TrDeviceScene *s) {
     S.pleaf_ids = s->pleaf_ids;
     S.bnodes = s->bnodes;
     S.pgrid = s->pgrid;
+    S.part_lo = s->part_lo;
+    S.part_hi = s->part_hi;
     S.centering = s->centering;
     for (int a = 0; a < 3; ++a) {
         S.gdim[a] = s->gdim[a];
@@ -822,7 +953,7 @@ int sm_count() {
     return n;
 }
 
-constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * (4 + 8 + 8) + 4 + 4;
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 4 + 4 + 4;
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
 }  // namespace
@@ -885,14 +1016,24 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (chunk > total_rays) chunk = total_rays;
     if (chunk < 32) chunk = 32;
     const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
+    // rays per group of lanes: flags bits 8-11 = log2(G) (0: default 8)
+    const int lg = (frame->flags >> 8) & 0xf;
+    const int gsize = lg ? (1 << lg) : 8;
+    void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
+    switch (gsize) {
+        case 4: march_fn = march_group_kernel<4>; break;
+        case 8: march_fn = march_group_kernel<8>; break;
+        case 16: march_fn = march_group_kernel<16>; break;
+        case 32: march_fn = march_group_kernel<32>; break;
+        default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 4, 8, 16 or 32");
+    }
     cudaError_t e;
-    if (smem > 48 * 1024) {
-        e = cudaFuncSetAttribute(march_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+    if (smem > 48 * 1024 - 12 * 1024) {
+        e = cudaFuncSetAttribute(march_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     }
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_kernel, MARCH_BLOCK, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fn, MARCH_BLOCK, smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     int64_t launches = 0, march_grid = 0;
@@ -903,9 +1044,8 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         char *base = reinterpret_cast<char *>(out->scratch);
         iv.hist = reinterpret_cast<uint32_t *>(base);
         iv.cursor = iv.hist + N_BUCKETS;
-        iv.b = reinterpret_cast<double *>(base + IV_FIXED_BYTES);
-        iv.a = iv.b + (int64_t)IV_CAP * F.n_rays;
-        iv.pid = reinterpret_cast<int32_t *>(iv.a + (int64_t)IV_CAP * F.n_rays);
+        iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
+        iv.pid = reinterpret_cast<int32_t *>(base + IV_FIXED_BYTES);
         iv.cnt = reinterpret_cast<uint32_t *>(iv.pid + (int64_t)IV_CAP * F.n_rays);
         iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
@@ -913,7 +1053,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         e = cudaMemsetAsync(iv.hist, 0, 2 * N_BUCKETS * sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
-        trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv);
+        trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
         order_rays_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(F, iv);
@@ -921,12 +1061,12 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         if (e != cudaSuccess) return cuda_fail(e, "order_rays_kernel launch");
         launches += 2;
         int64_t grid = (int64_t)sm_count() * per_sm;
-        const int64_t need = (F.n_rays + MARCH_BLOCK - 1) / MARCH_BLOCK;
+        const int64_t need = (F.n_rays * gsize + MARCH_BLOCK - 1) / MARCH_BLOCK;
         if (grid > need) grid = need;
         if (grid < 1) grid = 1;
-        march_kernel<<<(unsigned)grid, MARCH_BLOCK, smem, st>>>(S, E, F, iv, *out);
+        march_fn<<<(unsigned)grid, MARCH_BLOCK, smem, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
+        if (e != cudaSuccess) return cuda_fail(e, "march_group_kernel launch");
         ++launches;
         march_grid = grid;
     }

@@ -74,7 +74,8 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     for mode in modes:
         ref = orc.render(cam, mode, par, jitter=jitter)
-        for flags in (0, 1, 2, 3):  # with and without the leaf shortcut and the grid
+        # default, no grid index, and lane groups of 4 / 16 / 32 per ray
+        for flags in (0, 2, 0x200, 0x400, 0x500):
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 
