@@ -74,6 +74,15 @@ typedef struct TrBNode {
     int32_t pad[2];
 } TrBNode;
 
+/* Partition BSP node (pre-order; the left child is the next node).
+ * info >= 0: split on axis info & 3 at `split`, right child info >> 2.
+ * info <  0: leaf holding aux partitions leaf_pids[~info ..]. */
+typedef struct TrKNode {
+    double split;
+    int32_t info;
+    int32_t aux;
+} TrKNode;
+
 /* ------------------------------------------------- host-side builders */
 /* Opaque host object holding variable-size build results. */
 typedef struct TrHostBuf TrHostBuf;
@@ -115,6 +124,16 @@ int tr_bbvh_activity(const TrHostBuf *b, const uint8_t *active, uint8_t *out);
 int tr_bnodes_activity(int64_t n_nodes, const TrBNode *nodes, const uint8_t *active,
                        uint8_t *out);
 
+/* Axis-aligned BSP over the partition boxes (greedy separating planes; the
+ * KD split planes for KD partitions): front-to-back partition enumeration
+ * for the trace pass.  root6 = union box (lo xyz, hi xyz). */
+int tr_kbsp_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out);
+int tr_kbsp_sizes(const TrHostBuf *b, int64_t *sizes2);
+int tr_kbsp_copy(const TrHostBuf *b, TrKNode *nodes, int32_t *leaf_pids, double *root6);
+/* Per-epoch: out[node] = 1 if the subtree holds an active partition. */
+int tr_knodes_activity(int64_t n_nodes, const TrKNode *nodes, const int32_t *leaf_pids,
+                       const uint8_t *active, uint8_t *out);
+
 void tr_host_free(TrHostBuf *b);
 
 /* Pack tet records (host, OpenMP). inv/orig exactly as MeshSampler computes them. */
@@ -155,6 +174,10 @@ typedef struct TrDeviceScene {
     int32_t gdim[3];
     int32_t pad1;
     double gorg[3], gscale[3];
+    const TrKNode *knodes; /* tr_kbsp_* (NULL: trace with the partition BVH) */
+    const int32_t *kleaf_pids;
+    int64_t n_knodes;
+    double kroot[6];
 } TrDeviceScene;
 
 /* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
@@ -165,6 +188,7 @@ typedef struct TrEpoch {
     const double *tf_table;      /* (n_tf, 4) */
     int64_t n_tf;
     double tf_lo, tf_hi;
+    const uint8_t *knode_active; /* (n_knodes,) from tr_knodes_activity, or NULL */
 } TrEpoch;
 
 /* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
@@ -184,6 +208,8 @@ typedef struct TrFrame {
 
 #define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
+#define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
+#define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 8) */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)
@@ -227,6 +253,11 @@ int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t shard_count);
 /* Launch statistics of the last tr_render_frame on this thread:
  * [0] kernels launched, [1] grid blocks, [2] threads per block. */
 int tr_last_launch(int64_t *out3);
+
+/* Kernel event counters accumulated by frames rendered with TR_FLAG_STATS
+ * (rounds, partial rounds, lane samples, found, grid hits, descents, inline
+ * next_interval, pow calls, trace intervals, trace rays).  Synchronizes. */
+int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset);
 
 const char *tr_last_error(void);
 int tr_abi_version(void);

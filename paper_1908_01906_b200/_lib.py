@@ -31,6 +31,8 @@ class TrDeviceScene(C.Structure):
         ("mesh_lo", C.c_double * 3), ("mesh_hi", C.c_double * 3),
         ("pgrid", C.c_void_p), ("gdim", C.c_int32 * 3), ("pad1", C.c_int32),
         ("gorg", C.c_double * 3), ("gscale", C.c_double * 3),
+        ("knodes", C.c_void_p), ("kleaf_pids", C.c_void_p), ("n_knodes", C.c_int64),
+        ("kroot", C.c_double * 6),
     ]
 
 
@@ -38,7 +40,7 @@ class TrEpoch(C.Structure):
     _fields_ = [
         ("active", C.c_void_p), ("bnode_active", C.c_void_p), ("step", C.c_void_p),
         ("tf_table", C.c_void_p), ("n_tf", C.c_int64), ("tf_lo", C.c_double),
-        ("tf_hi", C.c_double),
+        ("tf_hi", C.c_double), ("knode_active", C.c_void_p),
     ]
 
 
@@ -71,9 +73,14 @@ PNODE_DTYPE = np.dtype([("lo0", "<f4", 3), ("hi0", "<f4", 3), ("lo1", "<f4", 3),
 PLEAF_DTYPE = np.dtype([("ex_lo", "<f4", 3), ("ex_hi", "<f4", 3), ("start", "<u4"),
                         ("count", "<u4")])
 BNODE_DTYPE = np.dtype([("box", "<f8", (2, 6)), ("child", "<i4", 2), ("pad", "<i4", 2)])
+KNODE_DTYPE = np.dtype([("split", "<f8"), ("info", "<i4"), ("aux", "<i4")])
 
 TR_FLAG_NO_LEAF_HINT = 1
 TR_FLAG_NO_GRID = 2
+TR_FLAG_STATS = 4
+TR_FLAG_NO_BSP = 8
+STAT_NAMES = ["rounds", "partial_rounds", "lane_samples", "found", "grid_hits", "descents",
+              "inline_intervals", "pow_calls", "trace_intervals", "trace_rays"]
 CHILD_NONE = -2**31
 
 # (name, restype, argtypes) for every symbol include/tetray_b200.h declares
@@ -91,6 +98,10 @@ _SIGNATURES = [
     ("tr_bbvh_copy", C.c_int, [C.c_void_p, C.c_void_p]),
     ("tr_bbvh_activity", C.c_int, [C.c_void_p, c_u8p, c_u8p]),
     ("tr_bnodes_activity", C.c_int, [C.c_int64, C.c_void_p, c_u8p, c_u8p]),
+    ("tr_kbsp_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.POINTER(C.c_void_p)]),
+    ("tr_kbsp_sizes", C.c_int, [C.c_void_p, c_i64p]),
+    ("tr_kbsp_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, c_f64p]),
+    ("tr_knodes_activity", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, c_u8p, c_u8p]),
     ("tr_host_free", None, [C.c_void_p]),
     ("tr_pack_tets", C.c_int, [C.c_int64, c_i64p, c_f64p, c_f64p, c_f64p, C.c_int32, C.c_void_p]),
     ("tr_tf_meta", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int64, C.c_double, C.c_double,
@@ -109,6 +120,7 @@ _SIGNATURES = [
     ("tr_scratch_bytes", C.c_int64, [C.c_int64]),
     ("tr_slots_per_rank", C.c_int64, [C.c_int64, C.c_int64, C.c_int32]),
     ("tr_last_launch", C.c_int, [c_i64p]),
+    ("tr_kernel_stats", C.c_int, [c_i64p, C.c_int32, C.c_int32]),
     ("tr_last_error", C.c_char_p, []),
     ("tr_abi_version", C.c_int, []),
 ]

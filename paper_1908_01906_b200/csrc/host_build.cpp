@@ -414,6 +414,70 @@ BRef b_build(BBuf &O, const double *lo, const double *hi, std::vector<int32_t> &
     return me;
 }
 
+// ====================================================== partition BSP tree
+// Axis-aligned BSP over the partition boxes, built by greedy separating cuts
+// (for KD-derived partitions the original split planes always separate).
+// A set that no plane separates becomes one multi-partition leaf.
+struct KBuf : TrHostBuf {
+    std::vector<TrKNode> nodes;
+    std::vector<int32_t> leaf_pids;
+    double root_lo[3], root_hi[3];
+};
+
+int32_t k_build(KBuf &O, const double *lo, const double *hi, std::vector<int32_t> &ids, int depth) {
+    const int32_t me = (int32_t)O.nodes.size();
+    O.nodes.push_back(TrKNode{});
+    const int64_t n = (int64_t)ids.size();
+    int best_axis = -1;
+    int64_t best_i = -1, best_bal = INT64_MAX;
+    double best_s = 0.0;
+    if (n > 1 && depth < 60) {
+        std::vector<int32_t> ord(ids);
+        for (int a = 0; a < 3; ++a) {
+            std::sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                const double lx = lo[3 * x + a], ly = lo[3 * y + a];
+                return lx < ly || (lx == ly && x < y);
+            });
+            double pref = -INFINITY;
+            for (int64_t i = 1; i < n; ++i) {
+                pref = std::max(pref, hi[3 * ord[i - 1] + a]);
+                const double l = lo[3 * ord[i] + a];
+                if (pref <= l) {
+                    const int64_t bal = std::llabs(2 * i - n);
+                    if (bal < best_bal) { best_bal = bal; best_i = i; best_axis = a; best_s = l; }
+                }
+            }
+        }
+    }
+    if (best_axis < 0) {  // leaf (one partition, or boxes no plane separates)
+        O.nodes[me].info = ~(int32_t)O.leaf_pids.size();
+        O.nodes[me].aux = (int32_t)n;
+        O.nodes[me].split = 0.0;
+        std::sort(ids.begin(), ids.end());
+        O.leaf_pids.insert(O.leaf_pids.end(), ids.begin(), ids.end());
+        return me;
+    }
+    // members split exactly as the winning sweep did: the first best_i by (lo, id)
+    std::vector<int32_t> L, R;
+    {
+        std::vector<int32_t> ord(ids);
+        const int a = best_axis;
+        std::sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+            const double lx = lo[3 * x + a], ly = lo[3 * y + a];
+            return lx < ly || (lx == ly && x < y);
+        });
+        L.assign(ord.begin(), ord.begin() + best_i);
+        R.assign(ord.begin() + best_i, ord.end());
+    }
+    std::vector<int32_t>().swap(ids);
+    O.nodes[me].split = best_s;
+    O.nodes[me].aux = 0;
+    k_build(O, lo, hi, L, depth + 1);  // left child = me + 1 (pre-order)
+    const int32_t r = k_build(O, lo, hi, R, depth + 1);
+    O.nodes[me].info = (r << 2) | best_axis;
+    return me;
+}
+
 // ============================================================ TF metadata
 // numpy's pairwise summation of a contiguous float64 vector (add.reduce).
 double np_pairwise_sum(const double *a, int64_t n) {
@@ -661,6 +725,64 @@ int tr_bbvh_activity(const TrHostBuf *b, const uint8_t *active, uint8_t *out) {
     auto B = dynamic_cast<const BBuf *>(b);
     if (!B) return tr_fail(TR_EINVAL, "tr_bbvh_activity: not a partition BVH");
     return tr_bnodes_activity((int64_t)B->nodes.size(), B->nodes.data(), active, out);
+}
+
+int tr_kbsp_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out) {
+    if (!out || n_parts <= 0 || n_parts >= (int64_t)(INT32_MAX >> 3))
+        return tr_fail(TR_EINVAL, "tr_kbsp_build: invalid arguments");
+    try {
+        KBuf *O = new KBuf();
+        for (int a = 0; a < 3; ++a) { O->root_lo[a] = INFINITY; O->root_hi[a] = -INFINITY; }
+        std::vector<int32_t> ids(n_parts);
+        for (int64_t i = 0; i < n_parts; ++i) {
+            ids[i] = (int32_t)i;
+            for (int a = 0; a < 3; ++a) {
+                O->root_lo[a] = std::min(O->root_lo[a], lo[3 * i + a]);
+                O->root_hi[a] = std::max(O->root_hi[a], hi[3 * i + a]);
+            }
+        }
+        k_build(*O, lo, hi, ids, 0);
+        *out = O;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_kbsp_build: out of host memory");
+    }
+}
+
+int tr_kbsp_sizes(const TrHostBuf *b, int64_t *sizes2) {
+    auto K = dynamic_cast<const KBuf *>(b);
+    if (!K || !sizes2) return tr_fail(TR_EINVAL, "tr_kbsp_sizes: not a BSP");
+    sizes2[0] = (int64_t)K->nodes.size();
+    sizes2[1] = (int64_t)K->leaf_pids.size();
+    return TR_OK;
+}
+
+int tr_kbsp_copy(const TrHostBuf *b, TrKNode *nodes, int32_t *leaf_pids, double *root6) {
+    auto K = dynamic_cast<const KBuf *>(b);
+    if (!K) return tr_fail(TR_EINVAL, "tr_kbsp_copy: not a BSP");
+    if (nodes) std::memcpy(nodes, K->nodes.data(), K->nodes.size() * sizeof(TrKNode));
+    if (leaf_pids) std::memcpy(leaf_pids, K->leaf_pids.data(), K->leaf_pids.size() * sizeof(int32_t));
+    if (root6)
+        for (int a = 0; a < 3; ++a) { root6[a] = K->root_lo[a]; root6[3 + a] = K->root_hi[a]; }
+    return TR_OK;
+}
+
+int tr_knodes_activity(int64_t n_nodes, const TrKNode *nodes, const int32_t *leaf_pids,
+                       const uint8_t *active, uint8_t *out) {
+    if (!nodes || !leaf_pids || !active || !out || n_nodes <= 0)
+        return tr_fail(TR_EINVAL, "tr_knodes_activity: invalid arguments");
+    for (int64_t i = n_nodes - 1; i >= 0; --i) {  // children follow their parent
+        const TrKNode &N = nodes[i];
+        uint8_t any = 0;
+        if (N.info < 0) {
+            const int32_t s = ~N.info;
+            for (int32_t k = 0; k < N.aux && !any; ++k) any = active[leaf_pids[s + k]] != 0;
+        } else {
+            any = (out[i + 1] | out[N.info >> 2]) ? 1 : 0;
+        }
+        out[i] = any;
+    }
+    return TR_OK;
 }
 
 void tr_host_free(TrHostBuf *b) { delete b; }

@@ -52,6 +52,23 @@ constexpr int32_t CHILD_NONE = INT32_MIN;
 constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
 constexpr unsigned FULL = 0xffffffffu;
 
+// Optional kernel statistics (TR_FLAG_STATS): counters read back with
+// tr_kernel_stats().  Indices:
+enum : int {
+    ST_ROUNDS = 0,       // group rounds with a ray
+    ST_PARTIAL,          // rounds with fewer samples than lanes
+    ST_SLOTS,            // lane-samples shaded
+    ST_FOUND,            // samples inside a tet
+    ST_GRID_HIT,         // located through the grid + exclusive box
+    ST_DESCENT,          // full BVH descents
+    ST_INLINE_IV,        // next_interval calls in the march (list overflow)
+    ST_POW,              // pow() evaluations
+    ST_TRACE_IV,         // intervals produced by the trace pass
+    ST_TRACE_RAYS,       // rays traced
+    ST_COUNT
+};
+__device__ unsigned long long g_stats[16];
+
 struct RayD {
     double ox, oy, oz, dx, dy, dz;
     double ix, iy, iz;  // 1/d per axis (valid where d != 0), K:36
@@ -135,6 +152,9 @@ struct SceneK {  // kernel copy of TrDeviceScene
     const double *__restrict__ part_lo;     // (P,3) partition boxes (next_interval's leaf boxes)
     const double *__restrict__ part_hi;
     const int32_t *__restrict__ pgrid;      // uniform-grid leaf candidates
+    const TrKNode *__restrict__ knodes;     // partition BSP (NULL: BVH trace)
+    const int32_t *__restrict__ kleaf_pids;
+    double kroot_lo[3], kroot_hi[3];
     int32_t gdim[3];
     int32_t centering;
     double gorg[3], gscale[3];
@@ -261,7 +281,8 @@ __device__ __forceinline__ int32_t grid_leaf(const SceneK &S, const PQuery &q) {
 // Order: the ray's current exclusive leaf (registers), the grid's candidate
 // leaf, else the full descent.  All three return the lowest containing index.
 __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
-                                             bool use_hint, bool use_grid, double &v) {
+                                             bool use_hint, bool use_grid, double &v,
+                                             bool stats = false) {
     double l[4];
     uint32_t pos;
     bool done = false;
@@ -277,11 +298,13 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
                 pos = scan_leaf_first(S, h.start, h.count, q, l);
                 if (use_hint) hint = h;
                 done = true;
+                if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
         }
     }
     if (!done) {
         int32_t leaf;
+        if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
         pos = locate_full(S, q, l, leaf);
         if (use_hint && leaf >= 0) load_hint(S, leaf, hint);
     }
@@ -318,6 +341,7 @@ __device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t 
 }
 
 struct EpochK {
+    const uint8_t *__restrict__ knode_active;
     const uint8_t *__restrict__ active;
     const uint8_t *__restrict__ bnode_active;
     const double *__restrict__ step;
@@ -397,6 +421,141 @@ __device__ int32_t next_interval(const SceneK &S, const EpochK &E, const RayD &r
     ra = best_a;
     rb = best_b;
     return best_id;
+}
+
+// ------------------------------------------------------ BSP interval trace
+
+constexpr int KBUF = 16;
+constexpr int KSTACK = 64;
+
+// Exact front-to-back interval sequence of one ray from a resumable BSP
+// traversal.  A partition's box lies inside its BSP cell, so the entry of the
+// nearest pending cell lower-bounds the clamped entry of every partition not
+// yet enumerated: next_interval's winner (K:173-230: min (clamped entry, pid)
+// among active partitions with exit > t_min + excl, excluding the last one)
+// is certain once it beats max(that bound, t_min) strictly.
+struct BspTrace {
+    int32_t st_node[KSTACK];
+    double st_tn[KSTACK], st_tf[KSTACK];
+    int sp;
+    int32_t c_pid[KBUF];
+    double c_pa[KBUF], c_pb[KBUF];
+    int nb;
+    bool overflow;
+};
+
+__device__ __forceinline__ double ray_o(const RayD &r, int a) { return a == 0 ? r.ox : (a == 1 ? r.oy : r.oz); }
+__device__ __forceinline__ double ray_d(const RayD &r, int a) { return a == 0 ? r.dx : (a == 1 ? r.dy : r.dz); }
+__device__ __forceinline__ double ray_i(const RayD &r, int a) { return a == 0 ? r.ix : (a == 1 ? r.iy : r.iz); }
+
+__device__ __forceinline__ void bsp_begin(const SceneK &S, const RayD &ray, BspTrace &T) {
+    T.sp = 0;
+    T.nb = 0;
+    T.overflow = false;
+    double r0, r1;
+    slab(ray, S.kroot_lo, S.kroot_hi, r0, r1);
+    if (r0 <= r1 && r1 > 0.0) {
+        T.st_node[0] = 0; T.st_tn[0] = r0; T.st_tf[0] = r1;
+        T.sp = 1;
+    }
+}
+
+// Pop subtrees until one leaf cell has been enumerated into the buffer.
+__device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD &ray, BspTrace &T) {
+    while (T.sp > 0) {
+        --T.sp;
+        int32_t node = T.st_node[T.sp];
+        double tn = T.st_tn[T.sp], tf = T.st_tf[T.sp];
+        bool leaf_done = false;
+        while (true) {
+            if (tf <= 0.0) break;                         // behind the origin: exits <= 0
+            if (E.knode_active && !__ldg(E.knode_active + node)) break;
+            const TrKNode *N = S.knodes + node;
+            const int32_t info = __ldg(&N->info);
+            if (info < 0) {                                // leaf cell: its partitions
+                const int32_t st = ~info, cnt = __ldg(&N->aux);
+                for (int32_t k = 0; k < cnt; ++k) {
+                    const int32_t pid = __ldg(S.kleaf_pids + st + k);
+                    if (!__ldg(E.active + pid)) continue;
+                    const double lo[3] = {__ldg(S.part_lo + 3 * pid), __ldg(S.part_lo + 3 * pid + 1),
+                                          __ldg(S.part_lo + 3 * pid + 2)};
+                    const double hi[3] = {__ldg(S.part_hi + 3 * pid), __ldg(S.part_hi + 3 * pid + 1),
+                                          __ldg(S.part_hi + 3 * pid + 2)};
+                    double pa, pb;
+                    slab(ray, lo, hi, pa, pb);
+                    if (pa > pb || !(pb > 0.0)) continue;
+                    if (T.nb == KBUF) { T.overflow = true; return; }
+                    T.c_pid[T.nb] = pid; T.c_pa[T.nb] = pa; T.c_pb[T.nb] = pb;
+                    ++T.nb;
+                }
+                leaf_done = true;
+                break;
+            }
+            const int axis = info & 3;
+            const double sp = __ldg(&N->split);
+            const int32_t left = node + 1, right = info >> 2;
+            const double d = ray_d(ray, axis), o = ray_o(ray, axis);
+            if (d == 0.0) {                                // parallel: one side, or both on the plane
+                if (o < sp) { node = left; continue; }
+                if (o > sp) { node = right; continue; }
+                if (T.sp == KSTACK) { T.overflow = true; return; }
+                T.st_node[T.sp] = right; T.st_tn[T.sp] = tn; T.st_tf[T.sp] = tf; ++T.sp;
+                node = left;
+                continue;
+            }
+            const double ts = (sp - o) * ray_i(ray, axis);
+            const int32_t nearc = d > 0.0 ? left : right, farc = d > 0.0 ? right : left;
+            if (ts < tn) { node = farc; continue; }
+            if (ts > tf) { node = nearc; continue; }
+            if (T.sp == KSTACK) { T.overflow = true; return; }
+            T.st_node[T.sp] = farc; T.st_tn[T.sp] = ts; T.st_tf[T.sp] = tf; ++T.sp;
+            node = nearc;
+            tf = ts;
+        }
+        if (leaf_done) return;
+    }
+}
+
+// next_interval (K:173-230) from the BSP state; -1 when the ray is done.
+__device__ int32_t bsp_next_interval(const SceneK &S, const EpochK &E, const RayD &ray,
+                                     BspTrace &T, double t_min, double excl, int32_t last,
+                                     double &ra, double &rb) {
+    const double thr = t_min + excl;
+    while (true) {
+        int32_t best = -1;
+        double best_a = INFINITY, best_b = INFINITY;
+        for (int i = 0; i < T.nb; ++i) {
+            const int32_t pid = T.c_pid[i];
+            const double pb = T.c_pb[i];
+            if (pid == last || pb <= thr) continue;
+            const double pa = T.c_pa[i];
+            const double a_cl = (pa > t_min) ? pa : t_min;
+            if (a_cl < best_a || (a_cl == best_a && pid < best)) { best = pid; best_a = a_cl; best_b = pb; }
+        }
+        if (T.sp == 0) {
+            ra = best_a; rb = best_b;
+            return best;
+        }
+        const double tn = T.st_tn[T.sp - 1];
+        const double bound = (tn > t_min) ? tn : t_min;
+        if (best >= 0 && best_a < bound) {
+            ra = best_a; rb = best_b;
+            return best;
+        }
+        bsp_enumerate_next(S, E, ray, T);
+        if (T.overflow) return -1;
+    }
+}
+
+// Drop candidates that no later query can return (exit behind the new t_min).
+__device__ __forceinline__ void bsp_compact(BspTrace &T, double t_min) {
+    int w = 0;
+    for (int i = 0; i < T.nb; ++i) {
+        if (T.c_pb[i] < t_min) continue;
+        T.c_pid[w] = T.c_pid[i]; T.c_pa[w] = T.c_pa[i]; T.c_pb[w] = T.c_pb[i];
+        ++w;
+    }
+    T.nb = w;
 }
 
 // K:300-309 with numba's 64-bit integer promotion.
@@ -522,21 +681,36 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 const double ta = (a > 0.0) ? a : 0.0;
                 if (a <= b && b - ta >= F.f.eps) cost = (b - ta) / F.f.s1 + 1.0;
             } else {
-                double t_min = 0.0;
-                int32_t last = -1;
-                while (true) {
-                    const double excl = (last < 0) ? 0.0 : F.f.eps;
-                    double a, b;
-                    const int32_t pid = next_interval(S, E, ray, t_min, excl, last, a, b);
-                    if (pid < 0) break;
-                    if (n == IV_CAP) { more = true; cost += 4.0 * IV_CAP; break; }
-                    iv.pid[(int64_t)n * F.n_rays + rr] = pid;
-                    ++n;
-                    if (b - a >= F.f.eps)
-                        cost += (b - a) / ((F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1) + 1.0;
-                    t_min = b - F.f.eps;
-                    last = pid;
+                bool use_bsp = S.knodes != nullptr && !(F.f.flags & TR_FLAG_NO_BSP);
+                BspTrace T;
+                if (use_bsp) bsp_begin(S, ray, T);
+                for (int attempt = 0; attempt < 2; ++attempt) {
+                    double t_min = 0.0;
+                    int32_t last = -1;
+                    n = 0; cost = 0.0; more = false;
+                    while (true) {
+                        const double excl = (last < 0) ? 0.0 : F.f.eps;
+                        double a, b;
+                        const int32_t pid = use_bsp
+                            ? bsp_next_interval(S, E, ray, T, t_min, excl, last, a, b)
+                            : next_interval(S, E, ray, t_min, excl, last, a, b);
+                        if (pid < 0) break;
+                        if (n == IV_CAP) { more = true; cost += 4.0 * IV_CAP; break; }
+                        iv.pid[(int64_t)n * F.n_rays + rr] = pid;
+                        ++n;
+                        if (b - a >= F.f.eps)
+                            cost += (b - a) / ((F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1) + 1.0;
+                        t_min = b - F.f.eps;
+                        last = pid;
+                        if (use_bsp) bsp_compact(T, t_min);
+                    }
+                    if (!(use_bsp && T.overflow)) break;
+                    use_bsp = false;  // candidate buffer overflowed: redo with the BVH
                 }
+            }
+            if (F.f.flags & TR_FLAG_STATS) {
+                atomicAdd(&g_stats[ST_TRACE_RAYS], 1ull);
+                atomicAdd(&g_stats[ST_TRACE_IV], (unsigned long long)n);
             }
             if (cost > 0.0) {
                 bucket = cost_bucket(cost);
@@ -607,6 +781,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK) hist[i] = 0ull;
     __syncthreads();
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
+    const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
@@ -673,6 +848,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         // ---- past the stored list (rare): next_interval inline, one interval per window
         const bool inline_iv = active && fr.mode != 0 && i_cur >= iv_n;
         if (inline_iv && ov_pid < 0 && more && j == 0) {
+            if (stats) atomicAdd(&g_stats[ST_INLINE_IV], 1ull);
             double a0, b0;
             ov_pid = next_interval(S, E, ray, tmin_c, (last_pid < 0) ? 0.0 : fr.eps, last_pid,
                                    a0, b0);
@@ -759,12 +935,15 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             LeafHint h;
             h.valid = false;
             double v;
-            if (field_at(S, q, h, false, use_grid, v) != UINT32_MAX) {
+            if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
+            if (field_at(S, q, h, false, use_grid, v, stats) != UINT32_MAX) {
+                if (stats) atomicAdd(&g_stats[ST_FOUND], 1ull);
                 double c[4];
                 tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
                 const double e = sstep / fr.s1;
                 const double x = 1.0 - c[3];
                 ca = 1.0 - ((e == 1.0) ? x : pow(x, e));  // glibc pow(x, 1) == x
+                if (stats && e != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
                 cr = c[0]; cg = c[1]; cb = c[2];
                 found = 1.0;
             }
@@ -777,6 +956,10 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         // outside every tet has ca = c = 0, which leaves acc bit-unchanged;
         // termination is only tested after a found sample, as in K:285-295.
         const int cnt = (int)((R < G) ? R : G);
+        if (stats && active && j == 0) {
+            atomicAdd(&g_stats[ST_ROUNDS], 1ull);
+            if (R < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
+        }
         int taken = cnt;
         bool term = false;
         if (active) {
@@ -932,6 +1115,9 @@ SceneK make_scene(const TrDeviceScene *s) {
     S.pgrid = s->pgrid;
     S.part_lo = s->part_lo;
     S.part_hi = s->part_hi;
+    S.knodes = s->knodes;
+    S.kleaf_pids = s->kleaf_pids;
+    for (int a = 0; a < 3; ++a) { S.kroot_lo[a] = s->kroot[a]; S.kroot_hi[a] = s->kroot[3 + a]; }
     S.centering = s->centering;
     for (int a = 0; a < 3; ++a) {
         S.gdim[a] = s->gdim[a];
@@ -993,6 +1179,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     SceneK S = make_scene(scene);
     EpochK E;
     E.active = epoch->active;
+    E.knode_active = epoch->knode_active;
     E.bnode_active = epoch->bnode_active;
     E.step = epoch->step;
     E.tf = epoch->tf_table;
@@ -1108,6 +1295,21 @@ int tr_scatter_tiles(int64_t width, int64_t height, int32_t count, const double 
         slots_per_rank, src_rgba, src_samples, src_visited, rgba, samples, visited);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "scatter_tiles_kernel launch");
+    return TR_OK;
+}
+
+int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset) {
+    unsigned long long h[16];
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats sync");
+    e = cudaMemcpyFromSymbol(h, g_stats, sizeof h);
+    if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats copy");
+    for (int i = 0; i < n && i < 16; ++i) out[i] = (int64_t)h[i];
+    if (reset) {
+        for (int i = 0; i < 16; ++i) h[i] = 0;
+        e = cudaMemcpyToSymbol(g_stats, h, sizeof h);
+        if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats reset");
+    }
     return TR_OK;
 }
 

@@ -7,6 +7,8 @@ Layout in HBM, all owned by torch tensors:
   pleaves    TrPLeaf[]          32 B: exclusive box (f32, inward) + id range
   pleaf_ids  uint32[]           ascending per leaf
   bnodes     TrBNode[]          112 B BVH2 nodes over partition boxes (f64)
+  knodes     TrKNode[]          16 B BSP nodes over partition boxes (trace pass)
+  pgrid      int32[]            uniform-grid leaf candidates
   scratch    per-ray interval lists of a ray chunk (IV_CAP x 20 B + 4 B per ray)
   epoch      one buffer per (active, sigma, tf) snapshot and (s1, s2, p):
              step f64[P] | tf f64[n,4] | active u8[P] | node activity u8[M]
@@ -102,6 +104,27 @@ def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEA
     return nodes, leaves, ids, grid
 
 
+def build_partition_bsp(lo: np.ndarray, hi: np.ndarray):
+    """Axis-aligned BSP over partition boxes (tr_kbsp_build): nodes, leaf pids, root box."""
+    L = _lib.lib()
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    hi = np.ascontiguousarray(hi, dtype=np.float64)
+    h = C.c_void_p()
+    _lib.check(L.tr_kbsp_build(len(lo), _lib.ptr(lo, C.c_double), _lib.ptr(hi, C.c_double),
+                               C.byref(h)), "tr_kbsp_build")
+    try:
+        sz = np.zeros(2, np.int64)
+        _lib.check(L.tr_kbsp_sizes(h, _lib.ptr(sz, C.c_int64)), "tr_kbsp_sizes")
+        nodes = np.zeros(int(sz[0]), dtype=_lib.KNODE_DTYPE)
+        pids = np.zeros(int(sz[1]), dtype=np.int32)
+        root = np.zeros(6)
+        _lib.check(L.tr_kbsp_copy(h, _lib.vptr(nodes), _lib.vptr(pids), _lib.ptr(root, C.c_double)),
+                   "tr_kbsp_copy")
+    finally:
+        L.tr_host_free(h)
+    return nodes, pids, root
+
+
 def pack_tet_records(mesh, sampler) -> np.ndarray:
     rec = np.empty(mesh.n_tets, dtype=_lib.TET_RECORD_DTYPE)
     orig = np.ascontiguousarray(sampler.tet_orig, dtype=np.float64)
@@ -131,6 +154,10 @@ class Epoch:
         _lib.check(_lib.lib().tr_step_sizes(P, _lib.ptr(sig, C.c_double), float(params.s1),
                                             float(params.s2), float(params.p),
                                             _lib.ptr(step, C.c_double)), "tr_step_sizes")
+        kact = np.empty(dev.n_knodes, dtype=np.uint8)
+        _lib.check(_lib.lib().tr_knodes_activity(dev.n_knodes, _lib.vptr(dev.knodes_host),
+                                                 _lib.vptr(dev.kpids_host), _lib.ptr(act, C.c_uint8),
+                                                 _lib.ptr(kact, C.c_uint8)), "tr_knodes_activity")
         bact = np.empty(dev.n_bnodes, dtype=np.uint8)
         _lib.check(_lib.lib().tr_bnodes_activity(dev.n_bnodes, _lib.vptr(dev.bnodes_host),
                                                  _lib.ptr(act, C.c_uint8), _lib.ptr(bact, C.c_uint8)),
@@ -143,7 +170,8 @@ class Epoch:
         o_tf = a64(8 * P)
         o_act = a64(o_tf + table.nbytes)
         o_bact = a64(o_act + P)
-        nbytes = a64(o_bact + dev.n_bnodes)
+        o_kact = a64(o_bact + dev.n_bnodes)
+        nbytes = a64(o_kact + dev.n_knodes)
         host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
         hv[:] = 0
@@ -151,6 +179,7 @@ class Epoch:
         hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
         hv[o_act:o_act + P] = act
         hv[o_bact:o_bact + dev.n_bnodes] = bact
+        hv[o_kact:o_kact + dev.n_knodes] = kact
         self.h2d_bytes = nbytes
         self.host = host
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev.device)
@@ -158,7 +187,7 @@ class Epoch:
         base = self.buf.data_ptr()
         self.desc = _lib.TrEpoch(active=base + o_act, bnode_active=base + o_bact, step=base,
                                  tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
-                                 tf_hi=self.tf_hi)
+                                 tf_hi=self.tf_hi, knode_active=base + o_kact)
         self.step_host = step
 
 
@@ -208,7 +237,10 @@ class DeviceScene:
             if not (isinstance(bnodes, np.ndarray) and bnodes.dtype == _lib.BNODE_DTYPE):
                 from .traversal import build_bvh_over_boxes
                 bnodes = build_bvh_over_boxes(part_lo, part_hi)
+            knodes, kpids, kroot = build_partition_bsp(part_lo, part_hi)
             self.build_s = time.perf_counter() - t0
+            self.knodes_host, self.kpids_host = knodes, kpids
+            self.n_knodes = int(len(knodes))
             self.bnodes_host = np.ascontiguousarray(bnodes)
             self.n_parts = int(part_lo.shape[0])
             self.n_bnodes = int(len(bnodes))
@@ -224,11 +256,14 @@ class DeviceScene:
             self.t_plo = _upload(part_lo, device)
             self.t_phi = _upload(part_hi, device)
             self.t_grid = _upload(grid.cells, device)
+            self.t_knodes = _upload(knodes, device)
+            self.t_kpids = _upload(kpids, device)
             self.grid = grid
             torch.cuda.synchronize(device)
         self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
                                                       self.t_pids, self.t_bnodes, self.t_plo,
-                                                      self.t_phi, self.t_grid))
+                                                      self.t_phi, self.t_grid, self.t_knodes,
+                                                      self.t_kpids))
         self.desc = _lib.TrDeviceScene(
             tets=self.t_tets.data_ptr(), pnodes=self.t_pnodes.data_ptr(),
             pleaves=self.t_pleaves.data_ptr(), pleaf_ids=self.t_pids.data_ptr(),
@@ -238,7 +273,9 @@ class DeviceScene:
             n_bnodes=self.n_bnodes,
             mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi),
             pgrid=self.t_grid.data_ptr(), gdim=(C.c_int32 * 3)(*grid.dims),
-            gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale))
+            gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale),
+            knodes=self.t_knodes.data_ptr(), kleaf_pids=self.t_kpids.data_ptr(),
+            n_knodes=self.n_knodes, kroot=(C.c_double * 6)(*kroot))
         self._epochs: OrderedDict = OrderedDict()
         self._frames: dict = {}
 
