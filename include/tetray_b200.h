@@ -210,9 +210,9 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
+#define TR_FLAG_HIST_SMEM 16   /* per-partition counts in a per-CTA shared copy (else global) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 8);
- * bits 12-13: 1 + log2 of the samples each lane shades per round (0 = 4);
- * bits 14-15: minimum resident CTAs per SM (0 = 2).  Tuning knobs only:
+ * bits 12-13: minimum resident CTAs per SM (0 = 2).  Tuning knobs only:
  * every setting renders the same frame. */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)

@@ -426,7 +426,7 @@ __device__ int32_t next_interval(const SceneK &S, const EpochK &E, const RayD &r
 // ------------------------------------------------------ BSP interval trace
 
 constexpr int KBUF = 16;
-constexpr int KSTACK = 40;
+constexpr int KSTACK = 64;
 
 // Exact front-to-back interval sequence of one ray from a resumable BSP
 // traversal.  A partition's box lies inside its BSP cell, so the entry of the
@@ -765,20 +765,13 @@ order_rays_kernel(FrameK F, IvBuf iv) {
 // independently, then the group composites the G results in sample order
 // with the exact early-termination rule (K:285-295).  Lanes whose group has
 // no ray take part in the collectives with empty windows.
-template <int G, int SS, int MINB>
-__global__ void __launch_bounds__(MARCH_BLOCK, MINB)
+template <int G>
+__global__ void __launch_bounds__(MARCH_BLOCK, 2)
 march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
-    constexpr int SPR = G * SS;                   // samples per group round
     extern __shared__ unsigned long long hist[];  // [n_parts] when F.hist_smem
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
-    // shaded samples of a round (lane j holds samples j*SS .. j*SS+SS-1):
-    // ca (-1: outside every tet), r, g, b
-    __shared__ double shade[MARCH_BLOCK * SS][4];
-    // the round's interval window, one entry per lane
-    __shared__ double win_a[MARCH_BLOCK], win_step[MARCH_BLOCK];
-    __shared__ long long win_incl[MARCH_BLOCK], win_rem[MARCH_BLOCK];
-    __shared__ int32_t win_pid[MARCH_BLOCK];
+    __shared__ double shade[MARCH_BLOCK][5];      // per-lane sample result: ca, r, g, b, (found)
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G;                   // lane in group
@@ -808,9 +801,6 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     int32_t ov_pid = -1;                       // inline interval past the list
     double ov_a = 0.0, ov_b = 0.0;
     double m0_a = 0.0, m0_b = 0.0;             // reference mode's single interval
-    LeafHint hint;                             // per-lane point-location cache (any ray)
-    hint.valid = false;
-    const bool use_hint = !(fr.flags & TR_FLAG_NO_LEAF_HINT);
 
     while (true) {
         // ---- refill: one queue slot per group that needs a ray
@@ -906,6 +896,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             a = (a > tmin_j) ? a : tmin_j;
         }
         if (valid && fr.mode == 2) step = __ldg(E.step + pid);
+        const double e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
         const bool marchable = valid && (b - a >= fr.eps);
         const int64_t n_i = marchable ? interval_samples(a, b, step, phase) : 0;
         int64_t rem = n_i - ((j == 0) ? k_cur : 0);
@@ -920,90 +911,84 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         const unsigned vbits = (__ballot_sync(FULL, valid) >> gbase) &
                                ((G == 32) ? FULL : ((1u << G) - 1u));
         const int nvalid = __popc(vbits);
-        win_a[threadIdx.x] = a;
-        win_step[threadIdx.x] = step;
-        win_incl[threadIdx.x] = incl;
-        win_rem[threadIdx.x] = rem;
-        win_pid[threadIdx.x] = pid;
-        __syncwarp();
-        const int cnt = (int)((R < SPR) ? R : SPR);
-        const int wb = threadIdx.x - j;           // my group's window / shade base
-
-        // ---- shade my SS consecutive samples (K:277-290); locality: the
-        // lane's leaf hint usually proves the next sample's leaf at once
-        int own = 0;
-#pragma unroll 1
-        for (int m = 0; m < SS; ++m) {
-            const int sidx = j * SS + m;
-            double ca = -1.0, cr = 0.0, cg = 0.0, cb = 0.0;
-            if (active && sidx < cnt) {
-                while (win_incl[wb + own] <= sidx) ++own;
-                const int64_t first = win_incl[wb + own] - win_rem[wb + own];
-                const int64_t sk = (int64_t)sidx - first + ((own == 0) ? k_cur : 0);
-                const double sa = win_a[wb + own], sstep = win_step[wb + own];
-                const double t = sa + ((double)sk + phase) * sstep;
-                const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy,
-                                            ray.oz + t * ray.dz);
-                double v;
-                if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
-                if (field_at(S, q, hint, use_hint, use_grid, v, stats) != UINT32_MAX) {
-                    if (stats) atomicAdd(&g_stats[ST_FOUND], 1ull);
-                    double c[4];
-                    tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
-                    const double e = sstep / fr.s1;
-                    const double x = 1.0 - c[3];
-                    ca = 1.0 - ((e == 1.0) ? x : pow(x, e));  // glibc pow(x, 1) == x
-                    if (stats && e != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
-                    cr = c[0]; cg = c[1]; cb = c[2];
-                }
-            }
-            double *mine = shade[threadIdx.x * SS + m];
-            mine[0] = ca; mine[1] = cr; mine[2] = cg; mine[3] = cb;
+        // my sample is the j-th of the round: owner = first window lane with incl > j
+        int owner = G;
+        int64_t own_incl = 0, own_rem = 0;
+#pragma unroll
+        for (int l = G - 1; l >= 0; --l) {
+            const int64_t x = __shfl_sync(FULL, incl, gbase + l);
+            const int64_t y = __shfl_sync(FULL, rem, gbase + l);
+            if (x > j) { owner = l; own_incl = x; own_rem = y; }
         }
+        const bool has = active && (int64_t)j < R;
+        const int src = gbase + (owner < G ? owner : 0);
+        const double sa = __shfl_sync(FULL, a, src);
+        const double sstep = __shfl_sync(FULL, step, src);
+        const double se = __shfl_sync(FULL, e_win, src);
+        const int32_t spid = __shfl_sync(FULL, pid, src);
+        const int64_t sfirst = own_incl - own_rem;  // round index of the owner's first sample
+        const int64_t sk = (int64_t)j - sfirst + ((owner == 0) ? k_cur : 0);
+
+        // ---- shade my sample (K:277-290)
+        double ca = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, found = 0.0;
+        if (has) {
+            const double t = sa + ((double)sk + phase) * sstep;
+            const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy, ray.oz + t * ray.dz);
+            LeafHint h;
+            h.valid = false;
+            double v;
+            if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
+            if (field_at(S, q, h, false, use_grid, v, stats) != UINT32_MAX) {
+                if (stats) atomicAdd(&g_stats[ST_FOUND], 1ull);
+                double c[4];
+                tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+                const double x = 1.0 - c[3];
+                ca = 1.0 - ((se == 1.0) ? x : pow(x, se));  // glibc pow(x, 1) == x
+                if (stats && se != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
+                cr = c[0]; cg = c[1]; cb = c[2];
+                found = 1.0;
+            }
+        }
+        double *mine = shade[threadIdx.x];
+        mine[0] = ca; mine[1] = cr; mine[2] = cg; mine[3] = cb; mine[4] = found;
         __syncwarp();
 
-        // ---- composite the round in sample order (K:285-295); termination
-        // is only tested after a sample inside a tet (ca >= 0)
+        // ---- composite the round in sample order (K:285-295).  A sample
+        // outside every tet has ca = c = 0, which leaves acc bit-unchanged;
+        // termination is only tested after a found sample, as in K:285-295.
+        const int cnt = (int)((R < G) ? R : G);
         if (stats && active && j == 0) {
             atomicAdd(&g_stats[ST_ROUNDS], 1ull);
-            if (R < SPR) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
+            if (R < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
         }
         int taken = cnt;
         bool term = false;
         if (active) {
-            const double(*grp)[4] = shade + wb * SS;
+            const double(*grp)[5] = shade + (threadIdx.x - j);
             for (int m = 0; m < cnt; ++m) {
-                const double cam = grp[m][0];
-                if (cam < 0.0) continue;
-                const double w = (1.0 - acc.a) * cam;
+                const double w = (1.0 - acc.a) * grp[m][0];
                 acc.r += w * grp[m][1];
                 acc.g += w * grp[m][2];
                 acc.b += w * grp[m][3];
                 acc.a += w;
-                if (acc.a >= fr.term) { taken = m + 1; term = true; break; }
+                if (grp[m][4] != 0.0 && acc.a >= fr.term) { taken = m + 1; term = true; break; }
             }
         }
         __syncwarp();
-        // per-partition samples: lane l adds the taken samples of window interval l
-        if (track && valid && active) {
-            const int64_t first = incl - rem;
-            const int64_t hi_s = (incl < taken) ? incl : (int64_t)taken;
-            const int64_t c = hi_s - first;
-            if (c > 0) {
-                if (F.hist_smem) atomicAdd(&hist[pid], (unsigned long long)c);
-                else atomicAdd((unsigned long long *)O.ppart + pid, (unsigned long long)c);
-            }
+        // per-partition samples: the first taken sample of each interval's run adds the run
+        if (track && has && (int64_t)j < taken && (int64_t)j == sfirst) {
+            const int64_t c = ((own_incl < taken) ? own_incl : (int64_t)taken) - (int64_t)j;
+            if (F.hist_smem) atomicAdd(&hist[spid], (unsigned long long)c);
+            else atomicAdd((unsigned long long *)O.ppart + spid, (unsigned long long)c);
         }
 
-        // ---- advance the group's cursor (collectives before any divergence)
-        const int64_t lastidx = term ? (int64_t)taken - 1 : (int64_t)SPR - 1;
-        const unsigned ob = (__ballot_sync(FULL, valid && incl > lastidx) >> gbase) &
-                            ((G == 32) ? FULL : ((1u << G) - 1u));
-        const int own_last = ob ? __ffs(ob) - 1 : 0;
-        const int64_t ol_incl = __shfl_sync(FULL, incl, gbase + own_last);
-        const int64_t ol_rem = __shfl_sync(FULL, rem, gbase + own_last);
-        const double b_before_own = __shfl_sync(FULL, prev_b, gbase + own_last);
-        const int32_t pid_before_own = __shfl_sync(FULL, prev_pid, gbase + own_last);
+        // ---- advance the group's cursor (all shuffles before any divergence)
+        const int lastj = (taken > 0) ? taken - 1 : 0;
+        const int own_last = __shfl_sync(FULL, owner, gbase + lastj);
+        const int64_t k_last = __shfl_sync(FULL, sk, gbase + lastj);
+        const int ol = (own_last < G) ? own_last : 0;
+        const double b_before_own = __shfl_sync(FULL, prev_b, gbase + ol);
+        const int32_t pid_before_own = __shfl_sync(FULL, prev_pid, gbase + ol);
         const int lv = (nvalid > 0) ? nvalid - 1 : 0;
         const double b_lastvalid = __shfl_sync(FULL, b, gbase + lv);
         const int32_t pid_lastvalid = __shfl_sync(FULL, pid, gbase + lv);
@@ -1013,14 +998,13 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             if (term) {  // K:388-389: the terminating interval is the last one visited
                 if (fr.mode != 0) visited += own_last + 1;
                 done = true;
-            } else if (R > SPR) {  // interval own_last continues in the next round
+            } else if (R > G) {  // interval own_last continues in the next round
                 if (fr.mode != 0 && !inline_iv && own_last > 0) {
                     visited += own_last;
                     i_cur += own_last;
                     tmin_c = b_before_own - fr.eps;
                     last_pid = pid_before_own;
                 }
-                const int64_t k_last = lastidx - (ol_incl - ol_rem) + ((own_last == 0) ? k_cur : 0);
                 k_cur = k_last + 1;
             } else if (fr.mode == 0) {  // the single interval is done
                 done = true;
@@ -1211,7 +1195,9 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (F.my_tiles < 0) F.my_tiles = 0;
     F.n_parts = (int32_t)scene->n_parts;
     const bool track = frame->track_ppart && frame->mode != 0;
-    F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX) ? 1 : 0;
+    // per-partition counts: global 64-bit RED atomics by default (a 64-bit
+    // shared atomic add is a CAS loop on sm_100a and the CTA copy costs L1)
+    F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX && (frame->flags & TR_FLAG_HIST_SMEM)) ? 1 : 0;
     const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
     // ray chunk = what the scratch interval lists can hold
     if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + IV_FIXED_BYTES)
@@ -1220,22 +1206,17 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (chunk > total_rays) chunk = total_rays;
     if (chunk < 32) chunk = 32;
     const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
-    // rays per group of lanes: flags bits 8-11 = log2(G) (0: default 8);
-    // bits 12-13: samples per lane per round (0: default 4);
-    // bits 14-15: minimum resident CTAs per SM (0: default 2)
+    // rays per group of lanes: flags bits 8-11 = log2(G) (0: default 8)
     const int lg = (frame->flags >> 8) & 0xf;
     const int gsize = lg ? (1 << lg) : 8;
-    const int ss = ((frame->flags >> 12) & 0x3) ? (1 << (((frame->flags >> 12) & 0x3) - 1)) : 4;
-    const int minb = ((frame->flags >> 14) & 0x3) ? ((frame->flags >> 14) & 0x3) : 2;
-    void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = nullptr;
-#define TR_PICK(GS, SSV, MB) \
-    if (gsize == GS && ss == SSV && minb == MB) march_fn = march_group_kernel<GS, SSV, MB>;
-    TR_PICK(4, 1, 2) TR_PICK(4, 2, 2) TR_PICK(4, 4, 2)
-    TR_PICK(8, 1, 2) TR_PICK(8, 2, 2) TR_PICK(8, 4, 2) TR_PICK(8, 4, 1) TR_PICK(8, 2, 3)
-    TR_PICK(16, 1, 2) TR_PICK(16, 2, 2) TR_PICK(16, 4, 2)
-    TR_PICK(32, 1, 2) TR_PICK(32, 2, 2)
-#undef TR_PICK
-    if (!march_fn) return tr_fail(TR_EINVAL, "tr_render_frame: unsupported group size / samples per lane");
+    void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
+    switch (gsize) {
+        case 4: march_fn = march_group_kernel<4>; break;
+        case 8: march_fn = march_group_kernel<8>; break;
+        case 16: march_fn = march_group_kernel<16>; break;
+        case 32: march_fn = march_group_kernel<32>; break;
+        default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 4, 8, 16 or 32");
+    }
     cudaError_t e;
     e = cudaFuncSetAttribute(march_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");

@@ -76,7 +76,7 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
         ref = orc.render(cam, mode, par, jitter=jitter)
         # default, no grid index, and lane groups of 4 / 16 / 32 per ray
         # default, no grid, no BSP, no leaf hint, and other lane-group shapes
-        for flags in (0, 2, 8, 1, 0x200, 0x1000, 0x2400, 0x1500):
+        for flags in (0, 2, 8, 16, 0x200, 0x400, 0x500, 0x3000):
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 
