@@ -241,6 +241,8 @@ def main():
           for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    mev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -249,7 +251,7 @@ def main():
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
             ev[k][0].record(stream)
-            runner.run(stream, kernel_events=kev[k])
+            runner.run(stream, kernel_events=kev[k], march_events=mev[k])
             ev[k][1].record(stream)
         torch.cuda.synchronize()
         time.sleep(0.1)
@@ -257,14 +259,16 @@ def main():
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     kern_ms = [a.elapsed_time(b) for a, b in kev]
+    march_ms = [a.elapsed_time(b) for a, b in mev]
     t_local = sum(step_ms) / 1000.0
     k_local = sum(kern_ms) / len(kern_ms) / 1000.0
+    m_local = sum(march_ms) / len(march_ms) / 1000.0
     if world > 1:
-        t = torch.tensor([t_local, k_local], dtype=torch.float64, device=dev)
+        t = torch.tensor([t_local, k_local, m_local], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        t_max, k_max = float(t[0]), float(t[1])
+        t_max, k_max, m_max = float(t[0]), float(t[1]), float(t[2])
     else:
-        t_max, k_max = t_local, k_local
+        t_max, k_max, m_max = t_local, k_local, m_local
     clocks = clk.summary()
     value = total_samples * args.steps / t_max
 
@@ -273,11 +277,15 @@ def main():
     my_samples = runner.local_samples()
     my_pixels = runner.local_pixels()
     alg_bytes = RECORD_BYTES[int(scene.mesh.centering)] * my_samples + PIXEL_BYTES * my_pixels
-    achieved = alg_bytes / k_max / 1e9
+    achieved = alg_bytes / m_max / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
             "frac": achieved / hbm, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-            "kernel": "render_frame_kernel", "kernel_ms": k_max * 1e3,
-            "alg_bytes_per_launch": alg_bytes}
+            "kernel": "march_group_kernel", "kernel_ms": m_max * 1e3,
+            "frame_kernels_ms": k_max * 1e3,
+            "frame_frac": alg_bytes / k_max / 1e9 / hbm,
+            "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_model": f"{RECORD_BYTES[int(scene.mesh.centering)]} B/sample x "
+                               f"{my_samples} samples + {PIXEL_BYTES} B/pixel x {my_pixels} pixels"}
 
     # e2e through render(): epoch H2D + outputs D2H inside the timed region
     e2e = None

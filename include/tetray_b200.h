@@ -211,7 +211,7 @@ typedef struct TrFrame {
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
 #define TR_FLAG_HIST_SMEM 16   /* per-partition counts in a per-CTA shared copy (else global) */
-/* flags bits 8-11: log2 of the lanes that march one ray together (0 = 8);
+/* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
  * bits 12-13: minimum resident CTAs per SM (0 = 2).  Tuning knobs only:
  * every setting renders the same frame. */
 
@@ -228,6 +228,8 @@ typedef struct TrOutputs {
     uint32_t *work;
     void *scratch;          /* interval lists (modes 1, 2); size via tr_scratch_bytes */
     int64_t scratch_bytes;  /* smaller than a frame's need => the frame runs in ray chunks */
+    void *ev_march_begin;   /* optional cudaEvent_t recorded before the first march launch */
+    void *ev_march_end;     /* optional cudaEvent_t recorded after the last march launch */
 } TrOutputs;
 
 /* Scratch bytes for n_rays rays in one chunk (pass W*H rounded up to 32). */

@@ -63,6 +63,7 @@ class TrOutputs(C.Structure):
         ("rgba", C.c_void_p), ("samples", C.c_void_p), ("visited", C.c_void_p),
         ("ppart", C.c_void_p), ("totals", C.c_void_p), ("work", C.c_void_p),
         ("scratch", C.c_void_p), ("scratch_bytes", C.c_int64),
+        ("ev_march_begin", C.c_void_p), ("ev_march_end", C.c_void_p),
     ]
 
 

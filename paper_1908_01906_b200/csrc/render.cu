@@ -1208,7 +1208,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
     // rays per group of lanes: flags bits 8-11 = log2(G) (0: default 8)
     const int lg = (frame->flags >> 8) & 0xf;
-    const int gsize = lg ? (1 << lg) : 8;
+    const int gsize = lg ? (1 << lg) : 4;
     void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
     switch (gsize) {
         case 4: march_fn = march_group_kernel<4>; break;
@@ -1252,11 +1252,19 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         const int64_t need = (F.n_rays * gsize + MARCH_BLOCK - 1) / MARCH_BLOCK;
         if (grid > need) grid = need;
         if (grid < 1) grid = 1;
+        if (out->ev_march_begin && r0 == 0) {
+            e = cudaEventRecord((cudaEvent_t)out->ev_march_begin, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(begin)");
+        }
         march_fn<<<(unsigned)grid, MARCH_BLOCK, smem, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "march_group_kernel launch");
         ++launches;
         march_grid = grid;
+        if (out->ev_march_end && r0 + chunk >= total_rays) {
+            e = cudaEventRecord((cudaEvent_t)out->ev_march_end, st);
+            if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(end)");
+        }
     }
     g_last_launch[0] = launches;
     g_last_launch[1] = march_grid;

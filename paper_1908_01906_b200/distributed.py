@@ -118,15 +118,28 @@ class ShardedFrame:
             self.local = None
 
     def launches_per_step(self) -> int:
-        return 2 if self.compact else 1
+        """Our kernels per frame: trace + order + march per ray chunk, plus
+        the tile scatter when sharded."""
+        n = self.w * self.h if not self.compact else self.slots * TILE_PIXELS
+        chunks = max(1, -(-n // (1 << 20)))
+        return 3 * chunks + (1 if self.compact else 0)
 
-    def run(self, stream, kernel_events=None):
+    def run(self, stream, kernel_events=None, march_events=None):
+        """One frame.  kernel_events brackets the whole render call (trace +
+        order + march kernels); march_events the march kernel alone."""
         fb = self.fb
         fb.counters.zero_()
+        out = fb.outputs()
+        if march_events is not None:
+            for ev in march_events:  # torch creates its CUDA event lazily on first record
+                if not ev.cuda_event:
+                    ev.record(stream)
+            out.ev_march_begin = march_events[0].cuda_event
+            out.ev_march_end = march_events[1].cuda_event
         if kernel_events is not None:
             kernel_events[0].record(stream)
         _lib.check(_lib.lib().tr_render_frame(C.byref(self.dscene.desc), C.byref(self.epoch.desc),
-                                              C.byref(self.frame), C.byref(fb.outputs()),
+                                              C.byref(self.frame), C.byref(out),
                                               C.c_void_p(stream.cuda_stream)), "tr_render_frame")
         if kernel_events is not None:
             kernel_events[1].record(stream)
