@@ -70,7 +70,7 @@ def peaks():
 
 def ncu_traffic():
     """DRAM bytes per render launch from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "ncu_render_frame.json"
+    p = ROOT / "profiles" / "r01" / "ncu_dram.json"
     if not p.exists():
         return None
     try:
