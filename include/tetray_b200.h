@@ -154,6 +154,15 @@ int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p
 double tr_step_size(double s1, double s2, double p, double sigma);
 double tr_opacity_correction(double alpha, double s, double s1);
 
+/* glibc pow restated (csrc/glibc_pow.cuh): 1 if the tables were found in the
+ * installed libm at build time (the device then evaluates the per-sample
+ * opacity correction bit-identically to the reference). */
+int tr_pow_glibc_available(void);
+/* Host evaluation of the restatement; *exact = 0 outside the restated path. */
+double tr_pow_glibc_host(double x, double y, int32_t *exact);
+/* Device evaluation over n argument pairs (device pointers). */
+int tr_pow_glibc_batch(int64_t n, const double *x, const double *y, double *out, void *stream);
+
 /* ------------------------------------------------- device entry points */
 
 /* Device-resident scene (device pointers, owned by the caller). */

@@ -16,7 +16,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtetray_b200.so"
 SOURCES = ["render.cu", "host_build.cpp", "common.cpp"]
-HEADERS = [ROOT / "include" / "tetray_b200.h", CSRC / "tr_internal.h"]
+HEADERS = [ROOT / "include" / "tetray_b200.h", CSRC / "tr_internal.h", CSRC / "glibc_pow.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -44,7 +44,9 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_library(force: bool = False, verbose: bool = False) -> Path:
-    deps = [CSRC / s for s in SOURCES] + HEADERS
+    from . import _glibc_pow
+    _glibc_pow.write_header()  # glibc pow tables from the installed libm
+    deps = [CSRC / s for s in SOURCES] + HEADERS + [CSRC / "glibc_pow_data.h"]
     if not force and not _stale(LIB, deps):
         return LIB
     tmp = LIB.with_suffix(".so.tmp")

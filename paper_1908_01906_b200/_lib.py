@@ -110,6 +110,9 @@ _SIGNATURES = [
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),
     ("tr_step_size", C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double]),
     ("tr_opacity_correction", C.c_double, [C.c_double, C.c_double, C.c_double]),
+    ("tr_pow_glibc_available", C.c_int, []),
+    ("tr_pow_glibc_host", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int32)]),
+    ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_render_frame", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch),
                                   C.POINTER(TrFrame), C.POINTER(TrOutputs), C.c_void_p]),
     ("tr_field_at_many", C.c_int, [C.POINTER(TrDeviceScene), C.c_int64, C.c_void_p, C.c_void_p,

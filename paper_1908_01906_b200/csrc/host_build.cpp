@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "glibc_pow.cuh"
 #include "tetray_b200.h"
 #include "tr_internal.h"
 
@@ -876,6 +877,30 @@ int tr_tf_meta(int64_t n_parts, const double *vrange, const double *T, int64_t n
     return TR_OK;
 }
 
+#if TR_HAVE_GLIBC_POW
+static const uint64_t H_POW_LOG[] = TR_POW_LOG_INIT;
+static const uint64_t H_POW_EXP_HEAD[] = TR_POW_EXP_HEAD_INIT;
+static const uint64_t H_POW_EXP_TAB[] = TR_POW_EXP_TAB_INIT;
+#endif
+
+int tr_pow_glibc_available(void) { return TR_HAVE_GLIBC_POW; }
+
+double tr_pow_glibc_host(double x, double y, int32_t *exact) {
+#if TR_HAVE_GLIBC_POW
+    if (!tr_pow_glibc_supported(x, y)) {
+        if (exact) *exact = 0;
+        return std::pow(x, y);
+    }
+    bool ex = false;
+    const double r = tr_pow_glibc(x, y, H_POW_LOG, H_POW_EXP_HEAD, H_POW_EXP_TAB, &ex);
+    if (exact) *exact = ex ? 1 : 0;
+    return r;
+#else
+    if (exact) *exact = 0;
+    return std::pow(x, y);
+#endif
+}
+
 double tr_step_size(double s1, double s2, double p, double sigma) {
     double m = (1.0 < sigma) ? 1.0 : sigma;  // Python min(sigma, 1.0)
     double v = s1 + (s2 - s1) * std::pow(std::fabs(m - 1.0), p);
@@ -888,6 +913,7 @@ double tr_opacity_correction(double alpha, double s, double s1) {
 
 int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out) {
     if (n < 0 || (n > 0 && (!sigma || !out))) return tr_fail(TR_EINVAL, "tr_step_sizes: invalid arguments");
+#pragma omp parallel for schedule(static) if (n > 2048)
     for (int64_t i = 0; i < n; ++i) out[i] = tr_step_size(s1, s2, p, sigma[i]);
     return TR_OK;
 }

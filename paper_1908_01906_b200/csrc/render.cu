@@ -35,6 +35,7 @@
 #include <cstdio>
 #include <string>
 
+#include "glibc_pow.cuh"
 #include "tetray_b200.h"
 #include "tr_internal.h"
 
@@ -141,6 +142,32 @@ __device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, 
     const double l0 = 1.0 - l1 - l2 - l3;
     l[0] = l0; l[1] = l1; l[2] = l2; l[3] = l3;
     return l0 >= -BARY_TOL && l1 >= -BARY_TOL && l2 >= -BARY_TOL && l3 >= -BARY_TOL;
+}
+
+#if TR_HAVE_GLIBC_POW
+__device__ const unsigned long long d_pow_log[] = TR_POW_LOG_INIT;
+__device__ const unsigned long long d_pow_ehead[] = TR_POW_EXP_HEAD_INIT;
+__device__ const unsigned long long d_pow_etab[] = TR_POW_EXP_TAB_INIT;
+#endif
+
+// x**y as the reference computes it (glibc pow, K:22 / K:27): the restated
+// glibc main path where it applies, CUDA pow elsewhere (never reached for
+// opacity correction: x = 1 - alpha in [0, 1], y = step/s1 in [1, 2^63)).
+__device__ __forceinline__ double ref_pow(double x, double y) {
+#if TR_HAVE_GLIBC_POW
+    if (tr_pow_glibc_supported(x, y)) {
+        bool exact;
+        const double r = tr_pow_glibc(x, y, (const uint64_t *)d_pow_log,
+                                      (const uint64_t *)d_pow_ehead, (const uint64_t *)d_pow_etab,
+                                      &exact);
+        // |y log x| >= 512: glibc under/overflows; for x < 1 the result is
+        // < 2^-738, so 1 - pow is 1.0 either way
+        if (exact || x < 1.0) return r;
+    } else if (x == 0.0 && y > 0.0) {
+        return 0.0;
+    }
+#endif
+    return pow(x, y);
 }
 
 struct SceneK {  // kernel copy of TrDeviceScene
@@ -943,7 +970,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 double c[4];
                 tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
                 const double x = 1.0 - c[3];
-                ca = 1.0 - ((se == 1.0) ? x : pow(x, se));  // glibc pow(x, 1) == x
+                ca = 1.0 - ((se == 1.0) ? x : ref_pow(x, se));  // glibc pow(x, 1) == x
                 if (stats && se != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
                 cr = c[0]; cg = c[1]; cb = c[2];
                 found = 1.0;
@@ -1070,6 +1097,13 @@ __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restri
         vals[i] = v;
         if (tet) tet[i] = pos != UINT32_MAX ? (int64_t)__ldg(S.pleaf_ids + pos) : -1;
     }
+}
+
+__global__ void pow_batch_kernel(int64_t n, const double *__restrict__ x,
+                                 const double *__restrict__ y, double *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = ref_pow(x[i], y[i]);
 }
 
 __global__ void scatter_tiles_kernel(int64_t width, int64_t height, int64_t tiles_x,
@@ -1319,6 +1353,19 @@ int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset) {
         e = cudaMemcpyToSymbol(g_stats, h, sizeof h);
         if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats reset");
     }
+    return TR_OK;
+}
+
+int tr_pow_glibc_batch(int64_t n, const double *x, const double *y, double *out, void *stream) {
+    if (n < 0 || (n > 0 && (!x || !y || !out)))
+        return tr_fail(TR_EINVAL, "tr_pow_glibc_batch: invalid arguments");
+    if (n == 0) return TR_OK;
+    int64_t grid = (n + 255) / 256;
+    const int64_t cap = (int64_t)sm_count() * 8;
+    if (grid > cap) grid = cap;
+    pow_batch_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(n, x, y, out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "pow_batch_kernel launch");
     return TR_OK;
 }
 

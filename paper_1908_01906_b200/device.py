@@ -154,14 +154,7 @@ class Epoch:
         _lib.check(_lib.lib().tr_step_sizes(P, _lib.ptr(sig, C.c_double), float(params.s1),
                                             float(params.s2), float(params.p),
                                             _lib.ptr(step, C.c_double)), "tr_step_sizes")
-        kact = np.empty(dev.n_knodes, dtype=np.uint8)
-        _lib.check(_lib.lib().tr_knodes_activity(dev.n_knodes, _lib.vptr(dev.knodes_host),
-                                                 _lib.vptr(dev.kpids_host), _lib.ptr(act, C.c_uint8),
-                                                 _lib.ptr(kact, C.c_uint8)), "tr_knodes_activity")
-        bact = np.empty(dev.n_bnodes, dtype=np.uint8)
-        _lib.check(_lib.lib().tr_bnodes_activity(dev.n_bnodes, _lib.vptr(dev.bnodes_host),
-                                                 _lib.ptr(act, C.c_uint8), _lib.ptr(bact, C.c_uint8)),
-                   "tr_bnodes_activity")
+        kact, bact = dev.activity(act)
         table = np.ascontiguousarray(tf.table, dtype=np.float64)
         self.n_tf = int(table.shape[0])
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
@@ -278,8 +271,27 @@ class DeviceScene:
             n_knodes=self.n_knodes, kroot=(C.c_double * 6)(*kroot))
         self._epochs: OrderedDict = OrderedDict()
         self._frames: dict = {}
+        self._act_key, self._act_val = None, None
+        self._desc_key, self._desc_val = None, None
 
     # ---------------------------------------------------------------- epochs
+    def activity(self, act: np.ndarray):
+        """Subtree-activity bits of both partition trees for an active mask
+        (reused while the mask is unchanged, e.g. across colour-only TF edits)."""
+        key = act.tobytes()
+        if self._act_key == key:
+            return self._act_val
+        kact = np.empty(self.n_knodes, dtype=np.uint8)
+        _lib.check(_lib.lib().tr_knodes_activity(self.n_knodes, _lib.vptr(self.knodes_host),
+                                                 _lib.vptr(self.kpids_host), _lib.ptr(act, C.c_uint8),
+                                                 _lib.ptr(kact, C.c_uint8)), "tr_knodes_activity")
+        bact = np.empty(self.n_bnodes, dtype=np.uint8)
+        _lib.check(_lib.lib().tr_bnodes_activity(self.n_bnodes, _lib.vptr(self.bnodes_host),
+                                                 _lib.ptr(act, C.c_uint8), _lib.ptr(bact, C.c_uint8)),
+                   "tr_bnodes_activity")
+        self._act_key, self._act_val = key, (kact, bact)
+        return kact, bact
+
     def epoch(self, meta_state, params) -> Epoch:
         key = (id(meta_state), float(params.s1), float(params.s2), float(params.p))
         ep = self._epochs.get(key)
@@ -303,6 +315,20 @@ class DeviceScene:
     def frame_desc(self, scene, camera, mode: int, params, jitter: bool, track: bool,
                    flags: int = 0, shard_rank: int = 0, shard_count: int = 1,
                    compact: bool = False) -> _lib.TrFrame:
+        key = (camera.position.tobytes(), camera.look_at.tobytes(), camera.up.tobytes(),
+               float(camera.fov_y_deg), int(camera.width), int(camera.height), mode,
+               float(params.s1), float(params.termination_opacity),
+               float(scene.traversal_config.epsilon), np.asarray(scene.background).tobytes(),
+               bool(jitter), bool(track), flags, shard_rank, shard_count, bool(compact))
+        if key == self._desc_key:
+            return self._desc_val
+        desc = self._frame_desc(scene, camera, mode, params, jitter, track, flags, shard_rank,
+                                shard_count, compact)
+        self._desc_key, self._desc_val = key, desc
+        return desc
+
+    def _frame_desc(self, scene, camera, mode, params, jitter, track, flags, shard_rank,
+                    shard_count, compact) -> _lib.TrFrame:
         right, up, fwd = camera.basis()
         w, h = int(camera.width), int(camera.height)
         bg = np.asarray(scene.background, dtype=np.float64).reshape(4)

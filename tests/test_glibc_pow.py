@@ -1,0 +1,69 @@
+"""The restated glibc pow (csrc/glibc_pow.cuh) against the live libm `pow`
+(Python's float ** is glibc pow, as numba's llvm.pow.f64 is): bit-identical
+on the opacity-correction domain (x = 1 - alpha in [0, 1], y = s/s1 >= 1)
+and beyond.  Host restatement on CPU; the device copy under -m gpu."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+
+
+@pytest.fixture(scope="module")
+def L(built_lib):
+    from paper_1908_01906_b200 import _lib
+    if not _lib.lib().tr_pow_glibc_available():
+        pytest.skip("glibc pow tables not found in this libm")
+    return _lib
+
+
+def _args(n, seed):
+    rng = np.random.default_rng(seed)
+    x = np.concatenate([
+        rng.uniform(0.0, 1.0, n),                       # 1 - alpha
+        1.0 - rng.uniform(0.0, 1e-6, n // 8),           # alpha ~ 0
+        rng.uniform(0.0, 1e-3, n // 8),                 # alpha ~ 1
+        1.0 - rng.integers(1, 1 << 20, n // 8) * 2.0 ** -53,
+        np.exp(rng.uniform(-700, 700, n // 8)),          # wide range
+        np.array([1.0, 0.5, 2.0 ** -53, 0.75, 0.9999]),
+    ])
+    y = np.concatenate([
+        rng.uniform(1.0, 8.0, n), rng.uniform(1.0, 8.0, n // 8), rng.uniform(1.0, 8.0, n // 8),
+        rng.uniform(1.0, 32.0, n // 8), rng.uniform(0.01, 4.0, n // 8),
+        np.array([2.0, 3.0, 8.0, 1.0000000000000002, 7.999999999999999]),
+    ])
+    return x, y
+
+
+def test_host_restatement_bit_identical_to_libm(L):
+    x, y = _args(200_000, 7)
+    lib = L.lib()
+    ex = C.c_int32()
+    checked = 0
+    for a, b in zip(x.tolist(), y.tolist()):
+        r = lib.tr_pow_glibc_host(a, b, C.byref(ex))
+        if ex.value:
+            assert r == a ** b, (a, b, r, a ** b)
+            checked += 1
+        elif a < 1.0 and b > 0.0:
+            assert 1.0 - r == 1.0 - a ** b  # under/overflowed pow: only 1 - pow is used
+    assert checked > 0.9 * len(x)
+
+
+@pytest.mark.gpu
+def test_device_restatement_bit_identical_to_libm(L):
+    import torch
+    x, y = _args(400_000, 11)
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.from_numpy(y).cuda()
+    out = torch.empty_like(xd)
+    L.check(L.lib().tr_pow_glibc_batch(len(x), C.c_void_p(xd.data_ptr()), C.c_void_p(yd.data_ptr()),
+                                       C.c_void_p(out.data_ptr()), None), "tr_pow_glibc_batch")
+    got = out.cpu().numpy()
+    want = np.array([a ** b for a, b in zip(x.tolist(), y.tolist())])
+    ca_got, ca_want = 1.0 - got, 1.0 - want
+    # pow itself is bit-identical wherever glibc does not under/overflow;
+    # 1 - pow (the opacity correction) is bit-identical everywhere
+    normal = (want > 1e-300) & np.isfinite(want)
+    assert np.array_equal(got[normal], want[normal])
+    assert np.array_equal(ca_got[x <= 1.0], ca_want[x <= 1.0])
