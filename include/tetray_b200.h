@@ -180,6 +180,7 @@ typedef struct TrDeviceScene {
     int64_t n_parts, n_bnodes;
     double mesh_lo[3], mesh_hi[3];
     const int32_t *pgrid;  /* tr_pbvh_grid cells */
+    const TrPLeaf *pgrid_leaf; /* per cell: copy of its candidate leaf's header (empty box: none) */
     int32_t gdim[3];
     int32_t pad1;
     double gorg[3], gscale[3];

@@ -29,7 +29,8 @@ class TrDeviceScene(C.Structure):
         ("bnodes", C.c_void_p), ("part_lo", C.c_void_p), ("part_hi", C.c_void_p),
         ("n_parts", C.c_int64), ("n_bnodes", C.c_int64),
         ("mesh_lo", C.c_double * 3), ("mesh_hi", C.c_double * 3),
-        ("pgrid", C.c_void_p), ("gdim", C.c_int32 * 3), ("pad1", C.c_int32),
+        ("pgrid", C.c_void_p), ("pgrid_leaf", C.c_void_p), ("gdim", C.c_int32 * 3),
+        ("pad1", C.c_int32),
         ("gorg", C.c_double * 3), ("gscale", C.c_double * 3),
         ("knodes", C.c_void_p), ("kleaf_pids", C.c_void_p), ("n_knodes", C.c_int64),
         ("kroot", C.c_double * 6),

@@ -179,6 +179,7 @@ struct SceneK {  // kernel copy of TrDeviceScene
     const double *__restrict__ part_lo;     // (P,3) partition boxes (next_interval's leaf boxes)
     const double *__restrict__ part_hi;
     const int32_t *__restrict__ pgrid;      // uniform-grid leaf candidates
+    const TrPLeaf *__restrict__ pgrid_leaf; // the candidate leaf's header per cell
     const TrKNode *__restrict__ knodes;     // partition BSP (NULL: BVH trace)
     const int32_t *__restrict__ kleaf_pids;
     double kroot_lo[3], kroot_hi[3];
@@ -292,16 +293,26 @@ __device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHin
     h.valid = true;
 }
 
-// Grid candidate leaf of q (-1: outside the grid or an empty cell).  Only a
+// Grid cell of q (-1: outside the grid).  The cell's candidate leaf is only a
 // hint: the caller accepts it after proving q strictly inside its exclusive box.
-__device__ __forceinline__ int32_t grid_leaf(const SceneK &S, const PQuery &q) {
+__device__ __forceinline__ int64_t grid_cell(const SceneK &S, const PQuery &q) {
     const double fx = (q.x - S.gorg[0]) * S.gscale[0];
     const double fy = (q.y - S.gorg[1]) * S.gscale[1];
     const double fz = (q.z - S.gorg[2]) * S.gscale[2];
     if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0)) return -1;
     const int64_t cx = (int64_t)fx, cy = (int64_t)fy, cz = (int64_t)fz;
     if (cx >= S.gdim[0] || cy >= S.gdim[1] || cz >= S.gdim[2]) return -1;
-    return __ldg(S.pgrid + (cx * S.gdim[1] + cy) * S.gdim[2] + cz);
+    return (cx * S.gdim[1] + cy) * S.gdim[2] + cz;
+}
+
+__device__ __forceinline__ void load_leaf(const TrPLeaf *lf, LeafHint &h) {
+    const float4 *p = reinterpret_cast<const float4 *>(lf);
+    const float4 a = __ldg(p), b = __ldg(p + 1);
+    h.lo[0] = a.x; h.lo[1] = a.y; h.lo[2] = a.z;
+    h.hi[0] = a.w; h.hi[1] = b.x; h.hi[2] = b.y;
+    h.start = __float_as_uint(b.z);
+    h.count = __float_as_uint(b.w);
+    h.valid = true;
 }
 
 // K:139-154.  Returns the record position (UINT32_MAX: outside every tet).
@@ -317,10 +328,10 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
         pos = scan_leaf_first(S, hint.start, hint.count, q, l);
         done = true;
     } else if (use_grid) {
-        const int32_t gl = grid_leaf(S, q);
-        if (gl >= 0) {
+        const int64_t gc = grid_cell(S, q);
+        if (gc >= 0) {
             LeafHint h;
-            load_hint(S, gl, h);
+            load_leaf(S.pgrid_leaf + gc, h);  // one load: the header is replicated per cell
             if (strictly_in(q, h.lo, h.hi)) {
                 pos = scan_leaf_first(S, h.start, h.count, q, l);
                 if (use_hint) hint = h;
@@ -828,6 +839,11 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     int32_t ov_pid = -1;                       // inline interval past the list
     double ov_a = 0.0, ov_b = 0.0;
     double m0_a = 0.0, m0_b = 0.0;             // reference mode's single interval
+    // this lane's window entry, kept while the window (i_cur) does not move
+    int32_t c_icur = -1, c_pid = -1;
+    double c_a = 0.0, c_b = 0.0, c_step = 0.0, c_e = 1.0;
+    int64_t c_n = 0;
+    bool c_valid = false;
 
     while (true) {
         // ---- refill: one queue slot per group that needs a ray
@@ -867,6 +883,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         iv_n = 1;
                     }
                     active = true;
+                    c_icur = -1;
                 }
             }
         }
@@ -891,7 +908,11 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         int32_t pid = -1;
         double a = 0.0, b = 0.0, step = fr.s1;
         bool valid = false;
-        if (active) {
+        const bool list_win = active && fr.mode != 0 && !inline_iv;
+        const bool cached = list_win && c_icur == i_cur;  // group-uniform
+        if (cached) {
+            pid = c_pid; a = c_a; b = c_b; step = c_step; valid = c_valid;
+        } else if (active) {
             if (fr.mode == 0) {
                 valid = (j == 0) && i_cur < 1;
                 a = m0_a;
@@ -918,14 +939,22 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         // list intervals: t_min = previous exit - eps, entry clamped to it (K:200, K:390)
         const double prev_b = __shfl_up_sync(FULL, b, 1, G);
         const int32_t prev_pid = __shfl_up_sync(FULL, pid, 1, G);
-        if (valid && fr.mode != 0 && !inline_iv) {
-            const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
-            a = (a > tmin_j) ? a : tmin_j;
+        double e_win = c_e;
+        int64_t n_i = c_n;
+        if (!cached) {
+            if (valid && fr.mode != 0 && !inline_iv) {
+                const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
+                a = (a > tmin_j) ? a : tmin_j;
+            }
+            if (valid && fr.mode == 2) step = __ldg(E.step + pid);
+            e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
+            const bool marchable = valid && (b - a >= fr.eps);
+            n_i = marchable ? interval_samples(a, b, step, phase) : 0;
+            if (list_win) {
+                c_icur = i_cur; c_pid = pid; c_a = a; c_b = b; c_step = step; c_e = e_win;
+                c_n = n_i; c_valid = valid;
+            }
         }
-        if (valid && fr.mode == 2) step = __ldg(E.step + pid);
-        const double e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
-        const bool marchable = valid && (b - a >= fr.eps);
-        const int64_t n_i = marchable ? interval_samples(a, b, step, phase) : 0;
         int64_t rem = n_i - ((j == 0) ? k_cur : 0);
         if (rem < 0) rem = 0;
         int64_t incl = rem;  // inclusive scan of remaining samples over the window
@@ -1148,6 +1177,7 @@ SceneK make_scene(const TrDeviceScene *s) {
     S.pleaf_ids = s->pleaf_ids;
     S.bnodes = s->bnodes;
     S.pgrid = s->pgrid;
+    S.pgrid_leaf = s->pgrid_leaf;
     S.part_lo = s->part_lo;
     S.part_hi = s->part_hi;
     S.knodes = s->knodes;

@@ -249,13 +249,20 @@ class DeviceScene:
             self.t_plo = _upload(part_lo, device)
             self.t_phi = _upload(part_hi, device)
             self.t_grid = _upload(grid.cells, device)
+            cell_leaf = np.zeros(len(grid.cells), dtype=_lib.PLEAF_DTYPE)
+            cell_leaf["ex_lo"] = 1.0   # empty box: no candidate
+            cell_leaf["ex_hi"] = 0.0
+            has = grid.cells >= 0
+            cell_leaf[has] = pleaves[grid.cells[has]]
+            self.t_grid_leaf = _upload(cell_leaf, device)
             self.t_knodes = _upload(knodes, device)
             self.t_kpids = _upload(kpids, device)
             self.grid = grid
             torch.cuda.synchronize(device)
         self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
                                                       self.t_pids, self.t_bnodes, self.t_plo,
-                                                      self.t_phi, self.t_grid, self.t_knodes,
+                                                      self.t_phi, self.t_grid, self.t_grid_leaf,
+                                                      self.t_knodes,
                                                       self.t_kpids))
         self.desc = _lib.TrDeviceScene(
             tets=self.t_tets.data_ptr(), pnodes=self.t_pnodes.data_ptr(),
@@ -265,7 +272,8 @@ class DeviceScene:
             part_lo=self.t_plo.data_ptr(), part_hi=self.t_phi.data_ptr(), n_parts=self.n_parts,
             n_bnodes=self.n_bnodes,
             mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi),
-            pgrid=self.t_grid.data_ptr(), gdim=(C.c_int32 * 3)(*grid.dims),
+            pgrid=self.t_grid.data_ptr(), pgrid_leaf=self.t_grid_leaf.data_ptr(),
+            gdim=(C.c_int32 * 3)(*grid.dims),
             gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale),
             knodes=self.t_knodes.data_ptr(), kleaf_pids=self.t_kpids.data_ptr(),
             n_knodes=self.n_knodes, kroot=(C.c_double * 6)(*kroot))
