@@ -221,6 +221,7 @@ typedef struct TrFrame {
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
 #define TR_FLAG_HIST_SMEM 16   /* per-partition counts in a per-CTA shared copy (else global) */
+#define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
  * bits 12-13: minimum resident CTAs per SM (0 = 2).  Tuning knobs only:
  * every setting renders the same frame. */

@@ -320,7 +320,7 @@ __device__ __forceinline__ void load_leaf(const TrPLeaf *lf, LeafHint &h) {
 // leaf, else the full descent.  All three return the lowest containing index.
 __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, LeafHint &hint,
                                              bool use_hint, bool use_grid, double &v,
-                                             bool stats = false) {
+                                             bool stats = false, bool grid_indirect = false) {
     double l[4];
     uint32_t pos;
     bool done = false;
@@ -331,7 +331,14 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
         const int64_t gc = grid_cell(S, q);
         if (gc >= 0) {
             LeafHint h;
-            load_leaf(S.pgrid_leaf + gc, h);  // one load: the header is replicated per cell
+            if (grid_indirect) {
+                const int32_t gl = __ldg(S.pgrid + gc);
+                h.valid = false;
+                if (gl >= 0) load_leaf(S.pleaves + gl, h);
+                else { h.lo[0] = 1.0f; h.hi[0] = 0.0f; h.lo[1] = h.lo[2] = h.hi[1] = h.hi[2] = 0.0f; }
+            } else {
+                load_leaf(S.pgrid_leaf + gc, h);  // one load: the header is replicated per cell
+            }
             if (strictly_in(q, h.lo, h.hi)) {
                 pos = scan_leaf_first(S, h.start, h.count, q, l);
                 if (use_hint) hint = h;
@@ -820,6 +827,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __syncthreads();
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
     const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
+    const bool grid_indirect = (fr.flags & TR_FLAG_GRID_INDIRECT) != 0;
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
@@ -839,11 +847,6 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     int32_t ov_pid = -1;                       // inline interval past the list
     double ov_a = 0.0, ov_b = 0.0;
     double m0_a = 0.0, m0_b = 0.0;             // reference mode's single interval
-    // this lane's window entry, kept while the window (i_cur) does not move
-    int32_t c_icur = -1, c_pid = -1;
-    double c_a = 0.0, c_b = 0.0, c_step = 0.0, c_e = 1.0;
-    int64_t c_n = 0;
-    bool c_valid = false;
 
     while (true) {
         // ---- refill: one queue slot per group that needs a ray
@@ -883,7 +886,6 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         iv_n = 1;
                     }
                     active = true;
-                    c_icur = -1;
                 }
             }
         }
@@ -908,11 +910,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         int32_t pid = -1;
         double a = 0.0, b = 0.0, step = fr.s1;
         bool valid = false;
-        const bool list_win = active && fr.mode != 0 && !inline_iv;
-        const bool cached = list_win && c_icur == i_cur;  // group-uniform
-        if (cached) {
-            pid = c_pid; a = c_a; b = c_b; step = c_step; valid = c_valid;
-        } else if (active) {
+        if (active) {
             if (fr.mode == 0) {
                 valid = (j == 0) && i_cur < 1;
                 a = m0_a;
@@ -939,22 +937,14 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         // list intervals: t_min = previous exit - eps, entry clamped to it (K:200, K:390)
         const double prev_b = __shfl_up_sync(FULL, b, 1, G);
         const int32_t prev_pid = __shfl_up_sync(FULL, pid, 1, G);
-        double e_win = c_e;
-        int64_t n_i = c_n;
-        if (!cached) {
-            if (valid && fr.mode != 0 && !inline_iv) {
-                const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
-                a = (a > tmin_j) ? a : tmin_j;
-            }
-            if (valid && fr.mode == 2) step = __ldg(E.step + pid);
-            e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
-            const bool marchable = valid && (b - a >= fr.eps);
-            n_i = marchable ? interval_samples(a, b, step, phase) : 0;
-            if (list_win) {
-                c_icur = i_cur; c_pid = pid; c_a = a; c_b = b; c_step = step; c_e = e_win;
-                c_n = n_i; c_valid = valid;
-            }
+        if (valid && fr.mode != 0 && !inline_iv) {
+            const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
+            a = (a > tmin_j) ? a : tmin_j;
         }
+        if (valid && fr.mode == 2) step = __ldg(E.step + pid);
+        const double e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
+        const bool marchable = valid && (b - a >= fr.eps);
+        const int64_t n_i = marchable ? interval_samples(a, b, step, phase) : 0;
         int64_t rem = n_i - ((j == 0) ? k_cur : 0);
         if (rem < 0) rem = 0;
         int64_t incl = rem;  // inclusive scan of remaining samples over the window
@@ -994,7 +984,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             h.valid = false;
             double v;
             if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
-            if (field_at(S, q, h, false, use_grid, v, stats) != UINT32_MAX) {
+            if (field_at(S, q, h, false, use_grid, v, stats, grid_indirect) != UINT32_MAX) {
                 if (stats) atomicAdd(&g_stats[ST_FOUND], 1ull);
                 double c[4];
                 tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
