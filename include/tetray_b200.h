@@ -136,10 +136,14 @@ int tr_knodes_activity(int64_t n_nodes, const TrKNode *nodes, const int32_t *lea
 
 void tr_host_free(TrHostBuf *b);
 
-/* Pack tet records (host, OpenMP). inv/orig exactly as MeshSampler computes them. */
+/* Pack tet records (host, OpenMP). inv/orig exactly as MeshSampler computes
+ * them; out[k] holds tet order[k] (order = point-BVH leaf order; NULL: k). */
 int tr_pack_tets(int64_t n_tets, const int64_t *tets, const double *tet_orig,
                  const double *tet_inv, const double *field, int32_t centering,
-                 TrTetRecord *out);
+                 const uint32_t *order, TrTetRecord *out);
+/* Padded tet boxes (mesh.py:248-250: vertex min/max -+ pad), OpenMP. */
+int tr_tet_boxes(int64_t n_tets, const double *vertices, const int64_t *tets, double pad,
+                 double *lo, double *hi);
 
 /* Transfer-function partition metadata (transfer.py:95-141): per partition
  * max opacity, raw variance (numpy reduction order reproduced), normalized

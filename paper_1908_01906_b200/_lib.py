@@ -105,7 +105,9 @@ _SIGNATURES = [
     ("tr_kbsp_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, c_f64p]),
     ("tr_knodes_activity", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, c_u8p, c_u8p]),
     ("tr_host_free", None, [C.c_void_p]),
-    ("tr_pack_tets", C.c_int, [C.c_int64, c_i64p, c_f64p, c_f64p, c_f64p, C.c_int32, C.c_void_p]),
+    ("tr_pack_tets", C.c_int, [C.c_int64, c_i64p, c_f64p, c_f64p, c_f64p, C.c_int32, C.c_void_p,
+                               C.c_void_p]),
+    ("tr_tet_boxes", C.c_int, [C.c_int64, c_f64p, c_i64p, C.c_double, c_f64p, c_f64p]),
     ("tr_tf_meta", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int64, C.c_double, C.c_double,
                              c_f64p, c_f64p, c_f64p, c_u8p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),

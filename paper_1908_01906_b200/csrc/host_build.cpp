@@ -165,8 +165,7 @@ struct PCtx {
     PBuf *out;
 };
 
-PRef p_make_leaf(PCtx &C, int64_t b, int64_t e) {
-    PBuf &O = *C.out;
+PRef p_make_leaf(PCtx &C, PBuf &O, int64_t b, int64_t e) {
     std::sort(C.idx.begin() + b, C.idx.begin() + e);
     TrPLeaf L;
     L.start = (uint32_t)O.ids.size();
@@ -196,9 +195,83 @@ void p_set_child(TrPNode &N, int c, const PRef &r) {
     N.minid[c] = r.minid;
 }
 
-PRef p_build(PCtx &C, int64_t b, int64_t e) {
+// Split position for [b, e): the object median on the axis of largest centre
+// extent, moved to the nearest change of key (three-way partition) so boxes
+// with equal centres never straddle a split.  -1: no split possible.
+int64_t p_choose_split(PCtx &C, int64_t b, int64_t e);
+
+PRef p_build(PCtx &C, PBuf &O, int64_t b, int64_t e) {
     const int64_t n = e - b;
-    if (n <= C.leaf_max) return p_make_leaf(C, b, e);
+    if (n <= C.leaf_max) return p_make_leaf(C, O, b, e);
+    int64_t split = p_choose_split(C, b, e);
+    if (split < 0) {
+        if (n <= 64) return p_make_leaf(C, O, b, e);
+        split = b + n / 2;  // identical centres everywhere: force a split
+    }
+    const size_t ni = O.nodes.size();
+    O.nodes.push_back(TrPNode{});
+    PRef l = p_build(C, O, b, split);
+    PRef r = p_build(C, O, split, e);
+    TrPNode &N = O.nodes[ni];
+    p_set_child(N, 0, l);
+    p_set_child(N, 1, r);
+    PRef me;
+    me.child = (int32_t)ni;
+    me.minid = std::min(l.minid, r.minid);
+    for (int a = 0; a < 3; ++a) { me.lo[a] = std::min(l.lo[a], r.lo[a]); me.hi[a] = std::max(l.hi[a], r.hi[a]); }
+    return me;
+}
+
+// Append subtree buffer S (built separately) to O, relocating node, leaf and
+// id indices; returns the relocated reference to its root.
+PRef p_splice(PBuf &O, PBuf &S, PRef r) {
+    const int32_t node_off = (int32_t)O.nodes.size(), leaf_off = (int32_t)O.leaves.size();
+    const uint32_t id_off = (uint32_t)O.ids.size();
+    for (TrPNode N : S.nodes) {
+        for (int c = 0; c < 2; ++c) {
+            if (N.child[c] >= 0) N.child[c] += node_off;
+            else if (N.child[c] != CHILD_NONE) N.child[c] = ~(~N.child[c] + leaf_off);
+        }
+        O.nodes.push_back(N);
+    }
+    for (TrPLeaf L : S.leaves) { L.start += id_off; O.leaves.push_back(L); }
+    O.leaf_box.insert(O.leaf_box.end(), S.leaf_box.begin(), S.leaf_box.end());
+    O.ids.insert(O.ids.end(), S.ids.begin(), S.ids.end());
+    PBuf().nodes.swap(S.nodes);
+    if (r.child >= 0) r.child += node_off;
+    else r.child = ~(~r.child + leaf_off);
+    return r;
+}
+
+// Task-parallel top levels (disjoint index ranges), sequential below.
+PRef p_build_par(PCtx &C, PBuf &O, int64_t b, int64_t e, int depth) {
+    const int64_t n = e - b;
+    if (n < (int64_t)(1 << 18) || depth >= 10) return p_build(C, O, b, e);
+    const int64_t split = p_choose_split(C, b, e);
+    if (split < 0) return p_build(C, O, b, e);
+    const size_t ni = O.nodes.size();
+    O.nodes.push_back(TrPNode{});
+    PBuf Lb, Rb;
+    PRef l, r;
+#pragma omp task shared(C, Lb, l)
+    l = p_build_par(C, Lb, b, split, depth + 1);
+#pragma omp task shared(C, Rb, r)
+    r = p_build_par(C, Rb, split, e, depth + 1);
+#pragma omp taskwait
+    l = p_splice(O, Lb, l);
+    r = p_splice(O, Rb, r);
+    TrPNode &N = O.nodes[ni];
+    p_set_child(N, 0, l);
+    p_set_child(N, 1, r);
+    PRef me;
+    me.child = (int32_t)ni;
+    me.minid = std::min(l.minid, r.minid);
+    for (int a = 0; a < 3; ++a) { me.lo[a] = std::min(l.lo[a], r.lo[a]); me.hi[a] = std::max(l.hi[a], r.hi[a]); }
+    return me;
+}
+
+int64_t p_choose_split(PCtx &C, int64_t b, int64_t e) {
+    const int64_t n = e - b;
     double klo[3] = {INFINITY, INFINITY, INFINITY}, khi[3] = {-INFINITY, -INFINITY, -INFINITY};
     for (int64_t k = b; k < e; ++k)
         for (int a = 0; a < 3; ++a) {
@@ -227,22 +300,7 @@ PRef p_build(PCtx &C, int64_t b, int64_t e) {
             if (s > b && s < e && (best < 0 || std::llabs(s - mid) < std::llabs(best - mid))) best = s;
         split = best;
     }
-    if (split < 0) {
-        if (n <= 64) return p_make_leaf(C, b, e);
-        split = b + n / 2;  // identical centres everywhere: force a split
-    }
-    const size_t ni = C.out->nodes.size();
-    C.out->nodes.push_back(TrPNode{});
-    PRef l = p_build(C, b, split);
-    PRef r = p_build(C, split, e);
-    TrPNode &N = C.out->nodes[ni];
-    p_set_child(N, 0, l);
-    p_set_child(N, 1, r);
-    PRef me;
-    me.child = (int32_t)ni;
-    me.minid = std::min(l.minid, r.minid);
-    for (int a = 0; a < 3; ++a) { me.lo[a] = std::min(l.lo[a], r.lo[a]); me.hi[a] = std::max(l.hi[a], r.hi[a]); }
-    return me;
+    return split;
 }
 
 inline bool boxes_meet(const double *a, const double *b) {  // closed boxes [lo(3), hi(3)]
@@ -612,7 +670,10 @@ int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, in
             for (int a = 0; a < 3; ++a) C.key[3 * t + a] = 0.5 * (box_lo[3 * t + a] + box_hi[3 * t + a]);
         }
         O->nodes.reserve(2 * (size_t)n_tets / 4 + 4);
-        PRef root = p_build(C, 0, n_tets);  // an internal root lands at index 0
+        PRef root;
+#pragma omp parallel
+#pragma omp single
+        root = p_build_par(C, *O, 0, n_tets, 0);  // an internal root lands at index 0
         if (root.child < 0) {  // whole mesh is one leaf: root node with one child
             TrPNode N{};
             p_set_child(N, 0, root);
@@ -790,12 +851,13 @@ void tr_host_free(TrHostBuf *b) { delete b; }
 
 int tr_pack_tets(int64_t n_tets, const int64_t *tets, const double *tet_orig,
                  const double *tet_inv, const double *field, int32_t centering,
-                 TrTetRecord *out) {
+                 const uint32_t *order, TrTetRecord *out) {
     if (n_tets <= 0 || !tets || !tet_orig || !tet_inv || !field || !out)
         return tr_fail(TR_EINVAL, "tr_pack_tets: invalid arguments");
 #pragma omp parallel for schedule(static)
-    for (int64_t t = 0; t < n_tets; ++t) {
-        TrTetRecord &R = out[t];
+    for (int64_t k = 0; k < n_tets; ++k) {
+        const int64_t t = order ? (int64_t)order[k] : k;
+        TrTetRecord &R = out[k];
         std::memcpy(R.inv, tet_inv + 9 * t, 72);
         std::memcpy(R.orig, tet_orig + 3 * t, 24);
         if (centering == 0) {
@@ -803,6 +865,23 @@ int tr_pack_tets(int64_t n_tets, const int64_t *tets, const double *tet_orig,
         } else {
             R.f[0] = field[t];
             R.f[1] = R.f[2] = R.f[3] = 0.0;
+        }
+    }
+    return TR_OK;
+}
+
+int tr_tet_boxes(int64_t n_tets, const double *vertices, const int64_t *tets, double pad,
+                 double *lo, double *hi) {
+    if (n_tets <= 0 || !vertices || !tets || !lo || !hi)
+        return tr_fail(TR_EINVAL, "tr_tet_boxes: invalid arguments");
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < n_tets; ++t) {
+        const int64_t *tv = tets + 4 * t;
+        for (int a = 0; a < 3; ++a) {
+            const double v0 = vertices[3 * tv[0] + a], v1 = vertices[3 * tv[1] + a];
+            const double v2 = vertices[3 * tv[2] + a], v3 = vertices[3 * tv[3] + a];
+            lo[3 * t + a] = std::min(std::min(v0, v1), std::min(v2, v3)) - pad;
+            hi[3 * t + a] = std::max(std::max(v0, v1), std::max(v2, v3)) + pad;
         }
     }
     return TR_OK;

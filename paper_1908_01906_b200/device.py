@@ -59,17 +59,21 @@ def resolve_device(device=None):
 def _upload(arr: np.ndarray, device):
     torch = _torch()
     raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-    return torch.from_numpy(raw.copy()).to(device)
+    return torch.from_numpy(raw).to(device)  # synchronous copy; `arr` outlives it
 
 
 def _padded_boxes(scene) -> tuple[np.ndarray, np.ndarray]:
-    sampler = scene.sampler
-    if hasattr(sampler, "padded_boxes"):
-        return sampler.padded_boxes()
-    mesh = scene.mesh  # a tetray Scene: same rule as mesh.py:248-250
-    lo, hi = mesh.tet_aabbs()
+    """Tet boxes padded by 1e-7 * diag (mesh.py:248-250), native + OpenMP."""
+    mesh = scene.mesh
     pad = BOX_PAD_REL * max(mesh.bounds.diagonal(), 1e-30)
-    return lo - pad, hi + pad
+    verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+    tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+    lo = np.empty((len(tets), 3))
+    hi = np.empty((len(tets), 3))
+    _lib.check(_lib.lib().tr_tet_boxes(len(tets), _lib.ptr(verts, C.c_double),
+                                       _lib.ptr(tets, C.c_int64), pad, _lib.ptr(lo, C.c_double),
+                                       _lib.ptr(hi, C.c_double)), "tr_tet_boxes")
+    return lo, hi
 
 
 class PointGrid:
@@ -125,8 +129,10 @@ def build_partition_bsp(lo: np.ndarray, hi: np.ndarray):
     return nodes, pids, root
 
 
-def pack_tet_records(mesh, sampler) -> np.ndarray:
+def pack_tet_records(mesh, sampler, order=None) -> np.ndarray:
+    """128-B records; record k holds tet order[k] (None: tet k)."""
     rec = np.empty(mesh.n_tets, dtype=_lib.TET_RECORD_DTYPE)
+    order = None if order is None else np.ascontiguousarray(order, dtype=np.uint32)
     orig = np.ascontiguousarray(sampler.tet_orig, dtype=np.float64)
     inv = np.ascontiguousarray(sampler.tet_inv, dtype=np.float64)
     tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
@@ -134,6 +140,7 @@ def pack_tet_records(mesh, sampler) -> np.ndarray:
     _lib.check(_lib.lib().tr_pack_tets(mesh.n_tets, _lib.ptr(tets, C.c_int64),
                                        _lib.ptr(orig, C.c_double), _lib.ptr(inv, C.c_double),
                                        _lib.ptr(fld, C.c_double), int(mesh.centering),
+                                       None if order is None else _lib.vptr(order),
                                        _lib.vptr(rec)), "tr_pack_tets")
     return rec
 
@@ -221,9 +228,12 @@ class DeviceScene:
         mesh, sampler = scene.mesh, scene.sampler
         with torch.cuda.device(device):
             t0 = time.perf_counter()
-            rec = pack_tet_records(mesh, sampler)
             lo, hi = _padded_boxes(scene)
             pnodes, pleaves, pids, grid = build_point_bvh(lo, hi)
+            del lo, hi
+            # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
+            # reads consecutive 128-B lines with no id indirection
+            rec = pack_tet_records(mesh, sampler, order=pids)
             part_lo = np.ascontiguousarray(scene.bvh.box_lo, dtype=np.float64)
             part_hi = np.ascontiguousarray(scene.bvh.box_hi, dtype=np.float64)
             bnodes = getattr(scene.bvh, "nodes", None)
@@ -239,9 +249,8 @@ class DeviceScene:
             self.n_bnodes = int(len(bnodes))
             self.n_tets = int(mesh.n_tets)
             self.pnodes_host, self.pleaves_host = pnodes, pleaves
-            # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
-            # reads consecutive 128-B lines with no id indirection
-            self.t_tets = _upload(rec[pids], device)
+            self.t_tets = _upload(rec, device)
+            del rec
             self.t_pnodes = _upload(pnodes, device)
             self.t_pleaves = _upload(pleaves, device)
             self.t_pids = _upload(pids, device)

@@ -71,9 +71,10 @@ def build_scene(pkg, name: str):
     if name == "radial16":
         return pkg.Scene.build(pkg.generate_synthetic(16, "radial", V),
                                _tf(pkg, radial16_tf_doc(16)), kd_config=K(48))
-    if name == "radial59":
-        return pkg.Scene.build(pkg.generate_synthetic(59, "radial", V),
-                               _tf(pkg, radial16_tf_doc(59)))
+    if name.startswith("radial") and name[6:].isdigit() and name not in ("radial16",):
+        n = int(name[6:])   # radial59 (1e6 tets), radial128 (1e7), radial272 (1e8): SURVEY §8d
+        return pkg.Scene.build(pkg.generate_synthetic(n, "radial", V),
+                               _tf(pkg, radial16_tf_doc(n)))
     if name == "voidcell":
         return pkg.Scene.build(pkg.generate_synthetic(3, "voidblock", C),
                                _banded(pkg, (0.0, 1.0)), kd_config=K(16))
@@ -113,8 +114,8 @@ def camera(pkg, name: str, scale: float = 1.0):
         # components, exercising slab's d == 0 branch (K:45-46)
         return Cam(position=[2.0, 2.0, 9.0], look_at=[2.0, 2.0, 2.0], up=[0, 1, 0],
                    fov_y_deg=30.0, width=33, height=31)
-    if name in ("radial16", "radial59"):
-        n = 16 if name == "radial16" else 59
+    if name.startswith("radial") and name[6:].isdigit() and name != "radial4":
+        n = int(name[6:])
         f = n / 16.0
         return Cam(position=[40.0 * f, 26.0 * f, 34.0 * f], look_at=[8.0 * f] * 3, up=[0, 1, 0],
                    fov_y_deg=35.0, width=int(512 * scale), height=int(512 * scale))
@@ -140,7 +141,7 @@ def params(pkg, name: str):
     P = pkg.AdaptiveParams
     if name in ("golden_radial4", "conftest48", "inside", "axis"):
         return P(s1=0.05, s2=0.3, p=2.0, termination_opacity=0.99)
-    if name in ("radial16", "radial59"):
+    if name.startswith("radial") and name[6:].isdigit():
         return P(s1=0.08, s2=0.64, p=2.0, termination_opacity=0.9999)
     if name == "voidcell":
         return P(s1=0.1, s2=0.1)

@@ -116,3 +116,67 @@ def test_exclusive_boxes_are_disjoint_from_other_leaf_boxes(B):
                 continue
             # open exclusive box vs closed leaf box: interiors must not meet
             assert np.any(blo >= ehi) or np.any(bhi <= elo), (a, b)
+
+
+def test_native_boxes_and_parallel_build_invariants(B):
+    """tr_tet_boxes equals numpy's padded boxes bit for bit; the task-parallel
+    point-BVH build (used above 2^18 tets) keeps every structural invariant."""
+    from paper_1908_01906_b200.device import _padded_boxes, build_point_bvh
+    m = B.generate_synthetic(40, "radial", B.Centering.VERTEX)   # 320,000 tets
+    sc = type("S", (), {})()
+    sc.mesh = m
+    lo, hi = _padded_boxes(sc)
+    nlo, nhi = m.tet_aabbs()
+    pad = 1e-7 * max(m.bounds.diagonal(), 1e-30)
+    assert np.array_equal(lo, nlo - pad) and np.array_equal(hi, nhi + pad)
+    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
+    assert np.array_equal(np.sort(ids), np.arange(m.n_tets, dtype=np.uint32))
+    starts, counts = leaves["start"].astype(np.int64), leaves["count"].astype(np.int64)
+    assert np.array_equal(np.sort(starts), np.concatenate([[0], np.cumsum(counts[np.argsort(starts)])[:-1]]))
+    # every reference is in range and every leaf / node is referenced exactly once
+    ch = nodes["child"].reshape(-1)
+    internal = ch[ch >= 0]
+    leafref = ~ch[(ch < 0) & (ch != -2 ** 31)]
+    assert np.array_equal(np.sort(internal), np.arange(1, len(nodes)))
+    assert np.array_equal(np.sort(leafref), np.arange(len(leaves)))
+    # min-id labels and f32 boxes bound their subtrees (bottom-up over nodes)
+    sub_min = np.full(len(nodes), 2 ** 32 - 1, dtype=np.int64)
+    sub_lo = np.full((len(nodes), 3), np.inf)
+    sub_hi = np.full((len(nodes), 3), -np.inf)
+    leaf_min = np.array([ids[s:s + c].min() for s, c in zip(starts, counts)], dtype=np.int64)
+    leaf_lo = np.array([lo[ids[s:s + c]].min(axis=0) for s, c in zip(starts, counts)])
+    leaf_hi = np.array([hi[ids[s:s + c]].max(axis=0) for s, c in zip(starts, counts)])
+    order = np.argsort(-np.arange(len(nodes)))
+    parent_done = np.zeros(len(nodes), bool)
+    # resolve children before parents: iterate until stable (children have larger ids
+    # within each spliced subtree, so a few passes suffice)
+    for _ in range(64):
+        changed = False
+        for i in order:
+            if parent_done[i]:
+                continue
+            vals = []
+            ok = True
+            for c in range(2):
+                x = int(nodes[i]["child"][c])
+                if x == -2 ** 31:
+                    continue
+                if x < 0:
+                    vals.append((leaf_min[~x], leaf_lo[~x], leaf_hi[~x]))
+                elif parent_done[x]:
+                    vals.append((sub_min[x], sub_lo[x], sub_hi[x]))
+                else:
+                    ok = False
+            if not ok:
+                continue
+            for c, (mn, blo, bhi) in zip(range(2), vals):
+                assert int(nodes[i]["minid"][c]) == mn
+                assert (nodes[i][f"lo{c}"].astype(np.float64) <= blo).all()
+                assert (nodes[i][f"hi{c}"].astype(np.float64) >= bhi).all()
+            sub_min[i] = min(v[0] for v in vals)
+            sub_lo[i] = np.min([v[1] for v in vals], axis=0)
+            sub_hi[i] = np.max([v[2] for v in vals], axis=0)
+            parent_done[i] = changed = True
+        if parent_done.all() or not changed:
+            break
+    assert parent_done.all()
