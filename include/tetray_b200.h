@@ -203,6 +203,8 @@ typedef struct TrEpoch {
     int64_t n_tf;
     double tf_lo, tf_hi;
     const uint8_t *knode_active; /* (n_knodes,) from tr_knodes_activity, or NULL */
+    const double *step_ratio;    /* (P,2) interleaved {step, step / s1} (opacity_correction's
+                                    exponent, K:27); only read in mode 2 */
 } TrEpoch;
 
 /* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
@@ -221,13 +223,15 @@ typedef struct TrFrame {
 } TrFrame;
 
 #define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
+#define TR_FLAG_SEQ_SCAN 64    /* leaf scan one record at a time, next one prefetched (tuning) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
-#define TR_FLAG_HIST_SMEM 16   /* per-partition counts in a per-CTA shared copy (else global) */
+#define TR_FLAG_HIST_SMEM 16   /* ignored (per-partition counts are per-interval global atomics) */
 #define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
- * bits 12-13: minimum resident CTAs per SM (0 = 2).  Tuning knobs only:
+ * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
+ * per SM (0 or 2: 2, 3: 3, 1: 4).  Tuning knobs only:
  * every setting renders the same frame. */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)

@@ -41,7 +41,7 @@ class TrEpoch(C.Structure):
     _fields_ = [
         ("active", C.c_void_p), ("bnode_active", C.c_void_p), ("step", C.c_void_p),
         ("tf_table", C.c_void_p), ("n_tf", C.c_int64), ("tf_lo", C.c_double),
-        ("tf_hi", C.c_double), ("knode_active", C.c_void_p),
+        ("tf_hi", C.c_double), ("knode_active", C.c_void_p), ("step_ratio", C.c_void_p),
     ]
 
 

@@ -69,10 +69,12 @@ TR_HD bool tr_pow_glibc_supported(double x, double y) {
     return (topx - 1u) < 0x7feu && (topy - 0x3beu) < 0x80u;  // x > 0 normal, finite
 }
 
-// log = pow_log_data (ln2hi, ln2lo, A[7], tab[128]{invc, pad, logc, logctail});
-// ehead = invln2N, shift, negln2hiN, negln2loN, C2..C5; etab = 128 x {tail, sbits}
-TR_HD double tr_pow_glibc(double x, double y, const uint64_t *log, const uint64_t *ehead,
-                          const uint64_t *etab, bool *exact) {
+// lhead = ln2hi, ln2lo, A[7]; ltab = 128 x {invc, pad, logc, logctail};
+// ehead = invln2N, shift, negln2hiN, negln2loN, C2..C5; etab = 128 x {tail, sbits}.
+// On the device the heads live in __constant__ memory (operands of the FP
+// instructions, no loads) and the tables in global memory, read with 16-B loads.
+TR_HD double tr_pow_glibc(double x, double y, const uint64_t *lhead, const uint64_t *ltab,
+                          const uint64_t *ehead, const uint64_t *etab, bool *exact) {
     // ---- log_inline(ix, &tail)
     const uint64_t ix = tr_as_u64(x);
     const uint64_t tmp = ix + 0xc0196aab00000000ull;  // ix - OFF, OFF = 0x3fe6955500000000
@@ -81,12 +83,18 @@ TR_HD double tr_pow_glibc(double x, double y, const uint64_t *log, const uint64_
     const uint64_t iz = ix - (tmp & 0xfff0000000000000ull);
     const double z = tr_as_double(iz);
     const double kd = (double)k;
-    const uint64_t *e = log + 9 + 4 * i;
+#ifdef __CUDA_ARCH__
+    const double2 e01 = __ldg(reinterpret_cast<const double2 *>(ltab) + 2 * i);
+    const double2 e23 = __ldg(reinterpret_cast<const double2 *>(ltab) + 2 * i + 1);
+    const double invc = e01.x, logc = e23.x, logctail = e23.y;
+#else
+    const uint64_t *e = ltab + 4 * i;
     const double invc = tr_as_double(e[0]), logc = tr_as_double(e[2]), logctail = tr_as_double(e[3]);
-    const double ln2hi = tr_as_double(log[0]), ln2lo = tr_as_double(log[1]);
-    const double A0 = tr_as_double(log[2]), A1 = tr_as_double(log[3]), A2 = tr_as_double(log[4]);
-    const double A3 = tr_as_double(log[5]), A4 = tr_as_double(log[6]), A5 = tr_as_double(log[7]);
-    const double A6 = tr_as_double(log[8]);
+#endif
+    const double ln2hi = tr_as_double(lhead[0]), ln2lo = tr_as_double(lhead[1]);
+    const double A0 = tr_as_double(lhead[2]), A1 = tr_as_double(lhead[3]), A2 = tr_as_double(lhead[4]);
+    const double A3 = tr_as_double(lhead[5]), A4 = tr_as_double(lhead[6]), A5 = tr_as_double(lhead[7]);
+    const double A6 = tr_as_double(lhead[8]);
     const double t1 = tr_fma(kd, ln2hi, logc);
     const double lo1 = tr_fma(kd, ln2lo, logctail);
     const double r = tr_fma(z, invc, -1.0);
@@ -129,10 +137,17 @@ TR_HD double tr_pow_glibc(double x, double y, const uint64_t *log, const uint64_
     rr = tr_fma(kd2, negln2lon, rr);
     const uint64_t top = ki << 45;
     const uint32_t idx = 2u * ((uint32_t)ki & 127u);
+#ifdef __CUDA_ARCH__
+    const double2 et2 = __ldg(reinterpret_cast<const double2 *>(etab) + (idx >> 1));
+    const double etail = et2.x;
+    const uint64_t sbits = tr_as_u64(et2.y) + top;
+#else
+    const double etail = tr_as_double(etab[idx]);
     const uint64_t sbits = etab[idx + 1] + top;
+#endif
     rr = elo + rr;
     const double c23 = tr_fma(rr, C3, C2);
-    const double tr = rr + tr_as_double(etab[idx]);
+    const double tr = rr + etail;
     const double r2 = rr * rr;
     const double c45 = tr_fma(rr, C5, C4);
     double t = tr_fma(c23, r2, tr);

@@ -971,7 +971,7 @@ double tr_pow_glibc_host(double x, double y, int32_t *exact) {
         return std::pow(x, y);
     }
     bool ex = false;
-    const double r = tr_pow_glibc(x, y, H_POW_LOG, H_POW_EXP_HEAD, H_POW_EXP_TAB, &ex);
+    const double r = tr_pow_glibc(x, y, H_POW_LOG, H_POW_LOG + 9, H_POW_EXP_HEAD, H_POW_EXP_TAB, &ex);
     if (exact) *exact = ex ? 1 : 0;
     return r;
 #else

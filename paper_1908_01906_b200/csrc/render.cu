@@ -18,16 +18,16 @@
 //       nothing to march are finished here, the rest get a cost bucket.
 //   order_rays_kernel  marching rays sorted into descending cost buckets
 //       (longest first, so the frame does not end on one long ray).
-//   march_group_kernel<G>  persistent CTAs; G lanes march ONE ray: each lane
-//       shades one consecutive sample (interval and k derived exactly from
-//       the list), then the group composites the G results in sample order
-//       with the exact early-termination rule.  Point location: uniform-grid
+//   march_kernel<G>  persistent CTAs; G lanes march ONE ray: each lane
+//       shades one consecutive sample (interval and k from the trace's prefix
+//       sample counts), then the group composites the G results in sample
+//       order with the exact early-termination rule.  Point location: uniform-grid
 //       candidate leaf proved by its exclusive box (a point strictly inside
 //       it can only lie in that leaf's tets, scanned in ascending id order:
 //       first hit = lowest index, the reference's tie rule K:119), else a
 //       full min-id-pruned BVH descent.
-//   The per-partition histogram is privatised per CTA in shared memory and
-//   merged with 64-bit integer atomics (exact, order independent).
+//   Per-partition samples are added per interval with 64-bit integer atomics
+//   (exact, order independent).
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -50,7 +50,6 @@ constexpr int TRACE_BLOCK = 128;
 constexpr int IV_CAP = 64;           // partition ids per ray kept in the scratch list
 constexpr int N_BUCKETS = 64;        // ray-cost buckets (4 per octave) for longest-first order
 constexpr int32_t CHILD_NONE = INT32_MIN;
-constexpr int HIST_SMEM_MAX = 8192;  // partitions counted in shared memory (u64)
 constexpr unsigned FULL = 0xffffffffu;
 
 // Optional kernel statistics (TR_FLAG_STATS): counters read back with
@@ -129,25 +128,40 @@ __device__ __forceinline__ bool strictly_in(const PQuery &q, const float *lo, co
            q.zu < hi[2];
 }
 
-// K:121-128: barycentrics of q in record k; true if all >= -BARY_TOL.
-__device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, uint32_t k,
-                                          const PQuery &q, double l[4]) {
+// The 96 B of a record the barycentric test reads (inverse + origin).
+struct RecM {
+    double2 a0, a1, a2, a3, a4, a5;
+};
+
+__device__ __forceinline__ RecM load_recm(const TrTetRecord *__restrict__ recs, uint32_t k) {
     const double2 *r = reinterpret_cast<const double2 *>(recs + k);
-    const double2 a0 = __ldg(r + 0), a1 = __ldg(r + 1), a2 = __ldg(r + 2);
-    const double2 a3 = __ldg(r + 3), a4 = __ldg(r + 4), a5 = __ldg(r + 5);
-    const double qx = q.x - a4.y, qy = q.y - a5.x, qz = q.z - a5.y;
-    const double l1 = a0.x * qx + a0.y * qy + a1.x * qz;
-    const double l2 = a1.y * qx + a2.x * qy + a2.y * qz;
-    const double l3 = a3.x * qx + a3.y * qy + a4.x * qz;
+    RecM m;
+    m.a0 = __ldg(r + 0); m.a1 = __ldg(r + 1); m.a2 = __ldg(r + 2);
+    m.a3 = __ldg(r + 3); m.a4 = __ldg(r + 4); m.a5 = __ldg(r + 5);
+    return m;
+}
+
+// K:121-128: barycentrics of q in a record; true if all >= -BARY_TOL.
+__device__ __forceinline__ bool bary_of(const RecM &m, const PQuery &q, double l[4]) {
+    const double qx = q.x - m.a4.y, qy = q.y - m.a5.x, qz = q.z - m.a5.y;
+    const double l1 = m.a0.x * qx + m.a0.y * qy + m.a1.x * qz;
+    const double l2 = m.a1.y * qx + m.a2.x * qy + m.a2.y * qz;
+    const double l3 = m.a3.x * qx + m.a3.y * qy + m.a4.x * qz;
     const double l0 = 1.0 - l1 - l2 - l3;
     l[0] = l0; l[1] = l1; l[2] = l2; l[3] = l3;
     return l0 >= -BARY_TOL && l1 >= -BARY_TOL && l2 >= -BARY_TOL && l3 >= -BARY_TOL;
 }
 
+__device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, uint32_t k,
+                                          const PQuery &q, double l[4]) {
+    return bary_of(load_recm(recs, k), q, l);
+}
+
 #if TR_HAVE_GLIBC_POW
-__device__ const unsigned long long d_pow_log[] = TR_POW_LOG_INIT;
-__device__ const unsigned long long d_pow_ehead[] = TR_POW_EXP_HEAD_INIT;
-__device__ const unsigned long long d_pow_etab[] = TR_POW_EXP_TAB_INIT;
+__constant__ unsigned long long c_pow_lhead[] = TR_POW_LOG_HEAD_INIT;
+__constant__ unsigned long long c_pow_ehead[] = TR_POW_EXP_HEAD_INIT;
+__device__ const __align__(16) unsigned long long d_pow_ltab[] = TR_POW_LOG_TAB_INIT;
+__device__ const __align__(16) unsigned long long d_pow_etab[] = TR_POW_EXP_TAB_INIT;
 #endif
 
 // x**y as the reference computes it (glibc pow, K:22 / K:27): the restated
@@ -157,9 +171,9 @@ __device__ __forceinline__ double ref_pow(double x, double y) {
 #if TR_HAVE_GLIBC_POW
     if (tr_pow_glibc_supported(x, y)) {
         bool exact;
-        const double r = tr_pow_glibc(x, y, (const uint64_t *)d_pow_log,
-                                      (const uint64_t *)d_pow_ehead, (const uint64_t *)d_pow_etab,
-                                      &exact);
+        const double r = tr_pow_glibc(x, y, (const uint64_t *)c_pow_lhead,
+                                      (const uint64_t *)d_pow_ltab, (const uint64_t *)c_pow_ehead,
+                                      (const uint64_t *)d_pow_etab, &exact);
         // |y log x| >= 512: glibc under/overflows; for x < 1 the result is
         // < 2^-738, so 1 - pow is 1.0 either way
         if (exact || x < 1.0) return r;
@@ -191,17 +205,31 @@ struct SceneK {  // kernel copy of TrDeviceScene
 
 // Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
 // ascending id order, so the first one containing q is the lowest index.
-// Tested two at a time so both records' loads are in flight together.
+// The next record's loads are issued before the current one is tested.
 __device__ __forceinline__ uint32_t scan_leaf_first(const SceneK &S, uint32_t start,
+                                                    uint32_t count, const PQuery &q, double l[4]) {
+    if (count == 0) return UINT32_MAX;
+    const uint32_t end = start + count;
+    RecM cur = load_recm(S.tets, start);
+    for (uint32_t k = start;; ++k) {
+        const bool has_next = k + 1 < end;
+        const RecM nxt = load_recm(S.tets, has_next ? k + 1 : k);
+        if (bary_of(cur, q, l)) return k;
+        if (!has_next) return UINT32_MAX;
+        cur = nxt;
+    }
+}
+
+// Pairwise variant: two records in flight per step, tested in order.
+__device__ __forceinline__ uint32_t scan_leaf_pairs(const SceneK &S, uint32_t start,
                                                     uint32_t count, const PQuery &q, double l[4]) {
     const uint32_t end = start + count;
     for (uint32_t k = start; k < end; k += 2) {
-        double la[4], lb[4];
-        const bool pa = bary_test(S.tets, k, q, la);
         const bool has_b = k + 1 < end;
-        const bool pb = bary_test(S.tets, has_b ? k + 1 : k, q, lb) && has_b;
-        if (pa) { l[0] = la[0]; l[1] = la[1]; l[2] = la[2]; l[3] = la[3]; return k; }
-        if (pb) { l[0] = lb[0]; l[1] = lb[1]; l[2] = lb[2]; l[3] = lb[3]; return k + 1; }
+        const RecM A = load_recm(S.tets, k);
+        const RecM Bm = load_recm(S.tets, has_b ? k + 1 : k);
+        if (bary_of(A, q, l)) return k;
+        if (has_b && bary_of(Bm, q, l)) return k + 1;
     }
     return UINT32_MAX;
 }
@@ -390,6 +418,7 @@ struct EpochK {
     const uint8_t *__restrict__ active;
     const uint8_t *__restrict__ bnode_active;
     const double *__restrict__ step;
+    const double *__restrict__ step_ratio;  // (P,2): step, step / s1
     const double *__restrict__ tf;
     int64_t n_tf;
     double tf_lo, tf_hi;
@@ -620,12 +649,22 @@ struct FrameK {
     int64_t tiles_x, n_tiles, my_tiles;
     int64_t ray_begin, n_rays;   // this chunk: rays [ray_begin, ray_begin + n_rays) in tile order
     int32_t n_parts;
-    int32_t hist_smem;
 };
 
-struct IvBuf {                   // per-chunk scratch, interval-major lists of partition ids
-    int32_t *pid;                // [IV_CAP][n_rays]
-    uint32_t *cnt;               // [n_rays]: n | bucket << 16 | 0x80000000 if more than IV_CAP
+// One stored interval of a ray (16 B): next_interval's clamped entry, the
+// partition, and the ray's inclusive prefix count of march_range samples.
+struct __align__(16) IvRec {
+    double a;
+    int32_t pid;     // -1: reference mode's mesh-box interval (K:346-353)
+    uint32_t cum;
+};
+constexpr uint32_t CUM_MAX = 0x7fffffffu;   // longer lists continue inline in the march
+constexpr uint32_t CNT_MORE = 0x80000000u;  // cnt word: intervals past the stored list
+
+struct IvBuf {                   // per-chunk scratch
+    IvRec *rec;                  // [n_rays][IV_CAP], ray-major
+    uint32_t *cnt;               // [n_rays]: n | bucket << 16 | CNT_MORE
+    double *tail;                // [n_rays]: t_min after the last stored interval (CNT_MORE only)
     uint32_t *order;             // marching rays, most expensive first
     uint32_t *hist, *cursor;     // [N_BUCKETS] each; bucket 0 = nothing to march
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
@@ -703,11 +742,11 @@ __device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &
 }
 
 // Phase 1 (one thread per ray, 8x4 pixel tiles per warp): the exact
-// partition-interval sequence (K:360-391 calling next_interval K:173-230),
-// stored as partition ids; the clamped (t_enter, t_exit) are recomputed
-// bit-identically in phase 2.  Rays with nothing to march (no hit, or only
-// degenerate intervals) are finished here; the others get a cost bucket
-// (~4 log2 of their sample count) for longest-first scheduling.
+// partition-interval sequence (K:360-391 calling next_interval K:173-230)
+// with each interval's clamped entry and the running count of the samples
+// march_range would take (K:277-280).  Rays with nothing to march (no hit,
+// or only degenerate intervals) are finished here; the others get a cost
+// bucket (~4 log2 of their sample count) for longest-first scheduling.
 __global__ void __launch_bounds__(TRACE_BLOCK)
 trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
@@ -718,21 +757,33 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         const Pixel px = ray_pixel(F, rr);
         if (px.valid) {
             const RayD ray = make_ray(F.f, px.ix, px.iy);
-            double cost = 0.0;
+            const double phase = F.f.jitter ? hash01(px.ix, px.iy) : 0.5;  // K:340
+            IvRec *rec = iv.rec + rr * IV_CAP;
+            uint32_t cum = 0;
             bool more = false;
-            if (F.f.mode == 0) {
+            double t_min = 0.0;
+            if (F.f.mode == 0) {  // K:346-353: the mesh box is the one interval
                 double a, b;
                 slab(ray, S.mesh_lo, S.mesh_hi, a, b);
                 const double ta = (a > 0.0) ? a : 0.0;
-                if (a <= b && b - ta >= F.f.eps) cost = (b - ta) / F.f.s1 + 1.0;
+                if (a <= b && b - ta >= F.f.eps) {
+                    const int64_t ns = interval_samples(ta, b, F.f.s1, phase);
+                    if (ns > (int64_t)CUM_MAX) {
+                        more = true;   // the march recomputes it inline
+                    } else {
+                        IvRec r; r.a = ta; r.pid = -1; r.cum = (uint32_t)ns;
+                        rec[0] = r;
+                        n = 1;
+                        cum = (uint32_t)ns;
+                    }
+                }
             } else {
                 bool use_bsp = S.knodes != nullptr && !(F.f.flags & TR_FLAG_NO_BSP);
                 BspTrace T;
                 if (use_bsp) bsp_begin(S, ray, T);
                 for (int attempt = 0; attempt < 2; ++attempt) {
-                    double t_min = 0.0;
                     int32_t last = -1;
-                    n = 0; cost = 0.0; more = false;
+                    n = 0; cum = 0; more = false; t_min = 0.0;
                     while (true) {
                         const double excl = (last < 0) ? 0.0 : F.f.eps;
                         double a, b;
@@ -740,12 +791,17 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                             ? bsp_next_interval(S, E, ray, T, t_min, excl, last, a, b)
                             : next_interval(S, E, ray, t_min, excl, last, a, b);
                         if (pid < 0) break;
-                        if (n == IV_CAP) { more = true; cost += 4.0 * IV_CAP; break; }
-                        iv.pid[(int64_t)n * F.n_rays + rr] = pid;
+                        if (n == IV_CAP) { more = true; break; }
+                        int64_t ns = 0;
+                        if (b - a >= F.f.eps)   // K:374
+                            ns = interval_samples(a, b, (F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1,
+                                                  phase);
+                        if ((int64_t)cum + ns > (int64_t)CUM_MAX) { more = true; break; }
+                        cum += (uint32_t)ns;
+                        IvRec r; r.a = a; r.pid = pid; r.cum = cum;
+                        rec[n] = r;
                         ++n;
-                        if (b - a >= F.f.eps)
-                            cost += (b - a) / ((F.f.mode == 2) ? __ldg(E.step + pid) : F.f.s1) + 1.0;
-                        t_min = b - F.f.eps;
+                        t_min = b - F.f.eps;   // K:390-391
                         last = pid;
                         if (use_bsp) bsp_compact(T, t_min);
                     }
@@ -753,18 +809,19 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     use_bsp = false;  // candidate buffer overflowed: redo with the BVH
                 }
             }
+            if (more) iv.tail[rr] = t_min;
             if (F.f.flags & TR_FLAG_STATS) {
                 atomicAdd(&g_stats[ST_TRACE_RAYS], 1ull);
                 atomicAdd(&g_stats[ST_TRACE_IV], (unsigned long long)n);
             }
-            if (cost > 0.0) {
-                bucket = cost_bucket(cost);
+            if (cum > 0 || more) {
+                bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
             } else {  // nothing to march: background, `visited` = every interval returned
                 const Acc zero = {0.0, 0.0, 0.0, 0.0};
                 write_pixel(F.f, O, px.out, zero, 0, (int32_t)n);
                 vis_done = n;
             }
-            iv.cnt[rr] = n | (bucket << 16) | (more ? 0x80000000u : 0u);
+            iv.cnt[rr] = n | (bucket << 16) | (more ? CNT_MORE : 0u);
         } else {
             iv.cnt[rr] = 0;
         }
@@ -804,49 +861,94 @@ order_rays_kernel(FrameK F, IvBuf iv) {
     iv.order[start[bucket] + base + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)rr;
 }
 
-// Phase 2: G lanes march one ray together.  Per round each lane of the
-// group takes one consecutive sample of the ray (across interval borders:
-// the window is the next G intervals of the list), locates and shades it
-// independently, then the group composites the G results in sample order
-// with the exact early-termination rule (K:285-295).  Lanes whose group has
-// no ray take part in the collectives with empty windows.
-template <int G>
-__global__ void __launch_bounds__(MARCH_BLOCK, 2)
-march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
+__device__ __forceinline__ IvRec load_rec(const IvRec *p) {
+    const int4 v = __ldg(reinterpret_cast<const int4 *>(p));
+    IvRec r;
+    r.a = __hiloint2double(v.y, v.x);
+    r.pid = v.z;
+    r.cum = (uint32_t)v.w;
+    return r;
+}
+
+// Inline continuation past the stored list (IV_CAP intervals or CUM_MAX
+// samples): the next interval with samples, from (t_min, last) (K:360-391).
+// Returns false when the ray has no further interval.  Run by one lane.
+struct Inline {
+    double t_min, a;
+    int64_t n, k;      // samples of the current inline interval, samples taken
+    int32_t last, pid;
+    int32_t visited;   // inline intervals returned so far
+    int32_t started;   // mode 0: the mesh-box interval was issued
+};
+
+__device__ bool inline_next(const SceneK &S, const EpochK &E, const TrFrame &fr, int64_t ix,
+                            int64_t iy, double phase, Inline &L) {
+    const RayD ray = make_ray(fr, ix, iy);
+    if (fr.mode == 0) {
+        if (L.started) return false;
+        L.started = 1;
+        double a, b;
+        slab(ray, S.mesh_lo, S.mesh_hi, a, b);
+        const double ta = (a > 0.0) ? a : 0.0;
+        if (!(a <= b && b - ta >= fr.eps)) return false;
+        L.a = ta; L.pid = -1; L.k = 0;
+        L.n = interval_samples(ta, b, fr.s1, phase);
+        return true;
+    }
+    while (true) {
+        double a, b;
+        const int32_t pid = next_interval(S, E, ray, L.t_min, (L.last < 0) ? 0.0 : fr.eps, L.last, a, b);
+        if (pid < 0) return false;
+        L.visited += 1;
+        L.t_min = b - fr.eps;
+        L.last = pid;
+        if (b - a >= fr.eps) {
+            L.a = a; L.pid = pid; L.k = 0;
+            L.n = interval_samples(a, b, (fr.mode == 2) ? __ldg(E.step + pid) : fr.s1, phase);
+            return true;
+        }
+    }
+}
+
+// Phase 2: G lanes march one ray together.  Per round lane j of the group
+// takes the ray's next-but-j sample: its interval is found from the stored
+// prefix counts, its position is t = a + (k + phase) * step (K:278), and it
+// is located, interpolated, classified and opacity-corrected independently;
+// the group then composites the round's samples in order with the exact
+// early-termination rule (K:285-295).  Groups without a ray take part in
+// the warp collectives with no sample.
+template <int G, int MINB>
+__global__ void __launch_bounds__(MARCH_BLOCK, MINB)
+march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
-    extern __shared__ unsigned long long hist[];  // [n_parts] when F.hist_smem
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
-    __shared__ double shade[MARCH_BLOCK][5];      // per-lane sample result: ca, r, g, b, (found)
+    __shared__ double4 shade[MARCH_BLOCK];              // per-lane sample result: ca, r, g, b
+    __shared__ Inline inl[MARCH_BLOCK / G];             // per-group inline state (rare path)
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G;                   // lane in group
     const int gbase = lane - j;               // first lane of my group
+    Inline &L = inl[threadIdx.x / G];
     const bool track = fr.track_ppart && fr.mode != 0;
-    if (track && F.hist_smem)
-        for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK) hist[i] = 0ull;
-    __syncthreads();
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
     const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
-    const bool grid_indirect = (fr.flags & TR_FLAG_GRID_INDIRECT) != 0;
+    const bool seq_scan = (fr.flags & TR_FLAG_SEQ_SCAN) != 0;
+    const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << gbase);
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
 
     // group-uniform ray state
-    bool active = false, exhausted = false;
+    bool active = false, exhausted = false, inline_mode = false;
     int64_t rr = 0, out = 0;
-    RayD ray;
-    double phase = 0.5;
+    int32_t pix = 0, piy = 0;
+    double ox = 0, oy = 0, oz = 0, dx = 0, dy = 0, dz = 0, phase = 0.5;
     Acc acc = {0.0, 0.0, 0.0, 0.0};
     int64_t samples = 0;
-    int32_t visited = 0;
-    int32_t i_cur = 0, iv_n = 0, last_pid = -1;
+    uint32_t taken = 0, c_tot = 0, c_before = 0;
+    int32_t i_cur = 0, n_iv = 0;
     bool more = false;
-    int64_t k_cur = 0;
-    double tmin_c = 0.0;
-    int32_t ov_pid = -1;                       // inline interval past the list
-    double ov_a = 0.0, ov_b = 0.0;
-    double m0_a = 0.0, m0_b = 0.0;             // reference mode's single interval
+    const IvRec *rec = nullptr;
 
     while (true) {
         // ---- refill: one queue slot per group that needs a ray
@@ -865,25 +967,32 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     rr = (int64_t)iv.order[qpos];
                     const Pixel px = ray_pixel(F, rr);
                     out = px.out;
-                    ray = make_ray(fr, px.ix, px.iy);
+                    pix = (int32_t)px.ix;
+                    piy = (int32_t)px.iy;
+                    const RayD ray = make_ray(fr, px.ix, px.iy);
+                    ox = ray.ox; oy = ray.oy; oz = ray.oz;
+                    dx = ray.dx; dy = ray.dy; dz = ray.dz;
                     phase = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
                     acc.r = acc.g = acc.b = acc.a = 0.0;
                     samples = 0;
-                    visited = 0;
+                    taken = 0;
                     i_cur = 0;
-                    k_cur = 0;
-                    tmin_c = 0.0;
-                    last_pid = -1;
-                    ov_pid = -1;
+                    c_before = 0;
                     const uint32_t c = iv.cnt[rr];
-                    iv_n = (int32_t)(c & 0xffffu);
-                    more = (c >> 31) != 0;
-                    if (fr.mode == 0) {  // K:346-353: the mesh box is the one interval
-                        double a0, b0;
-                        slab(ray, S.mesh_lo, S.mesh_hi, a0, b0);
-                        m0_a = (a0 > 0.0) ? a0 : 0.0;
-                        m0_b = b0;
-                        iv_n = 1;
+                    n_iv = (int32_t)(c & 0xffffu);
+                    more = (c & CNT_MORE) != 0;
+                    rec = iv.rec + rr * IV_CAP;
+                    c_tot = n_iv > 0 ? load_rec(rec + (n_iv - 1)).cum : 0u;
+                    inline_mode = false;
+                    if (c_tot == 0) {  // only inline intervals (the trace ran out of room)
+                        inline_mode = true;
+                        if (j == 0) {
+                            L.t_min = iv.tail[rr];
+                            L.last = n_iv > 0 ? load_rec(rec + (n_iv - 1)).pid : -1;
+                            L.visited = 0;
+                            L.started = 0;
+                            L.n = 0; L.k = 0;
+                        }
                     }
                     active = true;
                 }
@@ -891,200 +1000,201 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         }
         if (__all_sync(FULL, exhausted)) break;
 
-        // ---- past the stored list (rare): next_interval inline, one interval per window
-        const bool inline_iv = active && fr.mode != 0 && i_cur >= iv_n;
-        if (inline_iv && ov_pid < 0 && more && j == 0) {
-            if (stats) atomicAdd(&g_stats[ST_INLINE_IV], 1ull);
-            double a0, b0;
-            ov_pid = next_interval(S, E, ray, tmin_c, (last_pid < 0) ? 0.0 : fr.eps, last_pid,
-                                   a0, b0);
-            ov_a = a0;
-            ov_b = b0;
-        }
-        ov_pid = __shfl_sync(FULL, ov_pid, gbase);
-        ov_a = __shfl_sync(FULL, ov_a, gbase);
-        ov_b = __shfl_sync(FULL, ov_b, gbase);
-        if (inline_iv && ov_pid < 0) more = false;
+        // ---- inline mode: lane 0 fetches the next interval with samples when needed
+        bool idle = false;
+        if (active && inline_mode && j == 0 && L.k >= L.n)
+            idle = !inline_next(S, E, fr, pix, piy, phase, L);
+        __syncwarp();
+        idle = __shfl_sync(FULL, idle, gbase);
 
-        // ---- the window: intervals i_cur .. i_cur+G-1, one per lane
-        int32_t pid = -1;
-        double a = 0.0, b = 0.0, step = fr.s1;
-        bool valid = false;
-        if (active) {
-            if (fr.mode == 0) {
-                valid = (j == 0) && i_cur < 1;
-                a = m0_a;
-                b = m0_b;
-            } else if (inline_iv) {
-                valid = (j == 0) && ov_pid >= 0;
-                pid = ov_pid;
-                a = ov_a;
-                b = ov_b;
+        // ---- my sample
+        bool has = false;
+        double a = 0.0;
+        int32_t pid = -1, i_mine = 0;
+        uint32_t c0_mine = 0;
+        int64_t k = 0, remaining = 0;
+        if (active && !idle) {
+            if (!inline_mode) {
+                const uint32_t s = taken + (uint32_t)j;
+                remaining = (int64_t)(c_tot - taken);
+                if (s < c_tot) {
+                    int32_t i = i_cur;
+                    uint32_t c0 = c_before;
+                    IvRec r = load_rec(rec + i);
+                    while (r.cum <= s) { c0 = r.cum; ++i; r = load_rec(rec + i); }
+                    a = r.a;
+                    pid = r.pid;
+                    k = (int64_t)(s - c0);
+                    i_mine = i;
+                    c0_mine = c0;
+                    has = true;
+                }
             } else {
-                const int32_t ii = i_cur + j;
-                valid = ii < iv_n;
-                if (valid) {
-                    pid = iv.pid[(int64_t)ii * F.n_rays + rr];
-                    // next_interval's slab of the partition box (bit-identical)
-                    const double lo[3] = {__ldg(S.part_lo + 3 * pid), __ldg(S.part_lo + 3 * pid + 1),
-                                          __ldg(S.part_lo + 3 * pid + 2)};
-                    const double hi[3] = {__ldg(S.part_hi + 3 * pid), __ldg(S.part_hi + 3 * pid + 1),
-                                          __ldg(S.part_hi + 3 * pid + 2)};
-                    slab(ray, lo, hi, a, b);
+                remaining = L.n - L.k;
+                if ((int64_t)j < remaining) {
+                    a = L.a;
+                    pid = L.pid;
+                    k = L.k + j;
+                    has = true;
                 }
             }
         }
-        // list intervals: t_min = previous exit - eps, entry clamped to it (K:200, K:390)
-        const double prev_b = __shfl_up_sync(FULL, b, 1, G);
-        const int32_t prev_pid = __shfl_up_sync(FULL, pid, 1, G);
-        if (valid && fr.mode != 0 && !inline_iv) {
-            const double tmin_j = (j == 0) ? tmin_c : prev_b - fr.eps;
-            a = (a > tmin_j) ? a : tmin_j;
-        }
-        if (valid && fr.mode == 2) step = __ldg(E.step + pid);
-        const double e_win = step / fr.s1;  // opacity_correction's exponent (K:27), per interval
-        const bool marchable = valid && (b - a >= fr.eps);
-        const int64_t n_i = marchable ? interval_samples(a, b, step, phase) : 0;
-        int64_t rem = n_i - ((j == 0) ? k_cur : 0);
-        if (rem < 0) rem = 0;
-        int64_t incl = rem;  // inclusive scan of remaining samples over the window
-#pragma unroll
-        for (int d = 1; d < G; d <<= 1) {
-            const int64_t y = __shfl_up_sync(FULL, incl, d, G);
-            if (j >= d) incl += y;
-        }
-        const int64_t R = __shfl_sync(FULL, incl, gbase + G - 1);
-        const unsigned vbits = (__ballot_sync(FULL, valid) >> gbase) &
-                               ((G == 32) ? FULL : ((1u << G) - 1u));
-        const int nvalid = __popc(vbits);
-        // my sample is the j-th of the round: owner = first window lane with incl > j
-        int owner = G;
-        int64_t own_incl = 0, own_rem = 0;
-#pragma unroll
-        for (int l = G - 1; l >= 0; --l) {
-            const int64_t x = __shfl_sync(FULL, incl, gbase + l);
-            const int64_t y = __shfl_sync(FULL, rem, gbase + l);
-            if (x > j) { owner = l; own_incl = x; own_rem = y; }
-        }
-        const bool has = active && (int64_t)j < R;
-        const int src = gbase + (owner < G ? owner : 0);
-        const double sa = __shfl_sync(FULL, a, src);
-        const double sstep = __shfl_sync(FULL, step, src);
-        const double se = __shfl_sync(FULL, e_win, src);
-        const int32_t spid = __shfl_sync(FULL, pid, src);
-        const int64_t sfirst = own_incl - own_rem;  // round index of the owner's first sample
-        const int64_t sk = (int64_t)j - sfirst + ((owner == 0) ? k_cur : 0);
 
         // ---- shade my sample (K:277-290)
-        double ca = 0.0, cr = 0.0, cg = 0.0, cb = 0.0, found = 0.0;
+        double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
+        bool found = false;
         if (has) {
-            const double t = sa + ((double)sk + phase) * sstep;
-            const PQuery q = make_query(ray.ox + t * ray.dx, ray.oy + t * ray.dy, ray.oz + t * ray.dz);
-            LeafHint h;
-            h.valid = false;
-            double v;
+            double step = fr.s1, e = 1.0;
+            if (fr.mode == 2) {
+                const double2 se = __ldg(reinterpret_cast<const double2 *>(E.step_ratio) + pid);
+                step = se.x;
+                e = se.y;
+            }
+            const double t = a + ((double)k + phase) * step;
+            const PQuery q = make_query(ox + t * dx, oy + t * dy, oz + t * dz);
             if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
-            if (field_at(S, q, h, false, use_grid, v, stats, grid_indirect) != UINT32_MAX) {
-                if (stats) atomicAdd(&g_stats[ST_FOUND], 1ull);
+            // point location (K:93-136): the grid's candidate leaf proved by
+            // its exclusive box, else the full descent -- both exact
+            double l[4];
+            uint32_t pos = UINT32_MAX;
+            bool located = false;
+            if (!located && use_grid) {
+                const int64_t gc = grid_cell(S, q);
+                if (gc >= 0) {
+                    LeafHint hh;
+                    load_leaf(S.pgrid_leaf + gc, hh);
+                    if (strictly_in(q, hh.lo, hh.hi)) {
+                        pos = seq_scan ? scan_leaf_first(S, hh.start, hh.count, q, l)
+                                       : scan_leaf_pairs(S, hh.start, hh.count, q, l);
+                        located = true;
+                        if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
+                    }
+                }
+            }
+            if (!located) {
+                int32_t leaf;
+                if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
+                pos = locate_full(S, q, l, leaf);
+            }
+            double v = 0.0;
+            if (pos != UINT32_MAX) {
+                const double2 *rp = reinterpret_cast<const double2 *>(S.tets + pos);
+                if (S.centering == 0) {   // K:149-151
+                    const double2 f01 = __ldg(rp + 6), f23 = __ldg(rp + 7);
+                    v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
+                } else {                  // K:153
+                    v = __ldg(rp + 6).x;
+                }
+            }
+            if (pos != UINT32_MAX) {
                 double c[4];
                 tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
                 const double x = 1.0 - c[3];
-                ca = 1.0 - ((se == 1.0) ? x : ref_pow(x, se));  // glibc pow(x, 1) == x
-                if (stats && se != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
-                cr = c[0]; cg = c[1]; cb = c[2];
-                found = 1.0;
+                sh.x = 1.0 - ((e == 1.0) ? x : ref_pow(x, e));  // K:27; glibc pow(x, 1) == x
+                if (stats) {
+                    atomicAdd(&g_stats[ST_FOUND], 1ull);
+                    if (e != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
+                }
+                sh.y = c[0]; sh.z = c[1]; sh.w = c[2];
+                found = true;
             }
         }
-        double *mine = shade[threadIdx.x];
-        mine[0] = ca; mine[1] = cr; mine[2] = cg; mine[3] = cb; mine[4] = found;
+        shade[threadIdx.x] = sh;
+        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
 
         // ---- composite the round in sample order (K:285-295).  A sample
         // outside every tet has ca = c = 0, which leaves acc bit-unchanged;
-        // termination is only tested after a found sample, as in K:285-295.
-        const int cnt = (int)((R < G) ? R : G);
-        if (stats && active && j == 0) {
-            atomicAdd(&g_stats[ST_ROUNDS], 1ull);
-            if (R < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
-        }
-        int taken = cnt;
+        // termination is only tested after a found sample.
+        const int cnt = (int)((remaining < G) ? remaining : G);
+        int taken_r = cnt;
         bool term = false;
-        if (active) {
-            const double(*grp)[5] = shade + (threadIdx.x - j);
+        if (active && !idle) {
+            const double4 *grp = shade + (threadIdx.x - j);
             for (int m = 0; m < cnt; ++m) {
-                const double w = (1.0 - acc.a) * grp[m][0];
-                acc.r += w * grp[m][1];
-                acc.g += w * grp[m][2];
-                acc.b += w * grp[m][3];
+                const double4 g = grp[m];
+                const double w = (1.0 - acc.a) * g.x;
+                acc.r += w * g.y;
+                acc.g += w * g.z;
+                acc.b += w * g.w;
                 acc.a += w;
-                if (grp[m][4] != 0.0 && acc.a >= fr.term) { taken = m + 1; term = true; break; }
+                if (((fbits >> m) & 1u) && acc.a >= fr.term) { taken_r = m + 1; term = true; break; }
+            }
+            if (stats && j == 0) {
+                atomicAdd(&g_stats[ST_ROUNDS], 1ull);
+                if (cnt < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
             }
         }
         __syncwarp();
-        // per-partition samples: the first taken sample of each interval's run adds the run
-        if (track && has && (int64_t)j < taken && (int64_t)j == sfirst) {
-            const int64_t c = ((own_incl < taken) ? own_incl : (int64_t)taken) - (int64_t)j;
-            if (F.hist_smem) atomicAdd(&hist[spid], (unsigned long long)c);
-            else atomicAdd((unsigned long long *)O.ppart + spid, (unsigned long long)c);
-        }
 
         // ---- advance the group's cursor (all shuffles before any divergence)
-        const int lastj = (taken > 0) ? taken - 1 : 0;
-        const int own_last = __shfl_sync(FULL, owner, gbase + lastj);
-        const int64_t k_last = __shfl_sync(FULL, sk, gbase + lastj);
-        const int ol = (own_last < G) ? own_last : 0;
-        const double b_before_own = __shfl_sync(FULL, prev_b, gbase + ol);
-        const int32_t pid_before_own = __shfl_sync(FULL, prev_pid, gbase + ol);
-        const int lv = (nvalid > 0) ? nvalid - 1 : 0;
-        const double b_lastvalid = __shfl_sync(FULL, b, gbase + lv);
-        const int32_t pid_lastvalid = __shfl_sync(FULL, pid, gbase + lv);
+        const int src = gbase + ((taken_r > 0) ? taken_r - 1 : 0);
+        const int32_t i_last = __shfl_sync(FULL, i_mine, src);
+        const uint32_t c0_last = __shfl_sync(FULL, c0_mine, src);
+        bool done = false, flush = false;
+        int32_t flush_n = 0;
         if (active) {
-            samples += taken;
-            bool done = false;
-            if (term) {  // K:388-389: the terminating interval is the last one visited
-                if (fr.mode != 0) visited += own_last + 1;
+            if (idle) {  // inline intervals exhausted
                 done = true;
-            } else if (R > G) {  // interval own_last continues in the next round
-                if (fr.mode != 0 && !inline_iv && own_last > 0) {
-                    visited += own_last;
-                    i_cur += own_last;
-                    tmin_c = b_before_own - fr.eps;
-                    last_pid = pid_before_own;
-                }
-                k_cur = k_last + 1;
-            } else if (fr.mode == 0) {  // the single interval is done
-                done = true;
-            } else if (inline_iv) {
-                if (ov_pid < 0) {
+            } else if (!inline_mode) {
+                samples += taken_r;
+                taken += (uint32_t)taken_r;
+                i_cur = i_last;
+                c_before = c0_last;
+                if (term) {                       // K:388-389: the last interval visited
+                    flush = true; flush_n = i_last + 1;
                     done = true;
-                } else {
-                    visited += 1;
-                    tmin_c = ov_b - fr.eps;
-                    last_pid = ov_pid;
-                    ov_pid = -1;
-                    k_cur = 0;
+                } else if (taken == c_tot) {      // stored list consumed
+                    flush = true; flush_n = n_iv;
+                    if (more) {
+                        inline_mode = true;
+                        if (j == 0) {
+                            L.t_min = iv.tail[rr];
+                            L.last = n_iv > 0 ? rec[n_iv - 1].pid : -1;
+                            L.visited = 0;
+                            L.started = 1;       // mode 0 has one interval, stored
+                            L.n = 0; L.k = 0;
+                        }
+                    } else {
+                        done = true;
+                    }
                 }
-            } else {  // every interval of the window is consumed
-                visited += nvalid;
-                i_cur += nvalid;
-                k_cur = 0;
-                if (nvalid > 0) {
-                    tmin_c = b_lastvalid - fr.eps;
-                    last_pid = pid_lastvalid;
-                }
-                done = (i_cur >= iv_n) && !more;
-            }
-            if (done) {
+            } else {
+                samples += taken_r;
                 if (j == 0) {
-                    write_pixel(fr, O, out, acc, samples, visited);
-                    my_samples += (unsigned long long)samples;
-                    my_visited += (unsigned long long)visited;
+                    L.k += taken_r;
+                    if (track && L.pid >= 0)
+                        atomicAdd((unsigned long long *)O.ppart + L.pid, (unsigned long long)taken_r);
                 }
-                active = false;
+                if (term) done = true;
             }
         }
+        // per-partition samples of the stored intervals (K:386-387): the
+        // group's lanes add the intervals' counts, the last one clipped
+        if (flush && track) {
+            for (int32_t i = j; i < flush_n; i += G) {
+                const IvRec r = load_rec(rec + i);
+                const uint32_t lo = (i > 0) ? load_rec(rec + (i - 1)).cum : 0u;
+                const uint32_t hi = (r.cum < taken) ? r.cum : taken;
+                if (hi > lo) atomicAdd((unsigned long long *)O.ppart + r.pid, (unsigned long long)(hi - lo));
+            }
+        }
+        if (done) {
+            if (j == 0) {
+                int32_t visited = 0;
+                if (fr.mode != 0) {
+                    if (!inline_mode) visited = term ? i_last + 1 : n_iv;
+                    else visited = n_iv + L.visited;
+                }
+                write_pixel(fr, O, out, acc, samples, visited);
+                my_samples += (unsigned long long)samples;
+                my_visited += (unsigned long long)visited;
+            }
+            active = false;
+        }
+        __syncwarp();
     }
-    // block reduction of the frame totals (R:198-201) and histogram merge
+    // block reduction of the frame totals (R:198-201)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
         my_samples += __shfl_xor_sync(FULL, my_samples, off);
@@ -1098,9 +1208,7 @@ march_group_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (s) atomicAdd((unsigned long long *)O.totals, s);
         if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
     }
-    if (track && F.hist_smem)
-        for (int i = threadIdx.x; i < F.n_parts; i += MARCH_BLOCK)
-            if (hist[i]) atomicAdd((unsigned long long *)O.ppart + i, hist[i]);
+    (void)gmask;
 }
 
 __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restrict__ pts,
@@ -1194,7 +1302,7 @@ int sm_count() {
     return n;
 }
 
-constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 4 + 4 + 4;
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4;  // rec + tail + cnt + order
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
 }  // namespace
@@ -1226,7 +1334,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         epoch->n_tf < 2)
         return tr_fail(TR_EINVAL, "tr_render_frame: missing buffer");
     if (frame->mode != 0 && (!scene->bnodes || !epoch->active || !epoch->bnode_active ||
-                             (frame->mode == 2 && !epoch->step)))
+                             (frame->mode == 2 && (!epoch->step || !epoch->step_ratio))))
         return tr_fail(TR_EINVAL, "tr_render_frame: missing partition buffers");
     if (frame->track_ppart && frame->mode != 0 && !out->ppart)
         return tr_fail(TR_EINVAL, "tr_render_frame: missing ppart buffer");
@@ -1237,6 +1345,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     E.knode_active = epoch->knode_active;
     E.bnode_active = epoch->bnode_active;
     E.step = epoch->step;
+    E.step_ratio = epoch->step_ratio;
     E.tf = epoch->tf_table;
     E.n_tf = epoch->n_tf;
     E.tf_lo = epoch->tf_lo;
@@ -1248,10 +1357,6 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     F.my_tiles = (F.n_tiles - frame->shard_rank + frame->shard_count - 1) / frame->shard_count;
     if (F.my_tiles < 0) F.my_tiles = 0;
     F.n_parts = (int32_t)scene->n_parts;
-    const bool track = frame->track_ppart && frame->mode != 0;
-    // per-partition counts: global 64-bit RED atomics by default (a 64-bit
-    // shared atomic add is a CAS loop on sm_100a and the CTA copy costs L1)
-    F.hist_smem = (track && scene->n_parts <= HIST_SMEM_MAX && (frame->flags & TR_FLAG_HIST_SMEM)) ? 1 : 0;
     const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
     // ray chunk = what the scratch interval lists can hold
     if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + IV_FIXED_BYTES)
@@ -1259,23 +1364,23 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     int64_t chunk = (out->scratch_bytes - IV_FIXED_BYTES) / IV_BYTES_PER_RAY / 32 * 32;
     if (chunk > total_rays) chunk = total_rays;
     if (chunk < 32) chunk = 32;
-    const size_t smem = F.hist_smem ? (size_t)scene->n_parts * sizeof(unsigned long long) : 0;
-    // rays per group of lanes: flags bits 8-11 = log2(G) (0: default 8)
+    // lanes per ray: flags bits 8-11 = log2(G) (0: default 4); bits 12-13:
+    // minimum resident CTAs per SM of the G = 4 kernel (register budget; 0: 2)
     const int lg = (frame->flags >> 8) & 0xf;
     const int gsize = lg ? (1 << lg) : 4;
+    const int minb = (frame->flags >> 12) & 0x3;
     void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
     switch (gsize) {
-        case 4: march_fn = march_group_kernel<4>; break;
-        case 8: march_fn = march_group_kernel<8>; break;
-        case 16: march_fn = march_group_kernel<16>; break;
-        case 32: march_fn = march_group_kernel<32>; break;
-        default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 4, 8, 16 or 32");
+        case 2: march_fn = march_kernel<2, 2>; break;
+        case 4: march_fn = minb == 3 ? march_kernel<4, 3> : (minb == 1 ? march_kernel<4, 4> : march_kernel<4, 2>); break;
+        case 8: march_fn = march_kernel<8, 2>; break;
+        case 16: march_fn = march_kernel<16, 2>; break;
+        case 32: march_fn = march_kernel<32, 2>; break;
+        default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8, 16 or 32");
     }
     cudaError_t e;
-    e = cudaFuncSetAttribute(march_fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute");
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fn, MARCH_BLOCK, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fn, MARCH_BLOCK, 0);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     int64_t launches = 0, march_grid = 0;
@@ -1287,8 +1392,9 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.hist = reinterpret_cast<uint32_t *>(base);
         iv.cursor = iv.hist + N_BUCKETS;
         iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
-        iv.pid = reinterpret_cast<int32_t *>(base + IV_FIXED_BYTES);
-        iv.cnt = reinterpret_cast<uint32_t *>(iv.pid + (int64_t)IV_CAP * F.n_rays);
+        iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
+        iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * F.n_rays);
+        iv.cnt = reinterpret_cast<uint32_t *>(iv.tail + F.n_rays);
         iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
@@ -1310,9 +1416,9 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             e = cudaEventRecord((cudaEvent_t)out->ev_march_begin, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(begin)");
         }
-        march_fn<<<(unsigned)grid, MARCH_BLOCK, smem, st>>>(S, E, F, iv, *out);
+        march_fn<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "march_group_kernel launch");
+        if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
         ++launches;
         march_grid = grid;
         if (out->ev_march_end && r0 + chunk >= total_rays) {

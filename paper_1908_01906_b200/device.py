@@ -9,9 +9,9 @@ Layout in HBM, all owned by torch tensors:
   bnodes     TrBNode[]          112 B BVH2 nodes over partition boxes (f64)
   knodes     TrKNode[]          16 B BSP nodes over partition boxes (trace pass)
   pgrid      int32[]            uniform-grid leaf candidates
-  scratch    per-ray interval lists of a ray chunk (IV_CAP x 20 B + 4 B per ray)
+  scratch    per-ray interval lists of a ray chunk (IV_CAP x 16 B + 16 B per ray)
   epoch      one buffer per (active, sigma, tf) snapshot and (s1, s2, p):
-             step f64[P] | tf f64[n,4] | active u8[P] | node activity u8[M]
+             step f64[P] | (step, step/s1) f64[P,2] | tf f64[n,4] | active u8[P] | node activity u8[M]
 
 The scene is uploaded once per (sampler, partition BVH) pair and cached;
 transfer-function edits only create a new epoch (never touch geometry),
@@ -167,7 +167,12 @@ class Epoch:
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
         def a64(x):  # 64-B aligned sections (the kernel reads the TF with 16-B loads)
             return (x + 63) // 64 * 64
-        o_tf = a64(8 * P)
+        # opacity_correction's exponent s / s1 (K:27), IEEE division as in Python
+        ratio = np.empty((P, 2))
+        ratio[:, 0] = step
+        ratio[:, 1] = step / float(params.s1)
+        o_ratio = a64(8 * P)
+        o_tf = a64(o_ratio + ratio.nbytes)
         o_act = a64(o_tf + table.nbytes)
         o_bact = a64(o_act + P)
         o_kact = a64(o_bact + dev.n_bnodes)
@@ -176,6 +181,7 @@ class Epoch:
         hv = host.numpy()
         hv[:] = 0
         hv[:8 * P] = step.view(np.uint8)
+        hv[o_ratio:o_ratio + ratio.nbytes] = ratio.view(np.uint8).reshape(-1)
         hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
         hv[o_act:o_act + P] = act
         hv[o_bact:o_bact + dev.n_bnodes] = bact
@@ -187,7 +193,8 @@ class Epoch:
         base = self.buf.data_ptr()
         self.desc = _lib.TrEpoch(active=base + o_act, bnode_active=base + o_bact, step=base,
                                  tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
-                                 tf_hi=self.tf_hi, knode_active=base + o_kact)
+                                 tf_hi=self.tf_hi, knode_active=base + o_kact,
+                                 step_ratio=base + o_ratio)
         self.step_host = step
 
 

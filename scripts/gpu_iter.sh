@@ -6,7 +6,7 @@ timeout 600 python scripts/gpu_debug.py > gpurun_out/debug_$TAG.log 2>&1
 for m in reference skip skip-adaptive; do
   timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --mode $m >> gpurun_out/modes_$TAG.jsonl 2>>gpurun_out/modes_$TAG.err
 done
-for fl in 0x200 0x400 0x8; do
+for fl in 0x40 0x1 0x41 0x100 0x300 0x500; do
   timeout 300 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu --flags $fl >> gpurun_out/groups_$TAG.jsonl 2>>gpurun_out/modes_$TAG.err
 done
 if [ "$2" == "full" ]; then
