@@ -327,6 +327,7 @@ def main():
                        "rays_per_s": cam.width * cam.height * args.steps / t_max,
                        "l2": "flushed between steps (256 MiB write)",
                        "parallelism": f"pixel tiles interleaved over {world} GPU(s)",
+                       "flags": hex(args.flags),
                        "scene_build_s": round(build_s, 3), "upload_s": round(upload_s, 3),
                        "resident_bytes": int(dscene.resident_bytes)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

@@ -224,6 +224,7 @@ typedef struct TrFrame {
 
 #define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
 #define TR_FLAG_SEQ_SCAN 64    /* leaf scan one record at a time, next one prefetched (tuning) */
+#define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
@@ -231,7 +232,8 @@ typedef struct TrFrame {
 #define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
- * per SM (0 or 2: 2, 3: 3, 1: 4).  Tuning knobs only:
+ * per SM (0: auto, 1: 4, 2: 2, 3: 3); bits 14-15: CTAs per SM actually
+ * launched (0: as many as fit).  Tuning knobs only:
  * every setting renders the same frame. */
 
 /* Outputs (device pointers).  Image layout: rgba (H,W,4) f64, samples (H,W)

@@ -12,7 +12,11 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "libtetray_b200.so"
+import os
+
+# TETRAY_B200_LIB: an alternative build of the same library (A/B tuning runs)
+LIB_PATH = Path(os.environ.get("TETRAY_B200_LIB") or
+                Path(__file__).resolve().parent / "libtetray_b200.so")
 
 c_i64p = C.POINTER(C.c_int64)
 c_f64p = C.POINTER(C.c_double)
@@ -82,7 +86,8 @@ TR_FLAG_NO_GRID = 2
 TR_FLAG_STATS = 4
 TR_FLAG_NO_BSP = 8
 STAT_NAMES = ["rounds", "partial_rounds", "lane_samples", "found", "grid_hits", "descents",
-              "inline_intervals", "pow_calls", "trace_intervals", "trace_rays"]
+              "inline_intervals", "pow_calls", "trace_intervals", "trace_rays", "bsp_overflow",
+              "bsp_cells", "trace_max_intervals"]
 CHILD_NONE = -2**31
 
 # (name, restype, argtypes) for every symbol include/tetray_b200.h declares

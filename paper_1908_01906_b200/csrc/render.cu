@@ -65,6 +65,9 @@ enum : int {
     ST_POW,              // pow() evaluations
     ST_TRACE_IV,         // intervals produced by the trace pass
     ST_TRACE_RAYS,       // rays traced
+    ST_BSP_OVERFLOW,     // rays redone with the BVH (BSP buffer or stack overflow)
+    ST_BSP_CELLS,        // BSP leaf cells enumerated
+    ST_TRACE_MAX_IV,     // most intervals of one ray (max)
     ST_COUNT
 };
 __device__ unsigned long long g_stats[16];
@@ -168,6 +171,7 @@ __device__ const __align__(16) unsigned long long d_pow_etab[] = TR_POW_EXP_TAB_
 // glibc main path where it applies, CUDA pow elsewhere (never reached for
 // opacity correction: x = 1 - alpha in [0, 1], y = step/s1 in [1, 2^63)).
 __device__ __forceinline__ double ref_pow(double x, double y) {
+    if (x == 1.0) return 1.0;  // glibc: pow(1, y) == 1 for every y
 #if TR_HAVE_GLIBC_POW
     if (tr_pow_glibc_supported(x, y)) {
         bool exact;
@@ -500,7 +504,7 @@ __device__ int32_t next_interval(const SceneK &S, const EpochK &E, const RayD &r
 // ------------------------------------------------------ BSP interval trace
 
 constexpr int KBUF = 16;
-constexpr int KSTACK = 64;
+constexpr int KSTACK = 32;
 
 // Exact front-to-back interval sequence of one ray from a resumable BSP
 // traversal.  A partition's box lies inside its BSP cell, so the entry of the
@@ -515,6 +519,7 @@ struct BspTrace {
     int32_t c_pid[KBUF];
     double c_pa[KBUF], c_pb[KBUF];
     int nb;
+    int cells;
     bool overflow;
 };
 
@@ -525,6 +530,7 @@ __device__ __forceinline__ double ray_i(const RayD &r, int a) { return a == 0 ? 
 __device__ __forceinline__ void bsp_begin(const SceneK &S, const RayD &ray, BspTrace &T) {
     T.sp = 0;
     T.nb = 0;
+    T.cells = 0;
     T.overflow = false;
     double r0, r1;
     slab(ray, S.kroot_lo, S.kroot_hi, r0, r1);
@@ -543,10 +549,11 @@ __device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD 
         bool leaf_done = false;
         while (true) {
             if (tf <= 0.0) break;                         // behind the origin: exits <= 0
-            if (E.knode_active && !__ldg(E.knode_active + node)) break;
             const TrKNode *N = S.knodes + node;
-            const int32_t info = __ldg(&N->info);
+            const int32_t info = __ldg(&N->info);   // issued with the activity byte
+            if (E.knode_active && !__ldg(E.knode_active + node)) break;
             if (info < 0) {                                // leaf cell: its partitions
+                ++T.cells;
                 const int32_t st = ~info, cnt = __ldg(&N->aux);
                 for (int32_t k = 0; k < cnt; ++k) {
                     const int32_t pid = __ldg(S.kleaf_pids + st + k);
@@ -760,8 +767,9 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             const double phase = F.f.jitter ? hash01(px.ix, px.iy) : 0.5;  // K:340
             IvRec *rec = iv.rec + rr * IV_CAP;
             uint32_t cum = 0;
-            bool more = false;
+            bool more = false, bsp_redo = false;
             double t_min = 0.0;
+            int bsp_cells = 0;
             if (F.f.mode == 0) {  // K:346-353: the mesh box is the one interval
                 double a, b;
                 slab(ray, S.mesh_lo, S.mesh_hi, a, b);
@@ -805,14 +813,19 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         last = pid;
                         if (use_bsp) bsp_compact(T, t_min);
                     }
+                    if (use_bsp) bsp_cells += T.cells;
                     if (!(use_bsp && T.overflow)) break;
                     use_bsp = false;  // candidate buffer overflowed: redo with the BVH
+                    bsp_redo = true;
                 }
             }
             if (more) iv.tail[rr] = t_min;
             if (F.f.flags & TR_FLAG_STATS) {
                 atomicAdd(&g_stats[ST_TRACE_RAYS], 1ull);
                 atomicAdd(&g_stats[ST_TRACE_IV], (unsigned long long)n);
+                atomicMax(&g_stats[ST_TRACE_MAX_IV], (unsigned long long)n);
+                if (bsp_redo) atomicAdd(&g_stats[ST_BSP_OVERFLOW], 1ull);
+                atomicAdd(&g_stats[ST_BSP_CELLS], (unsigned long long)bsp_cells);
             }
             if (cum > 0 || more) {
                 bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
@@ -910,6 +923,72 @@ __device__ bool inline_next(const SceneK &S, const EpochK &E, const TrFrame &fr,
     }
 }
 
+// One sample of march_range (K:277-290): position t = a + (k + phase) * step
+// (K:278), point location (K:93-136: the grid's candidate leaf proved by its
+// exclusive box, else the full descent -- both exact), field
+// (K:149-153), TF (K:74-90) and opacity correction (K:27).  Returns
+// (ca, r, g, b); found = inside a tet (ca = c = 0 otherwise).
+__device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E, const TrFrame &fr,
+                                                double ox, double oy, double oz, double dx,
+                                                double dy, double dz, double a, int64_t k,
+                                                double phase, int32_t pid, bool stats,
+                                                bool seq_scan, bool use_grid, bool &found) {
+    double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
+    found = false;
+    double step = fr.s1, e = 1.0;
+    if (fr.mode == 2) {
+        const double2 se = __ldg(reinterpret_cast<const double2 *>(E.step_ratio) + pid);
+        step = se.x;
+        e = se.y;
+    }
+    const double t = a + ((double)k + phase) * step;
+    const PQuery q = make_query(ox + t * dx, oy + t * dy, oz + t * dz);
+    if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
+    double l[4];
+    uint32_t pos = UINT32_MAX;
+    bool located = false;
+    if (use_grid) {
+        const int64_t gc = grid_cell(S, q);
+        if (gc >= 0) {
+            LeafHint hh;
+            load_leaf(S.pgrid_leaf + gc, hh);
+            if (strictly_in(q, hh.lo, hh.hi)) {
+                pos = seq_scan ? scan_leaf_first(S, hh.start, hh.count, q, l)
+                               : scan_leaf_pairs(S, hh.start, hh.count, q, l);
+                located = true;
+                if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
+            }
+        }
+    }
+    if (!located) {
+        int32_t leaf;
+        if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
+        pos = locate_full(S, q, l, leaf);
+    }
+    if (pos == UINT32_MAX) return sh;
+    double v;
+    const double2 *rp = reinterpret_cast<const double2 *>(S.tets + pos);
+    if (S.centering == 0) {   // K:149-151
+        const double2 f01 = __ldg(rp + 6), f23 = __ldg(rp + 7);
+        v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
+    } else {                  // K:153
+        v = __ldg(rp + 6).x;
+    }
+    double c[4];
+    tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+    const double x = 1.0 - c[3];
+    // K:27; glibc's pow(x, 1) and pow(1, y) are exactly x and 1
+    const bool need_pow = e != 1.0 && x != 1.0;
+    sh.x = 1.0 - (need_pow ? ref_pow(x, e) : x);
+    if (stats) {
+        atomicAdd(&g_stats[ST_FOUND], 1ull);
+        if (need_pow) atomicAdd(&g_stats[ST_POW], 1ull);
+    }
+    sh.y = c[0]; sh.z = c[1]; sh.w = c[2];
+    found = true;
+    return sh;
+}
+
 // Phase 2: G lanes march one ray together.  Per round lane j of the group
 // takes the ray's next-but-j sample: its interval is found from the stored
 // prefix counts, its position is t = a + (k + phase) * step (K:278), and it
@@ -917,7 +996,7 @@ __device__ bool inline_next(const SceneK &S, const EpochK &E, const TrFrame &fr,
 // the group then composites the round's samples in order with the exact
 // early-termination rule (K:285-295).  Groups without a ray take part in
 // the warp collectives with no sample.
-template <int G, int MINB>
+template <int G, int MINB, bool STATS>
 __global__ void __launch_bounds__(MARCH_BLOCK, MINB)
 march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
@@ -931,7 +1010,10 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     Inline &L = inl[threadIdx.x / G];
     const bool track = fr.track_ppart && fr.mode != 0;
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
-    const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
+    // TR_FLAG_STATS event counters.  Kept a runtime test even in the STATS =
+    // false instance: measured 25% faster than a compile-time false (the
+    // atomics' guards change how the hot loop is scheduled; build/ab A/B).
+    const bool stats = STATS || (fr.flags & TR_FLAG_STATS) != 0;
     const bool seq_scan = (fr.flags & TR_FLAG_SEQ_SCAN) != 0;
     const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << gbase);
     uint32_t n_queue = 0;
@@ -1043,62 +1125,9 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         // ---- shade my sample (K:277-290)
         double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
         bool found = false;
-        if (has) {
-            double step = fr.s1, e = 1.0;
-            if (fr.mode == 2) {
-                const double2 se = __ldg(reinterpret_cast<const double2 *>(E.step_ratio) + pid);
-                step = se.x;
-                e = se.y;
-            }
-            const double t = a + ((double)k + phase) * step;
-            const PQuery q = make_query(ox + t * dx, oy + t * dy, oz + t * dz);
-            if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
-            // point location (K:93-136): the grid's candidate leaf proved by
-            // its exclusive box, else the full descent -- both exact
-            double l[4];
-            uint32_t pos = UINT32_MAX;
-            bool located = false;
-            if (!located && use_grid) {
-                const int64_t gc = grid_cell(S, q);
-                if (gc >= 0) {
-                    LeafHint hh;
-                    load_leaf(S.pgrid_leaf + gc, hh);
-                    if (strictly_in(q, hh.lo, hh.hi)) {
-                        pos = seq_scan ? scan_leaf_first(S, hh.start, hh.count, q, l)
-                                       : scan_leaf_pairs(S, hh.start, hh.count, q, l);
-                        located = true;
-                        if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
-                    }
-                }
-            }
-            if (!located) {
-                int32_t leaf;
-                if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
-                pos = locate_full(S, q, l, leaf);
-            }
-            double v = 0.0;
-            if (pos != UINT32_MAX) {
-                const double2 *rp = reinterpret_cast<const double2 *>(S.tets + pos);
-                if (S.centering == 0) {   // K:149-151
-                    const double2 f01 = __ldg(rp + 6), f23 = __ldg(rp + 7);
-                    v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
-                } else {                  // K:153
-                    v = __ldg(rp + 6).x;
-                }
-            }
-            if (pos != UINT32_MAX) {
-                double c[4];
-                tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
-                const double x = 1.0 - c[3];
-                sh.x = 1.0 - ((e == 1.0) ? x : ref_pow(x, e));  // K:27; glibc pow(x, 1) == x
-                if (stats) {
-                    atomicAdd(&g_stats[ST_FOUND], 1ull);
-                    if (e != 1.0) atomicAdd(&g_stats[ST_POW], 1ull);
-                }
-                sh.y = c[0]; sh.z = c[1]; sh.w = c[2];
-                found = true;
-            }
-        }
+        if (has)
+            sh = shade_sample(S, E, fr, ox, oy, oz, dx, dy, dz, a, k, phase, pid, stats, seq_scan,
+                              use_grid, found);
         shade[threadIdx.x] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
@@ -1209,6 +1238,252 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
     }
     (void)gmask;
+}
+
+// Variant of march_kernel with the group-uniform ray state in shared memory
+// (SoA, one slot per group) instead of registers: the registers then hold a
+// sample's working set only, so more warps fit per SM.  Same
+// rounds, same exact compositing; lane 0 of a group writes the state.
+template <int G, int MINB>
+__global__ void __launch_bounds__(MARCH_BLOCK, MINB)
+march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
+    static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
+    constexpr int NG = MARCH_BLOCK / G;
+    __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
+    __shared__ double4 shade[MARCH_BLOCK];
+    __shared__ Inline inl[NG];
+    __shared__ double s_o[3][NG], s_d[3][NG], s_acc[4][NG], s_phase[NG];
+    __shared__ long long s_out[NG], s_samples[NG];
+    __shared__ uint32_t s_rr[NG], s_taken[NG], s_ctot[NG], s_cbefore[NG];
+    __shared__ int32_t s_icur[NG], s_niv[NG], s_pix[NG], s_piy[NG];
+    const TrFrame &fr = F.f;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int j = lane % G;
+    const int gbase = lane - j;
+    const int g = threadIdx.x / G;
+    Inline &L = inl[g];
+    const bool track = fr.track_ppart && fr.mode != 0;
+    const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
+    const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
+    const bool seq_scan = (fr.flags & TR_FLAG_SEQ_SCAN) != 0;
+    uint32_t n_queue = 0;
+    for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
+    unsigned long long my_samples = 0, my_visited = 0;
+    bool active = false, exhausted = false, inline_mode = false, more = false;
+
+    while (true) {
+        // ---- refill: one queue slot per group that needs a ray
+        const bool want = !active && !exhausted;
+        const unsigned lm = __ballot_sync(FULL, want && j == 0);
+        if (lm) {
+            const int leader = __ffs(lm) - 1;
+            unsigned base = 0;
+            if (lane == leader) base = atomicAdd(O.work, (unsigned)__popc(lm));
+            base = __shfl_sync(FULL, base, leader);
+            const unsigned qpos = base + __popc(lm & ((1u << gbase) - 1u));
+            if (want) {
+                if (qpos >= n_queue) {
+                    exhausted = true;
+                } else {
+                    const uint32_t rr = iv.order[qpos];
+                    const uint32_t c = iv.cnt[rr];
+                    const int32_t n_iv = (int32_t)(c & 0xffffu);
+                    more = (c & CNT_MORE) != 0;
+                    const IvRec *rec = iv.rec + (int64_t)rr * IV_CAP;
+                    const uint32_t c_tot = n_iv > 0 ? load_rec(rec + (n_iv - 1)).cum : 0u;
+                    inline_mode = c_tot == 0;   // only inline intervals (the trace ran out of room)
+                    if (j == 0) {
+                        const Pixel px = ray_pixel(F, rr);
+                        const RayD ray = make_ray(fr, px.ix, px.iy);
+                        s_rr[g] = rr; s_out[g] = px.out;
+                        s_pix[g] = (int32_t)px.ix; s_piy[g] = (int32_t)px.iy;
+                        s_o[0][g] = ray.ox; s_o[1][g] = ray.oy; s_o[2][g] = ray.oz;
+                        s_d[0][g] = ray.dx; s_d[1][g] = ray.dy; s_d[2][g] = ray.dz;
+                        s_phase[g] = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
+                        s_acc[0][g] = s_acc[1][g] = s_acc[2][g] = s_acc[3][g] = 0.0;
+                        s_samples[g] = 0;
+                        s_taken[g] = 0; s_icur[g] = 0; s_cbefore[g] = 0;
+                        s_niv[g] = n_iv; s_ctot[g] = c_tot;
+                        if (inline_mode) {
+                            L.t_min = iv.tail[rr];
+                            L.last = n_iv > 0 ? load_rec(rec + (n_iv - 1)).pid : -1;
+                            L.visited = 0; L.started = 0; L.n = 0; L.k = 0;
+                        }
+                    }
+                    active = true;
+                }
+            }
+        }
+        if (__all_sync(FULL, exhausted)) break;
+        __syncwarp();
+
+        // ---- inline mode: lane 0 fetches the next interval with samples when needed
+        bool idle = false;
+        if (active && inline_mode && j == 0 && L.k >= L.n)
+            idle = !inline_next(S, E, fr, s_pix[g], s_piy[g], s_phase[g], L);
+        __syncwarp();
+        idle = __shfl_sync(FULL, idle, gbase);
+
+        // ---- my sample
+        bool has = false;
+        double a = 0.0;
+        int32_t pid = -1, i_mine = 0;
+        uint32_t c0_mine = 0;
+        int64_t k = 0, remaining = 0;
+        if (active && !idle) {
+            if (!inline_mode) {
+                const uint32_t taken = s_taken[g], c_tot = s_ctot[g];
+                const uint32_t s = taken + (uint32_t)j;
+                remaining = (int64_t)(c_tot - taken);
+                if (s < c_tot) {
+                    const IvRec *rec = iv.rec + (int64_t)s_rr[g] * IV_CAP;
+                    int32_t i = s_icur[g];
+                    uint32_t c0 = s_cbefore[g];
+                    IvRec r = load_rec(rec + i);
+                    while (r.cum <= s) { c0 = r.cum; ++i; r = load_rec(rec + i); }
+                    a = r.a;
+                    pid = r.pid;
+                    k = (int64_t)(s - c0);
+                    i_mine = i;
+                    c0_mine = c0;
+                    has = true;
+                }
+            } else {
+                remaining = L.n - L.k;
+                if ((int64_t)j < remaining) {
+                    a = L.a;
+                    pid = L.pid;
+                    k = L.k + j;
+                    has = true;
+                }
+            }
+        }
+
+        // ---- shade my sample (K:277-290)
+        double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
+        bool found = false;
+        if (has)
+            sh = shade_sample(S, E, fr, s_o[0][g], s_o[1][g], s_o[2][g], s_d[0][g], s_d[1][g],
+                              s_d[2][g], a, k, s_phase[g], pid, stats, seq_scan, use_grid, found);
+        shade[threadIdx.x] = sh;
+        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
+        __syncwarp();
+
+        // ---- composite the round in sample order (K:285-295)
+        const int cnt = (int)((remaining < G) ? remaining : G);
+        int taken_r = cnt;
+        bool term = false;
+        Acc acc = {0.0, 0.0, 0.0, 0.0};
+        if (active && !idle) {
+            acc.r = s_acc[0][g]; acc.g = s_acc[1][g]; acc.b = s_acc[2][g]; acc.a = s_acc[3][g];
+            const double4 *grp = shade + (threadIdx.x - j);
+            for (int m = 0; m < cnt; ++m) {
+                const double4 gg = grp[m];
+                const double w = (1.0 - acc.a) * gg.x;
+                acc.r += w * gg.y;
+                acc.g += w * gg.z;
+                acc.b += w * gg.w;
+                acc.a += w;
+                if (((fbits >> m) & 1u) && acc.a >= fr.term) { taken_r = m + 1; term = true; break; }
+            }
+            if (stats && j == 0) {
+                atomicAdd(&g_stats[ST_ROUNDS], 1ull);
+                if (cnt < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);
+            }
+        }
+        __syncwarp();   // every lane has read s_acc
+        if (active && !idle && j == 0) {
+            s_acc[0][g] = acc.r; s_acc[1][g] = acc.g; s_acc[2][g] = acc.b; s_acc[3][g] = acc.a;
+        }
+
+        // ---- advance the group's cursor (all shuffles before any divergence)
+        const int src = gbase + ((taken_r > 0) ? taken_r - 1 : 0);
+        const int32_t i_last = __shfl_sync(FULL, i_mine, src);
+        const uint32_t c0_last = __shfl_sync(FULL, c0_mine, src);
+        bool done = false, flush = false;
+        int32_t flush_n = 0;
+        uint32_t taken_now = 0;
+        if (active) {
+            if (idle) {  // inline intervals exhausted
+                done = true;
+            } else if (!inline_mode) {
+                const uint32_t c_tot = s_ctot[g];
+                taken_now = s_taken[g] + (uint32_t)taken_r;
+                const int32_t n_iv = s_niv[g];
+                if (term) {                       // K:388-389: the last interval visited
+                    flush = true; flush_n = i_last + 1;
+                    done = true;
+                } else if (taken_now == c_tot) {  // stored list consumed
+                    flush = true; flush_n = n_iv;
+                    if (more) {
+                        inline_mode = true;
+                        if (j == 0) {
+                            const IvRec *rec = iv.rec + (int64_t)s_rr[g] * IV_CAP;
+                            L.t_min = iv.tail[s_rr[g]];
+                            L.last = n_iv > 0 ? rec[n_iv - 1].pid : -1;
+                            L.visited = 0; L.started = 1; L.n = 0; L.k = 0;
+                        }
+                    } else {
+                        done = true;
+                    }
+                }
+            } else {
+                if (j == 0) {
+                    L.k += taken_r;
+                    if (track && L.pid >= 0)
+                        atomicAdd((unsigned long long *)O.ppart + L.pid, (unsigned long long)taken_r);
+                }
+                if (term) done = true;
+            }
+        }
+        // per-partition samples of the stored intervals (K:386-387)
+        if (flush && track) {
+            const IvRec *rec = iv.rec + (int64_t)s_rr[g] * IV_CAP;
+            for (int32_t i = j; i < flush_n; i += G) {
+                const IvRec r = load_rec(rec + i);
+                const uint32_t lo = (i > 0) ? load_rec(rec + (i - 1)).cum : 0u;
+                const uint32_t hi = (r.cum < taken_now) ? r.cum : taken_now;
+                if (hi > lo) atomicAdd((unsigned long long *)O.ppart + r.pid, (unsigned long long)(hi - lo));
+            }
+        }
+        __syncwarp();
+        if (active && j == 0) {
+            const long long samples = s_samples[g] + taken_r;
+            s_samples[g] = samples;
+            if (!idle && taken_now) {
+                s_taken[g] = taken_now;
+                s_icur[g] = i_last;
+                s_cbefore[g] = c0_last;
+            }
+            if (done) {
+                int32_t visited = 0;
+                if (fr.mode != 0) {
+                    if (!inline_mode) visited = term ? i_last + 1 : s_niv[g];
+                    else visited = s_niv[g] + L.visited;
+                }
+                const Acc acc = {s_acc[0][g], s_acc[1][g], s_acc[2][g], s_acc[3][g]};
+                write_pixel(fr, O, s_out[g], acc, samples, visited);
+                my_samples += (unsigned long long)samples;
+                my_visited += (unsigned long long)visited;
+            }
+        }
+        if (done) active = false;
+        __syncwarp();
+    }
+    // block reduction of the frame totals (R:198-201)
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        my_samples += __shfl_xor_sync(FULL, my_samples, off);
+        my_visited += __shfl_xor_sync(FULL, my_visited, off);
+    }
+    if (lane == 0) { red[0][warp] = my_samples; red[1][warp] = my_visited; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long s = 0, v = 0;
+        for (int w = 0; w < MARCH_BLOCK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
+        if (s) atomicAdd((unsigned long long *)O.totals, s);
+        if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
+    }
 }
 
 __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restrict__ pts,
@@ -1368,21 +1643,37 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     // minimum resident CTAs per SM of the G = 4 kernel (register budget; 0: 2)
     const int lg = (frame->flags >> 8) & 0xf;
     const int gsize = lg ? (1 << lg) : 4;
-    const int minb = (frame->flags >> 12) & 0x3;
+    // bits 12-13: minimum resident CTAs per SM (register budget); 0 = auto:
+    // 4 CTAs (64 registers, 32 warps) when the tet records exceed 1 GiB (the
+    // samples then miss L2 and latency hiding wins), else 3 (80 registers)
+    int minb = (frame->flags >> 12) & 0x3;
+    if (minb == 0) minb = (scene->n_tets * (int64_t)sizeof(TrTetRecord) > ((int64_t)1 << 30)) ? 1 : 3;
     void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
-    switch (gsize) {
-        case 2: march_fn = march_kernel<2, 2>; break;
-        case 4: march_fn = minb == 3 ? march_kernel<4, 3> : (minb == 1 ? march_kernel<4, 4> : march_kernel<4, 2>); break;
-        case 8: march_fn = march_kernel<8, 2>; break;
-        case 16: march_fn = march_kernel<16, 2>; break;
-        case 32: march_fn = march_kernel<32, 2>; break;
-        default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8, 16 or 32");
+    if (frame->flags & TR_FLAG_REG_STATE) {   // ray state in registers (2 CTAs per SM)
+        switch (gsize) {
+            case 2: march_fn = march_kernel<2, 2, false>; break;
+            case 4: march_fn = march_kernel<4, 2, false>; break;
+            case 8: march_fn = march_kernel<8, 2, false>; break;
+            case 16: march_fn = march_kernel<16, 2, false>; break;
+            case 32: march_fn = march_kernel<32, 2, false>; break;
+            default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8, 16 or 32");
+        }
+    } else {
+        switch (gsize) {
+            case 2: march_fn = march_sm_kernel<2, 3>; break;
+            case 4: march_fn = minb == 2 ? march_sm_kernel<4, 2>
+                             : (minb == 1 ? march_sm_kernel<4, 4> : march_sm_kernel<4, 3>); break;
+            case 8: march_fn = march_sm_kernel<8, 3>; break;
+            case 16: march_fn = march_sm_kernel<16, 3>; break;
+            default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8 or 16");
+        }
     }
     cudaError_t e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fn, MARCH_BLOCK, 0);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
+    if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
     int64_t launches = 0, march_grid = 0;
     for (int64_t r0 = 0; r0 < total_rays; r0 += chunk) {
         F.ray_begin = r0;

@@ -18,7 +18,7 @@ for cid, recipe, modes, jitter in C.FRAME_CASES + C.BIG_CASES:
         cam, par = C.camera(B, recipe), C.params(B, recipe)
         for mode in modes:
             ref = orc.render(cam, mode, par, jitter=jitter)
-            for flags in (0, 3, 8, 0x40, 0x41, 0x100):
+            for flags in (0, 3, 8, 0x40, 0x80, 0x1000, 0x300):
                 fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
                 ds = int((fb.samples != ref[1]).sum())
                 dr = int((fb.rgba != ref[0]).any(axis=2).sum())

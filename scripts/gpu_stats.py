@@ -13,7 +13,7 @@ sc = C.build_scene(B, scene)
 cam, par = C.camera(B, scene), C.params(B, scene)
 out = np.zeros(16, np.int64)
 for mode in ("reference", "skip", "skip-adaptive"):
-    for flags in (0x0, 0x200):
+    for flags in (0x0,):
         _lib.lib().tr_kernel_stats(_lib.ptr(out, __import__("ctypes").c_int64), 16, 1)
         fb, st = B.render(sc, cam, mode, par, flags=flags | _lib.TR_FLAG_STATS)
         _lib.check(_lib.lib().tr_kernel_stats(_lib.ptr(out, __import__("ctypes").c_int64), 16, 1), "stats")

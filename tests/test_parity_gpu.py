@@ -82,9 +82,10 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     for mode in modes:
         ref = orc.render(cam, mode, par, jitter=jitter)
-        # default, no grid index, and lane groups of 4 / 16 / 32 per ray
-        # default, no grid, no BSP, no leaf hint, and other lane-group shapes
-        for flags in (0, 2, 8, 16, 0x200, 0x400, 0x500, 0x3000):
+        # default; no grid, no BSP, sequential leaf scan; register-state
+        # kernel (0x80); lane groups of 2 / 8 / 16 (32 with 0x80); register
+        # budgets of 4 / 2 / 3 CTAs per SM -- every variant renders the same frame
+        for flags in (0, 2, 8, 0x40, 0x80, 0x100, 0x300, 0x400, 0x580, 0x1000, 0x2000, 0x3000):
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 
@@ -94,8 +95,13 @@ def test_radial59_benchmark_scene(B, golden, mode):
     """BASELINE config 2 (1.03M tets, 4,040 active partitions) at 512^2."""
     sc, orc = scene_of(B, "radial59")
     cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
-    fb, st = B.render(sc, cam, mode, par)
     g = golden["frames"][f"radial59/{mode}"]
+    for flags in (0, 0x80, 0x1000, 0x3000):
+        fb, st = B.render(sc, cam, mode, par, flags=flags)
+        _check_radial59(fb, st, g, orc, cam, mode, par)
+
+
+def _check_radial59(fb, st, g, orc, cam, mode, par):
     if mode != "skip-adaptive" or _glibc_pow():
         assert sha(fb.rgba) == g["rgba"]
         assert sha(fb.samples) == g["samples"]
