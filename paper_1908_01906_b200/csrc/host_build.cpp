@@ -380,7 +380,9 @@ void p_build_grid(PBuf &O) {
     const double side = std::cbrt(vol / (double)std::max<int64_t>(nl, 1));
     int64_t cells = 1;
     for (int a = 0; a < 3; ++a) {
-        double d = std::ceil(ext[a] / side);
+        // rounded, not ceiled: leaves of a regular mesh (one cube each) then
+        // get one cell each instead of cells straddling two leaves
+        double d = std::round(ext[a] / side);
         O.gdim[a] = (int32_t)std::min(std::max(d, 1.0), 2048.0);
         cells *= O.gdim[a];
         O.gorg[a] = lo[a];
