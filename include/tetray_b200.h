@@ -156,6 +156,10 @@ int tr_tf_meta(int64_t n_parts, const double *vrange, const double *tf_table, in
  * steps are bit-identical to the reference's. */
 int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out);
 double tr_step_size(double s1, double s2, double p, double sigma);
+/* Both epoch step arrays at once: step[n] and step_ratio[n][2] = {step,
+ * step / s1} (opacity_correction's exponent, K:27); either may be NULL. */
+int tr_epoch_steps(int64_t n, const double *sigma, double s1, double s2, double p, double *step,
+                   double *step_ratio);
 double tr_opacity_correction(double alpha, double s, double s1);
 
 /* glibc pow restated (csrc/glibc_pow.cuh): 1 if the tables were found in the

@@ -115,6 +115,8 @@ _SIGNATURES = [
     ("tr_tet_boxes", C.c_int, [C.c_int64, c_f64p, c_i64p, C.c_double, c_f64p, c_f64p]),
     ("tr_tf_meta", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int64, C.c_double, C.c_double,
                              c_f64p, c_f64p, c_f64p, c_u8p]),
+    ("tr_epoch_steps", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, C.c_void_p,
+                                 C.c_void_p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),
     ("tr_step_size", C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double]),
     ("tr_opacity_correction", C.c_double, [C.c_double, C.c_double, C.c_double]),

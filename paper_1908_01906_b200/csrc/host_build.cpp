@@ -993,9 +993,20 @@ double tr_opacity_correction(double alpha, double s, double s1) {
 }
 
 int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out) {
-    if (n < 0 || (n > 0 && (!sigma || !out))) return tr_fail(TR_EINVAL, "tr_step_sizes: invalid arguments");
-#pragma omp parallel for schedule(static) if (n > 2048)
-    for (int64_t i = 0; i < n; ++i) out[i] = tr_step_size(s1, s2, p, sigma[i]);
+    return tr_epoch_steps(n, sigma, s1, s2, p, out, nullptr);
+}
+
+int tr_epoch_steps(int64_t n, const double *sigma, double s1, double s2, double p, double *step,
+                   double *step_ratio) {
+    if (n < 0 || (n > 0 && (!sigma || (!step && !step_ratio))))
+        return tr_fail(TR_EINVAL, "tr_epoch_steps: invalid arguments");
+    // ~20 ns per pow: threads only pay off for very large partition counts
+#pragma omp parallel for schedule(static) if (n > 262144)
+    for (int64_t i = 0; i < n; ++i) {
+        const double s = tr_step_size(s1, s2, p, sigma[i]);
+        if (step) step[i] = s;
+        if (step_ratio) { step_ratio[2 * i] = s; step_ratio[2 * i + 1] = s / s1; }  // K:27 exponent
+    }
     return TR_OK;
 }
 

@@ -157,31 +157,27 @@ class Epoch:
         sig = np.ascontiguousarray(sigma, dtype=np.float64).reshape(-1)
         if len(act) != P or len(sig) != P:
             raise ValueError(f"metadata epoch has {len(act)} partitions, scene has {P}")
-        step = np.empty(P)
-        _lib.check(_lib.lib().tr_step_sizes(P, _lib.ptr(sig, C.c_double), float(params.s1),
-                                            float(params.s2), float(params.p),
-                                            _lib.ptr(step, C.c_double)), "tr_step_sizes")
         kact, bact = dev.activity(act)
         table = np.ascontiguousarray(tf.table, dtype=np.float64)
         self.n_tf = int(table.shape[0])
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
         def a64(x):  # 64-B aligned sections (the kernel reads the TF with 16-B loads)
             return (x + 63) // 64 * 64
-        # opacity_correction's exponent s / s1 (K:27), IEEE division as in Python
-        ratio = np.empty((P, 2))
-        ratio[:, 0] = step
-        ratio[:, 1] = step / float(params.s1)
+        # step f64[P] | (step, step / s1) f64[P,2] | tf | active | node activity
         o_ratio = a64(8 * P)
-        o_tf = a64(o_ratio + ratio.nbytes)
+        o_tf = a64(o_ratio + 16 * P)
         o_act = a64(o_tf + table.nbytes)
         o_bact = a64(o_act + P)
         o_kact = a64(o_bact + dev.n_bnodes)
         nbytes = a64(o_kact + dev.n_knodes)
         host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
-        hv[:] = 0
-        hv[:8 * P] = step.view(np.uint8)
-        hv[o_ratio:o_ratio + ratio.nbytes] = ratio.view(np.uint8).reshape(-1)
+        hp = host.data_ptr()
+        # per-partition step (K:20-22, glibc pow) and exponent s / s1 (K:27)
+        # written by the library straight into the pinned upload buffer
+        _lib.check(_lib.lib().tr_epoch_steps(P, _lib.ptr(sig, C.c_double), float(params.s1),
+                                             float(params.s2), float(params.p), hp, hp + o_ratio),
+                   "tr_epoch_steps")
         hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
         hv[o_act:o_act + P] = act
         hv[o_bact:o_bact + dev.n_bnodes] = bact
@@ -195,7 +191,7 @@ class Epoch:
                                  tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
                                  tf_hi=self.tf_hi, knode_active=base + o_kact,
                                  step_ratio=base + o_ratio)
-        self.step_host = step
+        self.step_host = hv[:8 * P].view(np.float64)
 
 
 class FrameBuffers:
