@@ -94,6 +94,12 @@ int tr_kd_build(int64_t n_vertices, const double *vertices, int64_t n_tets, cons
                 const double *field, int32_t centering, const double *mesh_lo,
                 const double *mesh_hi, int64_t max_leaf_elements, int64_t max_depth,
                 TrHostBuf **out);
+/* The same KD partitions in closed form for the synthetic N^3-cube mesh
+ * (mesh.py:147-231: five tets per cube, vertex field 0 = ramp, 1 = radial),
+ * without the mesh arrays (1e9-tet scenes).  with_ids (N <= 256) also lists
+ * the element ids; otherwise tr_kd_sizes reports 0 ids. */
+int tr_kd_build_grid(int64_t n, int32_t field, int64_t max_leaf_elements, int64_t max_depth,
+                     int32_t with_ids, TrHostBuf **out);
 /* sizes: [0] = n_parts, [1] = total element ids */
 int tr_kd_sizes(const TrHostBuf *kd, int64_t *sizes2);
 /* offsets[n_parts+1], ids[total], leaf_lo/hi[n_parts*3] (KD leaf boxes),
@@ -178,7 +184,7 @@ typedef struct TrDeviceScene {
     const TrTetRecord *tets;
     const TrPNode *pnodes;
     const TrPLeaf *pleaves;
-    const uint32_t *pleaf_ids;
+    const uint32_t *pleaf_ids;  /* tet id of each record; NULL: record k is tet k */
     int64_t n_tets, n_pnodes, n_pleaves;
     int32_t centering;
     int32_t pad0;
@@ -263,6 +269,17 @@ int64_t tr_scratch_bytes(int64_t n_rays);
 /* Replaces _kernels.render_frame (K:312-398). stream: cudaStream_t. */
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                     const TrOutputs *out, void *stream);
+
+/* Device build of the synthetic N^3-cube scene (mesh.py:147-231 generator,
+ * vertex field 0 = ramp, 1 = radial; csrc/synth.cu) straight into HBM: n_tets
+ * = 5 N^3 records in id order (pleaf_ids = NULL), one leaf per cube (the point
+ * grid is the cube grid: gorg 0, gscale 1, gdim N, pgrid_leaf = leaves) and
+ * N^3 - 1 BVH nodes.  inv10: host (10,3,3) inverse edge matrices of the 5 tets
+ * of an even then an odd cube (numpy's LAPACK, mesh.py:254).  pad = the box
+ * pad 1e-7 * diagonal (mesh.py:249).  For BASELINE config 4 (1e9 tets). */
+int tr_grid_scene_sizes(int64_t n, int64_t *n_tets, int64_t *n_leaves, int64_t *n_nodes);
+int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv10,
+                        TrTetRecord *recs, TrPLeaf *leaves, TrPNode *nodes, void *stream);
 
 /* Replaces _kernels.field_at_many (K:157-170): pts (n,3) f64 device;
  * found (n,) u8, vals (n,) f64, tet (n,) i64 (may be NULL) device. */

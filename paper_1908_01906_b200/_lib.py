@@ -94,6 +94,8 @@ CHILD_NONE = -2**31
 _SIGNATURES = [
     ("tr_kd_build", C.c_int, [C.c_int64, c_f64p, C.c_int64, c_i64p, c_f64p, C.c_int32, c_f64p,
                               c_f64p, C.c_int64, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("tr_kd_build_grid", C.c_int, [C.c_int64, C.c_int32, C.c_int64, C.c_int64, C.c_int32,
+                                   C.POINTER(C.c_void_p)]),
     ("tr_kd_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_kd_copy", C.c_int, [C.c_void_p, c_i64p, c_i64p, c_f64p, c_f64p, c_f64p, c_f64p, c_f64p]),
     ("tr_pbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int32, C.POINTER(C.c_void_p)]),
@@ -125,6 +127,9 @@ _SIGNATURES = [
     ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_render_frame", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch),
                                   C.POINTER(TrFrame), C.POINTER(TrOutputs), C.c_void_p]),
+    ("tr_grid_scene_sizes", C.c_int, [C.c_int64, c_i64p, c_i64p, c_i64p]),
+    ("tr_grid_scene_build", C.c_int, [C.c_int64, C.c_int32, C.c_double, c_f64p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_field_at_many", C.c_int, [C.POINTER(TrDeviceScene), C.c_int64, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_scatter_tiles", C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,

@@ -137,6 +137,107 @@ void kd_split(KdCtx &C, std::vector<int64_t> ids, const double *nlo, const doubl
     kd_split(C, std::move(right), rlo, nhi, depth + 1);
 }
 
+// ------------------------------------------- KD partitions of a cube grid
+// The same KD build (kd_split above, partitions.py:73-128) evaluated in closed
+// form on the synthetic generator's mesh (mesh.py:147-231): N^3 unit cubes,
+// five tets per cube, every tet spanning its whole cube on each axis, and
+// per axis the five centroids of a cube at offsets {.25, .25, .5, .75, .75}
+// (for both cube parities).  A node's elements are therefore always all tets
+// of an integer cube range, np.median is a closed form over those offsets,
+// the straddle tests split the range at the median (integer median: disjoint
+// halves; otherwise the median's cube slab goes to both sides), and the
+// value range is the field at the range's extreme vertices (the f32-rounded
+// field is monotone in the vertex distance).  tests/test_grid_scene.py checks
+// it against kd_split on generated meshes.
+struct GridKdCtx {
+    int64_t n;
+    int32_t field;  // 0 ramp (x), 1 radial (|p - n/2|)
+    int64_t max_leaf, max_depth;
+    bool with_ids;
+    KdBuf *out;
+};
+
+double grid_field(const GridKdCtx &C, const double p[3]) {
+    if (C.field == 0) return (double)(float)p[0];
+    const double h = (double)C.n / 2.0;  // mesh.py _radial: p - n / 2.0
+    const double d0 = p[0] - h, d1 = p[1] - h, d2 = p[2] - h;
+    return (double)(float)std::sqrt((d0 * d0 + d1 * d1) + d2 * d2);
+}
+
+void gkd_emit(GridKdCtx &C, const int64_t r0[3], const int64_t r1[3], const double *nlo,
+              const double *nhi) {
+    KdBuf &O = *C.out;
+    const int64_t n = C.n;
+    if (C.with_ids) {
+        std::vector<int64_t> ids;
+        for (int64_t x = r0[0]; x <= r1[0]; ++x)
+            for (int64_t y = r0[1]; y <= r1[1]; ++y)
+                for (int64_t z = r0[2]; z <= r1[2]; ++z) {
+                    const int64_t c = (x * n + y) * n + z;
+                    for (int k = 0; k < 5; ++k) ids.push_back(5 * c + k);
+                }
+        O.ids.insert(O.ids.end(), ids.begin(), ids.end());
+    }
+    const int64_t cnt = 5 * (r1[0] - r0[0] + 1) * (r1[1] - r0[1] + 1) * (r1[2] - r0[2] + 1);
+    O.offsets.push_back(O.offsets.back() + cnt);
+    // extreme vertices of [r0, r1 + 1]: nearest to / farthest from the field's minimum
+    double pmin[3], pmax[3];
+    for (int a = 0; a < 3; ++a) {
+        const double lo = (double)r0[a], hi = (double)(r1[a] + 1);
+        if (C.field == 0) { pmin[a] = lo; pmax[a] = (a == 0) ? hi : lo; continue; }
+        const double h = (double)C.n / 2.0;
+        const double cl = std::min(std::max(h, lo), hi);     // nearest real coordinate
+        const double f = std::floor(cl), c = std::ceil(cl);  // nearest vertex coordinate
+        pmin[a] = (cl - f <= c - cl) ? f : c;
+        pmax[a] = (h - lo >= hi - h) ? lo : hi;
+    }
+    O.vrange.push_back(grid_field(C, pmin));
+    O.vrange.push_back(grid_field(C, pmax));
+    for (int a = 0; a < 3; ++a) {
+        O.leaf_lo.push_back(nlo[a]);
+        O.leaf_hi.push_back(nhi[a]);
+        O.lo.push_back(std::max((double)r0[a], nlo[a]));
+        O.hi.push_back(std::min((double)(r1[a] + 1), nhi[a]));
+    }
+}
+
+void gkd_split(GridKdCtx &C, const int64_t r0[3], const int64_t r1[3], const double *nlo,
+               const double *nhi, int64_t depth) {
+    int64_t cnt[3];
+    for (int a = 0; a < 3; ++a) cnt[a] = r1[a] - r0[a] + 1;
+    const int64_t n = 5 * cnt[0] * cnt[1] * cnt[2];
+    if (n <= C.max_leaf || depth >= C.max_depth) { gkd_emit(C, r0, r1, nlo, nhi); return; }
+    int axis = 0;
+    double ext = nhi[0] - nlo[0];
+    for (int a = 1; a < 3; ++a)
+        if (nhi[a] - nlo[a] > ext) { ext = nhi[a] - nlo[a]; axis = a; }
+    // sorted centroid coordinates on `axis`: slab s holds 2S values at
+    // u+.25, S at u+.5, 2S at u+.75 (S = 5-tet cubes per slab / 1)
+    const int64_t S = n / (5 * cnt[axis]);
+    auto val = [&](int64_t pos) {
+        const int64_t s = pos / (5 * S), r = pos % (5 * S);
+        const double off = (r < 2 * S) ? 0.25 : ((r < 3 * S) ? 0.5 : 0.75);
+        return (double)(r0[axis] + s) + off;
+    };
+    const int64_t k = n / 2;
+    const double m = (n % 2) ? val(k) : (val(k - 1) + val(k)) / 2.0;  // np.median
+    // left: blo = u < m; right: bhi = u + 1 > m (no element is flat on m)
+    const double fm = std::floor(m);
+    const int64_t lmax = (fm == m) ? (int64_t)m - 1 : (int64_t)fm;
+    const int64_t rmin = (int64_t)fm;
+    const bool left_empty = lmax < r0[axis], right_empty = rmin > r1[axis];
+    const bool both_full = lmax >= r1[axis] && rmin <= r0[axis];
+    if (left_empty || right_empty || both_full) { gkd_emit(C, r0, r1, nlo, nhi); return; }
+    int64_t l1[3] = {r1[0], r1[1], r1[2]}, q0[3] = {r0[0], r0[1], r0[2]};
+    l1[axis] = std::min(r1[axis], lmax);
+    q0[axis] = std::max(r0[axis], rmin);
+    double lhi[3] = {nhi[0], nhi[1], nhi[2]}, rlo[3] = {nlo[0], nlo[1], nlo[2]};
+    lhi[axis] = m;
+    rlo[axis] = m;
+    gkd_split(C, r0, l1, nlo, lhi, depth + 1);
+    gkd_split(C, q0, r1, rlo, nhi, depth + 1);
+}
+
 // ====================================================== point-location BVH
 struct PBuf : TrHostBuf {
     std::vector<TrPNode> nodes;
@@ -625,6 +726,24 @@ int tr_kd_build(int64_t n_vertices, const double *vertices, int64_t n_tets, cons
         return TR_OK;
     } catch (const std::bad_alloc &) {
         return tr_fail(TR_ENOMEM, "tr_kd_build: out of host memory");
+    }
+}
+
+int tr_kd_build_grid(int64_t n, int32_t field, int64_t max_leaf_elements, int64_t max_depth,
+                     int32_t with_ids, TrHostBuf **out) {
+    if (!out || n < 1 || n > (1 << 20) || (field != 0 && field != 1) || max_leaf_elements < 1 ||
+        max_depth < 1 || (with_ids && n > 256))
+        return tr_fail(TR_EINVAL, "tr_kd_build_grid: invalid arguments");
+    try {
+        KdBuf *K = new KdBuf();
+        GridKdCtx C{n, field, max_leaf_elements, max_depth, with_ids != 0, K};
+        const int64_t r0[3] = {0, 0, 0}, r1[3] = {n - 1, n - 1, n - 1};
+        const double lo[3] = {0.0, 0.0, 0.0}, hi[3] = {(double)n, (double)n, (double)n};
+        gkd_split(C, r0, r1, lo, hi, 0);
+        *out = K;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_kd_build_grid: out of host memory");
     }
 }
 

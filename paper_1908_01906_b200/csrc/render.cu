@@ -243,7 +243,7 @@ __device__ __forceinline__ void scan_leaf_ids(const SceneK &S, uint32_t start, u
                                               const PQuery &q, uint32_t &best, uint32_t &best_pos,
                                               double l[4]) {
     for (uint32_t k = start; k < start + count; ++k) {
-        const uint32_t t = __ldg(S.pleaf_ids + k);
+        const uint32_t t = S.pleaf_ids ? __ldg(S.pleaf_ids + k) : k;   // NULL: records in id order
         if (t >= best) break;
         double lt[4];
         if (bary_test(S.tets, k, q, lt)) {
@@ -1497,7 +1497,7 @@ __global__ void field_at_many_kernel(SceneK S, int64_t n, const double *__restri
         const uint32_t pos = field_at(S, q, h, false, true, v);
         found[i] = pos != UINT32_MAX ? 1 : 0;
         vals[i] = v;
-        if (tet) tet[i] = pos != UINT32_MAX ? (int64_t)__ldg(S.pleaf_ids + pos) : -1;
+        if (tet) tet[i] = pos == UINT32_MAX ? -1 : (S.pleaf_ids ? (int64_t)__ldg(S.pleaf_ids + pos) : (int64_t)pos);
     }
 }
 
@@ -1604,7 +1604,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (frame->width < 1 || frame->height < 1 || frame->mode < 0 || frame->mode > 2 ||
         frame->shard_count < 1 || frame->shard_rank < 0 || frame->shard_rank >= frame->shard_count)
         return tr_fail(TR_EINVAL, "tr_render_frame: invalid frame");
-    if (!scene->tets || !scene->pnodes || !scene->pleaves || !scene->pleaf_ids || !out->rgba ||
+    if (!scene->tets || !scene->pnodes || !scene->pleaves || !out->rgba ||
         !out->samples || !out->visited || !out->totals || !out->work || !epoch->tf_table ||
         epoch->n_tf < 2)
         return tr_fail(TR_EINVAL, "tr_render_frame: missing buffer");

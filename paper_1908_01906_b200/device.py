@@ -228,15 +228,9 @@ class DeviceScene:
         torch = _torch()
         self.device = device
         self.lock = threading.Lock()
-        mesh, sampler = scene.mesh, scene.sampler
+        mesh = scene.mesh
         with torch.cuda.device(device):
             t0 = time.perf_counter()
-            lo, hi = _padded_boxes(scene)
-            pnodes, pleaves, pids, grid = build_point_bvh(lo, hi)
-            del lo, hi
-            # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
-            # reads consecutive 128-B lines with no id indirection
-            rec = pack_tet_records(mesh, sampler, order=pids)
             part_lo = np.ascontiguousarray(scene.bvh.box_lo, dtype=np.float64)
             part_hi = np.ascontiguousarray(scene.bvh.box_hi, dtype=np.float64)
             bnodes = getattr(scene.bvh, "nodes", None)
@@ -244,47 +238,40 @@ class DeviceScene:
                 from .traversal import build_bvh_over_boxes
                 bnodes = build_bvh_over_boxes(part_lo, part_hi)
             knodes, kpids, kroot = build_partition_bsp(part_lo, part_hi)
-            self.build_s = time.perf_counter() - t0
             self.knodes_host, self.kpids_host = knodes, kpids
             self.n_knodes = int(len(knodes))
             self.bnodes_host = np.ascontiguousarray(bnodes)
             self.n_parts = int(part_lo.shape[0])
             self.n_bnodes = int(len(bnodes))
             self.n_tets = int(mesh.n_tets)
-            self.pnodes_host, self.pleaves_host = pnodes, pleaves
-            self.t_tets = _upload(rec, device)
-            del rec
-            self.t_pnodes = _upload(pnodes, device)
-            self.t_pleaves = _upload(pleaves, device)
-            self.t_pids = _upload(pids, device)
+            if getattr(mesh, "device_generated", False):
+                point = self._point_structures_grid(scene)
+            else:
+                point = self._point_structures_host(scene)
+            self.build_s = time.perf_counter() - t0
             self.t_bnodes = _upload(bnodes, device)
             self.t_plo = _upload(part_lo, device)
             self.t_phi = _upload(part_hi, device)
-            self.t_grid = _upload(grid.cells, device)
-            cell_leaf = np.zeros(len(grid.cells), dtype=_lib.PLEAF_DTYPE)
-            cell_leaf["ex_lo"] = 1.0   # empty box: no candidate
-            cell_leaf["ex_hi"] = 0.0
-            has = grid.cells >= 0
-            cell_leaf[has] = pleaves[grid.cells[has]]
-            self.t_grid_leaf = _upload(cell_leaf, device)
             self.t_knodes = _upload(knodes, device)
             self.t_kpids = _upload(kpids, device)
-            self.grid = grid
             torch.cuda.synchronize(device)
+        grid = self.grid
         self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
                                                       self.t_pids, self.t_bnodes, self.t_plo,
                                                       self.t_phi, self.t_grid, self.t_grid_leaf,
-                                                      self.t_knodes,
-                                                      self.t_kpids))
+                                                      self.t_knodes, self.t_kpids)
+                                  if t is not None)
+        ptr = lambda t: 0 if t is None else t.data_ptr()
         self.desc = _lib.TrDeviceScene(
-            tets=self.t_tets.data_ptr(), pnodes=self.t_pnodes.data_ptr(),
-            pleaves=self.t_pleaves.data_ptr(), pleaf_ids=self.t_pids.data_ptr(),
-            n_tets=self.n_tets, n_pnodes=len(pnodes), n_pleaves=len(pleaves),
+            tets=ptr(self.t_tets), pnodes=ptr(self.t_pnodes),
+            pleaves=ptr(self.t_pleaves), pleaf_ids=ptr(self.t_pids),
+            n_tets=self.n_tets, n_pnodes=point[0], n_pleaves=point[1],
             centering=int(mesh.centering), bnodes=self.t_bnodes.data_ptr(),
             part_lo=self.t_plo.data_ptr(), part_hi=self.t_phi.data_ptr(), n_parts=self.n_parts,
             n_bnodes=self.n_bnodes,
             mesh_lo=(C.c_double * 3)(*mesh.bounds.lo), mesh_hi=(C.c_double * 3)(*mesh.bounds.hi),
-            pgrid=self.t_grid.data_ptr(), pgrid_leaf=self.t_grid_leaf.data_ptr(),
+            pgrid=ptr(self.t_grid),
+            pgrid_leaf=ptr(self.t_grid_leaf) if self.t_grid_leaf is not None else ptr(self.t_pleaves),
             gdim=(C.c_int32 * 3)(*grid.dims),
             gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale),
             knodes=self.t_knodes.data_ptr(), kleaf_pids=self.t_kpids.data_ptr(),
@@ -293,6 +280,63 @@ class DeviceScene:
         self._frames: dict = {}
         self._act_key, self._act_val = None, None
         self._desc_key, self._desc_val = None, None
+
+    def _point_structures_host(self, scene):
+        """Host builders (csrc/host_build.cpp) + upload: records in point-BVH
+        leaf order, BVH nodes, leaves, leaf ids and the grid with one copy of
+        its candidate leaf header per cell."""
+        device = self.device
+        mesh, sampler = scene.mesh, scene.sampler
+        lo, hi = _padded_boxes(scene)
+        pnodes, pleaves, pids, grid = build_point_bvh(lo, hi)
+        del lo, hi
+        # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
+        # reads consecutive 128-B lines with no id indirection
+        rec = pack_tet_records(mesh, sampler, order=pids)
+        self.pnodes_host, self.pleaves_host = pnodes, pleaves
+        self.t_tets = _upload(rec, device)
+        del rec
+        self.t_pnodes = _upload(pnodes, device)
+        self.t_pleaves = _upload(pleaves, device)
+        self.t_pids = _upload(pids, device)
+        self.t_grid = _upload(grid.cells, device)
+        cell_leaf = np.zeros(len(grid.cells), dtype=_lib.PLEAF_DTYPE)
+        cell_leaf["ex_lo"] = 1.0   # empty box: no candidate
+        cell_leaf["ex_hi"] = 0.0
+        has = grid.cells >= 0
+        cell_leaf[has] = pleaves[grid.cells[has]]
+        self.t_grid_leaf = _upload(cell_leaf, device)
+        self.grid = grid
+        return len(pnodes), len(pleaves)
+
+    def _point_structures_grid(self, scene):
+        """Synthetic cube-grid scene generated in HBM (tr_grid_scene_build,
+        csrc/synth.cu): records in id order, one leaf per cube, the cube grid
+        as the point grid (its leaf array doubles as the cell headers)."""
+        torch = _torch()
+        mesh, sampler = scene.mesh, scene.sampler
+        n = int(mesh.n)
+        sz = np.zeros(3, np.int64)
+        L = _lib.lib()
+        _lib.check(L.tr_grid_scene_sizes(n, _lib.ptr(sz[0:1], C.c_int64), _lib.ptr(sz[1:2], C.c_int64),
+                                         _lib.ptr(sz[2:3], C.c_int64)), "tr_grid_scene_sizes")
+        n_tets, n_leaves, n_nodes = (int(v) for v in sz)
+        self.t_tets = torch.empty(n_tets * 128, dtype=torch.uint8, device=self.device)
+        self.t_pleaves = torch.empty(n_leaves * 32, dtype=torch.uint8, device=self.device)
+        self.t_pnodes = torch.empty(n_nodes * 64, dtype=torch.uint8, device=self.device)
+        inv10 = np.ascontiguousarray(sampler.inv10, dtype=np.float64).reshape(90)
+        stream = torch.cuda.current_stream(self.device)
+        _lib.check(L.tr_grid_scene_build(n, int(mesh.field_id), float(sampler.pad),
+                                         _lib.ptr(inv10, C.c_double), self.t_tets.data_ptr(),
+                                         self.t_pleaves.data_ptr(), self.t_pnodes.data_ptr(),
+                                         C.c_void_p(stream.cuda_stream)), "tr_grid_scene_build")
+        torch.cuda.synchronize(self.device)
+        self.t_pids = None
+        self.t_grid = None
+        self.t_grid_leaf = None
+        self.pnodes_host = self.pleaves_host = None
+        self.grid = PointGrid(np.full(3, n, np.int32), np.zeros(3), np.ones(3), None)
+        return n_nodes, n_leaves
 
     # ---------------------------------------------------------------- epochs
     def activity(self, act: np.ndarray):

@@ -75,6 +75,11 @@ def build_scene(pkg, name: str):
         n = int(name[6:])   # radial59 (1e6 tets), radial128 (1e7), radial272 (1e8): SURVEY §8d
         return pkg.Scene.build(pkg.generate_synthetic(n, "radial", V),
                                _tf(pkg, radial16_tf_doc(n)))
+    if name.startswith("grid") and name[4:].isdigit():
+        # the same scene as radialN, generated in HBM without host mesh
+        # arrays (grid_scene.py; radial585 = BASELINE config 4, 1e9 tets)
+        n = int(name[4:])
+        return pkg.GridScene.build(n, _tf(pkg, radial16_tf_doc(n)))
     if name == "voidcell":
         return pkg.Scene.build(pkg.generate_synthetic(3, "voidblock", C),
                                _banded(pkg, (0.0, 1.0)), kd_config=K(16))
@@ -98,8 +103,13 @@ def build_scene(pkg, name: str):
     raise KeyError(name)
 
 
+def _grid_alias(name: str) -> str:
+    return "radial" + name[4:] if name.startswith("grid") and name[4:].isdigit() else name
+
+
 def camera(pkg, name: str, scale: float = 1.0):
     Cam = pkg.Camera
+    name = _grid_alias(name)
     if name == "golden_radial4":
         return Cam(position=[10.0, 6.0, 8.0], look_at=[2.0, 2.0, 2.0], up=[0, 1, 0],
                    fov_y_deg=40.0, width=64, height=64)
@@ -139,6 +149,7 @@ def camera(pkg, name: str, scale: float = 1.0):
 
 def params(pkg, name: str):
     P = pkg.AdaptiveParams
+    name = _grid_alias(name)
     if name in ("golden_radial4", "conftest48", "inside", "axis"):
         return P(s1=0.05, s2=0.3, p=2.0, termination_opacity=0.99)
     if name.startswith("radial") and name[6:].isdigit():

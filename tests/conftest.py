@@ -51,3 +51,9 @@ def built_lib():
     _build.build_library()
     _build.build_oracle()
     return True
+
+
+@pytest.fixture(scope="session")
+def B(built_lib):
+    import paper_1908_01906_b200 as B
+    return B
