@@ -272,14 +272,17 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
 
 /* Device build of the synthetic N^3-cube scene (mesh.py:147-231 generator,
  * vertex field 0 = ramp, 1 = radial; csrc/synth.cu) straight into HBM: n_tets
- * = 5 N^3 records in id order (pleaf_ids = NULL), one leaf per cube (the point
+ * = 5 N^3 records, one leaf per cube (the point
  * grid is the cube grid: gorg 0, gscale 1, gdim N, pgrid_leaf = leaves) and
  * N^3 - 1 BVH nodes.  inv10: host (10,3,3) inverse edge matrices of the 5 tets
  * of an even then an odd cube (numpy's LAPACK, mesh.py:254).  pad = the box
  * pad 1e-7 * diagonal (mesh.py:249).  For BASELINE config 4 (1e9 tets). */
 int tr_grid_scene_sizes(int64_t n, int64_t *n_tets, int64_t *n_leaves, int64_t *n_nodes);
 int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv10,
-                        TrTetRecord *recs, TrPLeaf *leaves, TrPNode *nodes, void *stream);
+                        TrTetRecord *recs, TrPLeaf *leaves, TrPNode *nodes, uint32_t *ids,
+                        void *stream);
+/* ids: NULL -> records in id order (pleaf_ids = NULL); else records in
+ * 8^3-cube brick order and ids[k] (n_tets u32) = tet id of record k. */
 
 /* Replaces _kernels.field_at_many (K:157-170): pts (n,3) f64 device;
  * found (n,) u8, vals (n,) f64, tet (n,) i64 (may be NULL) device. */

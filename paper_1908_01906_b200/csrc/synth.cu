@@ -10,7 +10,9 @@
 //     inverts with numpy's LAPACK (bit-identical to inverting all T: the
 //     integer edge matrices are translation invariant), and the f32-rounded
 //     analytic field at the 4 vertices (mesh.py:170-171, 230);
-//   * one leaf per cube (its 5 tets, ascending ids = record order), exclusive
+//   * records in 8^3-cube brick order (ids != NULL; ids[k] = tet id of record
+//     k) so that spatial neighbours share DRAM pages and L2 sets, or in id order;
+//   * one leaf per cube (its 5 tets, ascending ids, consecutive records), exclusive
 //     box = the cube shrunk by the box pad (no other cube's padded tet boxes
 //     reach inside it), rounded inward to f32;
 //   * the uniform point grid is the cube grid itself (origin 0, scale 1), so
@@ -48,8 +50,24 @@ __constant__ int8_t c_pattern[5][4][3] = {
 struct GridK {
     int64_t n;
     int32_t field;  // 0 ramp, 1 radial
+    int32_t brick;  // records in 8x8x8-cube brick order (else cube order)
     double pad;
 };
+
+constexpr int64_t BRICK = 8;
+
+// Record slot of cube (x, y, z): cube-major, or brick-major with the cubes of
+// a brick (8^3, clipped at the far faces) in x, y, z order -- dense, so the
+// 5 records of cube c start at 5 * cube_slot(c).
+__device__ __forceinline__ int64_t cube_slot(const GridK &G, int64_t x, int64_t y, int64_t z) {
+    const int64_t n = G.n;
+    if (!G.brick) return (x * n + y) * n + z;
+    const int64_t bx = x / BRICK, by = y / BRICK, bz = z / BRICK;
+    const int64_t sx = min(BRICK, n - bx * BRICK), sy = min(BRICK, n - by * BRICK);
+    const int64_t sz = min(BRICK, n - bz * BRICK);
+    const int64_t before = BRICK * bx * n * n + sx * BRICK * by * n + sx * sy * BRICK * bz;
+    return before + ((x - bx * BRICK) * sy + (y - by * BRICK)) * sz + (z - bz * BRICK);
+}
 
 // mesh.py _ramp / _radial, then .astype(float32).astype(float64)
 __device__ __forceinline__ double grid_field(const GridK &G, double x, double y, double z) {
@@ -59,7 +77,8 @@ __device__ __forceinline__ double grid_field(const GridK &G, double x, double y,
     return (double)__double2float_rn(sqrt((d0 * d0 + d1 * d1) + d2 * d2));
 }
 
-__global__ void grid_records_kernel(GridK G, const double *__restrict__ inv10, TrTetRecord *recs) {
+__global__ void grid_records_kernel(GridK G, const double *__restrict__ inv10, TrTetRecord *recs,
+                                    uint32_t *ids) {
     __shared__ double s_inv[90];
     for (int i = threadIdx.x; i < 90; i += blockDim.x) s_inv[i] = inv10[i];
     __syncthreads();
@@ -79,7 +98,9 @@ __global__ void grid_records_kernel(GridK G, const double *__restrict__ inv10, T
             v[q][2] = (double)(z + c_pattern[k][q][2]);
         }
         const double *m = s_inv + 9 * (par * 5 + k);
-        double2 *o = reinterpret_cast<double2 *>(recs + t);
+        const int64_t slot = 5 * cube_slot(G, x, y, z) + k;
+        if (ids) ids[slot] = (uint32_t)t;
+        double2 *o = reinterpret_cast<double2 *>(recs + slot);
         o[0] = make_double2(m[0], m[1]);
         o[1] = make_double2(m[2], m[3]);
         o[2] = make_double2(m[4], m[5]);
@@ -105,7 +126,7 @@ __global__ void grid_leaves_kernel(GridK G, TrPLeaf *leaves) {
             L.ex_lo[a] = __double2float_ru(lo);   // inward
             L.ex_hi[a] = __double2float_rd(hi);
         }
-        L.start = (uint32_t)(5 * c);
+        L.start = (uint32_t)(5 * cube_slot(G, q[0], q[1], q[2]));
         L.count = 5u;
         leaves[c] = L;
     }
@@ -208,20 +229,21 @@ int tr_grid_scene_sizes(int64_t n, int64_t *n_tets, int64_t *n_leaves, int64_t *
 }
 
 int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv10,
-                        TrTetRecord *recs, TrPLeaf *leaves, TrPNode *nodes, void *stream) {
+                        TrTetRecord *recs, TrPLeaf *leaves, TrPNode *nodes, uint32_t *ids,
+                        void *stream) {
     int64_t T, Lc, Nn;
     int rc = tr_grid_scene_sizes(n, &T, &Lc, &Nn);
     if (rc) return rc;
     if ((field != 0 && field != 1) || !(pad >= 0.0) || !inv10 || !recs || !leaves || !nodes)
         return tr_fail(TR_EINVAL, "tr_grid_scene_build: invalid arguments");
     cudaStream_t st = (cudaStream_t)stream;
-    GridK G{n, field, pad};
+    GridK G{n, field, ids != nullptr ? 1 : 0, pad};
     double *d_inv = nullptr;
     cudaError_t e = cudaMallocAsync(&d_inv, 90 * sizeof(double), st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync(inv10)");
     e = cudaMemcpyAsync(d_inv, inv10, 90 * sizeof(double), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(inv10)");
-    grid_records_kernel<<<grid_for(T), 256, 0, st>>>(G, d_inv, recs);
+    grid_records_kernel<<<grid_for(T), 256, 0, st>>>(G, d_inv, recs, ids);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "grid_records_kernel");
     grid_leaves_kernel<<<grid_for(Lc), 256, 0, st>>>(G, leaves);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "grid_leaves_kernel");

@@ -326,12 +326,16 @@ class DeviceScene:
         self.t_pnodes = torch.empty(n_nodes * 64, dtype=torch.uint8, device=self.device)
         inv10 = np.ascontiguousarray(sampler.inv10, dtype=np.float64).reshape(90)
         stream = torch.cuda.current_stream(self.device)
+        # brick-ordered records (+ their tet ids) unless GRID_ID_ORDER is asked for
+        brick = not getattr(scene, "grid_id_order", False)
+        self.t_pids = (torch.empty(n_tets, dtype=torch.int32, device=self.device)
+                       if brick else None)
         _lib.check(L.tr_grid_scene_build(n, int(mesh.field_id), float(sampler.pad),
                                          _lib.ptr(inv10, C.c_double), self.t_tets.data_ptr(),
                                          self.t_pleaves.data_ptr(), self.t_pnodes.data_ptr(),
+                                         None if self.t_pids is None else self.t_pids.data_ptr(),
                                          C.c_void_p(stream.cuda_stream)), "tr_grid_scene_build")
         torch.cuda.synchronize(self.device)
-        self.t_pids = None
         self.t_grid = None
         self.t_grid_leaf = None
         self.pnodes_host = self.pleaves_host = None

@@ -86,13 +86,26 @@ def test_grid_scene_limits(B):
 def test_grid_records_equal_host_packing(B):
     import torch
     from paper_1908_01906_b200.device import device_scene_for, pack_tet_records
-    for n in (1, 3, 8):
-        g = cases.build_scene(B, f"grid{n}")
-        dev = device_scene_for(g)
-        got = dev.t_tets.cpu().numpy()
+    for n in (1, 3, 8, 11):
         mesh = B.generate_synthetic(n, "radial", B.Centering.VERTEX)
-        want = pack_tet_records(mesh, B.MeshSampler(mesh))
-        assert np.array_equal(got, np.frombuffer(want.tobytes(), np.uint8)), n
+        want = np.frombuffer(pack_tet_records(mesh, B.MeshSampler(mesh)).tobytes(),
+                             np.uint8).reshape(-1, 128)
+        for id_order in (True, False):
+            g = cases.build_scene(B, f"grid{n}")
+            g.grid_id_order = id_order
+            dev = device_scene_for(g)
+            got = dev.t_tets.cpu().numpy().reshape(-1, 128)
+            if id_order:
+                assert dev.t_pids is None
+                assert np.array_equal(got, want), n
+            else:   # brick order: record k is tet ids[k], every tet exactly once
+                ids = dev.t_pids.cpu().numpy()
+                assert np.array_equal(np.sort(ids), np.arange(mesh.n_tets))
+                assert np.array_equal(got, want[ids]), n
+                from paper_1908_01906_b200 import _lib
+                lv = dev.t_pleaves.cpu().numpy().view(_lib.PLEAF_DTYPE)
+                # leaf c (cube c) starts at its cube's 5 records, ascending ids
+                assert np.array_equal(ids[lv["start"]], 5 * np.arange(n ** 3))
         torch.cuda.synchronize()
 
 
@@ -104,9 +117,11 @@ def test_grid_frames_equal_host_scene(B, n):
     cam, par = cases.camera(B, f"radial{max(n, 5)}"), cases.params(B, "radial16")
     if n == 4:
         cam = cases.camera(B, "golden_radial4")
+    g2 = cases.build_scene(B, f"grid{n}")
+    g2.grid_id_order = True
     for mode in ("reference", "skip", "skip-adaptive"):
-        for flags in (0, 2, 0x1000):
-            fg, sg = B.render(g, cam, mode, par, flags=flags)
+        for gs, flags in ((g, 0), (g, 2), (g, 0x1000), (g2, 0)):
+            fg, sg = B.render(gs, cam, mode, par, flags=flags)
             fr, sr = B.render(r, cam, mode, par)
             assert np.array_equal(fg.rgba, fr.rgba), (n, mode, flags)
             assert np.array_equal(fg.samples, fr.samples)
