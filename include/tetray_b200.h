@@ -158,6 +158,13 @@ int tr_tf_meta(int64_t n_parts, const double *vrange, const double *tf_table, in
                double tf_lo, double tf_hi, double *max_opacity, double *raw_variance,
                double *sigma, uint8_t *active);
 
+/* The same metadata on the GPU (csrc/meta.cu, one thread per partition,
+ * numpy's reduction order kept: identical results).  All pointers are device
+ * pointers; sigma / active may be NULL.  Synchronizes the stream. */
+int tr_tf_meta_device(int64_t n_parts, const double *vrange, const double *tf_table, int64_t n_tf,
+                      double tf_lo, double tf_hi, double *max_opacity, double *raw_variance,
+                      double *sigma, uint8_t *active, void *stream);
+
 /* step_size (K:20-22) per partition on the host with glibc pow, so adaptive
  * steps are bit-identical to the reference's. */
 int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out);
@@ -288,6 +295,20 @@ int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv1
  * found (n,) u8, vals (n,) f64, tet (n,) i64 (may be NULL) device. */
 int tr_field_at_many(const TrDeviceScene *scene, int64_t n, const double *pts, uint8_t *found,
                      double *vals, int64_t *tet, void *stream);
+
+/* Device epilogue (csrc/epilogue.cu), device pointers:
+ * imgio.framebuffer_rgb (imgio.py:36-39, 76-78): rgba (n,4) f64 -> rgb (n,3) u8;
+ * imgio.heatmap_rgb (imgio.py:81-87): counts (n) i64 -> rgb (n,3) u8 through
+ *   lut (256,3) u8, peak = 1 u64 of scratch (the frame maximum);
+ * metrics.ssim (metrics.py:48-80): two (h,w,3) u8 images, window x window
+ *   weights (f64), rec709 (3 f64), c1, c2 -> *sum = sum of the SSIM map over
+ *   the valid region (divide by its size for the mean). */
+int tr_quantize_rgb(const double *rgba, int64_t n_pixels, uint8_t *rgb, void *stream);
+int tr_heatmap_rgb(const int64_t *counts, int64_t n_pixels, const uint8_t *lut, uint8_t *rgb,
+                   uint64_t *peak, void *stream);
+int tr_ssim_rgb(const uint8_t *a, const uint8_t *b, int64_t height, int64_t width, int32_t window,
+                const double *weights, const double *rec709, double c1, double c2, double *sum,
+                void *stream);
 
 /* Multi-GPU merge: scatter gathered compact tiles (count ranks, slot-major)
  * into the image layout. */

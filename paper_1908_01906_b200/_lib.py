@@ -117,6 +117,9 @@ _SIGNATURES = [
     ("tr_tet_boxes", C.c_int, [C.c_int64, c_f64p, c_i64p, C.c_double, c_f64p, c_f64p]),
     ("tr_tf_meta", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int64, C.c_double, C.c_double,
                              c_f64p, c_f64p, c_f64p, c_u8p]),
+    ("tr_tf_meta_device", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
+                                    C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                    C.c_void_p]),
     ("tr_epoch_steps", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),
@@ -130,6 +133,11 @@ _SIGNATURES = [
     ("tr_grid_scene_sizes", C.c_int, [C.c_int64, c_i64p, c_i64p, c_i64p]),
     ("tr_grid_scene_build", C.c_int, [C.c_int64, C.c_int32, C.c_double, c_f64p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_quantize_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    ("tr_heatmap_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
+                                 C.c_void_p]),
+    ("tr_ssim_rgb", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, C.c_void_p,
+                              C.c_void_p, C.c_double, C.c_double, C.c_void_p, C.c_void_p]),
     ("tr_field_at_many", C.c_int, [C.POINTER(TrDeviceScene), C.c_int64, C.c_void_p, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_scatter_tiles", C.c_int, [C.c_int64, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p,

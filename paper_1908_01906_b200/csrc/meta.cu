@@ -1,0 +1,173 @@
+// meta.cu -- transfer-function partition metadata on the device.
+//
+// Replaces update_transfer_function's per-partition loop (transfer.py:95-167,
+// the paper's "parallelized across the partitions" step): for every partition
+// the TF rows overlapping its value range (the interpolated ends plus the
+// table rows strictly inside, transfer.py:96-110), their maximum opacity and
+// the variance of the opacity-weighted colours (transfer.py:113-124), then the
+// min-max normalisation to sigma and the active flags (transfer.py:127-141).
+// One thread per partition; the rows are regenerated on the fly instead of
+// stored, and every reduction keeps numpy's order -- the axis-0 mean summed
+// sequentially, the final mean with numpy's pairwise summation -- so the
+// results equal the host restatement (tr_tf_meta) and the reference bit for
+// bit (tests/test_tf_meta_device.py).  Compiled with -fmad=false like the
+// render kernels.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "tetray_b200.h"
+#include "tr_internal.h"
+
+namespace {
+
+struct Rows {  // the overlapping rows of one partition (transfer.py:96-110)
+    const double *T;
+    int64_t n, j0, k;
+    double lo, hi, rmin, rmax;
+};
+
+// K:74-90
+__device__ void tf_lookup(const double *T, int64_t n, double lo, double hi, double v, double c[4]) {
+    const double u = (v - lo) / (hi - lo) * (double)(n - 1);
+    if (u <= 0.0) { for (int q = 0; q < 4; ++q) c[q] = T[q]; return; }
+    if (u >= (double)(n - 1)) { for (int q = 0; q < 4; ++q) c[q] = T[4 * (n - 1) + q]; return; }
+    const int64_t j = (int64_t)floor(u);
+    const double f = u - (double)j;
+    for (int q = 0; q < 4; ++q) c[q] = T[4 * j + q] + f * (T[4 * (j + 1) + q] - T[4 * j + q]);
+}
+
+__device__ void row(const Rows &R, int64_t i, double c[4]) {
+    if (i == 0) { tf_lookup(R.T, R.n, R.lo, R.hi, R.rmin, c); return; }
+    if (i == R.k - 1) { tf_lookup(R.T, R.n, R.lo, R.hi, R.rmax, c); return; }
+    const double *t = R.T + 4 * (R.j0 + i - 1);
+    for (int q = 0; q < 4; ++q) c[q] = t[q];
+}
+
+// squared distance of row i's opacity-weighted colour to the mean
+__device__ double sqdist(const Rows &R, int64_t i, const double mean[3]) {
+    double c[4];
+    row(R, i, c);
+    const double d0 = c[0] * c[3] - mean[0], d1 = c[1] * c[3] - mean[1], d2 = c[2] * c[3] - mean[2];
+    return ((d0 * d0) + (d1 * d1)) + (d2 * d2);
+}
+
+// numpy's pairwise summation (add.reduce over a contiguous float64 vector)
+__device__ double pairwise(const Rows &R, const double mean[3], int64_t a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r += sqdist(R, a + i, mean);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = sqdist(R, a + j, mean);
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += sqdist(R, a + i + j, mean);
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += sqdist(R, a + i, mean);
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise(R, mean, a, n2) + pairwise(R, mean, a + n2, n - n2);
+}
+
+__global__ void tf_meta_kernel(int64_t P, const double *__restrict__ vrange, const double *T,
+                               int64_t n, double lo, double hi, double *mop, double *raw,
+                               int *err) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    Rows R;
+    R.T = T; R.n = n; R.lo = lo; R.hi = hi;
+    R.rmin = vrange[2 * p];
+    R.rmax = vrange[2 * p + 1];
+    if (R.rmin > R.rmax) { atomicExch(err, 1); return; }
+    const double u_min = (R.rmin - lo) / (hi - lo) * (double)(n - 1);
+    const double u_max = (R.rmax - lo) / (hi - lo) * (double)(n - 1);
+    // Python int(floor(.)) semantics, clamped so the cast cannot overflow
+    const double fl = fmin(fmax(floor(u_min), -2.0), (double)n + 2.0);
+    const double cl = fmin(fmax(ceil(u_max), -2.0), (double)n + 2.0);
+    const int64_t j0 = max((int64_t)fl + 1, (int64_t)0);
+    const int64_t j1 = min((int64_t)cl - 1, n - 1);
+    R.j0 = j0;
+    R.k = 2 + ((j1 >= j0) ? j1 - j0 + 1 : 0);
+    // alpha.max() and the axis-0 mean of the weighted colours (sequential)
+    double amax = -INFINITY, s[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = 0; i < R.k; ++i) {
+        double c[4];
+        row(R, i, c);
+        amax = (c[3] > amax) ? c[3] : amax;
+        for (int q = 0; q < 3; ++q) {
+            const double w = c[q] * c[3];
+            s[q] = (i == 0) ? w : s[q] + w;
+        }
+    }
+    const double mean[3] = {s[0] / (double)R.k, s[1] / (double)R.k, s[2] / (double)R.k};
+    raw[p] = pairwise(R, mean, 0, R.k) / (double)R.k;
+    mop[p] = amax;
+}
+
+// normalize_variances (transfer.py:127-141): one CTA reduces min / max
+__global__ void tf_normalize_kernel(int64_t P, const double *mop, const double *raw, double *sigma,
+                                    uint8_t *active) {
+    __shared__ double s_min[1024], s_max[1024];
+    double vmin = INFINITY, vmax = -INFINITY;
+    for (int64_t p = threadIdx.x; p < P; p += blockDim.x) {
+        vmin = fmin(vmin, raw[p]);
+        vmax = fmax(vmax, raw[p]);
+    }
+    s_min[threadIdx.x] = vmin;
+    s_max[threadIdx.x] = vmax;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            s_min[threadIdx.x] = fmin(s_min[threadIdx.x], s_min[threadIdx.x + o]);
+            s_max[threadIdx.x] = fmax(s_max[threadIdx.x], s_max[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    vmin = s_min[0];
+    vmax = s_max[0];
+    for (int64_t p = threadIdx.x; p < P; p += blockDim.x) {
+        if (sigma) sigma[p] = (vmax == vmin) ? 1.0 : (raw[p] - vmin) / (vmax - vmin);
+        if (active) active[p] = mop[p] > 0.0 ? 1 : 0;
+    }
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+    return tr_fail(TR_ECUDA, m.c_str());
+}
+
+}  // namespace
+
+extern "C" int tr_tf_meta_device(int64_t n_parts, const double *vrange, const double *tf_table,
+                                 int64_t n_tf, double tf_lo, double tf_hi, double *max_opacity,
+                                 double *raw_variance, double *sigma, uint8_t *active,
+                                 void *stream) {
+    if (n_parts <= 0 || !vrange || !tf_table || n_tf < 2 || !(tf_lo < tf_hi) || !max_opacity ||
+        !raw_variance)
+        return tr_fail(TR_EINVAL, "tr_tf_meta_device: invalid arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    int *d_err = nullptr;
+    cudaError_t e = cudaMallocAsync(&d_err, sizeof(int), st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMallocAsync");
+    cudaMemsetAsync(d_err, 0, sizeof(int), st);
+    const int64_t blocks = (n_parts + 127) / 128;
+    tf_meta_kernel<<<(unsigned)blocks, 128, 0, st>>>(n_parts, vrange, tf_table, n_tf, tf_lo, tf_hi,
+                                                     max_opacity, raw_variance, d_err);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "tf_meta_kernel");
+    tf_normalize_kernel<<<1, 1024, 0, st>>>(n_parts, max_opacity, raw_variance, sigma, active);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "tf_normalize_kernel");
+    int h_err = 0;
+    e = cudaMemcpyAsync(&h_err, d_err, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    cudaFreeAsync(d_err, st);
+    if (e != cudaSuccess) return cuda_fail(e, "tr_tf_meta_device");
+    if (h_err) return tr_fail(TR_EINVAL, "tr_tf_meta_device: invalid value range (min > max)");
+    return TR_OK;
+}
