@@ -249,7 +249,7 @@ typedef struct TrFrame {
 #define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
- * per SM (0: auto, 1: 4, 2: 2, 3: 3); bits 14-15: CTAs per SM actually
+ * per SM (0: 3, 1: 4, 2: 2, 3: 3); bits 14-15: CTAs per SM actually
  * launched (0: as many as fit).  Tuning knobs only:
  * every setting renders the same frame. */
 

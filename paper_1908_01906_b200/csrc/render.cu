@@ -1643,11 +1643,11 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     // minimum resident CTAs per SM of the G = 4 kernel (register budget; 0: 2)
     const int lg = (frame->flags >> 8) & 0xf;
     const int gsize = lg ? (1 << lg) : 4;
-    // bits 12-13: minimum resident CTAs per SM (register budget); 0 = auto:
-    // 4 CTAs (64 registers, 32 warps) when the tet records exceed 1 GiB (the
-    // samples then miss L2 and latency hiding wins), else 3 (80 registers)
+    // bits 12-13: minimum resident CTAs per SM (register budget); 0 = 3 CTAs
+    // (80 registers, 24 warps): measured best or within 3% from 1e6 to 1e9
+    // tets (32 warps spill and thrash L1; 16 hide too little latency)
     int minb = (frame->flags >> 12) & 0x3;
-    if (minb == 0) minb = (scene->n_tets * (int64_t)sizeof(TrTetRecord) > ((int64_t)1 << 30)) ? 1 : 3;
+    if (minb == 0) minb = 3;
     void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs);
     if (frame->flags & TR_FLAG_REG_STATE) {   // ray state in registers (2 CTAs per SM)
         switch (gsize) {
