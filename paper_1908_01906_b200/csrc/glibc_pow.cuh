@@ -84,9 +84,10 @@ TR_HD double tr_pow_glibc(double x, double y, const uint64_t *lhead, const uint6
     const double z = tr_as_double(iz);
     const double kd = (double)k;
 #ifdef __CUDA_ARCH__
-    const double2 e01 = __ldg(reinterpret_cast<const double2 *>(ltab) + 2 * i);
-    const double2 e23 = __ldg(reinterpret_cast<const double2 *>(ltab) + 2 * i + 1);
-    const double invc = e01.x, logc = e23.x, logctail = e23.y;
+    double invc, logc, logctail, pad_;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"   // one 32-B entry (ltab is 32-B aligned)
+        : "=d"(invc), "=d"(pad_), "=d"(logc), "=d"(logctail) : "l"(ltab + 4 * i));
+    (void)pad_;
 #else
     const uint64_t *e = ltab + 4 * i;
     const double invc = tr_as_double(e[0]), logc = tr_as_double(e[2]), logctail = tr_as_double(e[3]);

@@ -131,16 +131,39 @@ __device__ __forceinline__ bool strictly_in(const PQuery &q, const float *lo, co
            q.zu < hi[2];
 }
 
+// 32-B read-only loads (LDG.E.ENL2.256, sm_100): the march is bound by the
+// L1 data pipe's wavefronts (ncu: l1tex__data_pipe_lsu_wavefronts ~91% of
+// peak), and a warp-wide gather costs about one wavefront per distinct line
+// per instruction -- so each 32-B record chunk, TF row, pow table entry and
+// leaf header is fetched by one instruction instead of two.
+#ifndef TR_LD256
+#define TR_LD256 1
+#endif
+__device__ __forceinline__ double4 ldg256(const void *p) {
+    double4 v;
+#if TR_LD256
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+#else
+    const double2 a = __ldg(reinterpret_cast<const double2 *>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+    v = make_double4(a.x, a.y, b.x, b.y);
+#endif
+    return v;
+}
+
 // The 96 B of a record the barycentric test reads (inverse + origin).
 struct RecM {
     double2 a0, a1, a2, a3, a4, a5;
 };
 
 __device__ __forceinline__ RecM load_recm(const TrTetRecord *__restrict__ recs, uint32_t k) {
-    const double2 *r = reinterpret_cast<const double2 *>(recs + k);
+    const char *r = reinterpret_cast<const char *>(recs + k);
+    const double4 c0 = ldg256(r), c1 = ldg256(r + 32), c2 = ldg256(r + 64);
     RecM m;
-    m.a0 = __ldg(r + 0); m.a1 = __ldg(r + 1); m.a2 = __ldg(r + 2);
-    m.a3 = __ldg(r + 3); m.a4 = __ldg(r + 4); m.a5 = __ldg(r + 5);
+    m.a0 = make_double2(c0.x, c0.y); m.a1 = make_double2(c0.z, c0.w);
+    m.a2 = make_double2(c1.x, c1.y); m.a3 = make_double2(c1.z, c1.w);
+    m.a4 = make_double2(c2.x, c2.y); m.a5 = make_double2(c2.z, c2.w);
     return m;
 }
 
@@ -163,7 +186,7 @@ __device__ __forceinline__ bool bary_test(const TrTetRecord *__restrict__ recs, 
 #if TR_HAVE_GLIBC_POW
 __constant__ unsigned long long c_pow_lhead[] = TR_POW_LOG_HEAD_INIT;
 __constant__ unsigned long long c_pow_ehead[] = TR_POW_EXP_HEAD_INIT;
-__device__ const __align__(16) unsigned long long d_pow_ltab[] = TR_POW_LOG_TAB_INIT;
+__device__ const __align__(32) unsigned long long d_pow_ltab[] = TR_POW_LOG_TAB_INIT;
 __device__ const __align__(16) unsigned long long d_pow_etab[] = TR_POW_EXP_TAB_INIT;
 #endif
 
@@ -338,12 +361,14 @@ __device__ __forceinline__ int64_t grid_cell(const SceneK &S, const PQuery &q) {
 }
 
 __device__ __forceinline__ void load_leaf(const TrPLeaf *lf, LeafHint &h) {
-    const float4 *p = reinterpret_cast<const float4 *>(lf);
-    const float4 a = __ldg(p), b = __ldg(p + 1);
-    h.lo[0] = a.x; h.lo[1] = a.y; h.lo[2] = a.z;
-    h.hi[0] = a.w; h.hi[1] = b.x; h.hi[2] = b.y;
-    h.start = __float_as_uint(b.z);
-    h.count = __float_as_uint(b.w);
+    const double4 v = ldg256(lf);   // 8 x 32 bit: ex_lo[3], ex_hi[3], start, count
+    const long long w0 = __double_as_longlong(v.x), w1 = __double_as_longlong(v.y);
+    const long long w2 = __double_as_longlong(v.z), w3 = __double_as_longlong(v.w);
+    h.lo[0] = __int_as_float((int)w0); h.lo[1] = __int_as_float((int)(w0 >> 32));
+    h.lo[2] = __int_as_float((int)w1); h.hi[0] = __int_as_float((int)(w1 >> 32));
+    h.hi[1] = __int_as_float((int)w2); h.hi[2] = __int_as_float((int)(w2 >> 32));
+    h.start = (uint32_t)w3;
+    h.count = (uint32_t)((unsigned long long)w3 >> 32);
     h.valid = true;
 }
 
@@ -400,21 +425,20 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
 __device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t n, double lo,
                                           double hi, double v, double c[4]) {
     const double u = (v - lo) / (hi - lo) * (double)(n - 1);
-    const double2 *t2 = reinterpret_cast<const double2 *>(T);
     int64_t j;
     double f;
     bool interp = true;
     if (u <= 0.0) { j = 0; interp = false; }
     else if (u >= (double)(n - 1)) { j = n - 1; interp = false; }
     else { j = (int64_t)floor(u); }
-    const double2 a0 = __ldg(t2 + 2 * j), a1 = __ldg(t2 + 2 * j + 1);
-    if (!interp) { c[0] = a0.x; c[1] = a0.y; c[2] = a1.x; c[3] = a1.y; return; }
+    const double4 a = ldg256(T + 4 * j);
+    if (!interp) { c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; return; }
     f = u - (double)j;
-    const double2 b0 = __ldg(t2 + 2 * j + 2), b1 = __ldg(t2 + 2 * j + 3);
-    c[0] = a0.x + f * (b0.x - a0.x);
-    c[1] = a0.y + f * (b0.y - a0.y);
-    c[2] = a1.x + f * (b1.x - a1.x);
-    c[3] = a1.y + f * (b1.y - a1.y);
+    const double4 b = ldg256(T + 4 * j + 4);
+    c[0] = a.x + f * (b.x - a.x);
+    c[1] = a.y + f * (b.y - a.y);
+    c[2] = a.z + f * (b.z - a.z);
+    c[3] = a.w + f * (b.w - a.w);
 }
 
 struct EpochK {
@@ -969,8 +993,8 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
     double v;
     const double2 *rp = reinterpret_cast<const double2 *>(S.tets + pos);
     if (S.centering == 0) {   // K:149-151
-        const double2 f01 = __ldg(rp + 6), f23 = __ldg(rp + 7);
-        v = l[0] * f01.x + l[1] * f01.y + l[2] * f23.x + l[3] * f23.y;
+        const double4 f = ldg256(rp + 6);
+        v = l[0] * f.x + l[1] * f.y + l[2] * f.z + l[3] * f.w;
     } else {                  // K:153
         v = __ldg(rp + 6).x;
     }
@@ -1001,7 +1025,10 @@ __global__ void __launch_bounds__(MARCH_BLOCK, MINB)
 march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
-    __shared__ double4 shade[MARCH_BLOCK];              // per-lane sample result: ca, r, g, b
+    // per-lane sample result (ca, r, g, b) as [lane in group][group]: the G
+    // reads of a composite step hit consecutive entries across the warp's
+    // groups (no bank conflicts; [group][lane] was an 8-way conflict)
+    __shared__ double4 shade[G][MARCH_BLOCK / G];
     __shared__ Inline inl[MARCH_BLOCK / G];             // per-group inline state (rare path)
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1128,7 +1155,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (has)
             sh = shade_sample(S, E, fr, ox, oy, oz, dx, dy, dz, a, k, phase, pid, stats, seq_scan,
                               use_grid, found);
-        shade[threadIdx.x] = sh;
+        shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
 
@@ -1139,9 +1166,8 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         int taken_r = cnt;
         bool term = false;
         if (active && !idle) {
-            const double4 *grp = shade + (threadIdx.x - j);
             for (int m = 0; m < cnt; ++m) {
-                const double4 g = grp[m];
+                const double4 g = shade[m][threadIdx.x / G];
                 const double w = (1.0 - acc.a) * g.x;
                 acc.r += w * g.y;
                 acc.g += w * g.z;
@@ -1250,7 +1276,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
     constexpr int NG = MARCH_BLOCK / G;
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
-    __shared__ double4 shade[MARCH_BLOCK];
+    __shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free
     __shared__ Inline inl[NG];
     __shared__ double s_o[3][NG], s_d[3][NG], s_acc[4][NG], s_phase[NG];
     __shared__ long long s_out[NG], s_samples[NG];
@@ -1365,7 +1391,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (has)
             sh = shade_sample(S, E, fr, s_o[0][g], s_o[1][g], s_o[2][g], s_d[0][g], s_d[1][g],
                               s_d[2][g], a, k, s_phase[g], pid, stats, seq_scan, use_grid, found);
-        shade[threadIdx.x] = sh;
+        shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
 
@@ -1376,9 +1402,8 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         Acc acc = {0.0, 0.0, 0.0, 0.0};
         if (active && !idle) {
             acc.r = s_acc[0][g]; acc.g = s_acc[1][g]; acc.b = s_acc[2][g]; acc.a = s_acc[3][g];
-            const double4 *grp = shade + (threadIdx.x - j);
             for (int m = 0; m < cnt; ++m) {
-                const double4 gg = grp[m];
+                const double4 gg = shade[m][g];
                 const double w = (1.0 - acc.a) * gg.x;
                 acc.r += w * gg.y;
                 acc.g += w * gg.z;

@@ -9,12 +9,13 @@ sys.path.insert(0, str(ROOT))
 from paper_1908_01906_b200 import _build
 
 VARIANTS = {
-    "base": [],
-    "nopowshort": [("    if (x == 1.0) return 1.0;  // glibc: pow(1, y) == 1 for every y\n", ""),
-                   ("const bool need_pow = e != 1.0 && x != 1.0;", "const bool need_pow = e != 1.0;")],
-    "statsrt": [("constexpr bool stats = STATS;", "const bool stats = STATS || (fr.flags & TR_FLAG_STATS) != 0;")],
+    "shadeT": [],
+    "shadeL": [("__shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free",
+                "__shared__ double4 shade[MARCH_BLOCK / G][G];"),
+               ("        shade[j][threadIdx.x / G] = sh;\n        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;\n        __syncwarp();\n\n        // ---- composite the round in sample order (K:285-295)\n",
+                "        shade[threadIdx.x / G][j] = sh;\n        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;\n        __syncwarp();\n\n        // ---- composite the round in sample order (K:285-295)\n"),
+               ("const double4 gg = shade[m][g];", "const double4 gg = shade[g][m];")],
 }
-VARIANTS["both"] = VARIANTS["nopowshort"] + VARIANTS["statsrt"]
 
 def build(name, edits):
     d = ROOT / "build" / "ab" / name
