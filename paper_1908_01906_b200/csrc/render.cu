@@ -68,6 +68,8 @@ enum : int {
     ST_BSP_OVERFLOW,     // rays redone with the BVH (BSP buffer or stack overflow)
     ST_BSP_CELLS,        // BSP leaf cells enumerated
     ST_TRACE_MAX_IV,     // most intervals of one ray (max)
+    ST_BSP_NODES,        // BSP nodes visited by the trace
+    ST_TRACE_MAX_NODES,  // most BSP nodes visited by one ray (max)
     ST_COUNT
 };
 __device__ unsigned long long g_stats[16];
@@ -544,6 +546,7 @@ struct BspTrace {
     double c_pa[KBUF], c_pb[KBUF];
     int nb;
     int cells;
+    int nodes;
     bool overflow;
 };
 
@@ -555,6 +558,7 @@ __device__ __forceinline__ void bsp_begin(const SceneK &S, const RayD &ray, BspT
     T.sp = 0;
     T.nb = 0;
     T.cells = 0;
+    T.nodes = 0;
     T.overflow = false;
     double r0, r1;
     slab(ray, S.kroot_lo, S.kroot_hi, r0, r1);
@@ -573,6 +577,7 @@ __device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD 
         bool leaf_done = false;
         while (true) {
             if (tf <= 0.0) break;                         // behind the origin: exits <= 0
+            ++T.nodes;
             const TrKNode *N = S.knodes + node;
             const int32_t info = __ldg(&N->info);   // issued with the activity byte
             if (E.knode_active && !__ldg(E.knode_active + node)) break;
@@ -698,6 +703,7 @@ struct IvBuf {                   // per-chunk scratch
     double *tail;                // [n_rays]: t_min after the last stored interval (CNT_MORE only)
     uint32_t *order;             // marching rays, most expensive first
     uint32_t *hist, *cursor;     // [N_BUCKETS] each; bucket 0 = nothing to march
+    uint32_t *trace_ctr;         // next 32-ray tile of the trace pass
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
 };
 
@@ -778,9 +784,21 @@ __device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &
 // march_range would take (K:277-280).  Rays with nothing to march (no hit,
 // or only degenerate intervals) are finished here; the others get a cost
 // bucket (~4 log2 of their sample count) for longest-first scheduling.
+//
+// Persistent warps: each warp takes the next 32-ray tile from a counter, so
+// the long rays' tiles do not leave a wave tail (the grid is sized to the
+// resident warps).
 __global__ void __launch_bounds__(TRACE_BLOCK)
 trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
-    const int64_t rr = blockIdx.x * (int64_t)TRACE_BLOCK + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const uint32_t n_tiles = (uint32_t)((F.n_rays + 31) / 32);
+    unsigned long long vis_acc = 0;
+    while (true) {
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(iv.trace_ctr, 1u);
+    tile = __shfl_sync(FULL, tile, 0);
+    if (tile >= n_tiles) break;
+    const int64_t rr = (int64_t)tile * 32 + lane;
     uint32_t n = 0, bucket = 0;
     unsigned long long vis_done = 0;
     const bool in_chunk = rr < F.n_rays;
@@ -793,7 +811,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             uint32_t cum = 0;
             bool more = false, bsp_redo = false;
             double t_min = 0.0;
-            int bsp_cells = 0;
+            int bsp_cells = 0, bsp_nodes = 0;
             if (F.f.mode == 0) {  // K:346-353: the mesh box is the one interval
                 double a, b;
                 slab(ray, S.mesh_lo, S.mesh_hi, a, b);
@@ -837,7 +855,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         last = pid;
                         if (use_bsp) bsp_compact(T, t_min);
                     }
-                    if (use_bsp) bsp_cells += T.cells;
+                    if (use_bsp) { bsp_cells += T.cells; bsp_nodes += T.nodes; }
                     if (!(use_bsp && T.overflow)) break;
                     use_bsp = false;  // candidate buffer overflowed: redo with the BVH
                     bsp_redo = true;
@@ -850,6 +868,8 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 atomicMax(&g_stats[ST_TRACE_MAX_IV], (unsigned long long)n);
                 if (bsp_redo) atomicAdd(&g_stats[ST_BSP_OVERFLOW], 1ull);
                 atomicAdd(&g_stats[ST_BSP_CELLS], (unsigned long long)bsp_cells);
+                atomicAdd(&g_stats[ST_BSP_NODES], (unsigned long long)bsp_nodes);
+                atomicMax(&g_stats[ST_TRACE_MAX_NODES], (unsigned long long)bsp_nodes);
             }
             if (cum > 0 || more) {
                 bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
@@ -866,11 +886,13 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const unsigned vm = __ballot_sync(FULL, in_chunk);
     if (in_chunk) {
         const unsigned peers = __match_any_sync(vm, bucket);
-        if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
+        if (lane == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
+    }
+    vis_acc += vis_done;
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) vis_done += __shfl_xor_sync(FULL, vis_done, off);
-    if ((threadIdx.x & 31) == 0 && vis_done) atomicAdd(iv.totals + 1, vis_done);
+    for (int off = 16; off > 0; off >>= 1) vis_acc += __shfl_xor_sync(FULL, vis_acc, off);
+    if (lane == 0 && vis_acc) atomicAdd(iv.totals + 1, vis_acc);
 }
 
 // Marching rays of the chunk in descending cost buckets (order inside a
@@ -1699,6 +1721,10 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
+    int trace_per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_intervals_kernel, TRACE_BLOCK, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
+    if (trace_per_sm < 1) trace_per_sm = 1;
     int64_t launches = 0, march_grid = 0;
     for (int64_t r0 = 0; r0 < total_rays; r0 += chunk) {
         F.ray_begin = r0;
@@ -1707,6 +1733,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         char *base = reinterpret_cast<char *>(out->scratch);
         iv.hist = reinterpret_cast<uint32_t *>(base);
         iv.cursor = iv.hist + N_BUCKETS;
+        iv.trace_ctr = iv.cursor + N_BUCKETS;
         iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
         iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
         iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * F.n_rays);
@@ -1714,10 +1741,11 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
-        e = cudaMemsetAsync(iv.hist, 0, 2 * N_BUCKETS * sizeof(uint32_t), st);
+        e = cudaMemsetAsync(iv.hist, 0, (2 * N_BUCKETS + 1) * sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
-        trace_intervals_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
+        const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;
+        trace_intervals_kernel<<<(unsigned)trace_grid, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
         order_rays_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(F, iv);

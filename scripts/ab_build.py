@@ -9,12 +9,8 @@ sys.path.insert(0, str(ROOT))
 from paper_1908_01906_b200 import _build
 
 VARIANTS = {
-    "shadeT": [],
-    "shadeL": [("__shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free",
-                "__shared__ double4 shade[MARCH_BLOCK / G][G];"),
-               ("        shade[j][threadIdx.x / G] = sh;\n        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;\n        __syncwarp();\n\n        // ---- composite the round in sample order (K:285-295)\n",
-                "        shade[threadIdx.x / G][j] = sh;\n        const unsigned fbits = __ballot_sync(FULL, found) >> gbase;\n        __syncwarp();\n\n        // ---- composite the round in sample order (K:285-295)\n"),
-               ("const double4 gg = shade[m][g];", "const double4 gg = shade[g][m];")],
+    "new": [],
+    "head": "git:HEAD",   # render.cu as committed
 }
 
 def build(name, edits):
@@ -22,7 +18,12 @@ def build(name, edits):
     if d.exists():
         shutil.rmtree(d)
     shutil.copytree(_build.CSRC, d)
-    src = (d / "render.cu").read_text()
+    if isinstance(edits, str) and edits.startswith("git:"):
+        src = subprocess.run(["git", "show", edits[4:] + ":paper_1908_01906_b200/csrc/render.cu"],
+                             capture_output=True, text=True, cwd=ROOT, check=True).stdout
+        edits = []
+    else:
+        src = (d / "render.cu").read_text()
     for old, new in edits:
         assert old in src, (name, old)
         src = src.replace(old, new)
