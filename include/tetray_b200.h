@@ -247,7 +247,8 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
 #define TR_FLAG_HIST_SMEM 16   /* ignored (per-partition counts are per-interval global atomics) */
 #define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
-/* flags bits 8-11: log2 of the lanes that march one ray together (0 = 4);
+/* flags bits 8-11: log2 of the lanes that march one ray together (0 = chosen
+ * per ray chunk on the device, 4 or 16, from the rays' sample counts);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
  * per SM (0: 3, 1: 4, 2: 2, 3: 3); bits 14-15: CTAs per SM actually
  * launched (0: as many as fit).  Tuning knobs only:

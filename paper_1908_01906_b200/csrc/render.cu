@@ -70,6 +70,7 @@ enum : int {
     ST_TRACE_MAX_IV,     // most intervals of one ray (max)
     ST_BSP_NODES,        // BSP nodes visited by the trace
     ST_TRACE_MAX_NODES,  // most BSP nodes visited by one ray (max)
+    ST_MAX_RAY_SAMPLES,  // most samples of one ray's stored list (max)
     ST_COUNT
 };
 __device__ unsigned long long g_stats[16];
@@ -685,6 +686,8 @@ struct FrameK {
     int64_t tiles_x, n_tiles, my_tiles;
     int64_t ray_begin, n_rays;   // this chunk: rays [ray_begin, ray_begin + n_rays) in tile order
     int32_t n_parts;
+    int32_t auto_g;              // lanes per ray chosen on the device (march_lane_choice)
+    int64_t march_lanes;         // resident march lanes (CTAs x threads) for that choice
 };
 
 // One stored interval of a ray (16 B): next_interval's clamped entry, the
@@ -704,6 +707,8 @@ struct IvBuf {                   // per-chunk scratch
     uint32_t *order;             // marching rays, most expensive first
     uint32_t *hist, *cursor;     // [N_BUCKETS] each; bucket 0 = nothing to march
     uint32_t *trace_ctr;         // next 32-ray tile of the trace pass
+    unsigned long long *ray_stats;  // [0] sum, [1] max of the rays' stored sample counts
+    uint32_t *gsel;              // lanes per ray chosen for this chunk (auto mode)
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
 };
 
@@ -792,14 +797,15 @@ __global__ void __launch_bounds__(TRACE_BLOCK)
 trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const int lane = threadIdx.x & 31;
     const uint32_t n_tiles = (uint32_t)((F.n_rays + 31) / 32);
-    unsigned long long vis_acc = 0;
+    unsigned long long vis_acc = 0, cost_sum = 0;
+    uint32_t cost_max = 0;
     while (true) {
     uint32_t tile = 0;
     if (lane == 0) tile = atomicAdd(iv.trace_ctr, 1u);
     tile = __shfl_sync(FULL, tile, 0);
     if (tile >= n_tiles) break;
     const int64_t rr = (int64_t)tile * 32 + lane;
-    uint32_t n = 0, bucket = 0;
+    uint32_t n = 0, bucket = 0, ray_cost = 0;
     unsigned long long vis_done = 0;
     const bool in_chunk = rr < F.n_rays;
     if (in_chunk) {
@@ -870,6 +876,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 atomicAdd(&g_stats[ST_BSP_CELLS], (unsigned long long)bsp_cells);
                 atomicAdd(&g_stats[ST_BSP_NODES], (unsigned long long)bsp_nodes);
                 atomicMax(&g_stats[ST_TRACE_MAX_NODES], (unsigned long long)bsp_nodes);
+                atomicMax(&g_stats[ST_MAX_RAY_SAMPLES], (unsigned long long)cum);
             }
             if (cum > 0 || more) {
                 bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
@@ -879,6 +886,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 vis_done = n;
             }
             iv.cnt[rr] = n | (bucket << 16) | (more ? CNT_MORE : 0u);
+            ray_cost = cum + (more ? 1024u : 0u);
         } else {
             iv.cnt[rr] = 0;
         }
@@ -889,10 +897,20 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (lane == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
     }
     vis_acc += vis_done;
+    cost_sum += ray_cost;
+    cost_max = ray_cost > cost_max ? ray_cost : cost_max;
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) vis_acc += __shfl_xor_sync(FULL, vis_acc, off);
+    for (int off = 16; off > 0; off >>= 1) {
+        vis_acc += __shfl_xor_sync(FULL, vis_acc, off);
+        cost_sum += __shfl_xor_sync(FULL, cost_sum, off);
+        cost_max = max(cost_max, __shfl_xor_sync(FULL, cost_max, off));
+    }
     if (lane == 0 && vis_acc) atomicAdd(iv.totals + 1, vis_acc);
+    if (lane == 0 && cost_sum) {
+        atomicAdd(iv.ray_stats, cost_sum);
+        atomicMax(iv.ray_stats + 1, (unsigned long long)cost_max);
+    }
 }
 
 // Marching rays of the chunk in descending cost buckets (order inside a
@@ -900,6 +918,14 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
 __global__ void __launch_bounds__(TRACE_BLOCK)
 order_rays_kernel(FrameK F, IvBuf iv) {
     __shared__ uint32_t start[N_BUCKETS];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        // lanes per ray: 4, unless the longest ray's rounds at 4 lanes
+        // (max / 4) exceed the average lane's share of the work (sum /
+        // resident lanes) -- then 16, so long rays stop setting the frame
+        // time (1e9-tet scenes: up to 3,600 samples on one ray)
+        const unsigned long long sum = iv.ray_stats[0], mx = iv.ray_stats[1];
+        *iv.gsel = (mx * (unsigned long long)F.march_lanes <= 4ull * sum) ? 4u : 16u;
+    }
     if (threadIdx.x < N_BUCKETS) {
         uint32_t s = 0;
         for (int b = N_BUCKETS - 1; b > (int)threadIdx.x; --b) s += iv.hist[b];
@@ -1296,6 +1322,7 @@ template <int G, int MINB>
 __global__ void __launch_bounds__(MARCH_BLOCK, MINB)
 march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
+    if (F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
     constexpr int NG = MARCH_BLOCK / G;
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
     __shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free
@@ -1721,6 +1748,8 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
+    F.auto_g = (lg == 0 && !(frame->flags & TR_FLAG_REG_STATE) && minb == 3) ? 1 : 0;
+    F.march_lanes = (int64_t)sm_count() * per_sm * MARCH_BLOCK;
     int trace_per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_intervals_kernel, TRACE_BLOCK, 0);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
@@ -1734,6 +1763,8 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.hist = reinterpret_cast<uint32_t *>(base);
         iv.cursor = iv.hist + N_BUCKETS;
         iv.trace_ctr = iv.cursor + N_BUCKETS;
+        iv.ray_stats = reinterpret_cast<unsigned long long *>(base + 528);
+        iv.gsel = reinterpret_cast<uint32_t *>(base + 544);
         iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
         iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
         iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * F.n_rays);
@@ -1741,7 +1772,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
-        e = cudaMemsetAsync(iv.hist, 0, (2 * N_BUCKETS + 1) * sizeof(uint32_t), st);
+        e = cudaMemsetAsync(iv.hist, 0, 552, st);   // hist, cursor, trace_ctr, ray_stats, gsel
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
         const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;
@@ -1752,19 +1783,31 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "order_rays_kernel launch");
         launches += 2;
-        int64_t grid = (int64_t)sm_count() * per_sm;
-        const int64_t need = (F.n_rays * gsize + MARCH_BLOCK - 1) / MARCH_BLOCK;
-        if (grid > need) grid = need;
-        if (grid < 1) grid = 1;
         if (out->ev_march_begin && r0 == 0) {
             e = cudaEventRecord((cudaEvent_t)out->ev_march_begin, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(begin)");
         }
-        march_fn<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
-        e = cudaGetLastError();
-        if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
-        ++launches;
-        march_grid = grid;
+        // auto width: the G = 4 and 16 kernels are both launched and the one
+        // order_rays_kernel did not choose returns at once
+        void (*fns[2])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_fn, nullptr};
+        int gs[2] = {gsize, 0};
+        int nf = 1;
+        if (F.auto_g) {
+            fns[1] = march_sm_kernel<16, 3>;
+            gs[1] = 16;
+            nf = 2;
+        }
+        for (int q = 0; q < nf; ++q) {
+            int64_t grid = (int64_t)sm_count() * per_sm;
+            const int64_t need = (F.n_rays * gs[q] + MARCH_BLOCK - 1) / MARCH_BLOCK;
+            if (grid > need) grid = need;
+            if (grid < 1) grid = 1;
+            fns[q]<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
+            e = cudaGetLastError();
+            if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
+            ++launches;
+            if (q == 0) march_grid = grid;
+        }
         if (out->ev_march_end && r0 + chunk >= total_rays) {
             e = cudaEventRecord((cudaEvent_t)out->ev_march_end, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(end)");

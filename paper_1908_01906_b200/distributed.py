@@ -118,11 +118,15 @@ class ShardedFrame:
             self.local = None
 
     def launches_per_step(self) -> int:
-        """Our kernels per frame: trace + order + march per ray chunk, plus
-        the tile scatter when sharded."""
-        n = self.w * self.h if not self.compact else self.slots * TILE_PIXELS
-        chunks = max(1, -(-n // (1 << 20)))
-        return 3 * chunks + (1 if self.compact else 0)
+        """Our kernels per frame as the library counted them in the last
+        tr_render_frame (trace + order + march launches per ray chunk; the
+        auto lane width launches two march kernels, one returns at once),
+        plus the tile scatter when sharded."""
+        import ctypes as C
+        import numpy as np
+        out = np.zeros(3, np.int64)
+        _lib.check(_lib.lib().tr_last_launch(_lib.ptr(out, C.c_int64)), "tr_last_launch")
+        return int(out[0]) + (1 if self.compact else 0)
 
     def run(self, stream, kernel_events=None, march_events=None):
         """One frame.  kernel_events brackets the whole render call (trace +
