@@ -235,19 +235,12 @@ struct SceneK {  // kernel copy of TrDeviceScene
 
 // Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
 // ascending id order, so the first one containing q is the lowest index.
-// The next record's loads are issued before the current one is tested.
+// One record at a time (the fewest record loads).
 __device__ __forceinline__ uint32_t scan_leaf_first(const SceneK &S, uint32_t start,
                                                     uint32_t count, const PQuery &q, double l[4]) {
-    if (count == 0) return UINT32_MAX;
-    const uint32_t end = start + count;
-    RecM cur = load_recm(S.tets, start);
-    for (uint32_t k = start;; ++k) {
-        const bool has_next = k + 1 < end;
-        const RecM nxt = load_recm(S.tets, has_next ? k + 1 : k);
-        if (bary_of(cur, q, l)) return k;
-        if (!has_next) return UINT32_MAX;
-        cur = nxt;
-    }
+    for (uint32_t k = start; k < start + count; ++k)
+        if (bary_of(load_recm(S.tets, k), q, l)) return k;
+    return UINT32_MAX;
 }
 
 // Pairwise variant: two records in flight per step, tested in order.
@@ -1004,7 +997,7 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
                                                 double ox, double oy, double oz, double dx,
                                                 double dy, double dz, double a, int64_t k,
                                                 double phase, int32_t pid, bool stats,
-                                                bool seq_scan, bool use_grid, bool &found) {
+                                                bool pair_scan, bool use_grid, bool &found) {
     double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
     found = false;
     double step = fr.s1, e = 1.0;
@@ -1025,8 +1018,8 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
             LeafHint hh;
             load_leaf(S.pgrid_leaf + gc, hh);
             if (strictly_in(q, hh.lo, hh.hi)) {
-                pos = seq_scan ? scan_leaf_first(S, hh.start, hh.count, q, l)
-                               : scan_leaf_pairs(S, hh.start, hh.count, q, l);
+                pos = pair_scan ? scan_leaf_pairs(S, hh.start, hh.count, q, l)
+                                : scan_leaf_first(S, hh.start, hh.count, q, l);
                 located = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
@@ -1089,7 +1082,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     // false instance: measured 25% faster than a compile-time false (the
     // atomics' guards change how the hot loop is scheduled; build/ab A/B).
     const bool stats = STATS || (fr.flags & TR_FLAG_STATS) != 0;
-    const bool seq_scan = (fr.flags & TR_FLAG_SEQ_SCAN) != 0;
+    const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
     const unsigned gmask = (G == 32) ? FULL : (((1u << G) - 1u) << gbase);
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
@@ -1201,7 +1194,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
         bool found = false;
         if (has)
-            sh = shade_sample(S, E, fr, ox, oy, oz, dx, dy, dz, a, k, phase, pid, stats, seq_scan,
+            sh = shade_sample(S, E, fr, ox, oy, oz, dx, dy, dz, a, k, phase, pid, stats, pair_scan,
                               use_grid, found);
         shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
@@ -1340,7 +1333,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const bool track = fr.track_ppart && fr.mode != 0;
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
     const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
-    const bool seq_scan = (fr.flags & TR_FLAG_SEQ_SCAN) != 0;
+    const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
@@ -1439,7 +1432,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         bool found = false;
         if (has)
             sh = shade_sample(S, E, fr, s_o[0][g], s_o[1][g], s_o[2][g], s_d[0][g], s_d[1][g],
-                              s_d[2][g], a, k, s_phase[g], pid, stats, seq_scan, use_grid, found);
+                              s_d[2][g], a, k, s_phase[g], pid, stats, pair_scan, use_grid, found);
         shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();

@@ -82,7 +82,7 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     for mode in modes:
         ref = orc.render(cam, mode, par, jitter=jitter)
-        # default; no grid, no BSP, sequential leaf scan; register-state
+        # default; no grid, no BSP, pairwise leaf scan; register-state
         # kernel (0x80); lane groups of 2 / 8 / 16 (32 with 0x80); register
         # budgets of 4 / 2 / 3 CTAs per SM -- every variant renders the same frame
         for flags in (0, 2, 8, 0x40, 0x80, 0x100, 0x300, 0x400, 0x580, 0x1000, 0x2000, 0x3000):
