@@ -242,6 +242,7 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
 #define TR_FLAG_PAIR_SCAN 64   /* leaf scan two records at a time (tuning; default: one at a time) */
 #define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
+#define TR_FLAG_TILE_TIMING 0x10000 /* trace pass: SM cycles per 32-ray tile into the kernel stats (profiling) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
@@ -326,9 +327,12 @@ int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t shard_count);
  * [0] kernels launched, [1] grid blocks, [2] threads per block. */
 int tr_last_launch(int64_t *out3);
 
-/* Kernel event counters accumulated by frames rendered with TR_FLAG_STATS
- * (rounds, partial rounds, lane samples, found, grid hits, descents, inline
- * next_interval, pow calls, trace intervals, trace rays).  Synchronizes. */
+/* Kernel event counters (up to 32) accumulated by frames rendered with
+ * TR_FLAG_STATS: rounds, partial rounds, lane samples, found, grid hits,
+ * descents, inline next_interval, pow calls, trace intervals, trace rays, BSP
+ * overflows, BSP cells, max intervals per ray, BSP nodes, max nodes per ray,
+ * max samples per ray; with TR_FLAG_TILE_TIMING the trace's cycles per
+ * 32-ray tile (sum, max).  Names: _lib.STAT_NAMES.  Synchronizes. */
 int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset);
 
 const char *tr_last_error(void);

@@ -71,9 +71,11 @@ enum : int {
     ST_BSP_NODES,        // BSP nodes visited by the trace
     ST_TRACE_MAX_NODES,  // most BSP nodes visited by one ray (max)
     ST_MAX_RAY_SAMPLES,  // most samples of one ray's stored list (max)
+    ST_TILE_CYCLES,      // trace: SM cycles summed over 32-ray tiles (TR_FLAG_TILE_TIMING)
+    ST_TILE_MAX_CYCLES,  // trace: most cycles of one tile (max)
     ST_COUNT
 };
-__device__ unsigned long long g_stats[16];
+__device__ unsigned long long g_stats[32];
 
 struct RayD {
     double ox, oy, oz, dx, dy, dz;
@@ -797,6 +799,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     if (lane == 0) tile = atomicAdd(iv.trace_ctr, 1u);
     tile = __shfl_sync(FULL, tile, 0);
     if (tile >= n_tiles) break;
+    const long long tile_t0 = clock64();
     const int64_t rr = (int64_t)tile * 32 + lane;
     uint32_t n = 0, bucket = 0, ray_cost = 0;
     unsigned long long vis_done = 0;
@@ -888,6 +891,11 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     if (in_chunk) {
         const unsigned peers = __match_any_sync(vm, bucket);
         if (lane == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
+    }
+    if ((F.f.flags & TR_FLAG_TILE_TIMING) && lane == 0) {
+        const unsigned long long dt = (unsigned long long)(clock64() - tile_t0);
+        atomicAdd(&g_stats[ST_TILE_CYCLES], dt);
+        atomicMax(&g_stats[ST_TILE_MAX_CYCLES], dt);
     }
     vis_acc += vis_done;
     cost_sum += ray_cost;
@@ -1848,14 +1856,14 @@ int tr_scatter_tiles(int64_t width, int64_t height, int32_t count, const double 
 }
 
 int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset) {
-    unsigned long long h[16];
+    unsigned long long h[32];
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats sync");
     e = cudaMemcpyFromSymbol(h, g_stats, sizeof h);
     if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats copy");
-    for (int i = 0; i < n && i < 16; ++i) out[i] = (int64_t)h[i];
+    for (int i = 0; i < n && i < 32; ++i) out[i] = (int64_t)h[i];
     if (reset) {
-        for (int i = 0; i < 16; ++i) h[i] = 0;
+        for (int i = 0; i < 32; ++i) h[i] = 0;
         e = cudaMemcpyToSymbol(g_stats, h, sizeof h);
         if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats reset");
     }
