@@ -9,8 +9,7 @@ sys.path.insert(0, str(ROOT))
 from paper_1908_01906_b200 import _build
 
 VARIANTS = {
-    "fsm": [],
-    "head": "git:HEAD",   # render.cu as committed
+    "hint": [],
 }
 
 def build(name, edits):

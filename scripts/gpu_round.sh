@@ -14,11 +14,11 @@ for m in reference skip; do
 done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv \
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:march -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 6 -c 2 \
   -o gpurun_out/prof_march_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:trace -s 3 -c 1 \
   -o gpurun_out/prof_trace_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:march -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 2 -c 2 \
   -o gpurun_out/prof_march272_$TAG python bench.py --scene radial272 --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 300 python scripts/gpu_stats.py > gpurun_out/stats_$TAG.log 2>&1
 timeout 300 python scripts/e2e_breakdown.py > gpurun_out/e2e_$TAG.log 2>&1
