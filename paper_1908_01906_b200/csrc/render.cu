@@ -565,6 +565,9 @@ __device__ __forceinline__ void bsp_begin(const SceneK &S, const RayD &ray, BspT
 }
 
 // Pop subtrees until one leaf cell has been enumerated into the buffer.
+// COUNT: node / cell statistics (TR_FLAG_STATS builds only: T is in local
+// memory, so each counter update is a local load and store).
+template <bool COUNT>
 __device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD &ray, BspTrace &T) {
     while (T.sp > 0) {
         --T.sp;
@@ -573,12 +576,12 @@ __device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD 
         bool leaf_done = false;
         while (true) {
             if (tf <= 0.0) break;                         // behind the origin: exits <= 0
-            ++T.nodes;
+            if (COUNT) ++T.nodes;
             const TrKNode *N = S.knodes + node;
             const int32_t info = __ldg(&N->info);   // issued with the activity byte
             if (E.knode_active && !__ldg(E.knode_active + node)) break;
             if (info < 0) {                                // leaf cell: its partitions
-                ++T.cells;
+                if (COUNT) ++T.cells;
                 const int32_t st = ~info, cnt = __ldg(&N->aux);
                 for (int32_t k = 0; k < cnt; ++k) {
                     const int32_t pid = __ldg(S.kleaf_pids + st + k);
@@ -623,6 +626,7 @@ __device__ void bsp_enumerate_next(const SceneK &S, const EpochK &E, const RayD 
 }
 
 // next_interval (K:173-230) from the BSP state; -1 when the ray is done.
+template <bool COUNT>
 __device__ int32_t bsp_next_interval(const SceneK &S, const EpochK &E, const RayD &ray,
                                      BspTrace &T, double t_min, double excl, int32_t last,
                                      double &ra, double &rb) {
@@ -648,7 +652,7 @@ __device__ int32_t bsp_next_interval(const SceneK &S, const EpochK &E, const Ray
             ra = best_a; rb = best_b;
             return best;
         }
-        bsp_enumerate_next(S, E, ray, T);
+        bsp_enumerate_next<COUNT>(S, E, ray, T);
         if (T.overflow) return -1;
     }
 }
@@ -788,6 +792,7 @@ __device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &
 // Persistent warps: each warp takes the next 32-ray tile from a counter, so
 // the long rays' tiles do not leave a wave tail (the grid is sized to the
 // resident warps).
+template <bool COUNT>
 __global__ void __launch_bounds__(TRACE_BLOCK)
 trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const int lane = threadIdx.x & 31;
@@ -840,7 +845,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         const double excl = (last < 0) ? 0.0 : F.f.eps;
                         double a, b;
                         const int32_t pid = use_bsp
-                            ? bsp_next_interval(S, E, ray, T, t_min, excl, last, a, b)
+                            ? bsp_next_interval<COUNT>(S, E, ray, T, t_min, excl, last, a, b)
                             : next_interval(S, E, ray, t_min, excl, last, a, b);
                         if (pid < 0) break;
                         if (n == IV_CAP) { more = true; break; }
@@ -864,7 +869,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 }
             }
             if (more) iv.tail[rr] = t_min;
-            if (F.f.flags & TR_FLAG_STATS) {
+            if (COUNT) {
                 atomicAdd(&g_stats[ST_TRACE_RAYS], 1ull);
                 atomicAdd(&g_stats[ST_TRACE_IV], (unsigned long long)n);
                 atomicMax(&g_stats[ST_TRACE_MAX_IV], (unsigned long long)n);
@@ -1752,7 +1757,9 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     F.auto_g = (lg == 0 && !(frame->flags & TR_FLAG_REG_STATE) && minb == 3) ? 1 : 0;
     F.march_lanes = (int64_t)sm_count() * per_sm * MARCH_BLOCK;
     int trace_per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_intervals_kernel, TRACE_BLOCK, 0);
+    void (*trace_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) =
+        (frame->flags & TR_FLAG_STATS) ? trace_intervals_kernel<true> : trace_intervals_kernel<false>;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_fn, TRACE_BLOCK, 0);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
     if (trace_per_sm < 1) trace_per_sm = 1;
     int64_t launches = 0, march_grid = 0;
@@ -1777,7 +1784,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
         const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;
-        trace_intervals_kernel<<<(unsigned)trace_grid, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
+        trace_fn<<<(unsigned)trace_grid, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
         order_rays_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(F, iv);

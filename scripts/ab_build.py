@@ -9,7 +9,9 @@ sys.path.insert(0, str(ROOT))
 from paper_1908_01906_b200 import _build
 
 VARIANTS = {
-    "hint": [],
+    "count": [],
+    "k16b8": [("constexpr int KBUF = 16;", "constexpr int KBUF = 8;"), ("constexpr int KSTACK = 32;", "constexpr int KSTACK = 16;")],
+    "head": "git:HEAD",
 }
 
 def build(name, edits):
