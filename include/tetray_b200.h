@@ -120,6 +120,22 @@ int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *
 int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
                  int32_t *cells);
 
+/* Mean fraction of a grid cell covered by its candidate leaf's exclusive box
+ * (1 for the generator's regular meshes; low for unstructured meshes). */
+double tr_pbvh_coverage(const TrHostBuf *b);
+/* Cell candidate lists (the exact point-location path for unstructured
+ * meshes): a grid refined `refine` times per axis over the point BVH's grid;
+ * cell c lists the records (leaf order) whose padded tet boxes (box_lo/hi,
+ * by tet id) meet it, in ascending tet id; off[c] bit 31 marks cells over
+ * max_list entries (BVH descent there).  tbox: 8 floats per record = its
+ * padded box rounded outward (lo xyz, hi xyz, 2 pad). */
+int tr_cells_build(const TrHostBuf *pbvh, const double *box_lo, const double *box_hi,
+                   int32_t refine, int32_t max_list, TrHostBuf **out);
+/* sizes: [0] cells, [1] list entries, [2] records */
+int tr_cells_sizes(const TrHostBuf *cells, int64_t *sizes3);
+int tr_cells_copy(const TrHostBuf *cells, int32_t *dims3, double *org3, double *scale3,
+                  uint32_t *off, uint32_t *recs, float *tbox);
+
 /* Partition BVH (replaces traversal.build_partition_bvh, traversal.py:82-91). */
 int tr_bbvh_build(int64_t n_parts, const double *lo, const double *hi, TrHostBuf **out);
 int tr_bbvh_sizes(const TrHostBuf *b, int64_t *n_nodes);
@@ -209,6 +225,13 @@ typedef struct TrDeviceScene {
     const int32_t *kleaf_pids;
     int64_t n_knodes;
     double kroot[6];
+    /* cell candidate lists (tr_cells_*; NULL: none -- BVH descent instead) */
+    const uint32_t *cell_off;
+    const uint32_t *cell_recs;
+    const float *tbox;
+    int32_t cdim[3];
+    int32_t cells_first;   /* 1: skip the exclusive-leaf grid (it rarely proves a point) */
+    double corg[3], cscale[3];
 } TrDeviceScene;
 
 /* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
@@ -243,6 +266,7 @@ typedef struct TrFrame {
 #define TR_FLAG_PAIR_SCAN 64   /* leaf scan two records at a time (tuning; default: one at a time) */
 #define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
 #define TR_FLAG_TILE_TIMING 0x10000 /* trace pass: SM cycles per 32-ray tile into the kernel stats (profiling) */
+#define TR_FLAG_NO_CELLS 0x20000 /* ignore the cell candidate lists: BVH descent instead (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */

@@ -38,6 +38,9 @@ class TrDeviceScene(C.Structure):
         ("gorg", C.c_double * 3), ("gscale", C.c_double * 3),
         ("knodes", C.c_void_p), ("kleaf_pids", C.c_void_p), ("n_knodes", C.c_int64),
         ("kroot", C.c_double * 6),
+        ("cell_off", C.c_void_p), ("cell_recs", C.c_void_p), ("tbox", C.c_void_p),
+        ("cdim", C.c_int32 * 3), ("cells_first", C.c_int32),
+        ("corg", C.c_double * 3), ("cscale", C.c_double * 3),
     ]
 
 
@@ -103,6 +106,12 @@ _SIGNATURES = [
     ("tr_pbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_pbvh_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_pbvh_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p]),
+    ("tr_pbvh_coverage", C.c_double, [C.c_void_p]),
+    ("tr_cells_build", C.c_int, [C.c_void_p, c_f64p, c_f64p, C.c_int32, C.c_int32,
+                                 C.POINTER(C.c_void_p)]),
+    ("tr_cells_sizes", C.c_int, [C.c_void_p, c_i64p]),
+    ("tr_cells_copy", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
     ("tr_bbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.POINTER(C.c_void_p)]),
     ("tr_bbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_bbvh_copy", C.c_int, [C.c_void_p, C.c_void_p]),

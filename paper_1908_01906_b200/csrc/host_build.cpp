@@ -248,6 +248,7 @@ struct PBuf : TrHostBuf {
     std::vector<int32_t> grid;
     int32_t gdim[3] = {1, 1, 1};
     double gorg[3] = {0, 0, 0}, gscale[3] = {1, 1, 1};
+    double coverage = 0.0;   // mean fraction of a cell covered by its candidate's exclusive box
 };
 
 constexpr int32_t CHILD_NONE = INT32_MIN;
@@ -520,7 +521,29 @@ void p_build_grid(PBuf &O) {
                     if (ov > best[ci]) { best[ci] = ov; O.grid[ci] = (int32_t)L; }
                 }
     }
+    double cell_vol = 1.0, cov = 0.0;
+    for (int a = 0; a < 3; ++a) cell_vol /= O.gscale[a];
+    for (double b : best) cov += std::min(b / cell_vol, 1.0);
+    O.coverage = cells > 0 ? cov / (double)cells : 0.0;
 }
+
+// ------------------------------------------------ cell candidate lists
+// For meshes whose leaves do not line up with the grid (unstructured tets:
+// leaf boxes overlap, exclusive boxes shrink), the exact fallback per point
+// is a finer uniform grid whose cell lists EVERY record whose padded tet box
+// (mesh.py:248-250) meets the cell, in ascending tet id: a point's lowest-id
+// containing tet is the first accepting entry (the padded box of a tet that
+// accepts the point contains it, K:100-101).  Cell ranges use the kernel's
+// own expression floor((x - org) * scale) on the box corners, which is
+// monotone, so the lists are conservative.  Cells above max_list entries
+// are marked (offset high bit) and the kernel uses the BVH descent there.
+struct CBuf : TrHostBuf {
+    int32_t dim[3] = {1, 1, 1};
+    double org[3] = {0, 0, 0}, scale[3] = {1, 1, 1};
+    std::vector<uint32_t> off;    // n_cells + 1; bit 31 of off[c]: overflowed cell
+    std::vector<uint32_t> recs;   // record positions
+    std::vector<float> tbox;      // 8 floats per record: padded box rounded outward, pad
+};
 
 // ============================================================ partition BVH
 struct BBuf : TrHostBuf {
@@ -810,6 +833,112 @@ int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, in
     } catch (const std::bad_alloc &) {
         return tr_fail(TR_ENOMEM, "tr_pbvh_build: out of host memory");
     }
+}
+
+double tr_pbvh_coverage(const TrHostBuf *b) {
+    auto P = dynamic_cast<const PBuf *>(b);
+    return P ? P->coverage : 0.0;
+}
+
+int tr_cells_build(const TrHostBuf *b, const double *box_lo, const double *box_hi, int32_t refine,
+                   int32_t max_list, TrHostBuf **out) {
+    auto P = dynamic_cast<const PBuf *>(b);
+    if (!P || !box_lo || !box_hi || !out || refine < 1 || refine > 8 || max_list < 1)
+        return tr_fail(TR_EINVAL, "tr_cells_build: invalid arguments");
+    try {
+        CBuf *Cb = new CBuf();
+        int64_t n_cells = 1;
+        for (int a = 0; a < 3; ++a) {
+            Cb->dim[a] = (int32_t)std::min<int64_t>((int64_t)P->gdim[a] * refine, 4096);
+            Cb->org[a] = P->gorg[a];
+            Cb->scale[a] = P->gscale[a] * (double)Cb->dim[a] / (double)P->gdim[a];
+            n_cells *= Cb->dim[a];
+        }
+        const int64_t nrec = (int64_t)P->ids.size();
+        auto crange = [&](const double *lo, const double *hi, int64_t c0[3], int64_t c1[3]) {
+            for (int a = 0; a < 3; ++a) {
+                const double f0 = (lo[a] - Cb->org[a]) * Cb->scale[a], f1 = (hi[a] - Cb->org[a]) * Cb->scale[a];
+                c0[a] = std::min<int64_t>(std::max<int64_t>((int64_t)std::floor(f0), 0), Cb->dim[a] - 1);
+                c1[a] = std::min<int64_t>(std::max<int64_t>((int64_t)std::floor(f1), 0), Cb->dim[a] - 1);
+            }
+        };
+        std::vector<uint32_t> cnt((size_t)n_cells, 0u);
+        for (int64_t k = 0; k < nrec; ++k) {   // pass 1: counts
+            const uint32_t t = P->ids[k];
+            int64_t c0[3], c1[3];
+            crange(box_lo + 3 * (size_t)t, box_hi + 3 * (size_t)t, c0, c1);
+            for (int64_t x = c0[0]; x <= c1[0]; ++x)
+                for (int64_t y = c0[1]; y <= c1[1]; ++y)
+                    for (int64_t z = c0[2]; z <= c1[2]; ++z)
+                        ++cnt[(size_t)((x * Cb->dim[1] + y) * Cb->dim[2] + z)];
+        }
+        Cb->off.assign((size_t)n_cells + 1, 0u);
+        uint64_t total = 0;
+        for (int64_t c = 0; c < n_cells; ++c) {
+            Cb->off[c] = (uint32_t)total;
+            if (cnt[c] <= (uint32_t)max_list) total += cnt[c];
+            if (total >= 0x7fffffffull) { delete Cb; return tr_fail(TR_ENOMEM, "tr_cells_build: lists too large"); }
+        }
+        Cb->off[n_cells] = (uint32_t)total;
+        Cb->recs.assign((size_t)total, 0u);
+        std::vector<uint32_t> fill((size_t)n_cells, 0u);
+        for (int64_t k = 0; k < nrec; ++k) {   // pass 2: fill in record order
+            const uint32_t t = P->ids[k];
+            int64_t c0[3], c1[3];
+            crange(box_lo + 3 * (size_t)t, box_hi + 3 * (size_t)t, c0, c1);
+            for (int64_t x = c0[0]; x <= c1[0]; ++x)
+                for (int64_t y = c0[1]; y <= c1[1]; ++y)
+                    for (int64_t z = c0[2]; z <= c1[2]; ++z) {
+                        const size_t c = (size_t)((x * Cb->dim[1] + y) * Cb->dim[2] + z);
+                        if (cnt[c] <= (uint32_t)max_list) Cb->recs[Cb->off[c] + fill[c]++] = (uint32_t)k;
+                    }
+        }
+#pragma omp parallel for schedule(dynamic, 1024)
+        for (int64_t c = 0; c < n_cells; ++c) {   // ascending tet id within each cell
+            if (cnt[c] > (uint32_t)max_list) continue;
+            std::sort(Cb->recs.begin() + Cb->off[c], Cb->recs.begin() + Cb->off[c] + cnt[c],
+                      [&](uint32_t x, uint32_t y) { return P->ids[x] < P->ids[y]; });
+        }
+        for (int64_t c = 0; c < n_cells; ++c)
+            if (cnt[c] > (uint32_t)max_list) Cb->off[c] |= 0x80000000u;
+        Cb->tbox.assign((size_t)nrec * 8, 0.0f);
+#pragma omp parallel for schedule(static)
+        for (int64_t k = 0; k < nrec; ++k) {
+            const uint32_t t = P->ids[k];
+            for (int a = 0; a < 3; ++a) {
+                Cb->tbox[8 * (size_t)k + a] = f32_down(box_lo[3 * (size_t)t + a]);
+                Cb->tbox[8 * (size_t)k + 3 + a] = f32_up(box_hi[3 * (size_t)t + a]);
+            }
+        }
+        *out = Cb;
+        return TR_OK;
+    } catch (const std::bad_alloc &) {
+        return tr_fail(TR_ENOMEM, "tr_cells_build: out of host memory");
+    }
+}
+
+int tr_cells_sizes(const TrHostBuf *b, int64_t *sizes3) {
+    auto Cb = dynamic_cast<const CBuf *>(b);
+    if (!Cb || !sizes3) return tr_fail(TR_EINVAL, "tr_cells_sizes: not a cell list");
+    sizes3[0] = (int64_t)Cb->off.size() - 1;
+    sizes3[1] = (int64_t)Cb->recs.size();
+    sizes3[2] = (int64_t)Cb->tbox.size() / 8;
+    return TR_OK;
+}
+
+int tr_cells_copy(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3, uint32_t *off,
+                  uint32_t *recs, float *tbox) {
+    auto Cb = dynamic_cast<const CBuf *>(b);
+    if (!Cb) return tr_fail(TR_EINVAL, "tr_cells_copy: not a cell list");
+    for (int a = 0; a < 3; ++a) {
+        if (dims3) dims3[a] = Cb->dim[a];
+        if (org3) org3[a] = Cb->org[a];
+        if (scale3) scale3[a] = Cb->scale[a];
+    }
+    if (off) std::memcpy(off, Cb->off.data(), Cb->off.size() * sizeof(uint32_t));
+    if (recs && !Cb->recs.empty()) std::memcpy(recs, Cb->recs.data(), Cb->recs.size() * sizeof(uint32_t));
+    if (tbox && !Cb->tbox.empty()) std::memcpy(tbox, Cb->tbox.data(), Cb->tbox.size() * sizeof(float));
+    return TR_OK;
 }
 
 int tr_pbvh_sizes(const TrHostBuf *b, int64_t *s) {

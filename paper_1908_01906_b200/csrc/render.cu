@@ -233,6 +233,12 @@ struct SceneK {  // kernel copy of TrDeviceScene
     int32_t centering;
     double gorg[3], gscale[3];
     double mesh_lo[3], mesh_hi[3];
+    const uint32_t *__restrict__ cell_off;  // cell candidate lists (NULL: none)
+    const uint32_t *__restrict__ cell_recs;
+    const float4 *__restrict__ tbox;        // per record: padded box (2 x float4)
+    int32_t cdim[3];
+    int32_t cells_first;
+    double corg[3], cscale[3];
 };
 
 // Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
@@ -330,6 +336,36 @@ __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], i
     return best_pos;
 }
 
+// Cell candidate lists (tr_cells_build; unstructured meshes): the cell's
+// records are every tet whose padded box meets the cell, in ascending id, so
+// the first one whose box holds q and which accepts q is the lowest-index
+// containing tet (K:93-136).  Outside the cell grid no padded box can hold q.
+// Returns false when the cell overflowed (the caller runs the BVH descent).
+__device__ __forceinline__ bool locate_cells(const SceneK &S, const PQuery &q, double l[4],
+                                             uint32_t &pos) {
+    pos = UINT32_MAX;
+    int64_t c[3];
+    const double qv[3] = {q.x, q.y, q.z};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double f = (qv[a] - S.corg[a]) * S.cscale[a];   // the builder's expression
+        const double dim = (double)S.cdim[a];
+        if (!(f >= 0.0) || f >= dim * (1.0 + 1e-12)) return true;   // outside every padded box
+        const int64_t ci = (int64_t)f;
+        c[a] = ci < S.cdim[a] ? ci : S.cdim[a] - 1;
+    }
+    const int64_t cell = (c[0] * S.cdim[1] + c[1]) * S.cdim[2] + c[2];
+    const uint32_t o0 = __ldg(S.cell_off + cell), o1 = __ldg(S.cell_off + cell + 1) & 0x7fffffffu;
+    if (o0 & 0x80000000u) return false;
+    for (uint32_t k = o0; k < o1; ++k) {
+        const uint32_t r = __ldg(S.cell_recs + k);
+        const float4 b0 = __ldg(S.tbox + 2 * r), b1 = __ldg(S.tbox + 2 * r + 1);
+        if (!in_box(q, b0.x, b0.y, b0.z, b0.w, b1.x, b1.y)) continue;
+        if (bary_test(S.tets, r, q, l)) { pos = r; return true; }
+    }
+    return true;
+}
+
 struct LeafHint {  // the ray's current leaf: exclusive box + record range, in registers
     float lo[3], hi[3];
     uint32_t start, count;
@@ -402,6 +438,7 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
             }
         }
     }
+    if (!done && use_grid && S.cell_off) done = locate_cells(S, q, l, pos);
     if (!done) {
         int32_t leaf;
         if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
@@ -1010,7 +1047,8 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
                                                 double ox, double oy, double oz, double dx,
                                                 double dy, double dz, double a, int64_t k,
                                                 double phase, int32_t pid, bool stats,
-                                                bool pair_scan, bool use_grid, bool &found) {
+                                                bool pair_scan, bool use_grid, bool use_cells,
+                                                bool &found) {
     double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
     found = false;
     double step = fr.s1, e = 1.0;
@@ -1025,7 +1063,7 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
     double l[4];
     uint32_t pos = UINT32_MAX;
     bool located = false;
-    if (use_grid) {
+    if (use_grid && !(use_cells && S.cells_first)) {
         const int64_t gc = grid_cell(S, q);
         if (gc >= 0) {
             LeafHint hh;
@@ -1038,6 +1076,7 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
             }
         }
     }
+    if (!located && use_cells) located = locate_cells(S, q, l, pos);
     if (!located) {
         int32_t leaf;
         if (stats) atomicAdd(&g_stats[ST_DESCENT], 1ull);
@@ -1091,6 +1130,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     Inline &L = inl[threadIdx.x / G];
     const bool track = fr.track_ppart && fr.mode != 0;
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
+    const bool use_cells = S.cell_off != nullptr && !(fr.flags & TR_FLAG_NO_CELLS);
     // TR_FLAG_STATS event counters.  Kept a runtime test even in the STATS =
     // false instance: measured 25% faster than a compile-time false (the
     // atomics' guards change how the hot loop is scheduled; build/ab A/B).
@@ -1208,7 +1248,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         bool found = false;
         if (has)
             sh = shade_sample(S, E, fr, ox, oy, oz, dx, dy, dz, a, k, phase, pid, stats, pair_scan,
-                              use_grid, found);
+                              use_grid, use_cells, found);
         shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
@@ -1345,6 +1385,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     Inline &L = inl[g];
     const bool track = fr.track_ppart && fr.mode != 0;
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
+    const bool use_cells = S.cell_off != nullptr && !(fr.flags & TR_FLAG_NO_CELLS);
     const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
     const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
     uint32_t n_queue = 0;
@@ -1445,7 +1486,8 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         bool found = false;
         if (has)
             sh = shade_sample(S, E, fr, s_o[0][g], s_o[1][g], s_o[2][g], s_d[0][g], s_d[1][g],
-                              s_d[2][g], a, k, s_phase[g], pid, stats, pair_scan, use_grid, found);
+                              s_d[2][g], a, k, s_phase[g], pid, stats, pair_scan, use_grid, use_cells,
+                              found);
         shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
@@ -1643,6 +1685,12 @@ SceneK make_scene(const TrDeviceScene *s) {
         S.gscale[a] = s->gscale[a];
     }
     for (int a = 0; a < 3; ++a) { S.mesh_lo[a] = s->mesh_lo[a]; S.mesh_hi[a] = s->mesh_hi[a]; }
+    S.cell_off = s->cell_off;
+    S.cell_recs = s->cell_recs;
+    S.tbox = reinterpret_cast<const float4 *>(s->tbox);
+    for (int a = 0; a < 3; ++a) { S.cdim[a] = s->cdim[a]; S.corg[a] = s->corg[a]; S.cscale[a] = s->cscale[a]; }
+    S.cells_first = s->cells_first;
+    if (!s->cell_recs || !s->tbox) S.cell_off = nullptr;
     return S;
 }
 

@@ -83,7 +83,25 @@ class PointGrid:
         self.dims, self.org, self.scale, self.cells = dims, org, scale, cells
 
 
-def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEAF_MAX):
+class CellLists:
+    """tr_cells_build output: the exact point-location path for meshes whose
+    leaves do not line up with the grid (unstructured tets)."""
+
+    def __init__(self, dims, org, scale, off, recs, tbox):
+        self.dims, self.org, self.scale = dims, org, scale
+        self.off, self.recs, self.tbox = off, recs, tbox
+
+
+CELL_COVERAGE_MIN = 0.9   # below this mean grid coverage the cell lists are built
+CELL_REFINE = 2           # cell-list grid: the point grid refined 2x per axis
+CELL_MAX_LIST = 96        # longer lists fall back to the BVH descent
+
+
+def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEAF_MAX,
+                    cells=None):
+    """(nodes, leaves, ids, grid, cell lists or None).  cells=None: build the
+    cell lists when the grid's exclusive-box coverage is below
+    CELL_COVERAGE_MIN."""
     L = _lib.lib()
     box_lo = np.ascontiguousarray(box_lo, dtype=np.float64)
     box_hi = np.ascontiguousarray(box_hi, dtype=np.float64)
@@ -103,9 +121,27 @@ def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEA
         _lib.check(L.tr_pbvh_grid(h, _lib.vptr(grid.dims), _lib.ptr(grid.org, C.c_double),
                                   _lib.ptr(grid.scale, C.c_double), _lib.vptr(grid.cells)),
                    "tr_pbvh_grid")
+        grid.coverage = float(L.tr_pbvh_coverage(h))
+        lists = None
+        if cells or (cells is None and grid.coverage < CELL_COVERAGE_MIN):
+            hc = C.c_void_p()
+            _lib.check(L.tr_cells_build(h, _lib.ptr(box_lo, C.c_double), _lib.ptr(box_hi, C.c_double),
+                                        CELL_REFINE, CELL_MAX_LIST, C.byref(hc)), "tr_cells_build")
+            try:
+                cs = np.zeros(3, np.int64)
+                _lib.check(L.tr_cells_sizes(hc, _lib.ptr(cs, C.c_int64)), "tr_cells_sizes")
+                lists = CellLists(np.zeros(3, np.int32), np.zeros(3), np.zeros(3),
+                                  np.zeros(int(cs[0]) + 1, np.uint32),
+                                  np.zeros(max(int(cs[1]), 1), np.uint32),
+                                  np.zeros((int(cs[2]), 8), np.float32))
+                _lib.check(L.tr_cells_copy(hc, _lib.vptr(lists.dims), _lib.ptr(lists.org, C.c_double),
+                                           _lib.ptr(lists.scale, C.c_double), _lib.vptr(lists.off),
+                                           _lib.vptr(lists.recs), _lib.vptr(lists.tbox)), "tr_cells_copy")
+            finally:
+                L.tr_host_free(hc)
     finally:
         L.tr_host_free(h)
-    return nodes, leaves, ids, grid
+    return nodes, leaves, ids, grid, lists
 
 
 def build_partition_bsp(lo: np.ndarray, hi: np.ndarray):
@@ -276,6 +312,17 @@ class DeviceScene:
             gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale),
             knodes=self.t_knodes.data_ptr(), kleaf_pids=self.t_kpids.data_ptr(),
             n_knodes=self.n_knodes, kroot=(C.c_double * 6)(*kroot))
+        if self.cells is not None:
+            cl = self.cells
+            self.desc.cell_off = self.t_coff.data_ptr()
+            self.desc.cell_recs = self.t_crecs.data_ptr()
+            self.desc.tbox = self.t_tbox.data_ptr()
+            self.desc.cdim = (C.c_int32 * 3)(*cl.dims)
+            self.desc.corg = (C.c_double * 3)(*cl.org)
+            self.desc.cscale = (C.c_double * 3)(*cl.scale)
+            # the exclusive-leaf grid proves < half of the points: go to the lists first
+            self.desc.cells_first = 1 if getattr(self.grid, "coverage", 1.0) < 0.5 else 0
+            self.resident_bytes += sum(t.numel() for t in (self.t_coff, self.t_crecs, self.t_tbox))
         self._epochs: OrderedDict = OrderedDict()
         self._frames: dict = {}
         self._act_key, self._act_val = None, None
@@ -288,7 +335,8 @@ class DeviceScene:
         device = self.device
         mesh, sampler = scene.mesh, scene.sampler
         lo, hi = _padded_boxes(scene)
-        pnodes, pleaves, pids, grid = build_point_bvh(lo, hi)
+        pnodes, pleaves, pids, grid, lists = build_point_bvh(lo, hi,
+                                                             cells=getattr(scene, "cell_lists", None))
         del lo, hi
         # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
         # reads consecutive 128-B lines with no id indirection
@@ -307,6 +355,11 @@ class DeviceScene:
         cell_leaf[has] = pleaves[grid.cells[has]]
         self.t_grid_leaf = _upload(cell_leaf, device)
         self.grid = grid
+        self.cells = lists
+        if lists is not None:
+            self.t_coff = _upload(lists.off, device)
+            self.t_crecs = _upload(lists.recs, device)
+            self.t_tbox = _upload(lists.tbox, device)
         return len(pnodes), len(pleaves)
 
     def _point_structures_grid(self, scene):
@@ -338,6 +391,7 @@ class DeviceScene:
         torch.cuda.synchronize(self.device)
         self.t_grid = None
         self.t_grid_leaf = None
+        self.cells = None
         self.pnodes_host = self.pleaves_host = None
         self.grid = PointGrid(np.full(3, n, np.int32), np.zeros(3), np.ones(3), None)
         return n_nodes, n_leaves

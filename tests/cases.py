@@ -75,6 +75,17 @@ def build_scene(pkg, name: str):
         n = int(name[6:])   # radial59 (1e6 tets), radial128 (1e7), radial272 (1e8): SURVEY §8d
         return pkg.Scene.build(pkg.generate_synthetic(n, "radial", V),
                                _tf(pkg, radial16_tf_doc(n)))
+    if name.startswith("jitter") and name[6:].isdigit():
+        # an unstructured mesh: the radialN generator's interior vertices
+        # moved by up to 0.2 cell (seeded) -- leaves no longer align with a grid
+        n = int(name[6:])
+        m = pkg.generate_synthetic(n, "radial", V)
+        v = m.vertices.copy()
+        interior = ((v > 0.0) & (v < float(n))).all(axis=1)
+        rng = np.random.default_rng(1234)
+        v[interior] += rng.uniform(-0.2, 0.2, (int(interior.sum()), 3))
+        mesh = pkg.TetMesh(v, m.tets, m.field, V)
+        return pkg.Scene.build(mesh, _tf(pkg, radial16_tf_doc(n)))
     if name.startswith("grid") and name[4:].isdigit():
         # the same scene as radialN, generated in HBM without host mesh
         # arrays (grid_scene.py; radial585 = BASELINE config 4, 1e9 tets)
@@ -104,7 +115,11 @@ def build_scene(pkg, name: str):
 
 
 def _grid_alias(name: str) -> str:
-    return "radial" + name[4:] if name.startswith("grid") and name[4:].isdigit() else name
+    if name.startswith("grid") and name[4:].isdigit():
+        return "radial" + name[4:]
+    if name.startswith("jitter") and name[6:].isdigit():
+        return "radial" + name[6:]
+    return name
 
 
 def camera(pkg, name: str, scale: float = 1.0):

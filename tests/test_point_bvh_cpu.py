@@ -70,7 +70,7 @@ def test_exclusive_leaf_and_full_descent_agree_with_reference(B, recipe):
     from paper_1908_01906_b200.device import _padded_boxes, build_point_bvh
     sc = C.build_scene(B, recipe)
     lo, hi = _padded_boxes(sc)
-    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
+    nodes, leaves, ids, grid, _ = build_point_bvh(lo, hi)
     # (1) f32 child boxes contain the f64 padded boxes of everything below
     for n in nodes:
         for c, (blo, bhi) in enumerate(((n["lo0"], n["hi0"]), (n["lo1"], n["hi1"]))):
@@ -102,7 +102,7 @@ def test_exclusive_boxes_are_disjoint_from_other_leaf_boxes(B):
     from paper_1908_01906_b200.device import _padded_boxes, build_point_bvh
     sc = C.build_scene(B, "sinus")
     lo, hi = _padded_boxes(sc)
-    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
+    nodes, leaves, ids, grid, _ = build_point_bvh(lo, hi)
     boxes = []
     for lf in leaves:
         t = ids[lf["start"]:lf["start"] + lf["count"]]
@@ -129,7 +129,7 @@ def test_native_boxes_and_parallel_build_invariants(B):
     nlo, nhi = m.tet_aabbs()
     pad = 1e-7 * max(m.bounds.diagonal(), 1e-30)
     assert np.array_equal(lo, nlo - pad) and np.array_equal(hi, nhi + pad)
-    nodes, leaves, ids, grid = build_point_bvh(lo, hi)
+    nodes, leaves, ids, grid, _ = build_point_bvh(lo, hi)
     assert np.array_equal(np.sort(ids), np.arange(m.n_tets, dtype=np.uint32))
     starts, counts = leaves["start"].astype(np.int64), leaves["count"].astype(np.int64)
     assert np.array_equal(np.sort(starts), np.concatenate([[0], np.cumsum(counts[np.argsort(starts)])[:-1]]))
