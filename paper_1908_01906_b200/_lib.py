@@ -91,7 +91,7 @@ TR_FLAG_NO_BSP = 8
 STAT_NAMES = ["rounds", "partial_rounds", "lane_samples", "found", "grid_hits", "descents",
               "inline_intervals", "pow_calls", "trace_intervals", "trace_rays", "bsp_overflow",
               "bsp_cells", "trace_max_intervals", "bsp_nodes", "trace_max_nodes", "max_ray_samples",
-              "tile_cycles", "tile_max_cycles"]
+              "tile_cycles", "tile_max_cycles", "march_t0", "march_tq", "march_t1"]
 CHILD_NONE = -2**31
 
 # (name, restype, argtypes) for every symbol include/tetray_b200.h declares

@@ -73,9 +73,18 @@ enum : int {
     ST_MAX_RAY_SAMPLES,  // most samples of one ray's stored list (max)
     ST_TILE_CYCLES,      // trace: SM cycles summed over 32-ray tiles (TR_FLAG_TILE_TIMING)
     ST_TILE_MAX_CYCLES,  // trace: most cycles of one tile (max)
+    ST_MARCH_T0,         // march (TR_FLAG_TILE_TIMING): earliest CTA start, globaltimer ns (min)
+    ST_MARCH_TQ,         // first time a group found the ray queue empty (min)
+    ST_MARCH_T1,         // latest CTA end (max)
     ST_COUNT
 };
 __device__ unsigned long long g_stats[32];
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct RayD {
     double ox, oy, oz, dx, dy, dz;
@@ -1388,6 +1397,8 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const bool use_cells = S.cell_off != nullptr && !(fr.flags & TR_FLAG_NO_CELLS);
     const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
     const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
+    const bool timing = (fr.flags & TR_FLAG_TILE_TIMING) != 0;
+    if (timing && threadIdx.x == 0) atomicMin(&g_stats[ST_MARCH_T0], globaltimer_ns());
     uint32_t n_queue = 0;
     for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
@@ -1406,6 +1417,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             if (want) {
                 if (qpos >= n_queue) {
                     exhausted = true;
+                    if (timing && j == 0) atomicMin(&g_stats[ST_MARCH_TQ], globaltimer_ns());
                 } else {
                     const uint32_t rr = iv.order[qpos];
                     const uint32_t c = iv.cnt[rr];
@@ -1592,6 +1604,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         if (done) active = false;
         __syncwarp();
     }
+    if (timing && threadIdx.x == 0) atomicMax(&g_stats[ST_MARCH_T1], globaltimer_ns());
     // block reduction of the frame totals (R:198-201)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) {
@@ -1919,6 +1932,7 @@ int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset) {
     for (int i = 0; i < n && i < 32; ++i) out[i] = (int64_t)h[i];
     if (reset) {
         for (int i = 0; i < 32; ++i) h[i] = 0;
+        h[ST_MARCH_T0] = h[ST_MARCH_TQ] = ~0ull;   // atomicMin slots
         e = cudaMemcpyToSymbol(g_stats, h, sizeof h);
         if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats reset");
     }

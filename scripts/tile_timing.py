@@ -19,5 +19,8 @@ for scene in sys.argv[1:] or ["radial59"]:
             _lib.check(_lib.lib().tr_kernel_stats(_lib.ptr(out, ctypes.c_int64), 32, 1), "stats")
         d = dict(zip(_lib.STAT_NAMES, out.tolist()))
         tiles = (cam.width * cam.height + 31) // 32
+        q_ms = (d["march_tq"] - d["march_t0"]) / 1e6 if d["march_tq"] > d["march_t0"] else float("nan")
+        m_ms = (d["march_t1"] - d["march_t0"]) / 1e6
         print(scene, mode, "tiles", tiles, "avg cycles", d["tile_cycles"] / tiles, "max", d["tile_max_cycles"],
-              "device ms", round(st.device_ms, 3), flush=True)
+              "| march", round(m_ms, 3), "ms, queue empty after", round(q_ms, 3), "ms",
+              "| device ms", round(st.device_ms, 3), flush=True)
