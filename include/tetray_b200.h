@@ -181,6 +181,14 @@ int tr_tf_meta_device(int64_t n_parts, const double *vrange, const double *tf_ta
                       double tf_lo, double tf_hi, double *max_opacity, double *raw_variance,
                       double *sigma, uint8_t *active, void *stream);
 
+/* The epoch's step arrays on the device (device pointers): step[n] and
+ * step_ratio[n][2] from sigma[n] with the restated glibc pow; *inexact is set
+ * (to 1) if any entry fell outside the restated path -- the caller must then
+ * use tr_epoch_steps on the host (the bench/render path checks the domain on
+ * the host first, so no read-back is needed). */
+int tr_epoch_steps_device(int64_t n, const double *sigma, double s1, double s2, double p,
+                          double *step, double *step_ratio, int32_t *inexact, void *stream);
+
 /* step_size (K:20-22) per partition on the host with glibc pow, so adaptive
  * steps are bit-identical to the reference's. */
 int tr_step_sizes(int64_t n, const double *sigma, double s1, double s2, double p, double *out);
@@ -267,6 +275,7 @@ typedef struct TrFrame {
 #define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
 #define TR_FLAG_TILE_TIMING 0x10000 /* trace pass: SM cycles per 32-ray tile into the kernel stats (profiling) */
 #define TR_FLAG_NO_CELLS 0x20000 /* ignore the cell candidate lists: BVH descent instead (testing) */
+#define TR_FLAG_NO_BG_WRITER 0x40000 /* host framebuffer: trace writes background pixels itself (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
@@ -295,6 +304,12 @@ typedef struct TrOutputs {
     void *ev_march_begin;   /* optional cudaEvent_t recorded before the first march launch */
     void *ev_march_end;     /* optional cudaEvent_t recorded after the last march launch */
 } TrOutputs;
+
+/* Device address of page-locked host memory (cudaHostGetDevicePointer):
+ * TrOutputs.rgba / samples may point there, so the march writes each finished
+ * pixel straight into the caller's host framebuffer over PCIe while it runs
+ * (render() does this; no separate device->host copy after the frame). */
+int tr_host_device_pointer(void *host, void **dev);
 
 /* Scratch bytes for n_rays rays in one chunk (pass W*H rounded up to 32). */
 int64_t tr_scratch_bytes(int64_t n_rays);

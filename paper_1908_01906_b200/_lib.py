@@ -130,11 +130,14 @@ _SIGNATURES = [
     ("tr_tf_meta_device", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.c_double,
                                     C.c_double, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                     C.c_void_p]),
+    ("tr_epoch_steps_device", C.c_int, [C.c_int64, C.c_void_p, C.c_double, C.c_double, C.c_double,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_epoch_steps", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),
     ("tr_step_size", C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double]),
     ("tr_opacity_correction", C.c_double, [C.c_double, C.c_double, C.c_double]),
+    ("tr_host_device_pointer", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tr_pow_glibc_available", C.c_int, []),
     ("tr_pow_glibc_host", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int32)]),
     ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

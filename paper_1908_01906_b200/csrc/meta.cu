@@ -18,10 +18,51 @@
 #include <cstdint>
 #include <string>
 
+#include "glibc_pow.cuh"
 #include "tetray_b200.h"
 #include "tr_internal.h"
 
 namespace {
+
+#if TR_HAVE_GLIBC_POW
+__constant__ unsigned long long c_lhead[] = TR_POW_LOG_HEAD_INIT;
+__constant__ unsigned long long c_ehead[] = TR_POW_EXP_HEAD_INIT;
+__device__ const __align__(32) unsigned long long d_ltab[] = TR_POW_LOG_TAB_INIT;
+__device__ const __align__(32) unsigned long long d_etab[] = TR_POW_EXP_TAB_INIT;
+#endif
+
+// step_size (K:20-22) per partition: max(s1 + (s2 - s1) * |min(sigma, 1) - 1|^p, s1),
+// with glibc's pow restated (glibc_pow.cuh) -- bit-identical to the host's
+// tr_step_sizes wherever the restated path applies; elsewhere the entry is
+// flagged and the caller uses the host.  Also the K:27 exponent step / s1.
+__global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, double s1,
+                                   double s2, double p, double *step, double *ratio, int *inexact) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double sg = sigma[i];
+        const double m = (1.0 < sg) ? 1.0 : sg;   // Python min(sigma, 1.0)
+        const double x = fabs(m - 1.0);
+        double pw = 0.0;
+        bool ok = true;
+        if (x == 1.0) pw = 1.0;                    // glibc: pow(1, y) == 1
+        else if (x == 0.0 && p > 0.0) pw = 0.0;    // glibc: pow(+0, y > 0) == +0
+#if TR_HAVE_GLIBC_POW
+        else if (tr_pow_glibc_supported(x, p)) {
+            bool exact;
+            pw = tr_pow_glibc(x, p, (const uint64_t *)c_lhead, (const uint64_t *)d_ltab,
+                              (const uint64_t *)c_ehead, (const uint64_t *)d_etab, &exact);
+            ok = exact;
+        }
+#endif
+        else ok = false;
+        if (!ok) { atomicExch(inexact, 1); continue; }
+        const double v = s1 + (s2 - s1) * pw;
+        const double st = (s1 > v) ? s1 : v;       // Python max(v, s1)
+        step[i] = st;
+        ratio[2 * i] = st;
+        ratio[2 * i + 1] = st / s1;
+    }
+}
 
 struct Rows {  // the overlapping rows of one partition (transfer.py:96-110)
     const double *T;
@@ -54,26 +95,54 @@ __device__ double sqdist(const Rows &R, int64_t i, const double mean[3]) {
     return ((d0 * d0) + (d1 * d1)) + (d2 * d2);
 }
 
-// numpy's pairwise summation (add.reduce over a contiguous float64 vector)
-__device__ double pairwise(const Rows &R, const double mean[3], int64_t a, int64_t n) {
+// numpy's pairwise summation (add.reduce over a contiguous float64 vector):
+// blocks of <= 128 summed with 8 accumulators, larger ranges split at
+// n/2 rounded down to a multiple of 8 and the halves added.  Walked with an
+// explicit stack -- recursion would need a dynamically sized device stack.
+__device__ double pairwise_block(const Rows &R, const double mean[3], int64_t a, int64_t n) {
     if (n < 8) {
         double r = 0.0;
         for (int64_t i = 0; i < n; ++i) r += sqdist(R, a + i, mean);
         return r;
     }
-    if (n <= 128) {
-        double r[8];
-        for (int j = 0; j < 8; ++j) r[j] = sqdist(R, a + j, mean);
-        int64_t i = 8;
-        for (; i < n - (n % 8); i += 8)
-            for (int j = 0; j < 8; ++j) r[j] += sqdist(R, a + i + j, mean);
-        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        for (; i < n; ++i) res += sqdist(R, a + i, mean);
-        return res;
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = sqdist(R, a + j, mean);
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+        for (int j = 0; j < 8; ++j) r[j] += sqdist(R, a + i + j, mean);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += sqdist(R, a + i, mean);
+    return res;
+}
+
+__device__ double pairwise(const Rows &R, const double mean[3], int64_t a0, int64_t n0) {
+    constexpr int DEPTH = 64;  // halving from 2^63 rows
+    int64_t sa[DEPTH], sn[DEPTH];
+    double sl[DEPTH];
+    int sp = 0;
+    bool right[DEPTH];
+    sa[0] = a0; sn[0] = n0; right[0] = false;
+    for (;;) {
+        if (sn[sp] > 128) {  // descend into the left half
+            int64_t n2 = sn[sp] / 2;
+            n2 -= n2 % 8;
+            sa[sp + 1] = sa[sp]; sn[sp + 1] = n2; right[sp + 1] = false;
+            ++sp;
+            continue;
+        }
+        double ret = pairwise_block(R, mean, sa[sp], sn[sp]);
+        for (;;) {  // hand the sum up: a left half starts its sibling, a right half adds
+            if (sp == 0) return ret;
+            if (!right[sp]) {
+                const int64_t n2 = sn[sp];
+                sl[sp - 1] = ret;
+                sa[sp] = sa[sp - 1] + n2; sn[sp] = sn[sp - 1] - n2; right[sp] = true;
+                break;
+            }
+            --sp;
+            ret = sl[sp] + ret;
+        }
     }
-    int64_t n2 = n / 2;
-    n2 -= n2 % 8;
-    return pairwise(R, mean, a, n2) + pairwise(R, mean, a + n2, n - n2);
 }
 
 __global__ void tf_meta_kernel(int64_t P, const double *__restrict__ vrange, const double *T,
@@ -144,6 +213,20 @@ int cuda_fail(cudaError_t e, const char *where) {
 }
 
 }  // namespace
+
+extern "C" int tr_epoch_steps_device(int64_t n, const double *sigma, double s1, double s2,
+                                     double p, double *step, double *step_ratio, int32_t *inexact,
+                                     void *stream) {
+    if (n < 0 || (n > 0 && (!sigma || !step || !step_ratio || !inexact)))
+        return tr_fail(TR_EINVAL, "tr_epoch_steps_device: invalid arguments");
+    if (n == 0) return TR_OK;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    epoch_steps_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(n, sigma, s1, s2, p, step,
+                                                                         step_ratio, inexact);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "epoch_steps_kernel");
+}
 
 extern "C" int tr_tf_meta_device(int64_t n_parts, const double *vrange, const double *tf_table,
                                  int64_t n_tf, double tf_lo, double tf_hi, double *max_opacity,

@@ -33,6 +33,7 @@
 #include <climits>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
 
 #include "glibc_pow.cuh"
@@ -733,6 +734,7 @@ struct FrameK {
     int32_t n_parts;
     int32_t auto_g;              // lanes per ray chosen on the device (march_lane_choice)
     int64_t march_lanes;         // resident march lanes (CTAs x threads) for that choice
+    int32_t defer_bg;            // background pixels go to background_kernel (host framebuffer)
 };
 
 // One stored interval of a ray (16 B): next_interval's clamped entry, the
@@ -754,6 +756,7 @@ struct IvBuf {                   // per-chunk scratch
     uint32_t *trace_ctr;         // next 32-ray tile of the trace pass
     unsigned long long *ray_stats;  // [0] sum, [1] max of the rays' stored sample counts
     uint32_t *gsel;              // lanes per ray chosen for this chunk (auto mode)
+    uint32_t *n_bg;              // deferred background rays, listed from the top of `order`
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
 };
 
@@ -821,9 +824,15 @@ __device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &
     const double g = acc.g + (1.0 - acc.a) * fr.bg[1];
     const double bl = acc.b + (1.0 - acc.a) * fr.bg[2];
     const double al = acc.a + (1.0 - acc.a) * fr.bg[3];
-    double2 *px = reinterpret_cast<double2 *>(O.rgba + 4 * out);
-    px[0] = make_double2(r, g);
-    px[1] = make_double2(bl, al);
+    double *px = O.rgba + 4 * out;
+    if ((reinterpret_cast<uintptr_t>(px) & 31) == 0) {
+        // one 32-byte store: one PCIe write when the framebuffer is host memory
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};"
+                     :: "l"(px), "d"(r), "d"(g), "d"(bl), "d"(al) : "memory");
+    } else {
+        reinterpret_cast<double2 *>(px)[0] = make_double2(r, g);
+        reinterpret_cast<double2 *>(px)[1] = make_double2(bl, al);
+    }
     O.samples[out] = samples;
     O.visited[out] = visited;
 }
@@ -928,8 +937,18 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             if (cum > 0 || more) {
                 bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
             } else {  // nothing to march: background, `visited` = every interval returned
-                const Acc zero = {0.0, 0.0, 0.0, 0.0};
-                write_pixel(F.f, O, px.out, zero, 0, (int32_t)n);
+                if (F.defer_bg) {   // listed for background_kernel
+                    O.visited[px.out] = (int32_t)n;
+                    const unsigned m = __activemask();
+                    const int lead = __ffs(m) - 1;
+                    unsigned e0 = 0;
+                    if (lane == lead) e0 = atomicAdd(iv.n_bg, (unsigned)__popc(m));
+                    e0 = __shfl_sync(m, e0, lead) + __popc(m & ((1u << lane) - 1u));
+                    iv.order[F.n_rays - 1 - (int64_t)e0] = (uint32_t)rr;
+                } else {
+                    const Acc zero = {0.0, 0.0, 0.0, 0.0};
+                    write_pixel(F.f, O, px.out, zero, 0, (int32_t)n);
+                }
                 vis_done = n;
             }
             iv.cnt[rr] = n | (bucket << 16) | (more ? CNT_MORE : 0u);
@@ -962,6 +981,27 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     if (lane == 0 && cost_sum) {
         atomicAdd(iv.ray_stats, cost_sum);
         atomicMax(iv.ray_stats + 1, (unsigned long long)cost_max);
+    }
+}
+
+// The background pixels the trace listed (F.defer_bg: the framebuffer is
+// page-locked host memory), written by BG_CTAS small CTAs on a side stream
+// while the march runs.  They fit beside three march CTAs per SM (registers)
+// and their dependent-load chain paces them (~BG_CTAS x 64 pixels per ~1 us):
+// the PCIe stores trickle out beside the march instead of bursting at the
+// start of the trace, where they back up the memory system (measured: +105
+// us on the trace for 4.8 MB of background at 512^2).
+constexpr int BG_THREADS = 64;
+constexpr int BG_CTAS = 8;
+
+__global__ void __launch_bounds__(BG_THREADS)
+background_kernel(FrameK F, IvBuf iv, TrOutputs O) {
+    const uint32_t n = *iv.n_bg;
+    const Acc zero = {0.0, 0.0, 0.0, 0.0};
+    for (uint32_t e = blockIdx.x * BG_THREADS + threadIdx.x; e < n; e += gridDim.x * BG_THREADS) {
+        const uint32_t rr = iv.order[F.n_rays - 1 - (int64_t)e];
+        const Pixel px = ray_pixel(F, rr);
+        write_pixel(F.f, O, px.out, zero, 0, O.visited[px.out]);
     }
 }
 
@@ -1718,6 +1758,30 @@ int sm_count() {
     return n;
 }
 
+// Side stream + events of background_kernel, per device (created on first use).
+struct BgAux {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_trace = nullptr, ev_bg = nullptr;
+};
+static std::mutex g_bg_mutex;
+
+static int bg_aux(BgAux **out) {
+    static BgAux aux[64];
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev < 0 || dev >= 64) return tr_fail(TR_EINVAL, "tr_render_frame: device index out of range");
+    BgAux &a = aux[dev];
+    if (!a.stream) {
+        if ((e = cudaStreamCreateWithFlags(&a.stream, cudaStreamNonBlocking)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&a.ev_trace, cudaEventDisableTiming)) != cudaSuccess ||
+            (e = cudaEventCreateWithFlags(&a.ev_bg, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(e, "background stream setup");
+    }
+    *out = &a;
+    return TR_OK;
+}
+
 constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4;  // rec + tail + cnt + order
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
@@ -1823,6 +1887,23 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_fn, TRACE_BLOCK, 0);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
     if (trace_per_sm < 1) trace_per_sm = 1;
+    // a page-locked host framebuffer: the march's pixel stores go over PCIe
+    // as it runs; the background pixels go to background_kernel
+    F.defer_bg = 0;
+    {
+        cudaPointerAttributes pa;
+        if (cudaPointerGetAttributes(&pa, out->rgba) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+            !(frame->flags & TR_FLAG_NO_BG_WRITER))
+            F.defer_bg = 1;
+        else
+            cudaGetLastError();
+    }
+    BgAux *aux = nullptr;
+    std::unique_lock<std::mutex> bg_lock;
+    if (F.defer_bg) {
+        bg_lock = std::unique_lock<std::mutex>(g_bg_mutex);
+        if (int rc = bg_aux(&aux)) return rc;
+    }
     int64_t launches = 0, march_grid = 0;
     for (int64_t r0 = 0; r0 < total_rays; r0 += chunk) {
         F.ray_begin = r0;
@@ -1834,6 +1915,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.trace_ctr = iv.cursor + N_BUCKETS;
         iv.ray_stats = reinterpret_cast<unsigned long long *>(base + 528);
         iv.gsel = reinterpret_cast<uint32_t *>(base + 544);
+        iv.n_bg = reinterpret_cast<uint32_t *>(base + 548);
         iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
         iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
         iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * F.n_rays);
@@ -1841,13 +1923,23 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         iv.order = iv.cnt + F.n_rays;
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
-        e = cudaMemsetAsync(iv.hist, 0, 552, st);   // hist, cursor, trace_ctr, ray_stats, gsel
+        e = cudaMemsetAsync(iv.hist, 0, 552, st);   // hist, cursor, trace_ctr, ray_stats, gsel, n_bg
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
         const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;
         trace_fn<<<(unsigned)trace_grid, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "trace_intervals_kernel launch");
+        if (F.defer_bg) {
+            if ((e = cudaEventRecord(aux->ev_trace, st)) != cudaSuccess ||
+                (e = cudaStreamWaitEvent(aux->stream, aux->ev_trace, 0)) != cudaSuccess)
+                return cuda_fail(e, "background stream fork");
+            background_kernel<<<BG_CTAS, BG_THREADS, 0, aux->stream>>>(F, iv, *out);
+            if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "background_kernel launch");
+            if ((e = cudaEventRecord(aux->ev_bg, aux->stream)) != cudaSuccess)
+                return cuda_fail(e, "background stream record");
+            ++launches;
+        }
         order_rays_kernel<<<(unsigned)tg, TRACE_BLOCK, 0, st>>>(F, iv);
         e = cudaGetLastError();
         if (e != cudaSuccess) return cuda_fail(e, "order_rays_kernel launch");
@@ -1876,6 +1968,10 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
             ++launches;
             if (q == 0) march_grid = grid;
+        }
+        if (F.defer_bg) {   // join: the next chunk reuses the list; the frame ends after it
+            e = cudaStreamWaitEvent(st, aux->ev_bg, 0);
+            if (e != cudaSuccess) return cuda_fail(e, "background stream join");
         }
         if (out->ev_march_end && r0 + chunk >= total_rays) {
             e = cudaEventRecord((cudaEvent_t)out->ev_march_end, st);
@@ -1949,6 +2045,13 @@ int tr_pow_glibc_batch(int64_t n, const double *x, const double *y, double *out,
     pow_batch_kernel<<<(unsigned)grid, 256, 0, (cudaStream_t)stream>>>(n, x, y, out);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "pow_batch_kernel launch");
+    return TR_OK;
+}
+
+int tr_host_device_pointer(void *host, void **dev) {
+    if (!host || !dev) return tr_fail(TR_EINVAL, "tr_host_device_pointer: null");
+    cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostGetDevicePointer");
     return TR_OK;
 }
 

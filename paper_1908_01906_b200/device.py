@@ -22,6 +22,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 import threading
 import time
 import weakref
@@ -181,6 +182,31 @@ def pack_tet_records(mesh, sampler, order=None) -> np.ndarray:
     return rec
 
 
+def _steps_on_device(sigma: np.ndarray, p: float) -> bool:
+    """True when every |min(sigma, 1) - 1| ** p lies on glibc pow's restated
+    path (csrc/glibc_pow.cuh), so the device steps equal the host's bit for
+    bit: x in {0 (p > 0), 1} or x a positive normal double with 2^-65 <= |p| <
+    2^63 and |p ln x| well below the 512 exp-overflow bound."""
+    if not _lib.lib().tr_pow_glibc_available() or not np.isfinite(p):
+        return False
+    ap = abs(p)
+    if not (2.0 ** -65 <= ap < 2.0 ** 63):
+        return False
+    lo = max(math.exp(-499.0 / ap), float(np.finfo(np.float64).tiny))
+    hi = math.exp(499.0 / ap)
+    if p > 0.0 and lo < 2.0 ** -54:
+        # every sigma < 1 gives x = 1 - sigma >= 2^-53 > lo (Sterbenz), sigma >= 1
+        # gives x = 0: only the far end can leave the domain
+        return bool(sigma.min() >= 1.0 - hi)   # NaN fails
+    x = np.abs(np.minimum(sigma, 1.0) - 1.0)
+    if p <= 0.0 and not x.all():
+        return False
+    nz = x[x != 0.0]   # x == 1 is inside [lo, hi]
+    if nz.size == 0:
+        return True
+    return bool(nz.min() >= lo) and bool(nz.max() <= hi)   # NaN fails both
+
+
 class Epoch:
     """One uploaded (active, step, tf) snapshot."""
 
@@ -199,9 +225,10 @@ class Epoch:
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
         def a64(x):  # 64-B aligned sections (the kernel reads the TF with 16-B loads)
             return (x + 63) // 64 * 64
-        # step f64[P] | (step, step / s1) f64[P,2] | tf | active | node activity
+        # step f64[P] | (step, step / s1) f64[P,2] | sigma f64[P] | tf | active | node activity
         o_ratio = a64(8 * P)
-        o_tf = a64(o_ratio + 16 * P)
+        o_sigma = a64(o_ratio + 16 * P)
+        o_tf = a64(o_sigma + 8 * P)
         o_act = a64(o_tf + table.nbytes)
         o_bact = a64(o_act + P)
         o_kact = a64(o_bact + dev.n_bnodes)
@@ -209,25 +236,58 @@ class Epoch:
         host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
         hv = host.numpy()
         hp = host.data_ptr()
-        # per-partition step (K:20-22, glibc pow) and exponent s / s1 (K:27)
-        # written by the library straight into the pinned upload buffer
-        _lib.check(_lib.lib().tr_epoch_steps(P, _lib.ptr(sig, C.c_double), float(params.s1),
-                                             float(params.s2), float(params.p), hp, hp + o_ratio),
-                   "tr_epoch_steps")
+        hv[o_sigma:o_sigma + 8 * P] = sig.view(np.uint8)
         hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
         hv[o_act:o_act + P] = act
         hv[o_bact:o_bact + dev.n_bnodes] = bact
         hv[o_kact:o_kact + dev.n_knodes] = kact
-        self.h2d_bytes = nbytes
         self.host = host
         self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev.device)
-        self.buf.copy_(host, non_blocking=True)
         base = self.buf.data_ptr()
+        s1, s2, pw = float(params.s1), float(params.s2), float(params.p)
+        if _steps_on_device(sig, pw):
+            # per-partition step (K:20-22) and exponent s / s1 (K:27) computed
+            # on the device from sigma with the restated glibc pow; only
+            # sigma, the TF and the activity bits cross PCIe
+            self.buf[o_sigma:].copy_(host[o_sigma:], non_blocking=True)
+            self.h2d_bytes = nbytes - o_sigma
+            flag = torch.zeros(1, dtype=torch.int32, device=dev.device)
+            stream = torch.cuda.current_stream(dev.device)
+            _lib.check(_lib.lib().tr_epoch_steps_device(
+                P, C.c_void_p(base + o_sigma), s1, s2, pw, C.c_void_p(base), C.c_void_p(base + o_ratio),
+                C.c_void_p(flag.data_ptr()), C.c_void_p(stream.cuda_stream)), "tr_epoch_steps_device")
+            self._flag = flag
+            self._step_dev = True
+        else:
+            # host glibc pow, written into the upload buffer
+            _lib.check(_lib.lib().tr_epoch_steps(P, _lib.ptr(sig, C.c_double), s1, s2, pw, hp,
+                                                 hp + o_ratio), "tr_epoch_steps")
+            self.buf.copy_(host, non_blocking=True)
+            self.h2d_bytes = nbytes
+            self._step_dev = False
         self.desc = _lib.TrEpoch(active=base + o_act, bnode_active=base + o_bact, step=base,
                                  tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
                                  tf_hi=self.tf_hi, knode_active=base + o_kact,
                                  step_ratio=base + o_ratio)
-        self.step_host = hv[:8 * P].view(np.float64)
+        self._P = P
+
+    @property
+    def step_host(self) -> np.ndarray:
+        """The epoch's per-partition steps (read back when the device made them)."""
+        return self.buf[:8 * self._P].cpu().numpy().view(np.float64)
+
+
+# render() lets the kernels write rgba / samples into the page-locked result
+# arrays directly (TETRAY_B200_STAGED_OUTPUTS=1: device buffers + copies)
+DIRECT_HOST_OUTPUTS = os.environ.get("TETRAY_B200_STAGED_OUTPUTS", "0") != "1"
+
+
+def host_device_pointer(t) -> int:
+    """Device address of a page-locked (pin_memory) host tensor."""
+    p = C.c_void_p()
+    _lib.check(_lib.lib().tr_host_device_pointer(C.c_void_p(t.data_ptr()), C.byref(p)),
+               "tr_host_device_pointer")
+    return int(p.value)
 
 
 class FrameBuffers:
@@ -464,9 +524,11 @@ class DeviceScene:
             track_ppart=1 if track else 0, shard_rank=shard_rank, shard_count=shard_count,
             compact=1 if compact else 0, flags=flags)
 
-    def launch(self, frame: _lib.TrFrame, epoch: Epoch, fb: FrameBuffers, stream) -> None:
+    def launch(self, frame: _lib.TrFrame, epoch: Epoch, fb: FrameBuffers, stream,
+               out: Optional[_lib.TrOutputs] = None) -> None:
         fb.counters.zero_()
-        out = fb.outputs()
+        if out is None:
+            out = fb.outputs()
         fb.start.record(stream)
         _lib.check(_lib.lib().tr_render_frame(C.byref(self.desc), C.byref(epoch.desc),
                                               C.byref(frame), C.byref(out),
@@ -485,12 +547,21 @@ class DeviceScene:
             ep = self.epoch(meta, params)
             frame = self.frame_desc(scene, camera, mode, params, jitter, track, flags)
             fb = self.frame_buffers(w, h)
-            self.launch(frame, ep, fb, stream)
             rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
             samp_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
             cnt_h = torch.empty(3 + self.n_parts, dtype=torch.int64, pin_memory=True)
-            rgba_h.view(-1, 4).copy_(fb.rgba, non_blocking=True)
-            samp_h.view(-1).copy_(fb.samples, non_blocking=True)
+            if DIRECT_HOST_OUTPUTS:
+                # the kernels store each finished pixel straight into the
+                # page-locked result arrays, overlapping the device->host
+                # transfer with the march (tr_host_device_pointer)
+                out = fb.outputs()
+                out.rgba = host_device_pointer(rgba_h)
+                out.samples = host_device_pointer(samp_h)
+                self.launch(frame, ep, fb, stream, out)
+            else:
+                self.launch(frame, ep, fb, stream)
+                rgba_h.view(-1, 4).copy_(fb.rgba, non_blocking=True)
+                samp_h.view(-1).copy_(fb.samples, non_blocking=True)
             cnt_h.copy_(fb.counters, non_blocking=True)
             stream.synchronize()
             wall_ms = (time.perf_counter() - t0) * 1000.0

@@ -32,3 +32,22 @@ for _ in range(N):
     t0 = time.perf_counter(); dev._epochs.clear(); B.render(sc, cam, "skip-adaptive", par); tick("render() total (new epoch)", t0)
 for k, v in tt.items():
     print(f"{k:32s} {v / N * 1e3:8.3f} ms")
+
+# epoch pieces
+import ctypes as Cc
+import numpy as np
+from paper_1908_01906_b200 import _lib, device as DV
+active, sigma, tf = sc.meta_state()
+sig = np.ascontiguousarray(sigma, dtype=np.float64)
+out = np.empty_like(sig); rat = np.empty(2 * len(sig))
+def clock(f, n=200):
+    f(); t = time.perf_counter()
+    for _ in range(n): f()
+    return (time.perf_counter() - t) / n * 1e3
+print(f"{'host tr_epoch_steps':32s} {clock(lambda: _lib.lib().tr_epoch_steps(len(sig), _lib.ptr(sig, Cc.c_double), par.s1, par.s2, par.p, out.ctypes.data, rat.ctypes.data)):8.3f} ms")
+print(f"{'domain precheck':32s} {clock(lambda: DV._steps_on_device(sig, float(par.p))):8.3f} ms")
+print(f"{'Epoch() async':32s} {clock(lambda: DV.Epoch(dev, sc.meta_state(), par)):8.3f} ms")
+def ep_sync():
+    DV.Epoch(dev, sc.meta_state(), par); torch.cuda.synchronize()
+print(f"{'Epoch() + sync':32s} {clock(ep_sync):8.3f} ms")
+print(f"{'pinned 8 MB alloc (cached)':32s} {clock(lambda: torch.empty((512, 512, 4), dtype=torch.float64, pin_memory=True)):8.3f} ms")

@@ -56,3 +56,42 @@ def test_device_meta_rejects_inverted_range(B):
     tf = B.TransferFunction(table=np.ones((4, 4)), domain=(0.0, 1.0))
     with pytest.raises(RuntimeError):
         TR.partition_meta_arrays_device(tf, np.array([[0.5, 0.2]]))
+
+
+def _host_steps(sig, par):
+    import ctypes as C
+    from paper_1908_01906_b200 import _lib
+    sig = np.ascontiguousarray(sig, dtype=np.float64)
+    out = np.empty_like(sig)
+    ratio = np.empty(2 * len(sig))
+    _lib.check(_lib.lib().tr_epoch_steps(len(sig), _lib.ptr(sig, C.c_double), float(par.s1),
+                                         float(par.s2), float(par.p), out.ctypes.data,
+                                         ratio.ctypes.data), "tr_epoch_steps")
+    return out, ratio
+
+
+@pytest.mark.parametrize("recipe", ["radial16", "golden_radial4", "a6fog", "radial59"])
+def test_device_epoch_steps_equal_host(B, recipe):
+    """Epoch step sizes (K:20-22) and K:27 exponents made on the device with
+    the restated glibc pow are the host's bit for bit."""
+    from paper_1908_01906_b200 import device as DV
+    sc = cases.build_scene(B, recipe)
+    par = cases.params(B, recipe)
+    dev = DV.device_scene_for(sc)
+    rng = np.random.default_rng(5)
+    active, sigma, tf = sc.meta_state()
+    sigmas = [np.asarray(sigma, dtype=np.float64),
+              rng.choice([0.0, 1.0, 0.5, 2.0, 1e-300, 1 - 2**-52, 1e-12, 0.999], len(sigma)),
+              rng.uniform(0.0, 1.5, len(sigma))]
+    for p in (float(par.p), 1.0, 2.0, 3.7):
+        par2 = B.AdaptiveParams(s1=par.s1, s2=par.s2, p=p,
+                                termination_opacity=par.termination_opacity)
+        for sg in sigmas:
+            ep = DV.Epoch(dev, (active, sg, tf), par2)
+            assert ep._step_dev == DV._steps_on_device(sg, float(par2.p))
+            want, want_ratio = _host_steps(sg, par2)
+            assert np.array_equal(ep.step_host, want)
+            ratio = ep.buf[ep.desc.step_ratio - ep.buf.data_ptr():][:16 * len(sg)]
+            assert np.array_equal(ratio.cpu().numpy().view(np.float64), want_ratio)
+            if ep._step_dev:
+                assert int(ep._flag.item()) == 0
