@@ -290,6 +290,10 @@ def host_device_pointer(t) -> int:
     return int(p.value)
 
 
+# rays per trace/march chunk (interval-list scratch: ~1 KB per ray)
+MAX_CHUNK_RAYS = 1 << 20
+
+
 class FrameBuffers:
     """Device outputs of one frame shape, reused across frames."""
 
@@ -304,7 +308,7 @@ class FrameBuffers:
         self.counters = torch.empty(3 + dev.n_parts, dtype=torch.int64, device=d)
         # interval lists of one ray chunk (<= 1M rays; larger frames run in chunks)
         rays = ((n + 31) // 32) * 32
-        self.scratch_bytes = int(_lib.lib().tr_scratch_bytes(min(rays, 1 << 20)))
+        self.scratch_bytes = int(_lib.lib().tr_scratch_bytes(min(rays, MAX_CHUNK_RAYS)))
         self.scratch = torch.empty(self.scratch_bytes, dtype=torch.uint8, device=d)
         self.start = torch.cuda.Event(enable_timing=True)
         self.end = torch.cuda.Event(enable_timing=True)

@@ -9,9 +9,10 @@ sys.path.insert(0, str(ROOT))
 from paper_1908_01906_b200 import _build
 
 VARIANTS = {
-    "count": [],
-    "k16b8": [("constexpr int KBUF = 16;", "constexpr int KBUF = 8;"), ("constexpr int KSTACK = 32;", "constexpr int KSTACK = 16;")],
-    "head": "git:HEAD",
+    "cur": [],
+    "iv32": [("constexpr int IV_CAP = 64;", "constexpr int IV_CAP = 32;")],
+    "iv16": [("constexpr int IV_CAP = 64;", "constexpr int IV_CAP = 16;")],
+    "iv8": [("constexpr int IV_CAP = 64;", "constexpr int IV_CAP = 8;")],
 }
 
 def build(name, edits):

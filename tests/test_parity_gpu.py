@@ -101,6 +101,46 @@ def test_radial59_benchmark_scene(B, golden, mode):
         _check_radial59(fb, st, g, orc, cam, mode, par)
 
 
+@pytest.mark.parametrize("mode", ["reference", "skip-adaptive"])
+def test_radial59_output_paths(B, golden, mode, monkeypatch):
+    """The three ways the frame reaches the host are the same frame: pixels
+    stored into page-locked host memory by the kernels with the background
+    from the side-stream writer (default), the same with the trace writing the
+    background itself (TR_FLAG_NO_BG_WRITER), and device buffers + copies."""
+    from paper_1908_01906_b200 import device as DV
+    sc, orc = scene_of(B, "radial59")
+    cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
+    g = golden["frames"][f"radial59/{mode}"]
+    for staged, flags in ((False, 0), (False, 0x40000), (True, 0)):
+        monkeypatch.setattr(DV, "DIRECT_HOST_OUTPUTS", not staged)
+        fb, st = B.render(sc, cam, mode, par, flags=flags)
+        _check_radial59(fb, st, g, orc, cam, mode, par)
+
+
+@pytest.mark.parametrize("staged", [False, True])
+def test_chunked_frame_equals_single_chunk(B, monkeypatch, staged):
+    """A frame run in several ray chunks (small scratch) equals the one-chunk
+    frame, on both output paths (the background writer joins per chunk)."""
+    from paper_1908_01906_b200 import device as DV
+    sc, _ = scene_of(B, "radial16")
+    cam, par = C.camera(B, "radial16"), C.params(B, "radial16")
+    monkeypatch.setattr(DV, "DIRECT_HOST_OUTPUTS", not staged)
+    for mode in ("reference", "skip", "skip-adaptive"):
+        one = B.render(sc, cam, mode, par)
+        DV.device_scene_for(sc)._frames.clear()
+        monkeypatch.setattr(DV, "MAX_CHUNK_RAYS", 2048)
+        many = B.render(sc, cam, mode, par)
+        DV.device_scene_for(sc)._frames.clear()
+        monkeypatch.setattr(DV, "MAX_CHUNK_RAYS", 1 << 20)
+        assert cam.width * cam.height > 4 * 2048
+        assert np.array_equal(one[0].rgba, many[0].rgba), mode
+        assert np.array_equal(one[0].samples, many[0].samples), mode
+        assert one[1].total_samples == many[1].total_samples
+        assert one[1].partitions_visited_mean == many[1].partitions_visited_mean
+        if mode != "reference":
+            assert np.array_equal(one[1].per_partition_samples, many[1].per_partition_samples)
+
+
 def _check_radial59(fb, st, g, orc, cam, mode, par):
     if mode != "skip-adaptive" or _glibc_pow():
         assert sha(fb.rgba) == g["rgba"]
