@@ -318,6 +318,57 @@ int64_t tr_scratch_bytes(int64_t n_rays);
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                     const TrOutputs *out, void *stream);
 
+/* ---- Exact record-sharded (KD-brick) rendering ----
+ * The partitions are grouped into n_bricks convex bricks (KD subtrees); brick
+ * b's device scene holds only the tets within its box + a halo of the
+ * largest step, with global tet ids (lowest-id location unchanged).  Every
+ * rank traces the full interval list (the partition structures are small and
+ * replicated); the ray's samples are then marched in runs: the run of
+ * consecutive samples whose intervals belong to one brick is marched by that
+ * brick's rank from the per-ray state the previous run left (acc rgba,
+ * samples, position in the interval list), so compositing order and every
+ * count are exactly the single-GPU frame's.  Mode 0's one mesh-box interval
+ * is cut at the brick boxes (records keep its entry: sample k stays
+ * entry + (k + phase) s1).  Rounds repeat until no ray is active; between
+ * rounds the ranks exchange states (each active ray was advanced by exactly
+ * one rank: an int64 SUM all-reduce of the states, zero elsewhere, is exact).
+ * The frame must fit one ray chunk (tr_scratch_bytes(W*H)). */
+typedef struct TrRayState {   /* 64 B per ray */
+    double acc[4];
+    int64_t samples;
+    uint32_t taken;            /* samples of the ray done so far (cum space) */
+    int32_t icur;              /* interval holding sample `taken` */
+    uint32_t cbefore;          /* cum before interval icur */
+    uint32_t stop;             /* end of the current run (set by the plan) */
+    uint32_t flags;            /* 1 active, 2 done */
+    uint32_t pad;
+} TrRayState;
+
+typedef struct TrBricks {
+    int32_t rank;              /* the brick this call marches */
+    int32_t n_bricks;
+    const int16_t *owner;      /* [n_parts] brick of each partition (device) */
+    const double *brick_lo;    /* [n_bricks][3] brick boxes (device; mode 0 cut) */
+    const double *brick_hi;
+    TrRayState *state;         /* [rays] (device) */
+    uint32_t *queue;           /* [rays] rays of this brick's current run (device) */
+    uint32_t *counters;        /* [4] device: rays queued, rays active, error bits, spare */
+    int32_t zero_foreign;      /* 1: zero the states of rays another brick advances (SUM exchange) */
+    int32_t write_background;  /* 1: the trace writes the background pixels (one rank only) */
+} TrBricks;
+
+/* Trace + state init of a brick-sharded frame (any brick's scene: the
+ * partition structures are global).  counters[2] bit 0: a ray needs more than
+ * the stored interval list (unsupported; the caller raises). */
+int tr_brick_trace(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrBricks *bricks, const TrOutputs *out, void *stream);
+/* One round for brick `bricks->rank`: plan every active ray's next run, march
+ * the runs that are this brick's with its scene; rays that finish write their
+ * pixel, the others leave their state for the next run's brick.  counters[1]
+ * = rays still active when the plan ran. */
+int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrBricks *bricks, const TrOutputs *out, void *stream);
+
 /* Device build of the synthetic N^3-cube scene (mesh.py:147-231 generator,
  * vertex field 0 = ramp, 1 = radial; csrc/synth.cu) straight into HBM: n_tets
  * = 5 N^3 records, one leaf per cube (the point

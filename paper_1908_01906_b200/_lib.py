@@ -75,6 +75,17 @@ class TrOutputs(C.Structure):
     ]
 
 
+class TrBricks(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int32), ("n_bricks", C.c_int32),
+        ("owner", C.c_void_p), ("brick_lo", C.c_void_p), ("brick_hi", C.c_void_p),
+        ("state", C.c_void_p), ("queue", C.c_void_p), ("counters", C.c_void_p),
+        ("zero_foreign", C.c_int32), ("write_background", C.c_int32),
+    ]
+
+
+RAY_STATE_BYTES = 64   # TrRayState
+
 # numpy views of the device record layouts (sizes pinned by tests against the header)
 TET_RECORD_DTYPE = np.dtype([("inv", "<f8", 9), ("orig", "<f8", 3), ("f", "<f8", 4)])
 PNODE_DTYPE = np.dtype([("lo0", "<f4", 3), ("hi0", "<f4", 3), ("lo1", "<f4", 3),
@@ -143,6 +154,10 @@ _SIGNATURES = [
     ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_render_frame", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch),
                                   C.POINTER(TrFrame), C.POINTER(TrOutputs), C.c_void_p]),
+    ("tr_brick_trace", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),
+                                 C.POINTER(TrBricks), C.POINTER(TrOutputs), C.c_void_p]),
+    ("tr_brick_round", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),
+                                 C.POINTER(TrBricks), C.POINTER(TrOutputs), C.c_void_p]),
     ("tr_grid_scene_sizes", C.c_int, [C.c_int64, c_i64p, c_i64p, c_i64p]),
     ("tr_grid_scene_build", C.c_int, [C.c_int64, C.c_int32, C.c_double, c_f64p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),

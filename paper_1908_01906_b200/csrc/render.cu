@@ -735,6 +735,12 @@ struct FrameK {
     int32_t auto_g;              // lanes per ray chosen on the device (march_lane_choice)
     int64_t march_lanes;         // resident march lanes (CTAs x threads) for that choice
     int32_t defer_bg;            // background pixels go to background_kernel (host framebuffer)
+    // brick-sharded frame (tr_brick_*; B_on = 0 otherwise)
+    int32_t B_on, B_rank, B_n, B_write_bg, B_zero_foreign;
+    const int16_t *B_owner;
+    const double *B_lo, *B_hi;
+    TrRayState *B_state;
+    uint32_t *B_queue, *B_ctr;
 };
 
 // One stored interval of a ray (16 B): next_interval's clamped entry, the
@@ -837,6 +843,40 @@ __device__ __forceinline__ void write_pixel(const TrFrame &fr, const TrOutputs &
     O.visited[out] = visited;
 }
 
+// Mode 0 under brick sharding: the mesh-box interval [ta, b) cut where the
+// ray leaves each brick box (front to back).  Every record keeps a = ta and
+// pid = -1 - brick; cum = samples with t < the brick's exit (the forced
+// k = 0 sample counts in the first), the last = ns.  The march takes the
+// sample index itself as k in mode 0, so positions are unchanged.
+__device__ uint32_t brick_cut(const FrameK &F, const RayD &ray, double ta, double b, double phase,
+                              int64_t ns, IvRec *rec) {
+    constexpr int MAXB = 64;
+    double ex[MAXB];
+    int16_t id[MAXB];
+    int m = 0;
+    for (int k = 0; k < F.B_n && k < MAXB; ++k) {
+        const double lo[3] = {F.B_lo[3 * k], F.B_lo[3 * k + 1], F.B_lo[3 * k + 2]};
+        const double hi[3] = {F.B_hi[3 * k], F.B_hi[3 * k + 1], F.B_hi[3 * k + 2]};
+        double ea, eb;
+        slab(ray, lo, hi, ea, eb);
+        if (ea > eb || eb <= ta || ea >= b) continue;
+        // insertion by exit (convex, disjoint boxes: exits order like entries)
+        int q = m++;
+        while (q > 0 && ex[q - 1] > eb) { ex[q] = ex[q - 1]; id[q] = id[q - 1]; --q; }
+        ex[q] = eb; id[q] = (int16_t)k;
+    }
+    if (m == 0) { ex[0] = b; id[0] = 0; m = 1; }   // degenerate: the whole interval on brick 0
+    uint32_t n = 0;
+    for (int q = 0; q < m; ++q) {
+        int64_t c = (q == m - 1 || ex[q] >= b) ? ns : interval_samples(ta, ex[q], F.f.s1, phase);
+        if (c > ns) c = ns;
+        IvRec r; r.a = ta; r.pid = -1 - (int32_t)id[q]; r.cum = (uint32_t)c;
+        rec[n++] = r;
+        if (c == ns) break;
+    }
+    return n;
+}
+
 // Phase 1 (one thread per ray, 8x4 pixel tiles per warp): the exact
 // partition-interval sequence (K:360-391 calling next_interval K:173-230)
 // with each interval's clamped entry and the running count of the samples
@@ -882,6 +922,9 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     const int64_t ns = interval_samples(ta, b, F.f.s1, phase);
                     if (ns > (int64_t)CUM_MAX) {
                         more = true;   // the march recomputes it inline
+                    } else if (F.B_on) {
+                        n = brick_cut(F, ray, ta, b, phase, ns, rec);
+                        cum = (uint32_t)ns;
                     } else {
                         IvRec r; r.a = ta; r.pid = -1; r.cum = (uint32_t)ns;
                         rec[0] = r;
@@ -934,7 +977,15 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 atomicMax(&g_stats[ST_TRACE_MAX_NODES], (unsigned long long)bsp_nodes);
                 atomicMax(&g_stats[ST_MAX_RAY_SAMPLES], (unsigned long long)cum);
             }
-            if (cum > 0 || more) {
+            if (F.B_on) {
+                TrRayState z = {};
+                z.flags = (cum > 0) ? 1u : 0u;
+                if (more) { z.flags = 0u; atomicOr(F.B_ctr + 2, 1u); }
+                F.B_state[rr] = z;
+            }
+            if (F.B_on && !(cum > 0 || more) && !F.B_write_bg) {
+                // another rank writes this background pixel
+            } else if (cum > 0 || more) {
                 bucket = cost_bucket((double)cum + (more ? 1024.0 : 0.0));
             } else {  // nothing to march: background, `visited` = every interval returned
                 if (F.defer_bg) {   // listed for background_kernel
@@ -1413,11 +1464,11 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
 // (SoA, one slot per group) instead of registers: the registers then hold a
 // sample's working set only, so more warps fit per SM.  Same
 // rounds, same exact compositing; lane 0 of a group writes the state.
-template <int G, int MINB>
+template <int G, int MINB, bool BRICK = false>
 __global__ void __launch_bounds__(MARCH_BLOCK, MINB)
 march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
-    if (F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
+    if (!BRICK && F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
     constexpr int NG = MARCH_BLOCK / G;
     __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
     __shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free
@@ -1426,6 +1477,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __shared__ long long s_out[NG], s_samples[NG];
     __shared__ uint32_t s_rr[NG], s_taken[NG], s_ctot[NG], s_cbefore[NG];
     __shared__ int32_t s_icur[NG], s_niv[NG], s_pix[NG], s_piy[NG];
+    __shared__ uint32_t s_cfull[BRICK ? NG : 1], s_tbegin[BRICK ? NG : 1];   // brick runs
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G;
@@ -1440,7 +1492,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const bool timing = (fr.flags & TR_FLAG_TILE_TIMING) != 0;
     if (timing && threadIdx.x == 0) atomicMin(&g_stats[ST_MARCH_T0], globaltimer_ns());
     uint32_t n_queue = 0;
-    for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
+    if (BRICK) n_queue = *(volatile const uint32_t *)F.B_ctr;
+    else
+        for (int b = 1; b < N_BUCKETS; ++b) n_queue += iv.hist[b];
     unsigned long long my_samples = 0, my_visited = 0;
     bool active = false, exhausted = false, inline_mode = false, more = false;
 
@@ -1459,7 +1513,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     exhausted = true;
                     if (timing && j == 0) atomicMin(&g_stats[ST_MARCH_TQ], globaltimer_ns());
                 } else {
-                    const uint32_t rr = iv.order[qpos];
+                    const uint32_t rr = BRICK ? F.B_queue[qpos] : iv.order[qpos];
                     const uint32_t c = iv.cnt[rr];
                     const int32_t n_iv = (int32_t)(c & 0xffffu);
                     more = (c & CNT_MORE) != 0;
@@ -1478,6 +1532,16 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         s_samples[g] = 0;
                         s_taken[g] = 0; s_icur[g] = 0; s_cbefore[g] = 0;
                         s_niv[g] = n_iv; s_ctot[g] = c_tot;
+                        if (BRICK) {   // resume the ray where its previous run stopped
+                            const TrRayState st = F.B_state[rr];
+                            s_acc[0][g] = st.acc[0]; s_acc[1][g] = st.acc[1];
+                            s_acc[2][g] = st.acc[2]; s_acc[3][g] = st.acc[3];
+                            s_samples[g] = st.samples;
+                            s_taken[g] = st.taken; s_icur[g] = st.icur; s_cbefore[g] = st.cbefore;
+                            s_ctot[g] = st.stop;        // this brick's run ends here
+                            s_cfull[g] = c_tot;
+                            s_tbegin[g] = st.taken;
+                        }
                         if (inline_mode) {
                             L.t_min = iv.tail[rr];
                             L.last = n_iv > 0 ? load_rec(rec + (n_iv - 1)).pid : -1;
@@ -1517,7 +1581,8 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     while (r.cum <= s) { c0 = r.cum; ++i; r = load_rec(rec + i); }
                     a = r.a;
                     pid = r.pid;
-                    k = (int64_t)(s - c0);
+                    // mode 0: one interval, or (bricks) its cuts, all from the entry
+                    k = (int64_t)(BRICK && fr.mode == 0 ? s : s - c0);
                     i_mine = i;
                     c0_mine = c0;
                     has = true;
@@ -1574,7 +1639,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         const int src = gbase + ((taken_r > 0) ? taken_r - 1 : 0);
         const int32_t i_last = __shfl_sync(FULL, i_mine, src);
         const uint32_t c0_last = __shfl_sync(FULL, c0_mine, src);
-        bool done = false, flush = false;
+        bool done = false, flush = false, suspend = false;
         int32_t flush_n = 0;
         uint32_t taken_now = 0;
         if (active) {
@@ -1587,6 +1652,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 if (term) {                       // K:388-389: the last interval visited
                     flush = true; flush_n = i_last + 1;
                     done = true;
+                } else if (BRICK && taken_now == c_tot && c_tot != s_cfull[g]) {
+                    flush = true; flush_n = n_iv;   // run done: the next brick continues
+                    suspend = true;
                 } else if (taken_now == c_tot) {  // stored list consumed
                     flush = true; flush_n = n_iv;
                     if (more) {
@@ -1615,7 +1683,8 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
             const IvRec *rec = iv.rec + (int64_t)s_rr[g] * IV_CAP;
             for (int32_t i = j; i < flush_n; i += G) {
                 const IvRec r = load_rec(rec + i);
-                const uint32_t lo = (i > 0) ? load_rec(rec + (i - 1)).cum : 0u;
+                uint32_t lo = (i > 0) ? load_rec(rec + (i - 1)).cum : 0u;
+                if (BRICK && lo < s_tbegin[g]) lo = s_tbegin[g];   // this run's samples only
                 const uint32_t hi = (r.cum < taken_now) ? r.cum : taken_now;
                 if (hi > lo) atomicAdd((unsigned long long *)O.ppart + r.pid, (unsigned long long)(hi - lo));
             }
@@ -1639,9 +1708,22 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 write_pixel(fr, O, s_out[g], acc, samples, visited);
                 my_samples += (unsigned long long)samples;
                 my_visited += (unsigned long long)visited;
+                if (BRICK) {
+                    TrRayState st = {};
+                    st.flags = 2u;
+                    F.B_state[s_rr[g]] = st;
+                }
+            } else if (BRICK && suspend) {
+                TrRayState st = {};
+                st.acc[0] = s_acc[0][g]; st.acc[1] = s_acc[1][g];
+                st.acc[2] = s_acc[2][g]; st.acc[3] = s_acc[3][g];
+                st.samples = samples;
+                st.taken = s_taken[g]; st.icur = s_icur[g]; st.cbefore = s_cbefore[g];
+                st.flags = 1u;
+                F.B_state[s_rr[g]] = st;
             }
         }
-        if (done) active = false;
+        if (done || suspend) active = false;
         __syncwarp();
     }
     if (timing && threadIdx.x == 0) atomicMax(&g_stats[ST_MARCH_T1], globaltimer_ns());
@@ -1758,6 +1840,27 @@ int sm_count() {
     return n;
 }
 
+// Resident CTAs per SM of a kernel, cached per (device, kernel): the query
+// costs several microseconds of host time on every frame otherwise.
+static cudaError_t occupancy(int *out, const void *fn, int block) {
+    struct Ent { int dev; const void *fn; int block, n; };
+    static Ent cache[64];
+    static int n_cache = 0;
+    static std::mutex mu;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    for (int i = 0; i < n_cache; ++i)
+        if (cache[i].dev == dev && cache[i].fn == fn && cache[i].block == block) {
+            *out = cache[i].n;
+            return cudaSuccess;
+        }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, block, 0);
+    if (e == cudaSuccess && n_cache < 64) cache[n_cache++] = {dev, fn, block, *out};
+    return e;
+}
+
 // Side stream + events of background_kernel, per device (created on first use).
 struct BgAux {
     cudaStream_t stream = nullptr;
@@ -1785,6 +1888,63 @@ static int bg_aux(BgAux **out) {
 constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4;  // rec + tail + cnt + order
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
+// ---- brick-sharded frames (tr_brick_*)
+
+__device__ __forceinline__ int brick_of(const FrameK &F, int32_t pid) {
+    return pid >= 0 ? (int)__ldg(F.B_owner + pid) : (-1 - pid);
+}
+
+// Every active ray's next run: the interval holding sample `taken`, its
+// brick, and the run's end (the last following interval that is the same
+// brick's or holds no sample).  Runs of F.B_rank are queued; with
+// B_zero_foreign every other state is zeroed for the SUM exchange.
+__global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < F.n_rays; r0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t rr = r0 + threadIdx.x;
+        bool act = false, mine = false;
+        TrRayState st = {};
+        if (rr < F.n_rays) {
+            st = F.B_state[rr];
+            act = st.flags == 1u;
+        }
+        if (act) {
+            const uint32_t n_iv = iv.cnt[rr] & 0xffffu;
+            const IvRec *rec = iv.rec + rr * IV_CAP;
+            int32_t i = st.icur;
+            uint32_t c0 = st.cbefore;
+            IvRec r = load_rec(rec + i);
+            while (r.cum <= st.taken) { c0 = r.cum; ++i; r = load_rec(rec + i); }
+            const int b = brick_of(F, r.pid);
+            int32_t i2 = i;
+            uint32_t cend = r.cum;
+            while (i2 + 1 < (int32_t)n_iv) {
+                const IvRec r2 = load_rec(rec + i2 + 1);
+                if (r2.cum != cend && brick_of(F, r2.pid) != b) break;
+                ++i2;
+                cend = r2.cum;
+            }
+            if (b == F.B_rank) {
+                mine = true;
+                st.icur = i;
+                st.cbefore = c0;
+                st.stop = cend;
+                F.B_state[rr] = st;
+            }
+        }
+        if (rr < F.n_rays && !mine && F.B_zero_foreign) {
+            const TrRayState z = {};
+            F.B_state[rr] = z;
+        }
+        const unsigned am = __ballot_sync(FULL, act), mm = __ballot_sync(FULL, mine);
+        if (lane == 0 && am) atomicAdd(F.B_ctr + 1, (unsigned)__popc(am));
+        unsigned base = 0;
+        if (lane == 0 && mm) base = atomicAdd(F.B_ctr, (unsigned)__popc(mm));
+        base = __shfl_sync(FULL, base, 0);
+        if (mine) F.B_queue[base + __popc(mm & ((1u << lane) - 1u))] = (uint32_t)rr;
+    }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1802,8 +1962,28 @@ int64_t tr_scratch_bytes(int64_t n_rays) {
     return n_rays * IV_BYTES_PER_RAY + IV_FIXED_BYTES;
 }
 
-int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
-                    const TrOutputs *out, void *stream) {
+// Validation and the kernel-side views shared by tr_render_frame and the
+// brick-sharded calls.
+// The chunk's interval lists and counters in out->scratch.
+static IvBuf make_iv(const TrOutputs *out, int64_t n_rays) {
+    IvBuf iv;
+    char *base = reinterpret_cast<char *>(out->scratch);
+    iv.hist = reinterpret_cast<uint32_t *>(base);
+    iv.cursor = iv.hist + N_BUCKETS;
+    iv.trace_ctr = iv.cursor + N_BUCKETS;
+    iv.ray_stats = reinterpret_cast<unsigned long long *>(base + 528);
+    iv.gsel = reinterpret_cast<uint32_t *>(base + 544);
+    iv.n_bg = reinterpret_cast<uint32_t *>(base + 548);
+    iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
+    iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
+    iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * n_rays);
+    iv.cnt = reinterpret_cast<uint32_t *>(iv.tail + n_rays);
+    iv.order = iv.cnt + n_rays;
+    return iv;
+}
+
+static int prepare_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                         const TrOutputs *out, SceneK &S, EpochK &E, FrameK &F) {
     if (!scene || !epoch || !frame || !out)
         return tr_fail(TR_EINVAL, "tr_render_frame: null argument");
     if (frame->width < 1 || frame->height < 1 || frame->mode < 0 || frame->mode > 2 ||
@@ -1818,9 +1998,8 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         return tr_fail(TR_EINVAL, "tr_render_frame: missing partition buffers");
     if (frame->track_ppart && frame->mode != 0 && !out->ppart)
         return tr_fail(TR_EINVAL, "tr_render_frame: missing ppart buffer");
-    cudaStream_t st = (cudaStream_t)stream;
-    SceneK S = make_scene(scene);
-    EpochK E;
+    S = make_scene(scene);
+    E = EpochK{};
     E.active = epoch->active;
     E.knode_active = epoch->knode_active;
     E.bnode_active = epoch->bnode_active;
@@ -1830,13 +2009,23 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     E.n_tf = epoch->n_tf;
     E.tf_lo = epoch->tf_lo;
     E.tf_hi = epoch->tf_hi;
-    FrameK F;
+    F = FrameK{};
     F.f = *frame;
     F.tiles_x = (frame->width + TILE_W - 1) / TILE_W;
     F.n_tiles = tr_num_tiles(frame->width, frame->height);
     F.my_tiles = (F.n_tiles - frame->shard_rank + frame->shard_count - 1) / frame->shard_count;
     if (F.my_tiles < 0) F.my_tiles = 0;
     F.n_parts = (int32_t)scene->n_parts;
+    return TR_OK;
+}
+
+int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                    const TrOutputs *out, void *stream) {
+    SceneK S;
+    EpochK E;
+    FrameK F;
+    if (int rc = prepare_frame(scene, epoch, frame, out, S, E, F)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
     const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
     // ray chunk = what the scratch interval lists can hold
     if (!out->scratch || out->scratch_bytes < IV_BYTES_PER_RAY * 32 + IV_FIXED_BYTES)
@@ -1875,7 +2064,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     }
     cudaError_t e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, march_fn, MARCH_BLOCK, 0);
+    e = occupancy(&per_sm, (const void *)march_fn, MARCH_BLOCK);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
@@ -1884,7 +2073,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     int trace_per_sm = 0;
     void (*trace_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) =
         (frame->flags & TR_FLAG_STATS) ? trace_intervals_kernel<true> : trace_intervals_kernel<false>;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&trace_per_sm, trace_fn, TRACE_BLOCK, 0);
+    e = occupancy(&trace_per_sm, (const void *)trace_fn, TRACE_BLOCK);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
     if (trace_per_sm < 1) trace_per_sm = 1;
     // a page-locked host framebuffer: the march's pixel stores go over PCIe
@@ -1908,19 +2097,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     for (int64_t r0 = 0; r0 < total_rays; r0 += chunk) {
         F.ray_begin = r0;
         F.n_rays = (total_rays - r0 < chunk) ? total_rays - r0 : chunk;
-        IvBuf iv;
-        char *base = reinterpret_cast<char *>(out->scratch);
-        iv.hist = reinterpret_cast<uint32_t *>(base);
-        iv.cursor = iv.hist + N_BUCKETS;
-        iv.trace_ctr = iv.cursor + N_BUCKETS;
-        iv.ray_stats = reinterpret_cast<unsigned long long *>(base + 528);
-        iv.gsel = reinterpret_cast<uint32_t *>(base + 544);
-        iv.n_bg = reinterpret_cast<uint32_t *>(base + 548);
-        iv.totals = reinterpret_cast<unsigned long long *>(out->totals);
-        iv.rec = reinterpret_cast<IvRec *>(base + IV_FIXED_BYTES);
-        iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * F.n_rays);
-        iv.cnt = reinterpret_cast<uint32_t *>(iv.tail + F.n_rays);
-        iv.order = iv.cnt + F.n_rays;
+        IvBuf iv = make_iv(out, F.n_rays);
         e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st);
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
         e = cudaMemsetAsync(iv.hist, 0, 552, st);   // hist, cursor, trace_ctr, ray_stats, gsel, n_bg
@@ -2059,6 +2236,94 @@ int tr_last_launch(int64_t *out3) {
     if (!out3) return tr_fail(TR_EINVAL, "tr_last_launch: null");
     for (int i = 0; i < 3; ++i) out3[i] = g_last_launch[i];
     return TR_OK;
+}
+
+static int brick_setup(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                       const TrBricks *bricks, const TrOutputs *out, SceneK &S, EpochK &E,
+                       FrameK &F, IvBuf &iv) {
+    if (int rc = prepare_frame(scene, epoch, frame, out, S, E, F)) return rc;
+    if (!bricks || bricks->n_bricks < 1 || bricks->n_bricks > 64 || bricks->rank < 0 ||
+        bricks->rank >= bricks->n_bricks || !bricks->owner || !bricks->brick_lo ||
+        !bricks->brick_hi || !bricks->state || !bricks->queue || !bricks->counters)
+        return tr_fail(TR_EINVAL, "tr_brick: invalid TrBricks");
+    if (frame->flags & TR_FLAG_REG_STATE)
+        return tr_fail(TR_EINVAL, "tr_brick: TR_FLAG_REG_STATE is not supported");
+    const int64_t total_rays = F.my_tiles * (TILE_W * TILE_H);
+    if (!out->scratch || out->scratch_bytes < tr_scratch_bytes(total_rays))
+        return tr_fail(TR_EINVAL, "tr_brick: the frame must fit one ray chunk (scratch too small)");
+    F.ray_begin = 0;
+    F.n_rays = total_rays;
+    F.B_on = 1;
+    F.B_rank = bricks->rank;
+    F.B_n = bricks->n_bricks;
+    F.B_write_bg = bricks->write_background;
+    F.B_zero_foreign = bricks->zero_foreign;
+    F.B_owner = bricks->owner;
+    F.B_lo = bricks->brick_lo;
+    F.B_hi = bricks->brick_hi;
+    F.B_state = bricks->state;
+    F.B_queue = bricks->queue;
+    F.B_ctr = bricks->counters;
+    iv = make_iv(out, F.n_rays);
+    return TR_OK;
+}
+
+int tr_brick_trace(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrBricks *bricks, const TrOutputs *out, void *stream) {
+    SceneK S;
+    EpochK E;
+    FrameK F;
+    IvBuf iv;
+    if (int rc = brick_setup(scene, epoch, frame, bricks, out, S, E, F, iv)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(iv.hist, 0, 552, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(bricks->counters, 0, 16, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(bricks->state, 0, sizeof(TrRayState) * F.n_rays, st)) != cudaSuccess)
+        return cuda_fail(e, "tr_brick_trace memset");
+    if (F.n_rays == 0) return TR_OK;
+    void (*trace_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) =
+        (frame->flags & TR_FLAG_STATS) ? trace_intervals_kernel<true> : trace_intervals_kernel<false>;
+    int trace_per_sm = 0;
+    if ((e = occupancy(&trace_per_sm, (const void *)trace_fn, TRACE_BLOCK)) != cudaSuccess)
+        return cuda_fail(e, "occupancy(trace)");
+    if (trace_per_sm < 1) trace_per_sm = 1;
+    const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
+    const int64_t cap = (int64_t)sm_count() * trace_per_sm;
+    trace_fn<<<(unsigned)(tg < cap ? tg : cap), TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "trace_intervals_kernel launch (bricks)");
+}
+
+int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrBricks *bricks, const TrOutputs *out, void *stream) {
+    SceneK S;
+    EpochK E;
+    FrameK F;
+    IvBuf iv;
+    if (int rc = brick_setup(scene, epoch, frame, bricks, out, S, E, F, iv)) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if ((e = cudaMemsetAsync(bricks->counters, 0, 8, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st)) != cudaSuccess)
+        return cuda_fail(e, "tr_brick_round memset");
+    if (F.n_rays == 0) return TR_OK;
+    int64_t pg = (F.n_rays + 255) / 256;
+    if (pg > (int64_t)sm_count() * 8) pg = (int64_t)sm_count() * 8;
+    brick_plan_kernel<<<(unsigned)pg, 256, 0, st>>>(F, iv);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "brick_plan_kernel launch");
+    void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = march_sm_kernel<4, 3, true>;
+    int per_sm = 0;
+    if ((e = occupancy(&per_sm, (const void *)march_fn, MARCH_BLOCK)) != cudaSuccess)
+        return cuda_fail(e, "occupancy(march)");
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)sm_count() * per_sm;
+    const int64_t need = (F.n_rays * 4 + MARCH_BLOCK - 1) / MARCH_BLOCK;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    march_fn<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "march_sm_kernel launch (bricks)");
 }
 
 }  // extern "C"

@@ -168,13 +168,14 @@ def build_partition_bsp(lo: np.ndarray, hi: np.ndarray):
 
 def pack_tet_records(mesh, sampler, order=None) -> np.ndarray:
     """128-B records; record k holds tet order[k] (None: tet k)."""
-    rec = np.empty(mesh.n_tets, dtype=_lib.TET_RECORD_DTYPE)
     order = None if order is None else np.ascontiguousarray(order, dtype=np.uint32)
+    n = mesh.n_tets if order is None else len(order)
+    rec = np.empty(n, dtype=_lib.TET_RECORD_DTYPE)
     orig = np.ascontiguousarray(sampler.tet_orig, dtype=np.float64)
     inv = np.ascontiguousarray(sampler.tet_inv, dtype=np.float64)
     tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
     fld = np.ascontiguousarray(mesh.field, dtype=np.float64)
-    _lib.check(_lib.lib().tr_pack_tets(mesh.n_tets, _lib.ptr(tets, C.c_int64),
+    _lib.check(_lib.lib().tr_pack_tets(n, _lib.ptr(tets, C.c_int64),
                                        _lib.ptr(orig, C.c_double), _lib.ptr(inv, C.c_double),
                                        _lib.ptr(fld, C.c_double), int(mesh.centering),
                                        None if order is None else _lib.vptr(order),
@@ -251,7 +252,7 @@ class Epoch:
             # sigma, the TF and the activity bits cross PCIe
             self.buf[o_sigma:].copy_(host[o_sigma:], non_blocking=True)
             self.h2d_bytes = nbytes - o_sigma
-            flag = torch.zeros(1, dtype=torch.int32, device=dev.device)
+            flag = dev.epoch_flag()   # set only for entries outside the restated domain
             stream = torch.cuda.current_stream(dev.device)
             _lib.check(_lib.lib().tr_epoch_steps_device(
                 P, C.c_void_p(base + o_sigma), s1, s2, pw, C.c_void_p(base), C.c_void_p(base + o_ratio),
@@ -324,10 +325,13 @@ class FrameBuffers:
 class DeviceScene:
     """The scene's geometry in HBM plus its epoch and output caches."""
 
-    def __init__(self, scene, device):
+    def __init__(self, scene, device, tet_subset: Optional[np.ndarray] = None):
+        """tet_subset: ascending global tet ids this device holds (a brick of
+        a record-sharded frame, bricks.py); None = every tet."""
         torch = _torch()
         self.device = device
         self.lock = threading.Lock()
+        self.tet_subset = None if tet_subset is None else np.ascontiguousarray(tet_subset, np.int64)
         mesh = scene.mesh
         with torch.cuda.device(device):
             t0 = time.perf_counter()
@@ -343,7 +347,7 @@ class DeviceScene:
             self.bnodes_host = np.ascontiguousarray(bnodes)
             self.n_parts = int(part_lo.shape[0])
             self.n_bnodes = int(len(bnodes))
-            self.n_tets = int(mesh.n_tets)
+            self.n_tets = int(mesh.n_tets if self.tet_subset is None else len(self.tet_subset))
             if getattr(mesh, "device_generated", False):
                 point = self._point_structures_grid(scene)
             else:
@@ -399,9 +403,19 @@ class DeviceScene:
         device = self.device
         mesh, sampler = scene.mesh, scene.sampler
         lo, hi = _padded_boxes(scene)
+        sub = self.tet_subset
+        if sub is not None:   # ascending global ids: local order = id order
+            if len(sub) == 0:
+                raise ValueError("empty tet subset")
+            lo, hi = lo[sub], hi[sub]
         pnodes, pleaves, pids, grid, lists = build_point_bvh(lo, hi,
                                                              cells=getattr(scene, "cell_lists", None))
         del lo, hi
+        if sub is not None:
+            pids = sub[pids].astype(np.uint32)   # leaf ids as global tet ids
+            m = pnodes["minid"]                  # subtree minima too (descent pruning)
+            ok = m < len(sub)
+            m[ok] = sub[m[ok]].astype(np.uint32)
         # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
         # reads consecutive 128-B lines with no id indirection
         rec = pack_tet_records(mesh, sampler, order=pids)
@@ -489,6 +503,12 @@ class DeviceScene:
         else:
             self._epochs.move_to_end(key)
         return ep
+
+    def epoch_flag(self):
+        """int32 device word tr_epoch_steps_device sets on an inexact entry (shared)."""
+        if getattr(self, "_epoch_flag", None) is None:
+            self._epoch_flag = _torch().zeros(1, dtype=_torch().int32, device=self.device)
+        return self._epoch_flag
 
     def frame_buffers(self, width: int, height: int, compact_slots: int = 0) -> FrameBuffers:
         key = (width, height, compact_slots)

@@ -25,6 +25,7 @@ from pathlib import Path
 import numpy as np
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
+ROOT = Path(__file__).resolve().parent.parent
 
 TF_BANDED = {"domain": [0.0, 3.5],
              "rgba": [[0.0, 0.0, 1.0, 0.0], [0.0, 1.0, 1.0, 0.1], [0.0, 1.0, 0.0, 0.5],
