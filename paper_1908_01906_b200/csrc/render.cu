@@ -2076,6 +2076,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     e = occupancy(&trace_per_sm, (const void *)trace_fn, TRACE_BLOCK);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor(trace)");
     if (trace_per_sm < 1) trace_per_sm = 1;
+    if ((frame->flags >> 20) & 0x7) trace_per_sm = (frame->flags >> 20) & 0x7;   // tuning: trace CTAs per SM
     // a page-locked host framebuffer: the march's pixel stores go over PCIe
     // as it runs; the background pixels go to background_kernel
     F.defer_bg = 0;
