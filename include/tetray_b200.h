@@ -277,6 +277,7 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_CELLS 0x20000 /* ignore the cell candidate lists: BVH descent instead (testing) */
 #define TR_FLAG_NO_BG_WRITER 0x40000 /* host framebuffer: trace writes background pixels itself (testing) */
 /* flags bits 20-22: trace CTAs per SM (0 = occupancy maximum; tuning) */
+#define TR_FLAG_NO_CAND 0x800000 /* modes 1/2: intervals by the per-ray BSP walk, not the candidate raster (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */

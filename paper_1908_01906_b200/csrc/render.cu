@@ -49,6 +49,7 @@ constexpr int BSTACK = 64;
 constexpr int MARCH_BLOCK = 256;
 constexpr int TRACE_BLOCK = 128;
 constexpr int IV_CAP = 64;           // partition ids per ray kept in the scratch list
+constexpr int CAND_CAP = 48;         // partition slabs per ray kept by the candidate raster
 constexpr int N_BUCKETS = 64;        // ray-cost buckets (4 per octave) for longest-first order
 constexpr int32_t CHILD_NONE = INT32_MIN;
 constexpr unsigned FULL = 0xffffffffu;
@@ -735,6 +736,7 @@ struct FrameK {
     int32_t auto_g;              // lanes per ray chosen on the device (march_lane_choice)
     int64_t march_lanes;         // resident march lanes (CTAs x threads) for that choice
     int32_t defer_bg;            // background pixels go to background_kernel (host framebuffer)
+    int32_t use_cand;            // modes 1/2: intervals from the rasterised candidate lists
     // brick-sharded frame (tr_brick_*; B_on = 0 otherwise)
     int32_t B_on, B_rank, B_n, B_write_bg, B_zero_foreign;
     const int16_t *B_owner;
@@ -763,6 +765,10 @@ struct IvBuf {                   // per-chunk scratch
     unsigned long long *ray_stats;  // [0] sum, [1] max of the rays' stored sample counts
     uint32_t *gsel;              // lanes per ray chosen for this chunk (auto mode)
     uint32_t *n_bg;              // deferred background rays, listed from the top of `order`
+    double *cand_pa, *cand_pb;   // [CAND_CAP][n_rays] active partition slabs (use_cand), slot-major
+    int32_t *cand_pid;           //   so a warp's 32 rays read one slot in one coalesced load
+    uint32_t *ccount;            // [n_rays] slabs found (> CAND_CAP: the ray takes the BSP)
+    double *rinv;                // [3][n_rays] 1/d per axis (0 where d == 0) for the raster
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
 };
 
@@ -877,6 +883,219 @@ __device__ uint32_t brick_cut(const FrameK &F, const RayD &ray, double ta, doubl
     return n;
 }
 
+// next_interval (K:173-230) over the ray's complete candidate list: the
+// active partitions whose slab it hits.  Same rule as the BVH / BSP
+// enumerations: skip the excluded id and exits <= t_min + excl, winner = the
+// lexicographic minimum of (max(entry, t_min), pid).
+__device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n_rays, int64_t rr,
+                                                      uint32_t n, uint32_t &dead, double &dead_thr,
+                                                      double t_min, double excl, int32_t last,
+                                                      double &ra, double &rb) {
+    const double thr = t_min + excl;
+    int32_t best = -1;
+    double best_a = INFINITY, best_b = INFINITY;
+    // skip the prefix whose exits are <= thr: still dead while thr >= the
+    // threshold they were skipped at (fl(fl(b - eps) + eps) can step back an ulp)
+    if (thr < dead_thr) dead = 0;
+    while (dead < n && __ldg(iv.cand_pb + (int64_t)dead * n_rays + rr) <= thr) ++dead;
+    dead_thr = thr;
+    for (uint32_t i0 = dead; i0 < n; i0 += 4) {
+        double pa[4], pb[4];
+        int32_t pid[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {   // four slots' loads in flight together
+            const int64_t o = (int64_t)(i0 + u) * n_rays + rr;
+            const bool ok = i0 + u < n;
+            pa[u] = ok ? __ldg(iv.cand_pa + o) : 0.0;
+            pb[u] = ok ? __ldg(iv.cand_pb + o) : -INFINITY;
+            pid[u] = ok ? __ldg(iv.cand_pid + o) : -1;
+        }
+        if (pa[0] > best_a) break;   // entries ascend: nothing later can win
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (pid[u] == last || pb[u] <= thr) continue;   // also the padding (pb = -inf)
+            const double a_cl = (pa[u] > t_min) ? pa[u] : t_min;
+            if (a_cl >= INFINITY) continue;   // t_max = inf (K:366)
+            if (a_cl < best_a || (a_cl == best_a && pid[u] < best)) { best = pid[u]; best_a = a_cl; best_b = pb[u]; }
+        }
+    }
+    ra = best_a;
+    rb = best_b;
+    return best;
+}
+
+// chunk-local ray of pixel (ix, iy), -1 if another rank's or chunk's
+__device__ __forceinline__ int64_t pixel_ray(const FrameK &F, uint32_t ix, uint32_t iy) {
+    uint32_t tile = (iy / TILE_H) * (uint32_t)F.tiles_x + ix / TILE_W;
+    const uint32_t cnt = (uint32_t)F.f.shard_count;
+    if (cnt > 1) {
+        if (tile % cnt != (uint32_t)F.f.shard_rank) return -1;
+        tile /= cnt;
+    }
+    const int64_t g = (int64_t)tile * 32 + (iy % TILE_H) * TILE_W + (ix % TILE_W) - F.ray_begin;
+    return (g >= 0 && g < F.n_rays) ? g : -1;
+}
+
+// 1/d per axis of every ray of the chunk (make_ray, K:330-338) for the raster.
+__global__ void __launch_bounds__(256) ray_table_kernel(FrameK F, IvBuf iv) {
+    const int64_t rr = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (rr >= F.n_rays) return;
+    iv.ccount[rr] = 0;
+    const Pixel px = ray_pixel(F, rr);
+    double a = 0.0, b = 0.0, c = 0.0;
+    if (px.valid) {
+        const RayD ray = make_ray(F.f, px.ix, px.iy);
+        a = ray.ix; b = ray.iy; c = ray.iz;
+    }
+    iv.rinv[rr] = a;
+    iv.rinv[F.n_rays + rr] = b;
+    iv.rinv[2 * F.n_rays + rr] = c;
+}
+
+// Candidate raster: one CTA per active partition walks the pixels of its
+// box's screen rectangle (conservative: corners projected, 2 px margin, the
+// whole frame if a corner is not in front of the camera) and appends the
+// partition to every ray whose exact slab test (the trace's own make_ray and
+// slab) hits it with an exit > 0.  Work is spread over partitions x pixels,
+// so no ray's front-to-back walk sets the pass time.
+__global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
+    const TrFrame &fr = F.f;
+    __shared__ int64_t s_rect[4];   // ix0, ix1, iy0, iy1 (ix0 > ix1: nothing)
+    for (int32_t pid = blockIdx.x; pid < F.n_parts; pid += gridDim.x) {
+        if (!__ldg(E.active + pid)) continue;
+        const double lo[3] = {__ldg(S.part_lo + 3 * pid), __ldg(S.part_lo + 3 * pid + 1), __ldg(S.part_lo + 3 * pid + 2)};
+        const double hi[3] = {__ldg(S.part_hi + 3 * pid), __ldg(S.part_hi + 3 * pid + 1), __ldg(S.part_hi + 3 * pid + 2)};
+        __syncthreads();   // the previous partition's rectangle is read
+        if (threadIdx.x == 0) {
+        double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
+        bool full = false;
+        for (int c = 0; c < 8; ++c) {
+            const double v[3] = {((c & 1) ? hi[0] : lo[0]) - fr.cam_pos[0],
+                                 ((c & 2) ? hi[1] : lo[1]) - fr.cam_pos[1],
+                                 ((c & 4) ? hi[2] : lo[2]) - fr.cam_pos[2]};
+            const double z = v[0] * fr.cam_fwd[0] + v[1] * fr.cam_fwd[1] + v[2] * fr.cam_fwd[2];
+            const double len = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
+            if (!(z > 1e-6 * len)) { full = true; break; }
+            const double sx = (v[0] * fr.cam_right[0] + v[1] * fr.cam_right[1] + v[2] * fr.cam_right[2]) /
+                              z / (fr.aspect * fr.tan_half);
+            const double sy = (v[0] * fr.cam_up[0] + v[1] * fr.cam_up[1] + v[2] * fr.cam_up[2]) / z / fr.tan_half;
+            const double px = (sx + 1.0) * 0.5 * (double)fr.width - 0.5;
+            const double py = (1.0 - sy) * 0.5 * (double)fr.height - 0.5;
+            x0 = fmin(x0, px); x1 = fmax(x1, px); y0 = fmin(y0, py); y1 = fmax(y1, py);
+        }
+        int64_t ix0 = 0, ix1 = fr.width - 1, iy0 = 0, iy1 = fr.height - 1;
+        if (!full) {
+            if (!(x1 >= -2.0) || !(x0 <= (double)fr.width + 1.0) || !(y1 >= -2.0) ||
+                !(y0 <= (double)fr.height + 1.0)) {
+                ix0 = 1; ix1 = 0;   // off screen
+            } else {
+                ix0 = (int64_t)fmax(floor(x0) - 2.0, 0.0);
+                ix1 = (int64_t)fmin(ceil(x1) + 2.0, (double)(fr.width - 1));
+                iy0 = (int64_t)fmax(floor(y0) - 2.0, 0.0);
+                iy1 = (int64_t)fmin(ceil(y1) + 2.0, (double)(fr.height - 1));
+            }
+        }
+        s_rect[0] = ix0; s_rect[1] = ix1; s_rect[2] = iy0; s_rect[3] = iy1;
+        }
+        __syncthreads();
+        const int64_t ix0 = s_rect[0], ix1 = s_rect[1], iy0 = s_rect[2], iy1 = s_rect[3];
+        if (ix0 > ix1) continue;
+        const uint32_t rw = (uint32_t)(ix1 - ix0 + 1), npx = rw * (uint32_t)(iy1 - iy0 + 1);
+        for (uint32_t k = threadIdx.x; k < npx; k += blockDim.x) {
+            const uint32_t ix = (uint32_t)ix0 + k % rw, iy = (uint32_t)iy0 + k / rw;
+            const int64_t rr = pixel_ray(F, ix, iy);
+            if (rr < 0) continue;
+            RayD ray;   // the trace's make_ray, from the per-ray table (slab needs o, 1/d)
+            ray.ox = fr.cam_pos[0]; ray.oy = fr.cam_pos[1]; ray.oz = fr.cam_pos[2];
+            ray.ix = __ldg(iv.rinv + rr); ray.iy = __ldg(iv.rinv + F.n_rays + rr);
+            ray.iz = __ldg(iv.rinv + 2 * F.n_rays + rr);
+            ray.nx = ray.ix != 0.0; ray.ny = ray.iy != 0.0; ray.nz = ray.iz != 0.0;
+            double pa, pb;
+            slab(ray, lo, hi, pa, pb);
+            if (pa > pb || !(pb > 0.0)) continue;
+            const uint32_t slot = atomicAdd(iv.ccount + rr, 1u);
+            if (slot < (uint32_t)CAND_CAP) {
+                const int64_t o = (int64_t)slot * F.n_rays + rr;
+                iv.cand_pa[o] = pa; iv.cand_pb[o] = pb; iv.cand_pid[o] = pid;
+            }
+        }
+    }
+}
+
+// Each ray's candidates in ascending (entry, pid) order, so that
+// cand_next_interval can stop at the first entry beyond its best and skip
+// the dead prefix.  One CTA per 32-ray tile: the tile's slots are staged
+// through shared memory with coalesced loads/stores (the global layout is
+// slot-major), and each warp rank-sorts four rays (rank = number of smaller
+// keys; keys are distinct: one slab per partition).
+constexpr int SORT_THREADS = 256;
+
+__global__ void __launch_bounds__(SORT_THREADS) cand_sort_kernel(FrameK F, IvBuf iv) {
+    __shared__ double s_pa[CAND_CAP][32], s_pb[CAND_CAP][32];
+    __shared__ int32_t s_pid[CAND_CAP][32];
+    __shared__ uint32_t s_n[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t n_tiles = (F.n_rays + 31) / 32;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t r0 = t * 32;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            const int64_t rr = r0 + threadIdx.x;
+            const uint32_t n = rr < F.n_rays ? iv.ccount[rr] : 0u;
+            s_n[threadIdx.x] = (n >= 2 && n <= (uint32_t)CAND_CAP) ? n : 0u;
+        }
+        __syncthreads();
+        uint32_t nmax = 0;
+        for (int k = 0; k < 32; ++k) nmax = max(nmax, s_n[k]);
+        if (nmax == 0) continue;   // CTA-uniform
+        for (uint32_t idx = threadIdx.x; idx < nmax * 32; idx += SORT_THREADS) {
+            const uint32_t slot = idx >> 5, c = idx & 31;
+            if (slot < s_n[c]) {
+                const int64_t o = (int64_t)slot * F.n_rays + r0 + c;
+                s_pa[slot][c] = iv.cand_pa[o]; s_pb[slot][c] = iv.cand_pb[o]; s_pid[slot][c] = iv.cand_pid[o];
+            }
+        }
+        __syncthreads();
+        for (int c = warp; c < 32; c += SORT_THREADS / 32) {
+            const uint32_t n = s_n[c];
+            if (n == 0) continue;   // warp-uniform
+            double pa[2], pb[2];
+            int32_t pid[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t i = lane + 32 * h;
+                const bool ok = i < n;
+                pa[h] = ok ? s_pa[i][c] : INFINITY;
+                pb[h] = ok ? s_pb[i][c] : 0.0;
+                pid[h] = ok ? s_pid[i][c] : INT_MAX;
+            }
+            uint32_t rank[2] = {0u, 0u};
+            for (uint32_t j = 0; j < n; ++j) {
+                const double qa = s_pa[j][c];   // broadcast reads
+                const int32_t qid = s_pid[j][c];
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    rank[e] += (qa < pa[e] || (qa == pa[e] && qid < pid[e])) ? 1u : 0u;
+            }
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                if (lane + 32 * h < n) {
+                    s_pa[rank[h]][c] = pa[h]; s_pb[rank[h]][c] = pb[h]; s_pid[rank[h]][c] = pid[h];
+                }
+            }
+        }
+        __syncthreads();
+        for (uint32_t idx = threadIdx.x; idx < nmax * 32; idx += SORT_THREADS) {
+            const uint32_t slot = idx >> 5, c = idx & 31;
+            if (slot < s_n[c]) {
+                const int64_t o = (int64_t)slot * F.n_rays + r0 + c;
+                iv.cand_pa[o] = s_pa[slot][c]; iv.cand_pb[o] = s_pb[slot][c]; iv.cand_pid[o] = s_pid[slot][c];
+            }
+        }
+    }
+}
+
 // Phase 1 (one thread per ray, 8x4 pixel tiles per warp): the exact
 // partition-interval sequence (K:360-391 calling next_interval K:173-230)
 // with each interval's clamped entry and the running count of the samples
@@ -934,6 +1153,13 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 }
             } else {
                 bool use_bsp = S.knodes != nullptr && !(F.f.flags & TR_FLAG_NO_BSP);
+                uint32_t n_cand = 0, dead = 0;
+                double dead_thr = -INFINITY;
+                bool cands = false;
+                if (F.use_cand) {
+                    n_cand = iv.ccount[rr];
+                    if (n_cand <= (uint32_t)CAND_CAP) { cands = true; use_bsp = false; }
+                }
                 BspTrace T;
                 if (use_bsp) bsp_begin(S, ray, T);
                 for (int attempt = 0; attempt < 2; ++attempt) {
@@ -942,7 +1168,9 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     while (true) {
                         const double excl = (last < 0) ? 0.0 : F.f.eps;
                         double a, b;
-                        const int32_t pid = use_bsp
+                        const int32_t pid = cands
+                            ? cand_next_interval(iv, F.n_rays, rr, n_cand, dead, dead_thr, t_min, excl, last, a, b)
+                            : use_bsp
                             ? bsp_next_interval<COUNT>(S, E, ray, T, t_min, excl, last, a, b)
                             : next_interval(S, E, ray, t_min, excl, last, a, b);
                         if (pid < 0) break;
@@ -1885,7 +2113,7 @@ static int bg_aux(BgAux **out) {
     return TR_OK;
 }
 
-constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4;  // rec + tail + cnt + order
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4 + 4 + 24 + CAND_CAP * 20;  // rec + tail + cnt + order + ccount + rinv + cand
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
 // ---- brick-sharded frames (tr_brick_*)
@@ -1959,7 +2187,7 @@ int64_t tr_slots_per_rank(int64_t width, int64_t height, int32_t count) {
 }
 
 int64_t tr_scratch_bytes(int64_t n_rays) {
-    return n_rays * IV_BYTES_PER_RAY + IV_FIXED_BYTES;
+    return n_rays * IV_BYTES_PER_RAY + IV_FIXED_BYTES + 16;
 }
 
 // Validation and the kernel-side views shared by tr_render_frame and the
@@ -1979,7 +2207,29 @@ static IvBuf make_iv(const TrOutputs *out, int64_t n_rays) {
     iv.tail = reinterpret_cast<double *>(iv.rec + (int64_t)IV_CAP * n_rays);
     iv.cnt = reinterpret_cast<uint32_t *>(iv.tail + n_rays);
     iv.order = iv.cnt + n_rays;
+    iv.ccount = iv.order + n_rays;
+    char *c = base + IV_FIXED_BYTES + ((n_rays * (IV_CAP * 16 + 8 + 4 + 4 + 4) + 15) / 16) * 16;
+    iv.rinv = reinterpret_cast<double *>(c);
+    iv.cand_pa = iv.rinv + 3 * n_rays;
+    iv.cand_pb = iv.cand_pa + (int64_t)CAND_CAP * n_rays;
+    iv.cand_pid = reinterpret_cast<int32_t *>(iv.cand_pb + (int64_t)CAND_CAP * n_rays);
     return iv;
+}
+
+static cudaError_t launch_cand_raster(const SceneK &S, const EpochK &E, const FrameK &F,
+                                      const IvBuf &iv, cudaStream_t st) {
+    ray_table_kernel<<<(unsigned)((F.n_rays + 255) / 256), 256, 0, st>>>(F, iv);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    int64_t grid = F.n_parts;
+    if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
+    if (grid < 1) grid = 1;
+    cand_raster_kernel<<<(unsigned)grid, 256, 0, st>>>(S, E, F, iv);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    int64_t sg = (F.n_rays + 31) / 32;
+    if (sg > (int64_t)sm_count() * 4) sg = (int64_t)sm_count() * 4;
+    cand_sort_kernel<<<(unsigned)sg, SORT_THREADS, 0, st>>>(F, iv);
+    return cudaGetLastError();
 }
 
 static int prepare_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
@@ -2016,6 +2266,7 @@ static int prepare_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const
     F.my_tiles = (F.n_tiles - frame->shard_rank + frame->shard_count - 1) / frame->shard_count;
     if (F.my_tiles < 0) F.my_tiles = 0;
     F.n_parts = (int32_t)scene->n_parts;
+    F.use_cand = (frame->mode != 0 && !(frame->flags & TR_FLAG_NO_CAND)) ? 1 : 0;
     return TR_OK;
 }
 
@@ -2103,6 +2354,10 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(work)");
         e = cudaMemsetAsync(iv.hist, 0, 552, st);   // hist, cursor, trace_ctr, ray_stats, gsel, n_bg
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
+        if (F.use_cand) {
+            if ((e = launch_cand_raster(S, E, F, iv, st)) != cudaSuccess) return cuda_fail(e, "cand_raster_kernel");
+            ++launches;
+        }
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
         const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;
         trace_fn<<<(unsigned)trace_grid, TRACE_BLOCK, 0, st>>>(S, E, F, iv, *out);
@@ -2283,6 +2538,8 @@ int tr_brick_trace(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
         (e = cudaMemsetAsync(bricks->state, 0, sizeof(TrRayState) * F.n_rays, st)) != cudaSuccess)
         return cuda_fail(e, "tr_brick_trace memset");
     if (F.n_rays == 0) return TR_OK;
+    if (F.use_cand && (e = launch_cand_raster(S, E, F, iv, st)) != cudaSuccess)
+        return cuda_fail(e, "cand_raster_kernel (bricks)");
     void (*trace_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) =
         (frame->flags & TR_FLAG_STATS) ? trace_intervals_kernel<true> : trace_intervals_kernel<false>;
     int trace_per_sm = 0;
