@@ -910,7 +910,8 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
             pb[u] = ok ? __ldg(iv.cand_pb + o) : -INFINITY;
             pid[u] = ok ? __ldg(iv.cand_pid + o) : -1;
         }
-        if (pa[0] > best_a) break;   // entries ascend: nothing later can win
+        // slots ascend by entry rounded down to float: nothing later can win
+        if ((double)__double2float_rd(pa[0]) > best_a) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (pid[u] == last || pb[u] <= thr) continue;   // also the padding (pb = -inf)
@@ -960,48 +961,52 @@ __global__ void __launch_bounds__(256) ray_table_kernel(FrameK F, IvBuf iv) {
 // so no ray's front-to-back walk sets the pass time.
 __global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv) {
     const TrFrame &fr = F.f;
-    __shared__ int64_t s_rect[4];   // ix0, ix1, iy0, iy1 (ix0 > ix1: nothing)
-    for (int32_t pid = blockIdx.x; pid < F.n_parts; pid += gridDim.x) {
-        if (!__ldg(E.active + pid)) continue;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t pid = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); pid < F.n_parts; pid += warps) {
+        if (!__ldg(E.active + pid)) continue;   // warp-uniform
         const double lo[3] = {__ldg(S.part_lo + 3 * pid), __ldg(S.part_lo + 3 * pid + 1), __ldg(S.part_lo + 3 * pid + 2)};
         const double hi[3] = {__ldg(S.part_hi + 3 * pid), __ldg(S.part_hi + 3 * pid + 1), __ldg(S.part_hi + 3 * pid + 2)};
-        __syncthreads();   // the previous partition's rectangle is read
-        if (threadIdx.x == 0) {
+        // lanes 0-7 project one box corner each
         double x0 = INFINITY, x1 = -INFINITY, y0 = INFINITY, y1 = -INFINITY;
         bool full = false;
-        for (int c = 0; c < 8; ++c) {
+        if (lane < 8) {
+            const int c = lane;
             const double v[3] = {((c & 1) ? hi[0] : lo[0]) - fr.cam_pos[0],
                                  ((c & 2) ? hi[1] : lo[1]) - fr.cam_pos[1],
                                  ((c & 4) ? hi[2] : lo[2]) - fr.cam_pos[2]};
             const double z = v[0] * fr.cam_fwd[0] + v[1] * fr.cam_fwd[1] + v[2] * fr.cam_fwd[2];
             const double len = fabs(v[0]) + fabs(v[1]) + fabs(v[2]);
-            if (!(z > 1e-6 * len)) { full = true; break; }
-            const double sx = (v[0] * fr.cam_right[0] + v[1] * fr.cam_right[1] + v[2] * fr.cam_right[2]) /
-                              z / (fr.aspect * fr.tan_half);
-            const double sy = (v[0] * fr.cam_up[0] + v[1] * fr.cam_up[1] + v[2] * fr.cam_up[2]) / z / fr.tan_half;
-            const double px = (sx + 1.0) * 0.5 * (double)fr.width - 0.5;
-            const double py = (1.0 - sy) * 0.5 * (double)fr.height - 0.5;
-            x0 = fmin(x0, px); x1 = fmax(x1, px); y0 = fmin(y0, py); y1 = fmax(y1, py);
+            if (!(z > 1e-6 * len)) {
+                full = true;
+            } else {
+                const double sx = (v[0] * fr.cam_right[0] + v[1] * fr.cam_right[1] + v[2] * fr.cam_right[2]) /
+                                  z / (fr.aspect * fr.tan_half);
+                const double sy = (v[0] * fr.cam_up[0] + v[1] * fr.cam_up[1] + v[2] * fr.cam_up[2]) / z / fr.tan_half;
+                x0 = x1 = (sx + 1.0) * 0.5 * (double)fr.width - 0.5;
+                y0 = y1 = (1.0 - sy) * 0.5 * (double)fr.height - 0.5;
+            }
         }
+        full = __any_sync(FULL, full);
+#pragma unroll
+        for (int off = 4; off > 0; off >>= 1) {
+            x0 = fmin(x0, __shfl_xor_sync(FULL, x0, off)); x1 = fmax(x1, __shfl_xor_sync(FULL, x1, off));
+            y0 = fmin(y0, __shfl_xor_sync(FULL, y0, off)); y1 = fmax(y1, __shfl_xor_sync(FULL, y1, off));
+        }
+        x0 = __shfl_sync(FULL, x0, 0); x1 = __shfl_sync(FULL, x1, 0);
+        y0 = __shfl_sync(FULL, y0, 0); y1 = __shfl_sync(FULL, y1, 0);
         int64_t ix0 = 0, ix1 = fr.width - 1, iy0 = 0, iy1 = fr.height - 1;
         if (!full) {
             if (!(x1 >= -2.0) || !(x0 <= (double)fr.width + 1.0) || !(y1 >= -2.0) ||
-                !(y0 <= (double)fr.height + 1.0)) {
-                ix0 = 1; ix1 = 0;   // off screen
-            } else {
-                ix0 = (int64_t)fmax(floor(x0) - 2.0, 0.0);
-                ix1 = (int64_t)fmin(ceil(x1) + 2.0, (double)(fr.width - 1));
-                iy0 = (int64_t)fmax(floor(y0) - 2.0, 0.0);
-                iy1 = (int64_t)fmin(ceil(y1) + 2.0, (double)(fr.height - 1));
-            }
+                !(y0 <= (double)fr.height + 1.0))
+                continue;   // off screen
+            ix0 = (int64_t)fmax(floor(x0) - 2.0, 0.0);
+            ix1 = (int64_t)fmin(ceil(x1) + 2.0, (double)(fr.width - 1));
+            iy0 = (int64_t)fmax(floor(y0) - 2.0, 0.0);
+            iy1 = (int64_t)fmin(ceil(y1) + 2.0, (double)(fr.height - 1));
         }
-        s_rect[0] = ix0; s_rect[1] = ix1; s_rect[2] = iy0; s_rect[3] = iy1;
-        }
-        __syncthreads();
-        const int64_t ix0 = s_rect[0], ix1 = s_rect[1], iy0 = s_rect[2], iy1 = s_rect[3];
-        if (ix0 > ix1) continue;
         const uint32_t rw = (uint32_t)(ix1 - ix0 + 1), npx = rw * (uint32_t)(iy1 - iy0 + 1);
-        for (uint32_t k = threadIdx.x; k < npx; k += blockDim.x) {
+        for (uint32_t k = lane; k < npx; k += 32) {
             const uint32_t ix = (uint32_t)ix0 + k % rw, iy = (uint32_t)iy0 + k / rw;
             const int64_t rr = pixel_ray(F, ix, iy);
             if (rr < 0) continue;
@@ -1016,7 +1021,7 @@ __global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E,
             const uint32_t slot = atomicAdd(iv.ccount + rr, 1u);
             if (slot < (uint32_t)CAND_CAP) {
                 const int64_t o = (int64_t)slot * F.n_rays + rr;
-                iv.cand_pa[o] = pa; iv.cand_pb[o] = pb; iv.cand_pid[o] = pid;
+                iv.cand_pa[o] = pa; iv.cand_pb[o] = pb; iv.cand_pid[o] = (int32_t)pid;
             }
         }
     }
@@ -1024,73 +1029,106 @@ __global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E,
 
 // Each ray's candidates in ascending (entry, pid) order, so that
 // cand_next_interval can stop at the first entry beyond its best and skip
-// the dead prefix.  One CTA per 32-ray tile: the tile's slots are staged
-// through shared memory with coalesced loads/stores (the global layout is
-// slot-major), and each warp rank-sorts four rays (rank = number of smaller
-// keys; keys are distinct: one slab per partition).
+// the dead prefix.  One warp per ray: a bitonic network over the lanes for
+// up to 32 slabs, a rank sort (rank = number of smaller keys) beyond.  Keys
+// are distinct (one slab per partition).
+__device__ __forceinline__ bool cand_less(double a, int32_t ia, double b, int32_t ib) {
+    return a < b || (a == b && ia < ib);
+}
+
+// order-preserving bits of a float
+__device__ __forceinline__ uint32_t float_key(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 constexpr int SORT_THREADS = 256;
 
 __global__ void __launch_bounds__(SORT_THREADS) cand_sort_kernel(FrameK F, IvBuf iv) {
-    __shared__ double s_pa[CAND_CAP][32], s_pb[CAND_CAP][32];
-    __shared__ int32_t s_pid[CAND_CAP][32];
-    __shared__ uint32_t s_n[32];
+    // a 32-ray tile staged through shared memory (coalesced global slot rows;
+    // rows padded to 33 so a warp reading one ray's column hits 32 banks)
+    __shared__ double s_pa[CAND_CAP][33], s_pb[CAND_CAP][33];
+    __shared__ int32_t s_pid[CAND_CAP][33];
+    __shared__ uint32_t s_n[32], s_nmax;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t n_tiles = (F.n_rays + 31) / 32;
     for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
         const int64_t r0 = t * 32;
         __syncthreads();
-        if (threadIdx.x < 32) {
-            const int64_t rr = r0 + threadIdx.x;
-            const uint32_t n = rr < F.n_rays ? iv.ccount[rr] : 0u;
-            s_n[threadIdx.x] = (n >= 2 && n <= (uint32_t)CAND_CAP) ? n : 0u;
+        if (warp == 0) {
+            const int64_t rr = r0 + lane;
+            uint32_t n = rr < F.n_rays ? iv.ccount[rr] : 0u;
+            n = (n >= 2 && n <= (uint32_t)CAND_CAP) ? n : 0u;
+            s_n[lane] = n;
+            uint32_t m = n;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(FULL, m, off));
+            if (lane == 0) s_nmax = m;
         }
         __syncthreads();
-        uint32_t nmax = 0;
-        for (int k = 0; k < 32; ++k) nmax = max(nmax, s_n[k]);
+        const uint32_t nmax = s_nmax;
         if (nmax == 0) continue;   // CTA-uniform
-        for (uint32_t idx = threadIdx.x; idx < nmax * 32; idx += SORT_THREADS) {
-            const uint32_t slot = idx >> 5, c = idx & 31;
-            if (slot < s_n[c]) {
-                const int64_t o = (int64_t)slot * F.n_rays + r0 + c;
-                s_pa[slot][c] = iv.cand_pa[o]; s_pb[slot][c] = iv.cand_pb[o]; s_pid[slot][c] = iv.cand_pid[o];
+        for (uint32_t slot = warp; slot < nmax; slot += SORT_THREADS / 32) {
+            if ((uint32_t)slot < s_n[lane]) {
+                const int64_t o = (int64_t)slot * F.n_rays + r0 + lane;
+                s_pa[slot][lane] = iv.cand_pa[o]; s_pb[slot][lane] = iv.cand_pb[o]; s_pid[slot][lane] = iv.cand_pid[o];
             }
         }
         __syncthreads();
         for (int c = warp; c < 32; c += SORT_THREADS / 32) {
             const uint32_t n = s_n[c];
             if (n == 0) continue;   // warp-uniform
-            double pa[2], pb[2];
-            int32_t pid[2];
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const uint32_t i = lane + 32 * h;
-                const bool ok = i < n;
-                pa[h] = ok ? s_pa[i][c] : INFINITY;
-                pb[h] = ok ? s_pb[i][c] : 0.0;
-                pid[h] = ok ? s_pid[i][c] : INT_MAX;
-            }
-            uint32_t rank[2] = {0u, 0u};
-            for (uint32_t j = 0; j < n; ++j) {
-                const double qa = s_pa[j][c];   // broadcast reads
-                const int32_t qid = s_pid[j][c];
-#pragma unroll
-                for (int e = 0; e < 2; ++e)
-                    rank[e] += (qa < pa[e] || (qa == pa[e] && qid < pid[e])) ? 1u : 0u;
-            }
-            __syncwarp();
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                if (lane + 32 * h < n) {
-                    s_pa[rank[h]][c] = pa[h]; s_pb[rank[h]][c] = pb[h]; s_pid[rank[h]][c] = pid[h];
+            if (n <= 32) {
+                // bitonic network on 32-bit keys: the entry rounded down to
+                // float (monotone: a later slot never has a smaller entry than
+                // an earlier slot's key -- all cand_next_interval's early exit
+                // needs), the slot index as payload
+                const bool ok = (uint32_t)lane < n;
+                uint32_t key = ok ? float_key(__double2float_rd(s_pa[lane][c])) : 0xffffffffu;
+                int32_t idx = lane;
+                for (int k = 2; k <= 32; k <<= 1) {
+                    for (int j = k >> 1; j > 0; j >>= 1) {
+                        const uint32_t qk = __shfl_xor_sync(FULL, key, j);
+                        const int32_t qi = __shfl_xor_sync(FULL, idx, j);
+                        const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+                        const bool qless = qk < key || (qk == key && qi < idx);
+                        if ((lower == up) ? qless : !qless) { key = qk; idx = qi; }
+                    }
                 }
+                double sa = 0.0, sb = 0.0;
+                int32_t sid = 0;
+                if (ok) { sa = s_pa[idx][c]; sb = s_pb[idx][c]; sid = s_pid[idx][c]; }
+                __syncwarp();
+                if (ok) { s_pa[lane][c] = sa; s_pb[lane][c] = sb; s_pid[lane][c] = sid; }
+            } else {   // rank sort on the exact keys (entry, pid)
+                double pa[2], pb[2];
+                int32_t pid[2];
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t i = lane + 32 * h;
+                    const bool ok = i < n;
+                    pa[h] = ok ? s_pa[i][c] : INFINITY;
+                    pb[h] = ok ? s_pb[i][c] : 0.0;
+                    pid[h] = ok ? s_pid[i][c] : INT_MAX;
+                }
+                uint32_t rank[2] = {0u, 0u};
+                for (uint32_t j = 0; j < n; ++j) {
+                    const double qa = s_pa[j][c];
+                    const int32_t qid = s_pid[j][c];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) rank[e] += cand_less(qa, qid, pa[e], pid[e]) ? 1u : 0u;
+                }
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                    if (lane + 32 * h < n) { s_pa[rank[h]][c] = pa[h]; s_pb[rank[h]][c] = pb[h]; s_pid[rank[h]][c] = pid[h]; }
             }
         }
         __syncthreads();
-        for (uint32_t idx = threadIdx.x; idx < nmax * 32; idx += SORT_THREADS) {
-            const uint32_t slot = idx >> 5, c = idx & 31;
-            if (slot < s_n[c]) {
-                const int64_t o = (int64_t)slot * F.n_rays + r0 + c;
-                iv.cand_pa[o] = s_pa[slot][c]; iv.cand_pb[o] = s_pb[slot][c]; iv.cand_pid[o] = s_pid[slot][c];
+        for (uint32_t slot = warp; slot < nmax; slot += SORT_THREADS / 32) {
+            if ((uint32_t)slot < s_n[lane]) {
+                const int64_t o = (int64_t)slot * F.n_rays + r0 + lane;
+                iv.cand_pa[o] = s_pa[slot][lane]; iv.cand_pb[o] = s_pb[slot][lane]; iv.cand_pid[o] = s_pid[slot][lane];
             }
         }
     }
@@ -2221,13 +2259,13 @@ static cudaError_t launch_cand_raster(const SceneK &S, const EpochK &E, const Fr
     ray_table_kernel<<<(unsigned)((F.n_rays + 255) / 256), 256, 0, st>>>(F, iv);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    int64_t grid = F.n_parts;
+    int64_t grid = (F.n_parts + 7) / 8;   // a warp per partition
     if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
     if (grid < 1) grid = 1;
     cand_raster_kernel<<<(unsigned)grid, 256, 0, st>>>(S, E, F, iv);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    int64_t sg = (F.n_rays + 31) / 32;
-    if (sg > (int64_t)sm_count() * 4) sg = (int64_t)sm_count() * 4;
+    int64_t sg = (F.n_rays + 31) / 32;   // a CTA per 32-ray tile
+    if (sg > (int64_t)sm_count() * 6) sg = (int64_t)sm_count() * 6;
     cand_sort_kernel<<<(unsigned)sg, SORT_THREADS, 0, st>>>(F, iv);
     return cudaGetLastError();
 }
