@@ -2394,7 +2394,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(hist)");
         if (F.use_cand) {
             if ((e = launch_cand_raster(S, E, F, iv, st)) != cudaSuccess) return cuda_fail(e, "cand_raster_kernel");
-            ++launches;
+            launches += 3;   // ray table, raster, sort
         }
         const int64_t tg = (F.n_rays + TRACE_BLOCK - 1) / TRACE_BLOCK;
         const int64_t trace_grid = (tg < (int64_t)sm_count() * trace_per_sm) ? tg : (int64_t)sm_count() * trace_per_sm;

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Full measurement session -> gpurun_out/*_TAG*: GPU tests, smoke, bench line,
 # reference arm, modes, launch list, ncu captures (radial59 march + trace,
-# radial272 march), kernel statistics, e2e breakdown.
+# radial272 march; the candidate raster, sort and trace), kernel statistics, e2e breakdown.
 TAG=${1:-r01}
 mkdir -p gpurun_out
 { free -g; nproc; nvidia-smi --query-gpu=name,memory.total,clocks.max.sm --format=csv; } > gpurun_out/box_$TAG.txt 2>&1
@@ -16,7 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 6 -c 2 \
   -o gpurun_out/prof_march_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:trace -s 3 -c 1 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:"trace|cand_" -s 9 -c 3 \
   -o gpurun_out/prof_trace_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 2 -c 2 \
   -o gpurun_out/prof_march272_$TAG python bench.py --scene radial272 --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
