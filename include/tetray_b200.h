@@ -429,6 +429,10 @@ int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset);
 
 const char *tr_last_error(void);
 int tr_abi_version(void);
+/* sizeof of TrDeviceScene, TrEpoch, TrFrame, TrOutputs, TrBricks, TrRayState,
+ * TrTetRecord, TrPNode, TrPLeaf, TrBNode, TrKNode (the first n; bindings check
+ * their struct layouts against it). */
+int tr_struct_sizes(int64_t *out, int32_t n);
 
 #ifdef __cplusplus
 }

@@ -178,6 +178,7 @@ _SIGNATURES = [
     ("tr_kernel_stats", C.c_int, [c_i64p, C.c_int32, C.c_int32]),
     ("tr_last_error", C.c_char_p, []),
     ("tr_abi_version", C.c_int, []),
+    ("tr_struct_sizes", C.c_int, [C.POINTER(C.c_int64), C.c_int32]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

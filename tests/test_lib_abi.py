@@ -42,6 +42,16 @@ def test_record_layouts_match_header(L):
     assert L.lib().tr_abi_version() == 1
 
 
+def test_ctypes_structs_match_the_c_layouts(L):
+    sizes = (C.c_int64 * 11)()
+    assert L.lib().tr_struct_sizes(sizes, 11) == 0
+    want = [C.sizeof(L.TrDeviceScene), C.sizeof(L.TrEpoch), C.sizeof(L.TrFrame),
+            C.sizeof(L.TrOutputs), C.sizeof(L.TrBricks), L.RAY_STATE_BYTES,
+            L.TET_RECORD_DTYPE.itemsize, L.PNODE_DTYPE.itemsize, L.PLEAF_DTYPE.itemsize,
+            L.BNODE_DTYPE.itemsize, L.KNODE_DTYPE.itemsize]
+    assert list(sizes) == want
+
+
 def test_errors_are_reported_not_aborted(L):
     lib = L.lib()
     rc = lib.tr_render_frame(None, None, None, None, None)
