@@ -255,6 +255,20 @@ typedef struct TrEpoch {
                                     exponent, K:27); only read in mode 2 */
 } TrEpoch;
 
+/* One metadata epoch in one call (R:169; scene.py:78-82): packs sigma, the TF
+ * table and the activity bits into the page-locked host_buf, copies them to
+ * dev_buf (tr_epoch_bytes(...) bytes) on `stream` and computes the per-partition
+ * steps there (steps_on_device: tr_epoch_steps_device, the caller having
+ * checked the restated pow domain; else tr_epoch_steps on the host and the
+ * whole buffer is copied).  Fills `out` with the device section pointers. */
+int64_t tr_epoch_bytes(int64_t n_parts, int64_t n_tf, int64_t n_bnodes, int64_t n_knodes);
+int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8_t *active,
+                    const uint8_t *bnode_active, int64_t n_bnodes, const uint8_t *knode_active,
+                    int64_t n_knodes, const double *tf_table, int64_t n_tf, double tf_lo,
+                    double tf_hi, double s1, double s2, double p, int32_t steps_on_device,
+                    void *host_buf, void *dev_buf, int64_t buf_bytes, int32_t *inexact,
+                    TrEpoch *out, int64_t *h2d_bytes, void *stream);
+
 /* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
 typedef struct TrFrame {
     double cam_pos[3], cam_right[3], cam_up[3], cam_fwd[3];
@@ -278,6 +292,7 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_BG_WRITER 0x40000 /* host framebuffer: trace writes background pixels itself (testing) */
 /* flags bits 20-22: trace CTAs per SM (0 = occupancy maximum; tuning) */
 #define TR_FLAG_NO_CAND 0x800000 /* modes 1/2: intervals by the per-ray BSP walk, not the candidate raster (testing) */
+#define TR_FLAG_FORCE_CAND 0x1000000 /* the candidate raster also above 1M pixels (default there: the BSP walk) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */

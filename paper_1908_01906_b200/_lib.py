@@ -143,6 +143,11 @@ _SIGNATURES = [
                                     C.c_void_p]),
     ("tr_epoch_steps_device", C.c_int, [C.c_int64, C.c_void_p, C.c_double, C.c_double, C.c_double,
                                         C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_epoch_bytes", C.c_int64, [C.c_int64, C.c_int64, C.c_int64, C.c_int64]),
+    ("tr_epoch_upload", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                  C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_double,
+                                  C.c_double, C.c_double, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
+                                  C.c_void_p, C.POINTER(TrEpoch), C.POINTER(C.c_int64), C.c_void_p]),
     ("tr_epoch_steps", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),

@@ -16,6 +16,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstring>
 #include <string>
 
 #include "glibc_pow.cuh"
@@ -252,5 +253,74 @@ extern "C" int tr_tf_meta_device(int64_t n_parts, const double *vrange, const do
     cudaFreeAsync(d_err, st);
     if (e != cudaSuccess) return cuda_fail(e, "tr_tf_meta_device");
     if (h_err) return tr_fail(TR_EINVAL, "tr_tf_meta_device: invalid value range (min > max)");
+    return TR_OK;
+}
+
+namespace {
+inline int64_t a64(int64_t x) { return (x + 63) / 64 * 64; }
+}
+
+// The epoch's device buffer, 64-B aligned sections:
+//   step f64[P] | (step, step / s1) f64[P,2] | sigma f64[P] | tf f64[n_tf,4] |
+//   active u8[P] | bnode activity u8[n_b] | knode activity u8[n_k]
+extern "C" int64_t tr_epoch_bytes(int64_t n_parts, int64_t n_tf, int64_t n_bnodes,
+                                  int64_t n_knodes) {
+    const int64_t o_ratio = a64(8 * n_parts), o_sigma = a64(o_ratio + 16 * n_parts);
+    const int64_t o_tf = a64(o_sigma + 8 * n_parts), o_act = a64(o_tf + 32 * n_tf);
+    const int64_t o_bact = a64(o_act + n_parts), o_kact = a64(o_bact + n_bnodes);
+    return a64(o_kact + n_knodes);
+}
+
+extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8_t *active,
+                               const uint8_t *bnode_active, int64_t n_bnodes,
+                               const uint8_t *knode_active, int64_t n_knodes,
+                               const double *tf_table, int64_t n_tf, double tf_lo, double tf_hi,
+                               double s1, double s2, double p, int32_t steps_on_device,
+                               void *host_buf, void *dev_buf, int64_t buf_bytes, int32_t *inexact,
+                               TrEpoch *out, int64_t *h2d_bytes, void *stream) {
+    if (n_parts < 1 || !sigma || !active || !tf_table || n_tf < 2 || !host_buf || !dev_buf || !out ||
+        n_bnodes < 0 || n_knodes < 0 || (n_bnodes && !bnode_active) || (n_knodes && !knode_active) ||
+        (steps_on_device && !inexact))
+        return tr_fail(TR_EINVAL, "tr_epoch_upload: invalid arguments");
+    if (buf_bytes < tr_epoch_bytes(n_parts, n_tf, n_bnodes, n_knodes))
+        return tr_fail(TR_EINVAL, "tr_epoch_upload: buffer too small");
+    const int64_t o_ratio = a64(8 * n_parts), o_sigma = a64(o_ratio + 16 * n_parts);
+    const int64_t o_tf = a64(o_sigma + 8 * n_parts), o_act = a64(o_tf + 32 * n_tf);
+    const int64_t o_bact = a64(o_act + n_parts), o_kact = a64(o_bact + n_bnodes);
+    const int64_t nbytes = a64(o_kact + n_knodes);
+    char *h = static_cast<char *>(host_buf), *d = static_cast<char *>(dev_buf);
+    std::memcpy(h + o_sigma, sigma, 8 * n_parts);
+    std::memcpy(h + o_tf, tf_table, 32 * n_tf);
+    std::memcpy(h + o_act, active, n_parts);
+    if (n_bnodes) std::memcpy(h + o_bact, bnode_active, n_bnodes);
+    if (n_knodes) std::memcpy(h + o_kact, knode_active, n_knodes);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e;
+    if (steps_on_device) {
+        // only sigma, the TF and the activity bits cross PCIe
+        e = cudaMemcpyAsync(d + o_sigma, h + o_sigma, nbytes - o_sigma, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "tr_epoch_upload H2D");
+        if (int rc = tr_epoch_steps_device(n_parts, reinterpret_cast<const double *>(d + o_sigma), s1,
+                                           s2, p, reinterpret_cast<double *>(d),
+                                           reinterpret_cast<double *>(d + o_ratio), inexact, stream))
+            return rc;
+        if (h2d_bytes) *h2d_bytes = nbytes - o_sigma;
+    } else {
+        if (int rc = tr_epoch_steps(n_parts, sigma, s1, s2, p, reinterpret_cast<double *>(h),
+                                    reinterpret_cast<double *>(h + o_ratio)))
+            return rc;
+        e = cudaMemcpyAsync(d, h, nbytes, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return cuda_fail(e, "tr_epoch_upload H2D");
+        if (h2d_bytes) *h2d_bytes = nbytes;
+    }
+    out->active = reinterpret_cast<const uint8_t *>(d + o_act);
+    out->bnode_active = reinterpret_cast<const uint8_t *>(d + o_bact);
+    out->step = reinterpret_cast<const double *>(d);
+    out->tf_table = reinterpret_cast<const double *>(d + o_tf);
+    out->n_tf = n_tf;
+    out->tf_lo = tf_lo;
+    out->tf_hi = tf_hi;
+    out->knode_active = reinterpret_cast<const uint8_t *>(d + o_kact);
+    out->step_ratio = reinterpret_cast<const double *>(d + o_ratio);
     return TR_OK;
 }

@@ -224,53 +224,30 @@ class Epoch:
         table = np.ascontiguousarray(tf.table, dtype=np.float64)
         self.n_tf = int(table.shape[0])
         self.tf_lo, self.tf_hi = float(tf.domain[0]), float(tf.domain[1])
-        def a64(x):  # 64-B aligned sections (the kernel reads the TF with 16-B loads)
-            return (x + 63) // 64 * 64
-        # step f64[P] | (step, step / s1) f64[P,2] | sigma f64[P] | tf | active | node activity
-        o_ratio = a64(8 * P)
-        o_sigma = a64(o_ratio + 16 * P)
-        o_tf = a64(o_sigma + 8 * P)
-        o_act = a64(o_tf + table.nbytes)
-        o_bact = a64(o_act + P)
-        o_kact = a64(o_bact + dev.n_bnodes)
-        nbytes = a64(o_kact + dev.n_knodes)
-        host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-        hv = host.numpy()
-        hp = host.data_ptr()
-        hv[o_sigma:o_sigma + 8 * P] = sig.view(np.uint8)
-        hv[o_tf:o_tf + table.nbytes] = table.view(np.uint8).reshape(-1)
-        hv[o_act:o_act + P] = act
-        hv[o_bact:o_bact + dev.n_bnodes] = bact
-        hv[o_kact:o_kact + dev.n_knodes] = kact
-        self.host = host
-        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev.device)
-        base = self.buf.data_ptr()
         s1, s2, pw = float(params.s1), float(params.s2), float(params.p)
-        if _steps_on_device(sig, pw):
-            # per-partition step (K:20-22) and exponent s / s1 (K:27) computed
-            # on the device from sigma with the restated glibc pow; only
-            # sigma, the TF and the activity bits cross PCIe
-            self.buf[o_sigma:].copy_(host[o_sigma:], non_blocking=True)
-            self.h2d_bytes = nbytes - o_sigma
-            flag = dev.epoch_flag()   # set only for entries outside the restated domain
-            stream = torch.cuda.current_stream(dev.device)
-            _lib.check(_lib.lib().tr_epoch_steps_device(
-                P, C.c_void_p(base + o_sigma), s1, s2, pw, C.c_void_p(base), C.c_void_p(base + o_ratio),
-                C.c_void_p(flag.data_ptr()), C.c_void_p(stream.cuda_stream)), "tr_epoch_steps_device")
-            self._flag = flag
-            self._step_dev = True
-        else:
-            # host glibc pow, written into the upload buffer
-            _lib.check(_lib.lib().tr_epoch_steps(P, _lib.ptr(sig, C.c_double), s1, s2, pw, hp,
-                                                 hp + o_ratio), "tr_epoch_steps")
-            self.buf.copy_(host, non_blocking=True)
-            self.h2d_bytes = nbytes
-            self._step_dev = False
-        self.desc = _lib.TrEpoch(active=base + o_act, bnode_active=base + o_bact, step=base,
-                                 tf_table=base + o_tf, n_tf=self.n_tf, tf_lo=self.tf_lo,
-                                 tf_hi=self.tf_hi, knode_active=base + o_kact,
-                                 step_ratio=base + o_ratio)
+        # one pinned staging buffer + one device buffer; sections and upload
+        # in C (tr_epoch_upload; layout in tr_epoch_bytes)
+        L = _lib.lib()
+        nbytes = int(L.tr_epoch_bytes(P, self.n_tf, dev.n_bnodes, dev.n_knodes))
+        self.host = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        self.buf = torch.empty(nbytes, dtype=torch.uint8, device=dev.device)
+        # step sizes (K:20-22) and exponents (K:27) on the device when every
+        # |min(sigma, 1) - 1| ** p is on the restated glibc pow's path
+        self._step_dev = _steps_on_device(sig, pw)
+        self._flag = dev.epoch_flag()
+        self.desc = _lib.TrEpoch()
+        h2d = C.c_int64(0)
+        stream = torch.cuda.current_stream(dev.device)
+        _lib.check(L.tr_epoch_upload(
+            P, sig.ctypes.data, act.ctypes.data, bact.ctypes.data, dev.n_bnodes, kact.ctypes.data,
+            dev.n_knodes, table.ctypes.data, self.n_tf, self.tf_lo, self.tf_hi, s1, s2, pw,
+            1 if self._step_dev else 0, self.host.data_ptr(), self.buf.data_ptr(), nbytes,
+            self._flag.data_ptr(), C.byref(self.desc), C.byref(h2d), stream.cuda_stream),
+            "tr_epoch_upload")
+        self.h2d_bytes = int(h2d.value)
         self._P = P
+        # the copy is not torch's: keep the staging buffer alive until it has run
+        dev.hold_until_done(self.host, stream)
 
     @property
     def step_host(self) -> np.ndarray:
@@ -503,6 +480,17 @@ class DeviceScene:
         else:
             self._epochs.move_to_end(key)
         return ep
+
+    def hold_until_done(self, obj, stream) -> None:
+        """Keep `obj` (e.g. a pinned staging buffer read by an async copy
+        torch does not track) referenced until `stream` passes this point."""
+        torch = _torch()
+        q = self.__dict__.setdefault("_inflight", [])
+        while q and q[0][0].query():
+            q.pop(0)
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        q.append((ev, obj))
 
     def epoch_flag(self):
         """int32 device word tr_epoch_steps_device sets on an inexact entry (shared)."""
