@@ -899,8 +899,8 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
     // skip the prefix whose exits are <= thr: still dead while thr >= the
     // threshold they were skipped at (fl(fl(b - eps) + eps) can step back an ulp)
     if (thr < dead_thr) dead = 0;
-    while (dead < n && __ldg(iv.cand_pb + (int64_t)dead * n_rays + rr) <= thr) ++dead;
     dead_thr = thr;
+    bool prefix = true;   // still in the run of dead slots from `dead`
     for (uint32_t i0 = dead; i0 < n; i0 += 4) {
         double pa[4], pb[4];
         int32_t pid[4];
@@ -916,7 +916,12 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
         if ((double)__double2float_rd(pa[0]) > best_a) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            if (pid[u] == last || pb[u] <= thr) continue;   // also the padding (pb = -inf)
+            if (pb[u] <= thr) {   // dead for good (also the padding, pb = -inf)
+                if (prefix) dead = min(i0 + u + 1, n);
+                continue;
+            }
+            prefix = false;
+            if (pid[u] == last) continue;
             const double a_cl = (pa[u] > t_min) ? pa[u] : t_min;
             if (a_cl >= INFINITY) continue;   // t_max = inf (K:366)
             if (a_cl < best_a || (a_cl == best_a && pid[u] < best)) { best = pid[u]; best_a = a_cl; best_b = pb[u]; }
@@ -2284,8 +2289,9 @@ static cudaError_t launch_cand_raster(const SceneK &S, const EpochK &E, const Fr
     if (grid < 1) grid = 1;
     cand_raster_kernel<<<(unsigned)grid, 256, 0, st>>>(S, E, G, iv);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    int64_t sg = (F.n_rays + 31) / 32;   // a CTA per 32-ray tile
-    if (sg > (int64_t)sm_count() * 6) sg = (int64_t)sm_count() * 6;
+    // a CTA per 32-ray tile, no grid stride: empty tiles retire at once and
+    // the scheduler refills their slots
+    const int64_t sg = (F.n_rays + 31) / 32;
     cand_sort_kernel<<<(unsigned)sg, SORT_THREADS, 0, st>>>(F, iv);
     return cudaGetLastError();
 }
