@@ -2280,10 +2280,10 @@ static cudaError_t launch_cand_raster(const SceneK &S, const EpochK &E, const Fr
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     FrameK G = F;
-    // warps per partition rectangle ~ pixels of the chunk's band / 32K (8 at
+    // warps per partition rectangle ~ pixels of the chunk's band / 256K (1 at
     // 512^2; rectangles grow with the frame, so large frames spread wider)
     const int64_t rows = (F.n_rays / 32 + F.tiles_x - 1) / F.tiles_x * TILE_H;
-    G.raster_sub = (int32_t)std::min<int64_t>(std::max<int64_t>(F.f.width * rows / 32768, 1), 64);
+    G.raster_sub = (int32_t)std::min<int64_t>(std::max<int64_t>(F.f.width * rows / 262144, 1), 64);
     int64_t grid = (F.n_parts * G.raster_sub + 7) / 8;
     if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
     if (grid < 1) grid = 1;
