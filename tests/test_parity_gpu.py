@@ -82,10 +82,13 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     for mode in modes:
         ref = orc.render(cam, mode, par, jitter=jitter)
-        # default; no grid, no BSP, pairwise leaf scan; register-state
-        # kernel (0x80); lane groups of 2 / 8 / 16 (32 with 0x80); register
-        # budgets of 4 / 2 / 3 CTAs per SM -- every variant renders the same frame
-        for flags in (0, 2, 8, 0x40, 0x80, 0x100, 0x300, 0x400, 0x580, 0x1000, 0x2000, 0x3000):
+        # default (candidate raster); no grid; pairwise leaf scan;
+        # register-state kernel (0x80); lane groups of 2 / 8 / 16 (32 with
+        # 0x80); register budgets of 4 / 2 / 3 CTAs per SM; the BSP walk
+        # (0x800000) and the BVH next_interval (0x800008) instead of the
+        # raster -- every variant renders the same frame
+        for flags in (0, 2, 0x40, 0x80, 0x100, 0x300, 0x400, 0x580, 0x1000, 0x2000, 0x3000,
+                      0x800000, 0x800008):
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 
@@ -96,7 +99,7 @@ def test_radial59_benchmark_scene(B, golden, mode):
     sc, orc = scene_of(B, "radial59")
     cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
     g = golden["frames"][f"radial59/{mode}"]
-    for flags in (0, 0x80, 0x1000, 0x3000):
+    for flags in (0, 0x80, 0x1000, 0x3000, 0x800000):
         fb, st = B.render(sc, cam, mode, par, flags=flags)
         _check_radial59(fb, st, g, orc, cam, mode, par)
 
@@ -139,6 +142,24 @@ def test_chunked_frame_equals_single_chunk(B, monkeypatch, staged):
         assert one[1].partitions_visited_mean == many[1].partitions_visited_mean
         if mode != "reference":
             assert np.array_equal(one[1].per_partition_samples, many[1].per_partition_samples)
+
+
+def test_large_frames_candidate_raster_equals_bsp_walk(B):
+    """Above 1M pixels the BSP walk is the default; the forced candidate
+    raster (rectangles split over warps, multi-chunk) gives the same frame."""
+    from paper_1908_01906_b200 import device as DV
+    sc, _ = scene_of(B, "radial16")
+    c0 = C.camera(B, "radial16")
+    cam = B.Camera(position=c0.position, look_at=c0.look_at, up=c0.up, fov_y_deg=c0.fov_y_deg,
+                   width=1283, height=1021)   # ragged tiles, > 1M pixels
+    par = C.params(B, "radial16")
+    for mode in ("skip", "skip-adaptive"):
+        a = B.render(sc, cam, mode, par)
+        b = B.render(sc, cam, mode, par, flags=0x1000000)
+        assert np.array_equal(a[0].rgba, b[0].rgba)
+        assert np.array_equal(a[0].samples, b[0].samples)
+        assert np.array_equal(a[1].per_partition_samples, b[1].per_partition_samples)
+        assert a[1].partitions_visited_mean == b[1].partitions_visited_mean
 
 
 def _check_radial59(fb, st, g, orc, cam, mode, par):
