@@ -74,3 +74,32 @@ def test_device_restatement_bit_identical_to_libm(L):
         restated = np.abs(y * np.log(x)) < 500.0   # glibc's main path (no under/overflow)
     assert np.array_equal(got[restated], want[restated])
     assert np.array_equal(ca_got[x <= 1.0], ca_want[x <= 1.0])
+
+
+def test_epoch_domain_precheck_is_conservative(L):
+    """device._steps_on_device (the numpy precheck that sends an epoch's step
+    sizes to the device) only accepts sigma vectors whose every
+    |min(sigma, 1) - 1| ** p the restatement evaluates exactly -- or that
+    the kernel's own x == 0 / x == 1 shortcuts cover -- and the results
+    equal libm's."""
+    from paper_1908_01906_b200 import device as DV
+    lib = L.lib()
+    ex = C.c_int32()
+    rng = np.random.default_rng(11)
+    cases = [rng.uniform(0.0, 1.0, 64), rng.uniform(-0.5, 2.0, 64), np.array([0.0, 1.0, 2.0, 0.5]),
+             np.array([1.0 - 2.0 ** -52, 2.0 ** -1074, 1e-300, 0.999999]), rng.uniform(0.0, 1e-12, 64),
+             np.array([np.nan, 0.5]), np.array([-1e300, 0.5]), np.array([np.inf])]
+    accepted = 0
+    for sig in cases:
+        for p in (1.0, 2.0, 3.7, 11.0, 40.0, 200.0, 1e6):
+            if not DV._steps_on_device(sig, p):
+                continue
+            accepted += 1
+            for s in sig.tolist():
+                x = abs(min(s, 1.0) - 1.0)
+                if x in (0.0, 1.0):
+                    continue
+                r = lib.tr_pow_glibc_host(x, p, C.byref(ex))
+                assert ex.value == 1, (s, p)
+                assert r == x ** p
+    assert accepted > 10
