@@ -926,6 +926,8 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
             if (a_cl >= INFINITY) continue;   // t_max = inf (K:366)
             if (a_cl < best_a || (a_cl == best_a && pid[u] < best)) { best = pid[u]; best_a = a_cl; best_b = pb[u]; }
         }
+        // the group's last key already bounds every later slot: no next load
+        if (i0 + 3 < n && (double)__double2float_rd(pa[3]) > best_a) break;
     }
     ra = best_a;
     rb = best_b;
