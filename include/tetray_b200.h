@@ -327,6 +327,11 @@ typedef struct TrOutputs {
  * pixel straight into the caller's host framebuffer over PCIe while it runs
  * (render() does this; no separate device->host copy after the frame). */
 int tr_host_device_pointer(void *host, void **dev);
+/* Stream-ordered memset / copy (cudaMemsetAsync, cudaMemcpyAsync with
+ * cudaMemcpyDefault): the per-frame counter reset and read-back without a
+ * framework dispatcher in between. */
+int tr_memset_async(void *dst, int32_t value, int64_t bytes, void *stream);
+int tr_copy_async(void *dst, const void *src, int64_t bytes, void *stream);
 
 /* Scratch bytes for n_rays rays in one chunk (pass W*H rounded up to 32). */
 int64_t tr_scratch_bytes(int64_t n_rays);

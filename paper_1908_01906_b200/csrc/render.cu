@@ -2552,6 +2552,18 @@ int tr_pow_glibc_batch(int64_t n, const double *x, const double *y, double *out,
     return TR_OK;
 }
 
+int tr_memset_async(void *dst, int32_t value, int64_t bytes, void *stream) {
+    if (!dst || bytes < 0) return tr_fail(TR_EINVAL, "tr_memset_async: invalid arguments");
+    cudaError_t e = cudaMemsetAsync(dst, value, (size_t)bytes, (cudaStream_t)stream);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "cudaMemsetAsync");
+}
+
+int tr_copy_async(void *dst, const void *src, int64_t bytes, void *stream) {
+    if (!dst || !src || bytes < 0) return tr_fail(TR_EINVAL, "tr_copy_async: invalid arguments");
+    cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, (cudaStream_t)stream);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "cudaMemcpyAsync");
+}
+
 int tr_host_device_pointer(void *host, void **dev) {
     if (!host || !dev) return tr_fail(TR_EINVAL, "tr_host_device_pointer: null");
     cudaError_t e = cudaHostGetDevicePointer(dev, host, 0);

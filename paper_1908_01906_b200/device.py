@@ -260,12 +260,21 @@ class Epoch:
 DIRECT_HOST_OUTPUTS = os.environ.get("TETRAY_B200_STAGED_OUTPUTS", "0") != "1"
 
 
+_HOST_DEV: dict = {}   # page-locked block address -> device address (blocks are reused)
+
+
 def host_device_pointer(t) -> int:
     """Device address of a page-locked (pin_memory) host tensor."""
-    p = C.c_void_p()
-    _lib.check(_lib.lib().tr_host_device_pointer(C.c_void_p(t.data_ptr()), C.byref(p)),
-               "tr_host_device_pointer")
-    return int(p.value)
+    h = t.data_ptr()
+    d = _HOST_DEV.get(h)
+    if d is None:
+        p = C.c_void_p()
+        _lib.check(_lib.lib().tr_host_device_pointer(C.c_void_p(h), C.byref(p)),
+                   "tr_host_device_pointer")
+        d = _HOST_DEV[h] = int(p.value)
+        if len(_HOST_DEV) > 4096:
+            _HOST_DEV.clear()
+    return d
 
 
 # rays per trace/march chunk (interval-list scratch: ~1 KB per ray)
@@ -538,7 +547,8 @@ class DeviceScene:
 
     def launch(self, frame: _lib.TrFrame, epoch: Epoch, fb: FrameBuffers, stream,
                out: Optional[_lib.TrOutputs] = None) -> None:
-        fb.counters.zero_()
+        _lib.check(_lib.lib().tr_memset_async(fb.counters.data_ptr(), 0, 8 * fb.counters.numel(),
+                                              stream.cuda_stream), "tr_memset_async")
         if out is None:
             out = fb.outputs()
         fb.start.record(stream)
@@ -574,7 +584,9 @@ class DeviceScene:
                 self.launch(frame, ep, fb, stream)
                 rgba_h.view(-1, 4).copy_(fb.rgba, non_blocking=True)
                 samp_h.view(-1).copy_(fb.samples, non_blocking=True)
-            cnt_h.copy_(fb.counters, non_blocking=True)
+            _lib.check(_lib.lib().tr_copy_async(cnt_h.data_ptr(), fb.counters.data_ptr(),
+                                                8 * fb.counters.numel(), stream.cuda_stream),
+                       "tr_copy_async")
             stream.synchronize()
             wall_ms = (time.perf_counter() - t0) * 1000.0
             dev_ms = fb.start.elapsed_time(fb.end)
