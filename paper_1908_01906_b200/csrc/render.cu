@@ -889,10 +889,17 @@ __device__ uint32_t brick_cut(const FrameK &F, const RayD &ray, double ta, doubl
 // active partitions whose slab it hits.  Same rule as the BVH / BSP
 // enumerations: skip the excluded id and exits <= t_min + excl, winner = the
 // lexicographic minimum of (max(entry, t_min), pid).
+// The last 4-slot group a ray loaded (consecutive intervals mostly reuse it).
+struct CandWin {
+    uint32_t base;   // first slot (a multiple of 4); UINT32_MAX: empty
+    double pa[4], pb[4];
+    int32_t pid[4];
+};
+
 __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n_rays, int64_t rr,
                                                       uint32_t n, uint32_t &dead, double &dead_thr,
-                                                      double t_min, double excl, int32_t last,
-                                                      double &ra, double &rb) {
+                                                      CandWin &w, double t_min, double excl,
+                                                      int32_t last, double &ra, double &rb) {
     const double thr = t_min + excl;
     int32_t best = -1;
     double best_a = INFINITY, best_b = INFINITY;
@@ -901,23 +908,27 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
     if (thr < dead_thr) dead = 0;
     dead_thr = thr;
     bool prefix = true;   // still in the run of dead slots from `dead`
-    for (uint32_t i0 = dead; i0 < n; i0 += 4) {
-        double pa[4], pb[4];
-        int32_t pid[4];
+    // aligned groups; slots below `dead` in the first one are dead again
+    for (uint32_t i0 = dead & ~3u; i0 < n; i0 += 4) {
+        if (w.base != i0) {
+            w.base = i0;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {   // four slots' loads in flight together
-            const int64_t o = (int64_t)(i0 + u) * n_rays + rr;
-            const bool ok = i0 + u < n;
-            pa[u] = ok ? __ldg(iv.cand_pa + o) : 0.0;
-            pb[u] = ok ? __ldg(iv.cand_pb + o) : -INFINITY;
-            pid[u] = ok ? __ldg(iv.cand_pid + o) : -1;
+            for (int u = 0; u < 4; ++u) {   // four slots' loads in flight together
+                const int64_t o = (int64_t)(i0 + u) * n_rays + rr;
+                const bool ok = i0 + u < n;
+                w.pa[u] = ok ? __ldg(iv.cand_pa + o) : 0.0;
+                w.pb[u] = ok ? __ldg(iv.cand_pb + o) : -INFINITY;
+                w.pid[u] = ok ? __ldg(iv.cand_pid + o) : -1;
+            }
         }
+        const double *pa = w.pa, *pb = w.pb;
+        const int32_t *pid = w.pid;
         // slots ascend by entry rounded down to float: nothing later can win
         if ((double)__double2float_rd(pa[0]) > best_a) break;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (pb[u] <= thr) {   // dead for good (also the padding, pb = -inf)
-                if (prefix) dead = min(i0 + u + 1, n);
+                if (prefix && i0 + u + 1 > dead) dead = min(i0 + u + 1, n);
                 continue;
             }
             prefix = false;
@@ -1215,6 +1226,8 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 bool use_bsp = S.knodes != nullptr && !(F.f.flags & TR_FLAG_NO_BSP);
                 uint32_t n_cand = 0, dead = 0;
                 double dead_thr = -INFINITY;
+                CandWin win;
+                win.base = UINT32_MAX;
                 bool cands = false;
                 if (F.use_cand) {
                     n_cand = iv.ccount[rr];
@@ -1229,7 +1242,7 @@ trace_intervals_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         const double excl = (last < 0) ? 0.0 : F.f.eps;
                         double a, b;
                         const int32_t pid = cands
-                            ? cand_next_interval(iv, F.n_rays, rr, n_cand, dead, dead_thr, t_min, excl, last, a, b)
+                            ? cand_next_interval(iv, F.n_rays, rr, n_cand, dead, dead_thr, win, t_min, excl, last, a, b)
                             : use_bsp
                             ? bsp_next_interval<COUNT>(S, E, ray, T, t_min, excl, last, a, b)
                             : next_interval(S, E, ray, t_min, excl, last, a, b);
