@@ -32,13 +32,15 @@ def render():
         out = fb.outputs()
         out.rgba = DV.host_device_pointer(rgba_h)
         out.samples = DV.host_device_pointer(samp_h); tick("outputs")
-        fb.counters.zero_(); tick("counters zero_")
+        DV._lib.check(DV._lib.lib().tr_memset_async(fb.counters.data_ptr(), 0, 8 * fb.counters.numel(),
+                                                   stream.cuda_stream), "tr_memset_async"); tick("counters reset")
         fb.start.record(stream); tick("event record")
         DV._lib.check(DV._lib.lib().tr_render_frame(DV.C.byref(dev.desc), DV.C.byref(ep.desc),
                                                   DV.C.byref(frame), DV.C.byref(out),
                                                   DV.C.c_void_p(stream.cuda_stream)), "tr_render_frame"); tick("tr_render_frame")
         fb.end.record(stream); tick("event record 2")
-        cnt_h.copy_(fb.counters, non_blocking=True); tick("cnt copy")
+        DV._lib.check(DV._lib.lib().tr_copy_async(cnt_h.data_ptr(), fb.counters.data_ptr(),
+                                                 8 * fb.counters.numel(), stream.cuda_stream), "tr_copy_async"); tick("counters copy")
         stream.synchronize(); tick("sync")
         dev_ms = fb.start.elapsed_time(fb.end); tick("elapsed")
     cnt = cnt_h.numpy()

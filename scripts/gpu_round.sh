@@ -21,5 +21,5 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:"tra
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 2 -c 2 \
   -o gpurun_out/prof_march272_$TAG python bench.py --scene radial272 --steps 1 --warmup 1 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 300 python scripts/gpu_stats.py > gpurun_out/stats_$TAG.log 2>&1
-timeout 300 python scripts/e2e_breakdown.py > gpurun_out/e2e_$TAG.log 2>&1
+{ timeout 300 python scripts/e2e_phases.py; echo; timeout 300 python scripts/e2e_jitter.py 300; } > gpurun_out/e2e_$TAG.log 2>&1
 echo done
