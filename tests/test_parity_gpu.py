@@ -162,6 +162,25 @@ def test_large_frames_candidate_raster_equals_bsp_walk(B):
         assert a[1].partitions_visited_mean == b[1].partitions_visited_mean
 
 
+def test_tiny_and_empty_frames(B):
+    """1x1 .. 9x7 frames and a camera looking away from the mesh: the
+    candidate raster and the BSP walk agree with the oracle."""
+    sc, orc = scene_of(B, "golden_radial4")
+    par = C.params(B, "golden_radial4")
+    base = C.camera(B, "golden_radial4")
+    cams = [B.Camera(position=base.position, look_at=base.look_at, up=base.up,
+                     fov_y_deg=base.fov_y_deg, width=w, height=h)
+            for w, h in ((1, 1), (3, 2), (9, 7), (8, 4), (33, 1))]
+    cams.append(B.Camera(position=[10.0, 6.0, 8.0], look_at=[20.0, 10.0, 14.0], up=[0, 1, 0],
+                         fov_y_deg=40.0, width=16, height=12))   # looking away
+    for cam in cams:
+        for mode in ("reference", "skip", "skip-adaptive"):
+            ref = orc.render(cam, mode, par)
+            for flags in (0, 0x800000):
+                fb, st = B.render(sc, cam, mode, par, flags=flags)
+                _compare(fb, st, ref, mode, None)
+
+
 def _check_radial59(fb, st, g, orc, cam, mode, par):
     if mode != "skip-adaptive" or _glibc_pow():
         assert sha(fb.rgba) == g["rgba"]
