@@ -255,6 +255,7 @@ def main():
             ev[k][1].record(stream)
         torch.cuda.synchronize()
         time.sleep(0.1)
+    launches_per_step = runner.launches_per_step()   # of the timed frames (not the e2e ones)
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -340,7 +341,7 @@ def main():
                        "scene_build_s": round(build_s, 3), "upload_s": round(upload_s, 3),
                        "resident_bytes": int(dscene.resident_bytes)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": runner.launches_per_step() * args.steps,
+            "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
