@@ -284,7 +284,7 @@ typedef struct TrFrame {
     int32_t pad0;
 } TrFrame;
 
-#define TR_FLAG_NO_LEAF_HINT 1 /* disable the per-ray exclusive-leaf shortcut (testing) */
+#define TR_FLAG_NO_LEAF_HINT 1 /* ignored (the per-ray leaf hint was removed; kept for ABI stability) */
 #define TR_FLAG_PAIR_SCAN 64   /* leaf scan two records at a time (tuning; default: one at a time) */
 #define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
 #define TR_FLAG_TILE_TIMING 0x10000 /* trace pass: SM cycles per 32-ray tile into the kernel stats (profiling) */
@@ -295,9 +295,9 @@ typedef struct TrFrame {
 #define TR_FLAG_FORCE_CAND 0x1000000 /* the candidate raster also above 1M pixels (default there: the BSP walk) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
-#define TR_FLAG_NO_BSP 8       /* trace intervals with the partition BVH, not the BSP */
+#define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */
 #define TR_FLAG_HIST_SMEM 16   /* ignored (per-partition counts are per-interval global atomics) */
-#define TR_FLAG_GRID_INDIRECT 32 /* grid cell -> leaf id -> leaf header (else the cell's copy) */
+#define TR_FLAG_GRID_INDIRECT 32 /* ignored (grid cells always carry their leaf header; kept for ABI stability) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = chosen
  * per ray chunk on the device, 4 or 16, from the rays' sample counts);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
