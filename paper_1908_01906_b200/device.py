@@ -183,12 +183,18 @@ def pack_tet_records(mesh, sampler, order=None) -> np.ndarray:
     return rec
 
 
+_POW_RESTATED = None   # the library restates glibc pow (tables found at build time)
+
+
 def _steps_on_device(sigma: np.ndarray, p: float) -> bool:
     """True when every |min(sigma, 1) - 1| ** p lies on glibc pow's restated
     path (csrc/glibc_pow.cuh), so the device steps equal the host's bit for
     bit: x in {0 (p > 0), 1} or x a positive normal double with 2^-65 <= |p| <
     2^63 and |p ln x| well below the 512 exp-overflow bound."""
-    if not _lib.lib().tr_pow_glibc_available() or not np.isfinite(p):
+    global _POW_RESTATED
+    if _POW_RESTATED is None:
+        _POW_RESTATED = bool(_lib.lib().tr_pow_glibc_available())
+    if not _POW_RESTATED or not math.isfinite(p):
         return False
     ap = abs(p)
     if not (2.0 ** -65 <= ap < 2.0 ** 63):
@@ -211,7 +217,10 @@ def _steps_on_device(sigma: np.ndarray, p: float) -> bool:
 class Epoch:
     """One uploaded (active, step, tf) snapshot."""
 
-    def __init__(self, dev: "DeviceScene", meta_state, params):
+    def __init__(self, dev: "DeviceScene", meta_state, params, stream=None, hold: bool = True):
+        """stream: the upload stream (default: the current one).  hold=False
+        when the caller synchronizes `stream` before the epoch can be
+        dropped (render()): the staging buffer needs no keep-alive record."""
         torch = _torch()
         active, sigma, tf = meta_state
         self.meta_state = meta_state  # pins the tuple so its id stays unique
@@ -237,7 +246,8 @@ class Epoch:
         self._flag = dev.epoch_flag()
         self.desc = _lib.TrEpoch()
         h2d = C.c_int64(0)
-        stream = torch.cuda.current_stream(dev.device)
+        if stream is None:
+            stream = torch.cuda.current_stream(dev.device)
         _lib.check(L.tr_epoch_upload(
             P, sig.ctypes.data, act.ctypes.data, bact.ctypes.data, dev.n_bnodes, kact.ctypes.data,
             dev.n_knodes, table.ctypes.data, self.n_tf, self.tf_lo, self.tf_hi, s1, s2, pw,
@@ -247,7 +257,8 @@ class Epoch:
         self.h2d_bytes = int(h2d.value)
         self._P = P
         # the copy is not torch's: keep the staging buffer alive until it has run
-        dev.hold_until_done(self.host, stream)
+        if hold:
+            dev.hold_until_done(self.host, stream)
 
     @property
     def step_host(self) -> np.ndarray:
@@ -478,11 +489,11 @@ class DeviceScene:
         self._act_key, self._act_val = key, (kact, bact)
         return kact, bact
 
-    def epoch(self, meta_state, params) -> Epoch:
+    def epoch(self, meta_state, params, stream=None, hold: bool = True) -> Epoch:
         key = (id(meta_state), float(params.s1), float(params.s2), float(params.p))
         ep = self._epochs.get(key)
         if ep is None or ep.meta_state is not meta_state:
-            ep = Epoch(self, meta_state, params)
+            ep = Epoch(self, meta_state, params, stream, hold)
             self._epochs[key] = ep
             while len(self._epochs) > 8:
                 self._epochs.popitem(last=False)
@@ -566,7 +577,7 @@ class DeviceScene:
             t0 = time.perf_counter()
             stream = torch.cuda.current_stream(self.device)
             meta = scene.meta_state()
-            ep = self.epoch(meta, params)
+            ep = self.epoch(meta, params, stream, hold=False)   # synchronized below
             frame = self.frame_desc(scene, camera, mode, params, jitter, track, flags)
             fb = self.frame_buffers(w, h)
             rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
