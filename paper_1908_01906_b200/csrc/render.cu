@@ -769,6 +769,7 @@ struct IvBuf {                   // per-chunk scratch
     uint32_t *n_bg;              // deferred background rays, listed from the top of `order`
     double *cand_pa, *cand_pb;   // [CAND_CAP][n_rays] active partition slabs (use_cand), slot-major
     int32_t *cand_pid;           //   so a warp's 32 rays read one slot in one coalesced load
+    float *cand_nkey;            // [CAND_CAP][n_rays] the next slot's sort key (+inf after the last)
     uint32_t *ccount;            // [n_rays] slabs found (> CAND_CAP: the ray takes the BSP)
     double *rinv;                // [3][n_rays] 1/d per axis (0 where d == 0) for the raster
     unsigned long long *totals;  // frame totals (trace-finished rays add their visited)
@@ -894,6 +895,7 @@ struct CandWin {
     uint32_t base;   // first slot (a multiple of 4); UINT32_MAX: empty
     double pa[4], pb[4];
     int32_t pid[4];
+    float nkey3;     // sort key of slot base + 4
 };
 
 __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n_rays, int64_t rr,
@@ -920,6 +922,7 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
                 w.pb[u] = ok ? __ldg(iv.cand_pb + o) : -INFINITY;
                 w.pid[u] = ok ? __ldg(iv.cand_pid + o) : -1;
             }
+            w.nkey3 = i0 + 4 < n ? __ldg(iv.cand_nkey + (int64_t)(i0 + 3) * n_rays + rr) : INFINITY;
         }
         const double *pa = w.pa, *pb = w.pb;
         const int32_t *pid = w.pid;
@@ -937,8 +940,9 @@ __device__ __forceinline__ int32_t cand_next_interval(const IvBuf &iv, int64_t n
             if (a_cl >= INFINITY) continue;   // t_max = inf (K:366)
             if (a_cl < best_a || (a_cl == best_a && pid[u] < best)) { best = pid[u]; best_a = a_cl; best_b = pb[u]; }
         }
-        // the group's last key already bounds every later slot: no next load
-        if (i0 + 3 < n && (double)__double2float_rd(pa[3]) > best_a) break;
+        // the next group's first key (kept with this group's last slot)
+        // bounds every later slot: stop without loading it
+        if (i0 + 4 < n && (double)w.nkey3 > best_a) break;
     }
     ra = best_a;
     rb = best_b;
@@ -1162,6 +1166,8 @@ __global__ void __launch_bounds__(SORT_THREADS) cand_sort_kernel(FrameK F, IvBuf
             if ((uint32_t)slot < s_n[lane]) {
                 const int64_t o = (int64_t)slot * F.n_rays + r0 + lane;
                 iv.cand_pa[o] = s_pa[slot][lane]; iv.cand_pb[o] = s_pb[slot][lane]; iv.cand_pid[o] = s_pid[slot][lane];
+                iv.cand_nkey[o] = (uint32_t)slot + 1 < s_n[lane] ? __double2float_rd(s_pa[slot + 1][lane])
+                                                                 : INFINITY;
             }
         }
     }
@@ -2186,7 +2192,7 @@ static int bg_aux(BgAux **out) {
     return TR_OK;
 }
 
-constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4 + 4 + 24 + CAND_CAP * 20;  // rec + tail + cnt + order + ccount + rinv + cand
+constexpr int64_t IV_BYTES_PER_RAY = IV_CAP * 16 + 8 + 4 + 4 + 4 + 24 + CAND_CAP * 24;  // rec + tail + cnt + order + ccount + rinv + cand
 constexpr int64_t IV_FIXED_BYTES = 1024;
 
 // ---- brick-sharded frames (tr_brick_*)
@@ -2286,6 +2292,7 @@ static IvBuf make_iv(const TrOutputs *out, int64_t n_rays) {
     iv.cand_pa = iv.rinv + 3 * n_rays;
     iv.cand_pb = iv.cand_pa + (int64_t)CAND_CAP * n_rays;
     iv.cand_pid = reinterpret_cast<int32_t *>(iv.cand_pb + (int64_t)CAND_CAP * n_rays);
+    iv.cand_nkey = reinterpret_cast<float *>(iv.cand_pid + (int64_t)CAND_CAP * n_rays);
     return iv;
 }
 
