@@ -1043,8 +1043,12 @@ __global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E,
         if (iy0 > iy1) continue;
         const uint32_t rw = (uint32_t)(ix1 - ix0 + 1);
         const uint32_t nrow = (uint32_t)((iy1 - iy0) / nsub + 1), npx = rw * nrow;
-        for (uint32_t k = lane; k < npx; k += 32) {
-            const uint32_t ix = (uint32_t)ix0 + k % rw, iy = (uint32_t)iy0 + (k / rw) * (uint32_t)nsub;
+        // (row, column) of pixel k stepped incrementally: no division per pixel
+        const uint32_t dcol = 32u % rw, drow = 32u / rw;
+        uint32_t col = (uint32_t)lane % rw, row = (uint32_t)lane / rw;
+        for (uint32_t k = lane; k < npx; k += 32, col += dcol, row += drow) {
+            if (col >= rw) { col -= rw; ++row; }
+            const uint32_t ix = (uint32_t)ix0 + col, iy = (uint32_t)iy0 + row * (uint32_t)nsub;
             const int64_t rr = pixel_ray(F, ix, iy);
             if (rr < 0) continue;
             RayD ray;   // the trace's make_ray, from the per-ray table (slab needs o, 1/d)
