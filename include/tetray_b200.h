@@ -253,6 +253,8 @@ typedef struct TrEpoch {
     const uint8_t *knode_active; /* (n_knodes,) from tr_knodes_activity, or NULL */
     const double *step_ratio;    /* (P,2) interleaved {step, step / s1} (opacity_correction's
                                     exponent, K:27); only read in mode 2 */
+    const int32_t *inexact;      /* device word, nonzero if a device step was inexact (entries
+                                    NaN; render() raises); NULL when the host made the steps */
 } TrEpoch;
 
 /* One metadata epoch in one call (R:169; scene.py:78-82): packs sigma, the TF
@@ -266,8 +268,8 @@ int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8_t *active,
                     const uint8_t *bnode_active, int64_t n_bnodes, const uint8_t *knode_active,
                     int64_t n_knodes, const double *tf_table, int64_t n_tf, double tf_lo,
                     double tf_hi, double s1, double s2, double p, int32_t steps_on_device,
-                    void *host_buf, void *dev_buf, int64_t buf_bytes, int32_t *inexact,
-                    TrEpoch *out, int64_t *h2d_bytes, void *stream);
+                    void *host_buf, void *dev_buf, int64_t buf_bytes, TrEpoch *out,
+                    int64_t *h2d_bytes, void *stream);
 
 /* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
 typedef struct TrFrame {
@@ -284,7 +286,6 @@ typedef struct TrFrame {
     int32_t pad0;
 } TrFrame;
 
-#define TR_FLAG_NO_LEAF_HINT 1 /* ignored (the per-ray leaf hint was removed; kept for ABI stability) */
 #define TR_FLAG_PAIR_SCAN 64   /* leaf scan two records at a time (tuning; default: one at a time) */
 #define TR_FLAG_REG_STATE 128  /* march with the per-ray state in registers (tuning; default: shared memory) */
 #define TR_FLAG_TILE_TIMING 0x10000 /* trace pass: SM cycles per 32-ray tile into the kernel stats (profiling) */
@@ -296,8 +297,6 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */
-#define TR_FLAG_HIST_SMEM 16   /* ignored (per-partition counts are per-interval global atomics) */
-#define TR_FLAG_GRID_INDIRECT 32 /* ignored (grid cells always carry their leaf header; kept for ABI stability) */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = chosen
  * per ray chunk on the device, 4 or 16, from the rays' sample counts);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs

@@ -49,6 +49,7 @@ class TrEpoch(C.Structure):
         ("active", C.c_void_p), ("bnode_active", C.c_void_p), ("step", C.c_void_p),
         ("tf_table", C.c_void_p), ("n_tf", C.c_int64), ("tf_lo", C.c_double),
         ("tf_hi", C.c_double), ("knode_active", C.c_void_p), ("step_ratio", C.c_void_p),
+        ("inexact", C.c_void_p),
     ]
 
 
@@ -95,7 +96,6 @@ PLEAF_DTYPE = np.dtype([("ex_lo", "<f4", 3), ("ex_hi", "<f4", 3), ("start", "<u4
 BNODE_DTYPE = np.dtype([("box", "<f8", (2, 6)), ("child", "<i4", 2), ("pad", "<i4", 2)])
 KNODE_DTYPE = np.dtype([("split", "<f8"), ("info", "<i4"), ("aux", "<i4")])
 
-TR_FLAG_NO_LEAF_HINT = 1
 TR_FLAG_NO_GRID = 2
 TR_FLAG_STATS = 4
 TR_FLAG_NO_BSP = 8
@@ -147,7 +147,7 @@ _SIGNATURES = [
     ("tr_epoch_upload", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
                                   C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_double, C.c_double,
                                   C.c_double, C.c_double, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64,
-                                  C.c_void_p, C.POINTER(TrEpoch), C.POINTER(C.c_int64), C.c_void_p]),
+                                  C.POINTER(TrEpoch), C.POINTER(C.c_int64), C.c_void_p]),
     ("tr_epoch_steps", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, C.c_void_p,
                                  C.c_void_p]),
     ("tr_step_sizes", C.c_int, [C.c_int64, c_f64p, C.c_double, C.c_double, C.c_double, c_f64p]),

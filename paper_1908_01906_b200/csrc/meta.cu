@@ -35,7 +35,8 @@ __device__ const __align__(32) unsigned long long d_etab[] = TR_POW_EXP_TAB_INIT
 // step_size (K:20-22) per partition: max(s1 + (s2 - s1) * |min(sigma, 1) - 1|^p, s1),
 // with glibc's pow restated (glibc_pow.cuh) -- bit-identical to the host's
 // tr_step_sizes wherever the restated path applies; elsewhere the entry is
-// flagged and the caller uses the host.  Also the K:27 exponent step / s1.
+// NaN and *inexact is set (render() checks it and raises: the host precheck
+// admitted a sigma it should not have).  Also the K:27 exponent step / s1.
 __global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, double s1,
                                    double s2, double p, double *step, double *ratio, int *inexact) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
@@ -56,7 +57,11 @@ __global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, 
         }
 #endif
         else ok = false;
-        if (!ok) { atomicExch(inexact, 1); continue; }
+        if (!ok) {
+            atomicExch(inexact, 1);
+            step[i] = ratio[2 * i] = ratio[2 * i + 1] = __longlong_as_double(0x7ff8000000000000ll);
+            continue;
+        }
         const double v = s1 + (s2 - s1) * pw;
         const double st = (s1 > v) ? s1 : v;       // Python max(v, s1)
         step[i] = st;
@@ -262,13 +267,14 @@ inline int64_t a64(int64_t x) { return (x + 63) / 64 * 64; }
 
 // The epoch's device buffer, 64-B aligned sections:
 //   step f64[P] | (step, step / s1) f64[P,2] | sigma f64[P] | tf f64[n_tf,4] |
-//   active u8[P] | bnode activity u8[n_b] | knode activity u8[n_k]
+//   active u8[P] | bnode activity u8[n_b] | knode activity u8[n_k] | inexact i32
+// (the inexact word is zero in the staging buffer, so every upload resets it)
 extern "C" int64_t tr_epoch_bytes(int64_t n_parts, int64_t n_tf, int64_t n_bnodes,
                                   int64_t n_knodes) {
     const int64_t o_ratio = a64(8 * n_parts), o_sigma = a64(o_ratio + 16 * n_parts);
     const int64_t o_tf = a64(o_sigma + 8 * n_parts), o_act = a64(o_tf + 32 * n_tf);
     const int64_t o_bact = a64(o_act + n_parts), o_kact = a64(o_bact + n_bnodes);
-    return a64(o_kact + n_knodes);
+    return a64(o_kact + n_knodes) + 64;
 }
 
 extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8_t *active,
@@ -276,19 +282,20 @@ extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8
                                const uint8_t *knode_active, int64_t n_knodes,
                                const double *tf_table, int64_t n_tf, double tf_lo, double tf_hi,
                                double s1, double s2, double p, int32_t steps_on_device,
-                               void *host_buf, void *dev_buf, int64_t buf_bytes, int32_t *inexact,
-                               TrEpoch *out, int64_t *h2d_bytes, void *stream) {
+                               void *host_buf, void *dev_buf, int64_t buf_bytes, TrEpoch *out,
+                               int64_t *h2d_bytes, void *stream) {
     if (n_parts < 1 || !sigma || !active || !tf_table || n_tf < 2 || !host_buf || !dev_buf || !out ||
-        n_bnodes < 0 || n_knodes < 0 || (n_bnodes && !bnode_active) || (n_knodes && !knode_active) ||
-        (steps_on_device && !inexact))
+        n_bnodes < 0 || n_knodes < 0 || (n_bnodes && !bnode_active) || (n_knodes && !knode_active))
         return tr_fail(TR_EINVAL, "tr_epoch_upload: invalid arguments");
     if (buf_bytes < tr_epoch_bytes(n_parts, n_tf, n_bnodes, n_knodes))
         return tr_fail(TR_EINVAL, "tr_epoch_upload: buffer too small");
     const int64_t o_ratio = a64(8 * n_parts), o_sigma = a64(o_ratio + 16 * n_parts);
     const int64_t o_tf = a64(o_sigma + 8 * n_parts), o_act = a64(o_tf + 32 * n_tf);
     const int64_t o_bact = a64(o_act + n_parts), o_kact = a64(o_bact + n_bnodes);
-    const int64_t nbytes = a64(o_kact + n_knodes);
+    const int64_t o_flag = a64(o_kact + n_knodes), nbytes = o_flag + 64;
     char *h = static_cast<char *>(host_buf), *d = static_cast<char *>(dev_buf);
+    std::memset(h + o_flag, 0, 64);
+    int32_t *inexact = reinterpret_cast<int32_t *>(d + o_flag);
     std::memcpy(h + o_sigma, sigma, 8 * n_parts);
     std::memcpy(h + o_tf, tf_table, 32 * n_tf);
     std::memcpy(h + o_act, active, n_parts);
@@ -322,5 +329,6 @@ extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8
     out->tf_hi = tf_hi;
     out->knode_active = reinterpret_cast<const uint8_t *>(d + o_kact);
     out->step_ratio = reinterpret_cast<const double *>(d + o_ratio);
+    out->inexact = steps_on_device ? inexact : nullptr;
     return TR_OK;
 }

@@ -243,7 +243,6 @@ class Epoch:
         # step sizes (K:20-22) and exponents (K:27) on the device when every
         # |min(sigma, 1) - 1| ** p is on the restated glibc pow's path
         self._step_dev = _steps_on_device(sig, pw)
-        self._flag = dev.epoch_flag()
         self.desc = _lib.TrEpoch()
         h2d = C.c_int64(0)
         if stream is None:
@@ -252,10 +251,12 @@ class Epoch:
             P, sig.ctypes.data, act.ctypes.data, bact.ctypes.data, dev.n_bnodes, kact.ctypes.data,
             dev.n_knodes, table.ctypes.data, self.n_tf, self.tf_lo, self.tf_hi, s1, s2, pw,
             1 if self._step_dev else 0, self.host.data_ptr(), self.buf.data_ptr(), nbytes,
-            self._flag.data_ptr(), C.byref(self.desc), C.byref(h2d), stream.cuda_stream),
+            C.byref(self.desc), C.byref(h2d), stream.cuda_stream),
             "tr_epoch_upload")
         self.h2d_bytes = int(h2d.value)
         self._P = P
+        # device steps: the first frame reads back the epoch's inexact word
+        self.verified = not self.desc.inexact
         # the copy is not torch's: keep the staging buffer alive until it has run
         if hold:
             dev.hold_until_done(self.host, stream)
@@ -512,12 +513,6 @@ class DeviceScene:
         ev.record(stream)
         q.append((ev, obj))
 
-    def epoch_flag(self):
-        """int32 device word tr_epoch_steps_device sets on an inexact entry (shared)."""
-        if getattr(self, "_epoch_flag", None) is None:
-            self._epoch_flag = _torch().zeros(1, dtype=_torch().int32, device=self.device)
-        return self._epoch_flag
-
     def frame_buffers(self, width: int, height: int, compact_slots: int = 0) -> FrameBuffers:
         key = (width, height, compact_slots)
         fb = self._frames.get(key)
@@ -582,7 +577,7 @@ class DeviceScene:
             fb = self.frame_buffers(w, h)
             rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
             samp_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
-            cnt_h = torch.empty(3 + self.n_parts, dtype=torch.int64, pin_memory=True)
+            cnt_h = torch.empty(4 + self.n_parts, dtype=torch.int64, pin_memory=True)
             if DIRECT_HOST_OUTPUTS:
                 # the kernels store each finished pixel straight into the
                 # page-locked result arrays, overlapping the device->host
@@ -598,7 +593,17 @@ class DeviceScene:
             _lib.check(_lib.lib().tr_copy_async(cnt_h.data_ptr(), fb.counters.data_ptr(),
                                                 8 * fb.counters.numel(), stream.cuda_stream),
                        "tr_copy_async")
+            if not ep.verified:
+                cnt_h[-1] = 0
+                _lib.check(_lib.lib().tr_copy_async(cnt_h.data_ptr() + 8 * (3 + self.n_parts),
+                                                    ep.desc.inexact, 4, stream.cuda_stream),
+                           "tr_copy_async")
             stream.synchronize()
+            if not ep.verified:
+                if int(cnt_h[-1]) != 0:
+                    raise RuntimeError("device step sizes of this epoch are inexact (sigma outside "
+                                       "the restated glibc pow domain); frame discarded")
+                ep.verified = True
             wall_ms = (time.perf_counter() - t0) * 1000.0
             dev_ms = fb.start.elapsed_time(fb.end)
         cnt = cnt_h.numpy()
@@ -609,9 +614,16 @@ class DeviceScene:
         stats = RenderStats(
             total_samples=int(cnt[0]), wall_ms=wall_ms,
             partitions_visited_mean=float(np.float64(cnt[1]) / np.float64(w * h)),
-            per_partition_samples=cnt[3:].copy() if track else None,
-            samples=samples, device_ms=float(dev_ms), gpu_launches=1)
+            per_partition_samples=cnt[3:3 + self.n_parts].copy() if track else None,
+            samples=samples, device_ms=float(dev_ms), gpu_launches=last_launches())
         return fbuf, stats
+
+
+def last_launches() -> int:
+    """Kernels of ours the last tr_render_frame launched (tr_last_launch)."""
+    out = np.zeros(3, np.int64)
+    _lib.check(_lib.lib().tr_last_launch(_lib.ptr(out, C.c_int64)), "tr_last_launch")
+    return int(out[0])
 
 
 def device_scene_for(scene, device=None) -> DeviceScene:

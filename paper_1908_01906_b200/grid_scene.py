@@ -29,13 +29,11 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from . import traversal as traversal_mod
-from .geometry import AABB
+from .boxes import Box
 from .mesh import BOX_PAD_REL, Centering, _inverse_edge_matrices, generate_synthetic
 from .partitions import KdArrays, KdBuildConfig, Partition, default_config
 from .scene import Scene
 from .transfer import TransferFunction
-from .traversal import TraversalConfig
 
 FIELD_IDS = {"ramp": 0, "radial": 1}
 
@@ -56,7 +54,7 @@ class GridMesh:
         self.centering = Centering.VERTEX
         self.n_tets = 5 * self.n ** 3
         self.n_vertices = (self.n + 1) ** 3
-        self.bounds = AABB(np.zeros(3), np.full(3, float(self.n)))
+        self.bounds = Box(np.zeros(3), np.full(3, float(self.n)))
         self.synthetic = (self.n, field)
 
 
@@ -106,9 +104,9 @@ def build_grid_partitions(n: int, field: str, config: KdBuildConfig) -> list[Par
     parts = []
     empty = np.empty(0, np.int64)
     for i in range(len(kd.offsets) - 1):
-        p = Partition(id=i, bounds=AABB(kd.lo[i], kd.hi[i]), element_ids=empty,
+        p = Partition(id=i, bounds=Box(kd.lo[i], kd.hi[i]), element_ids=empty,
                       value_range=(float(kd.vrange[i, 0]), float(kd.vrange[i, 1])),
-                      leaf_bounds=AABB(kd.leaf_lo[i], kd.leaf_hi[i]))
+                      leaf_bounds=Box(kd.leaf_lo[i], kd.leaf_hi[i]))
         p.n_elements = int(kd.offsets[i + 1] - kd.offsets[i])
         parts.append(p)
     return parts
@@ -122,15 +120,6 @@ class GridScene(Scene):
               kd_config: Optional[KdBuildConfig] = None, epsilon: Optional[float] = None,
               background=None) -> "GridScene":
         mesh = GridMesh(n, field)
-        kd = kd_config or default_config(mesh.n_tets)
-        tc = (TraversalConfig(epsilon) if epsilon is not None
-              else TraversalConfig.for_diagonal(mesh.bounds.diagonal()))
-        scene = cls(mesh=mesh, sampler=GridSampler(mesh),
-                    partitions=build_grid_partitions(n, field, kd), kd_config=kd,
-                    traversal_config=tc)
-        if background is not None:
-            scene.background = np.asarray(background, dtype=np.float64).reshape(4)
-        scene.bvh = traversal_mod.build_partition_bvh(scene.partitions)
-        scene.counters["partition_bvh_builds"] = scene.counters.get("partition_bvh_builds", 0) + 1
-        scene.set_transfer_function(tf)
-        return scene
+        kd = kd_config if kd_config is not None else default_config(mesh.n_tets)
+        return cls._assemble(mesh, GridSampler(mesh), build_grid_partitions(n, field, kd), kd, tf,
+                             epsilon, background)

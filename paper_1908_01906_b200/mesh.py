@@ -16,7 +16,7 @@ from typing import Optional
 
 import numpy as np
 
-from .geometry import AABB
+from .boxes import Box
 
 MAGIC = b"TET1"
 _HEADER = struct.Struct("<4sBQQ")          # mesh.py:4-8 / 24-25
@@ -64,7 +64,7 @@ class TetMesh:
         self.synthetic: Optional[tuple] = None  # (n, field name) for generate_synthetic meshes
         if validate:
             self._validate()
-        self.bounds = AABB.from_points(self.vertices)
+        self.bounds = Box.around(self.vertices)
 
     def _validate(self) -> None:
         nv, nt = len(self.vertices), len(self.tets)

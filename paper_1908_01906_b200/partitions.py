@@ -13,7 +13,7 @@ from typing import Optional
 import numpy as np
 
 from . import _lib
-from .geometry import AABB
+from .boxes import Box
 from .mesh import Centering, TetMesh
 
 
@@ -40,11 +40,11 @@ def default_config(n_tets: int) -> KdBuildConfig:
 @dataclass
 class Partition:
     id: int
-    bounds: AABB
+    bounds: Box
     element_ids: np.ndarray
     value_range: tuple[float, float]
     meta: Optional[object] = None
-    leaf_bounds: Optional[AABB] = None
+    leaf_bounds: Optional[Box] = None
 
 
 def element_value_ranges(mesh: TetMesh) -> np.ndarray:
@@ -54,11 +54,11 @@ def element_value_ranges(mesh: TetMesh) -> np.ndarray:
     return np.stack([mesh.field, mesh.field], axis=1)
 
 
-def refine_partition_bounds(partition: Partition, mesh: TetMesh, leaf_bounds: AABB) -> Partition:
+def refine_partition_bounds(partition: Partition, mesh: TetMesh, leaf_bounds: Box) -> Partition:
     if len(partition.element_ids) == 0:
         raise ValueError("partition has no elements")
     pts = mesh.vertices[mesh.tets[partition.element_ids]].reshape(-1, 3)
-    partition.bounds = AABB.from_points(pts).intersection(leaf_bounds)
+    partition.bounds = Box.around(pts).clipped_to(leaf_bounds)
     return partition
 
 
@@ -105,9 +105,9 @@ def build_partitions(mesh: TetMesh, config: Optional[KdBuildConfig] = None) -> l
     parts = []
     for i in range(len(kd.offsets) - 1):
         ids = kd.ids[kd.offsets[i]:kd.offsets[i + 1]]
-        parts.append(Partition(id=i, bounds=AABB(kd.lo[i], kd.hi[i]), element_ids=ids,
+        parts.append(Partition(id=i, bounds=Box(kd.lo[i], kd.hi[i]), element_ids=ids,
                                value_range=(float(kd.vrange[i, 0]), float(kd.vrange[i, 1])),
-                               leaf_bounds=AABB(kd.leaf_lo[i], kd.leaf_hi[i])))
+                               leaf_bounds=Box(kd.leaf_lo[i], kd.leaf_hi[i])))
     return parts
 
 

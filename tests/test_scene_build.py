@@ -92,20 +92,3 @@ def test_tet1_roundtrip(B, tmp_path):
     with pytest.raises(B.MeshFormatError):
         (tmp_path / "bad.tet").write_bytes(b"TET2" + bytes(40))
         B.load_mesh(tmp_path / "bad.tet")
-
-
-def test_scene_config_roundtrip(B, tmp_path):
-    import json
-    m = B.generate_synthetic(4, "radial", B.Centering.VERTEX)
-    B.save_mesh(m, tmp_path / "radial4.tet")
-    (tmp_path / "tf.json").write_text(json.dumps(C.TF_BANDED))
-    (tmp_path / "scene.json").write_text(json.dumps({
-        "mesh": "radial4.tet", "transfer_function": "tf.json",
-        "camera": {"position": [10, 6, 8], "look_at": [2, 2, 2], "width": 64, "height": 64,
-                   "fov_y_deg": 40.0},
-        "params": {"s1": 0.05, "s2": 0.3, "mode": "skip-adaptive"},
-        "kd": {"max_leaf_elements": 40}, "epsilon": None}))
-    cfg = B.load_scene_config(tmp_path / "scene.json")
-    sc = B.build_scene_from_config(cfg)
-    assert sc.n_partitions == 8 and cfg.mode == "skip-adaptive"
-    assert cfg.camera.width == 64 and cfg.params.termination_opacity == 0.99

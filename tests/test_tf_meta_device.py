@@ -94,4 +94,7 @@ def test_device_epoch_steps_equal_host(B, recipe):
             ratio = ep.buf[ep.desc.step_ratio - ep.buf.data_ptr():][:16 * len(sg)]
             assert np.array_equal(ratio.cpu().numpy().view(np.float64), want_ratio)
             if ep._step_dev:
-                assert int(ep._flag.item()) == 0
+                flag = ep.buf[ep.desc.inexact - ep.buf.data_ptr():][:4]
+                assert int(flag.cpu().numpy().view(np.int32)[0]) == 0
+            else:
+                assert not ep.desc.inexact
