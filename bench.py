@@ -1,20 +1,42 @@
 #!/usr/bin/env python3
 """Benchmark of the tetray render hot path on B200 (BASELINE.json metric).
 
-Workload (BASELINE config 2): radial59 -- 1,026,895 tets,
-default KD partitions (8,192; 4,040 active), the radial16 TF scaled to N=59,
-camera [40,26,34]*59/16 -> [29.5]^3, fov 35, 512x512, s1=0.08, s2=0.64, p=2,
+Workload (BASELINE config 3: headline the >= 1e8-tet scene,
+where every sample's tet record is a DRAM miss): radial272 -- 100,618,240
+tets, default KD partitions (8,192), the radial16 TF scaled to N=272, camera
+[40,26,34]*272/16 -> [136]^3, fov 35, 512x512, s1=0.08, s2=0.64, p=2,
 termination 0.9999, mode skip-adaptive (the paper's headline mode).
+`--scene radial59` is BASELINE config 2 (1e6 tets).  On the GPU arm a radialN
+scene with N >= 128 is generated in HBM (GridScene, csrc/synth.cu) -- the
+same scene bit for bit: tests/test_parity_big_gpu.py renders it equal to the
+reference's own radial272 frames; `--host-build` uses the general host path.
 
 One step = one frame.  Items = samples (point queries, RenderStats.total_samples).
-  value   device-timed: scene + epoch resident in HBM, CUDA events around the
-          render kernel on its stream, L2 flushed (256 MiB write) between steps
-  e2e     through the public render() API: per step the metadata epoch is
-          re-uploaded from pinned host memory (H2D) and rgba + samples +
-          counters are read back (D2H); wall clock, max over ranks
-N > 1: strong scaling -- the frame's 8x4 pixel tiles are interleaved over the
-ranks, partial tiles all-gathered and per-partition counts all-reduced
-over NCCL (paper_1908_01906_b200/distributed.py).
+  value     device-timed: scene + epoch resident in HBM, CUDA events around
+            the frame's kernels on their stream, L2 flushed (256 MiB write)
+            between steps (the 13 GB of records exceed L2 anyway)
+  e2e       the public render() API with host buffers: per step the metadata
+            epoch is re-uploaded from pinned host memory (H2D) and rgba +
+            samples + counters are read back (D2H)
+  roofline  march_sm_kernel (the dominant kernel): SURVEY §8d algorithmic
+            bytes (128 B/sample + 44 B/pixel) / its event-timed duration;
+            `traffic` = ncu dram__bytes_read.sum + dram__bytes_write.sum of
+            that kernel, measured live by an ncu subprocess on this workload
+            (null when ncu is unavailable)
+  cpu_baseline  the oracle (oracle/oracle.c, a bit-exact C port of the
+            numba kernel) on its own scene build, all host cores, a bounded
+            sample of whole frames
+N > 1 (`--gpus N` re-launches itself under torch.distributed.run when
+WORLD_SIZE is unset): strong scaling of the one frame -- 8x4 pixel tiles
+interleaved over the ranks, each rank's tiles gathered to rank 0 and the
+counters reduced there over NCCL (paper_1908_01906_b200/distributed.py).
+
+--impl reference: the reference's own render() (pkg/src/tetray/render.py:161-205,
+numba, installed under baseline/_ref) with all host threads, on whole frames
+of the same workload, rank 0 only.  Its Scene is the stock dataclasses
+assembled around the oracle's C restatement of the generator, KD split and
+BVH build (oracle/stock_scene.py; the stock Python builders need ~40 min at
+1e8 tets).  libtetray_b200.so is never loaded on that path.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
 """
@@ -22,8 +44,13 @@ over NCCL (paper_1908_01906_b200/distributed.py).
 from __future__ import annotations
 
 import argparse
+import csv
+import io
 import json
 import os
+import platform
+import shutil
+import socket
 import statistics
 import subprocess
 import sys
@@ -41,43 +68,68 @@ METRIC = BASELINE["metric"]
 UNIT = "samples/s"
 RECORD_BYTES = {0: 128, 1: 104}   # algorithmic bytes per sample (vertex / cell), SURVEY §8d
 PIXEL_BYTES = 44                  # rgba f64x4 + samples i64 + visited i32
+MODES = ("reference", "skip", "skip-adaptive")
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--scene", default="radial59")
-    ap.add_argument("--mode", default="skip-adaptive")
+    ap.add_argument("--scene", default="radial272")
+    ap.add_argument("--mode", default="skip-adaptive", choices=MODES)
     ap.add_argument("--scale", type=float, default=1.0, help="image size multiplier (512*scale)")
+    ap.add_argument("--host-build", action="store_true",
+                    help="build radialN through the general host path, not GridScene")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=8.0)
+    ap.add_argument("--no-traffic", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-budget-s", type=float, default=900.0,
+                    help="reference arm: stop timing whole frames after this many seconds")
     ap.add_argument("--flags", type=lambda x: int(x, 0), default=0,
                     help="TR_FLAG_* bits (tuning experiments; bits 8-11 = log2 group size)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
+
+
+def scene_n(name: str) -> int:
+    for pre in ("radial", "grid"):
+        if name.startswith(pre) and name[len(pre):].isdigit():
+            return int(name[len(pre):])
+    return 0
+
+
+def public_name(name: str) -> str:
+    """gridN is radialN generated in HBM: the workload is named radialN."""
+    return f"radial{scene_n(name)}" if name.startswith("grid") else name
+
+
+def workload_config(args, n_tets, n_parts, samples) -> dict:
+    """The `config` dict -- identical in both arms for the same workload."""
+    w = h = int(512 * args.scale)
+    scene = public_name(args.scene)
+    return {"workload": f"{scene} {w}x{h} {args.mode}", "scene": scene, "mode": args.mode,
+            "width": w, "height": h, "n_tets": int(n_tets), "n_partitions": int(n_parts),
+            "samples_per_frame": int(samples)}
 
 
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """DRAM bytes per render launch from the committed ncu --set full summary."""
-    p = ROOT / "profiles" / "r01" / "ncu_dram.json"
-    if not p.exists():
-        return None
+def cpu_model() -> str:
     try:
-        d = json.loads(p.read_text())
-        return d.get("dram_bytes_per_launch")
-    except Exception:
-        return None
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class Clocks:
@@ -132,21 +184,44 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def build_workload(B, args):
+# ---------------------------------------------------------------- workloads
+
+def build_gpu_workload(B, args):
     import cases as C
+    n = scene_n(args.scene)
+    name = args.scene
+    if name.startswith("radial") and n >= 128 and not args.host_build:
+        name = f"grid{n}"
     t0 = time.perf_counter()
-    scene = C.build_scene(B, args.scene)
-    cam = C.camera(B, args.scene, scale=args.scale)
-    par = C.params(B, args.scene)
+    scene = C.build_scene(B, name)
+    cam = C.camera(B, name, scale=args.scale)
+    par = C.params(B, name)
     return scene, cam, par, time.perf_counter() - t0
 
 
-def cpu_reference(scene, cam, par, args, budget_s):
-    """The oracle port on all host cores, full frames until `budget_s` elapses."""
+def build_oracle_workload(args):
+    """The oracle's own scene (oracle/scene.py), camera and params."""
+    import cases as C
+    import oracle.scene as OS
+    n = scene_n(args.scene)
+    if not n or not args.scene.startswith(("radial", "grid")):
+        raise SystemExit(f"the oracle builds radialN / gridN scenes only, not {args.scene!r}")
+    leaf = 48 if n == 16 else None   # tests/cases.py: radial16 uses KdBuildConfig(48)
+    scene = OS.GridScene(n, OS.TF.from_json(C.radial16_tf_doc(n)), max_leaf=leaf)
+    return scene, C.camera(OS, public_name(args.scene), scale=args.scale), \
+        C.params(OS, public_name(args.scene))
+
+
+def cpu_reference(args, budget_s):
+    """The oracle port on all host cores, on its own scene build: whole
+    frames until `budget_s` of rendering has elapsed (>= 1 frame)."""
     from oracle.oracle import OracleScene
+    t0 = time.perf_counter()
+    scene, cam, par = build_oracle_workload(args)
     orc = OracleScene(scene)
+    build_s = time.perf_counter() - t0
     threads = os.cpu_count() or 1
-    orc.render(cam, args.mode, par, threads=threads, rows=(0, 8))  # warm caches
+    orc.render(cam, args.mode, par, threads=threads, rows=(0, 8))  # page in
     t0 = time.perf_counter()
     frames, samples = 0, 0
     while True:
@@ -157,50 +232,139 @@ def cpu_reference(scene, cam, par, args, budget_s):
             break
     dt = time.perf_counter() - t0
     return {"value": samples / dt, "unit": UNIT, "cores": threads, "kind": "port",
-            "sample": f"{frames} full {cam.width}x{cam.height} {args.mode} frame(s) of "
-                      f"{args.scene} in {dt:.2f} s (oracle/oracle.c, OpenMP over rows)",
-            "ms_per_frame": dt * 1000.0 / frames}
+            "cpu_model": cpu_model(),
+            "sample": f"{frames} whole {cam.width}x{cam.height} {args.mode} frame(s) of "
+                      f"{public_name(args.scene)} in {dt:.2f} s (oracle/oracle.c, OpenMP over "
+                      f"rows, {threads} threads; scene built by oracle/build.c in {build_s:.1f} s)",
+            "ms_per_frame": dt * 1000.0 / frames, "samples_per_frame": samples // frames}
 
+
+def ncu_traffic(args):
+    """DRAM bytes (read + write) per launch of march_sm_kernel on this
+    workload, from an `ncu` subprocess (cold caches, --cache-control all);
+    the largest of the frame's march launches (the unchosen lane width
+    returns at once).  None when ncu is not available."""
+    ncu = shutil.which("ncu") or ("/usr/local/cuda/bin/ncu"
+                                  if Path("/usr/local/cuda/bin/ncu").exists() else None)
+    if ncu is None or os.environ.get("TETRAY_BENCH_UNDER_NCU"):
+        return None, "ncu not available"
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum",
+           "--clock-control", "none", "-k", "regex:march_sm", "-c", "4", "--csv",
+           sys.executable, str(ROOT / "bench.py"), "--scene", args.scene, "--mode", args.mode,
+           "--scale", str(args.scale), "--steps", "1", "--warmup", "0", "--no-e2e", "--no-cpu",
+           "--no-traffic"] + (["--host-build"] if args.host_build else [])
+    env = dict(os.environ, TETRAY_BENCH_UNDER_NCU="1")
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        env.pop(k, None)
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=900, env=env)
+    except (OSError, subprocess.TimeoutExpired) as e:
+        return None, f"ncu failed: {e}"
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith('"')]
+    per = {}
+    for row in csv.DictReader(io.StringIO("\n".join(lines))):
+        try:
+            v = float(row["Metric Value"].replace(",", ""))
+        except (KeyError, ValueError):
+            continue
+        unit = row.get("Metric Unit", "")
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6,
+                 "GB": 1e9}.get(unit, 1)
+        per.setdefault(row["ID"], {})[row["Metric Name"]] = v * scale
+    best = None
+    for d in per.values():
+        t = d.get("dram__bytes_read.sum", 0.0) + d.get("dram__bytes_write.sum", 0.0)
+        if best is None or t > best:
+            best = t
+    if best is None:
+        return None, f"no march_sm launch in ncu output (rc {res.returncode})"
+    return int(best), "ncu dram__bytes_read.sum + dram__bytes_write.sum, this workload"
+
+
+# ------------------------------------------------------------ reference arm
 
 def run_reference(args, rank):
+    """The stock reference render() on whole frames of the workload."""
     if rank != 0:
         return 0
-    import paper_1908_01906_b200 as B
-    scene, cam, par, _ = build_workload(B, args)
-    from oracle.oracle import OracleScene
-    orc = OracleScene(scene)
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tetray_bench_numba")
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "tetray").exists():
+        print(json.dumps({"impl": "reference",
+                          "unavailable": "baseline/_ref (pip install --target baseline/_ref "
+                                         "of /root/reference/pkg) is missing"}), flush=True)
+        return 0
+    sys.path.insert(0, str(ref))
+    import cases as C
+    import tetray
+    from oracle.stock_scene import build_stock_scene
+    n = scene_n(args.scene)
+    t0 = time.perf_counter()
+    if n >= 128 or args.scene.startswith("grid"):
+        scene = build_stock_scene(tetray, n, C.radial16_tf_doc(n))
+    else:
+        scene = C.build_scene(tetray, public_name(args.scene))    # the stock Scene.build
+    build_s = time.perf_counter() - t0
+    cam = C.camera(tetray, public_name(args.scene), scale=args.scale)
+    par = C.params(tetray, public_name(args.scene))
     threads = os.cpu_count() or 1
-    for _ in range(max(args.warmup, 1) if args.warmup else 0):
-        orc.render(cam, args.mode, par, threads=threads, rows=(0, cam.height // 8))
-    # each step: a bounded row band (1/8 of the frame), so K steps stay within minutes
-    band = max(1, cam.height // 8)
-    times, samples = [], 0
-    for k in range(args.steps):
-        r0 = (k * band) % cam.height
+    for _ in range(args.warmup):   # the first frame also JIT-compiles the numba kernels
+        tetray.render(scene, cam, args.mode, par, threads=threads)
+    times, walls, samples = [], [], None
+    t_start = time.perf_counter()
+    for _ in range(args.steps):
         t0 = time.perf_counter()
-        _, s, _, _ = orc.render(cam, args.mode, par, threads=threads, rows=(r0, min(r0 + band, cam.height)))
+        fb, st = tetray.render(scene, cam, args.mode, par, threads=threads)
         times.append(time.perf_counter() - t0)
-        samples += int(s.sum())
+        walls.append(st.wall_ms)
+        samples = st.total_samples
+        if time.perf_counter() - t_start > args.ref_budget_s:
+            break
     tot = sum(times)
-    v = samples / tot
+    v = samples * len(times) / tot
+    try:
+        import numba
+        nthreads = numba.config.NUMBA_NUM_THREADS
+    except Exception:   # pragma: no cover
+        nthreads = None
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": tot * 1000.0 / args.steps, "higher_is_better": True,
+            "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
+            "ms_per_step": tot * 1000.0 / len(times), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.scene} {cam.width}x{cam.height} {args.mode}",
-                       "scene": args.scene, "mode": args.mode, "width": cam.width,
-                       "height": cam.height, "n_tets": scene.mesh.n_tets,
-                       "n_partitions": scene.n_partitions, "l2": "n/a (CPU)"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} row bands of {band} rows "
-                                       f"(oracle/oracle.c, OpenMP)"},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": workload_config(args, scene.mesh.n_tets, len(scene.partitions), samples),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "cpu_model": cpu_model(), "numba_num_threads": nthreads,
+                             "sample": f"{len(times)} whole frame(s) through the stock "
+                                       f"tetray.render(threads={threads}) (numba)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "detail": {"scene_build_s": round(build_s, 2),
+                       "render_wall_ms_median": statistics.median(walls),
+                       "steps_requested": args.steps,
+                       "scene": "stock tetray dataclasses around oracle/build.c arrays"
+                                if n >= 128 else "stock tetray Scene.build"}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def main():
-    args = parse()
+# ------------------------------------------------------------------ GPU arm
+
+def relaunch_distributed(argv) -> int:
+    """`--gpus N` without a torchrun environment: run N ranks of this script."""
+    args = parse(argv)
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), str(Path(__file__).resolve())] + list(argv)
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(argv)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -216,10 +380,12 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nranks = 1
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+        nranks = dist.get_world_size()
 
-    scene, cam, par, build_s = build_workload(B, args)
+    scene, cam, par, build_s = build_gpu_workload(B, args)
     t0 = time.perf_counter()
     dscene = device_scene_for(scene, dev)
     upload_s = time.perf_counter() - t0
@@ -230,13 +396,12 @@ def main():
 
     runner = D.ShardedFrame(dscene, scene, cam, mode_id, par, track=track,
                             rank=rank if world > 1 else 0, world=world, flags=args.flags)
-    # warm-up
     for _ in range(args.warmup):
         runner.run(stream)
     torch.cuda.synchronize()
-    total_samples = runner.total_samples()
+    total_samples = runner.total_samples() if rank == 0 else 0
 
-    # timed region: K steps, L2 flushed between steps, kernel timed with events
+    # timed region: K steps, L2 flushed between steps, frame timed with events
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
@@ -255,7 +420,7 @@ def main():
             ev[k][1].record(stream)
         torch.cuda.synchronize()
         time.sleep(0.1)
-    launches_per_step = runner.launches_per_step()   # of the timed frames (not the e2e ones)
+    launches_per_step = runner.launches_per_step()
     if world > 1:
         dist.barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -273,31 +438,30 @@ def main():
     clocks = clk.summary()
     value = total_samples * args.steps / t_max
 
-    # roofline of the dominant kernel (render_frame_kernel), per launch
+    # roofline of the dominant kernel (march_sm_kernel), per launch, rank 0's share
     hbm, peak_kind = peaks()
     my_samples = runner.local_samples()
     my_pixels = runner.local_pixels()
-    alg_bytes = RECORD_BYTES[int(scene.mesh.centering)] * my_samples + PIXEL_BYTES * my_pixels
-    achieved = alg_bytes / m_max / 1e9
+    rb = RECORD_BYTES[int(scene.mesh.centering)]
+    alg_bytes = rb * my_samples + PIXEL_BYTES * my_pixels
+    achieved = alg_bytes / m_local / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-            "frac": achieved / hbm, "traffic": ncu_traffic(), "peak_kind": peak_kind,
-            "kernel": "march_sm_kernel", "kernel_ms": m_max * 1e3,
-            "frame_kernels_ms": k_max * 1e3,
-            "frame_frac": alg_bytes / k_max / 1e9 / hbm,
+            "frac": achieved / hbm, "traffic": None, "peak_kind": peak_kind,
+            "kernel": "march_sm_kernel", "kernel_ms": m_local * 1e3,
+            "frame_kernels_ms": k_local * 1e3,
+            "frame_frac": alg_bytes / k_local / 1e9 / hbm,
             "alg_bytes_per_launch": alg_bytes,
-            "alg_bytes_model": f"{RECORD_BYTES[int(scene.mesh.centering)]} B/sample x "
-                               f"{my_samples} samples + {PIXEL_BYTES} B/pixel x {my_pixels} pixels"}
+            "alg_bytes_model": f"{rb} B/sample x {my_samples} samples + {PIXEL_BYTES} B/pixel x "
+                               f"{my_pixels} pixels (SURVEY.md §8d)"}
 
-    # e2e through render(): epoch H2D + outputs D2H inside the timed region
+    # e2e through the public render(): epoch H2D + outputs D2H inside the timed region
     e2e = None
     if not args.no_e2e:
         if world > 1:
-            e2e = D.bench_e2e_sharded(runner, args.steps, rank, world)
+            e2e = D.bench_e2e_sharded(scene, cam, args.mode, par, args.steps, dev)
         else:
             fb = None
             for _ in range(max(args.warmup, 3)):
-                # hold the previous frame like the timed loop does, so the
-                # page-locked result buffers are in the host cache already
                 dscene._epochs.clear()
                 fb, st = B.render(scene, cam, args.mode, par, device=dev)
             per = []
@@ -310,17 +474,24 @@ def main():
                 per.append(time.perf_counter() - t1)
             dt = time.perf_counter() - t0
             ep = next(iter(dscene._epochs.values()))
-            h2d = ep.h2d_bytes
             d2h = fb.rgba.nbytes + fb.samples.nbytes + 8 * (3 + scene.n_partitions)
             e2e = {"value": st.total_samples * e2e_steps / dt, "unit": UNIT,
-                   "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                   "h2d_bytes_per_step": int(ep.h2d_bytes), "d2h_bytes_per_step": int(d2h),
                    "ms_per_step": dt * 1000.0 / e2e_steps, "steps": e2e_steps,
                    "ms_per_step_median": statistics.median(per) * 1000.0,
                    "ms_per_step_min": min(per) * 1000.0}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_reference(scene, cam, par, args, args.cpu_seconds)
+        cpu = cpu_reference(args, args.cpu_seconds)
+        if cpu["samples_per_frame"] != total_samples:
+            raise RuntimeError(f"oracle frame has {cpu['samples_per_frame']} samples, the GPU "
+                               f"frame {total_samples}")
+
+    if rank == 0 and not args.no_traffic:
+        roof["traffic"], roof["traffic_source"] = ncu_traffic(args)
+        if roof["traffic"]:
+            roof["traffic_per_sample"] = roof["traffic"] / max(my_samples, 1)
 
     if rank == 0:
         line = {
@@ -328,21 +499,19 @@ def main():
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max * 1000.0 / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.scene} {cam.width}x{cam.height} {args.mode}",
-                       "scene": args.scene, "mode": args.mode, "width": cam.width,
-                       "height": cam.height, "n_tets": scene.mesh.n_tets,
-                       "n_partitions": scene.n_partitions,
-                       "n_active": int(scene.meta_state()[0].sum()),
-                       "samples_per_frame": total_samples,
-                       "rays_per_s": cam.width * cam.height * args.steps / t_max,
-                       "l2": "flushed between steps (256 MiB write)",
-                       "parallelism": f"pixel tiles interleaved over {world} GPU(s)",
-                       "flags": hex(args.flags),
-                       "scene_build_s": round(build_s, 3), "upload_s": round(upload_s, 3),
-                       "resident_bytes": int(dscene.resident_bytes)},
+            "config": workload_config(args, scene.mesh.n_tets, scene.n_partitions,
+                                      total_samples),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "clocks": clocks,
+            "detail": {"l2": "flushed between steps (256 MiB write)",
+                       "rays_per_s": cam.width * cam.height * args.steps / t_max,
+                       "n_active": int(scene.meta_state()[0].sum()),
+                       "parallelism": f"pixel tiles interleaved over {world} GPU(s)",
+                       "comm_nranks": nranks, "flags": hex(args.flags),
+                       "scene_path": type(scene).__name__,
+                       "scene_build_s": round(build_s, 3), "upload_s": round(upload_s, 3),
+                       "resident_bytes": int(dscene.resident_bytes)},
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -48,6 +48,10 @@ def lib():
         L.orc_step_size.argtypes = [C.c_double] * 4
         L.orc_opacity_correction.restype = C.c_double
         L.orc_opacity_correction.argtypes = [C.c_double] * 3
+        L.orc_tf_sample.restype = None
+        L.orc_tf_sample.argtypes = [f64p, C.c_long, C.c_double, C.c_double, C.c_double, f64p]
+        L.orc_build_bvh_fast.restype = C.c_int64
+        L.orc_build_bvh_fast.argtypes = L.orc_build_bvh.argtypes
         L.orc_hash01.restype = C.c_double
         L.orc_hash01.argtypes = [C.c_int64, C.c_int64]
         mesh_args = [f64p, f64p, i64p, i64p, i64p, i64p, i64p, i64p, f64p, f64p, f64p, C.c_int64]
@@ -83,7 +87,7 @@ def _p(a, t):
 class FlatBVH:
     """Reference-layout BVH (bvh.py:24-38) built by orc_build_bvh."""
 
-    def __init__(self, lo: np.ndarray, hi: np.ndarray, leaf_size: int):
+    def __init__(self, lo: np.ndarray, hi: np.ndarray, leaf_size: int, fast: bool = True):
         lo = np.ascontiguousarray(lo, dtype=np.float64)
         hi = np.ascontiguousarray(hi, dtype=np.float64)
         n = len(lo)
@@ -95,7 +99,8 @@ class FlatBVH:
         self.start = np.zeros(m, np.int64)
         self.count = np.zeros(m, np.int64)
         self.prim = np.zeros(n, np.int64)
-        k = lib().orc_build_bvh(n, _p(lo, C.c_double), _p(hi, C.c_double), leaf_size,
+        build = lib().orc_build_bvh_fast if fast else lib().orc_build_bvh
+        k = build(n, _p(lo, C.c_double), _p(hi, C.c_double), leaf_size,
                                 _p(self.node_lo, C.c_double), _p(self.node_hi, C.c_double),
                                 _p(self.left, C.c_int64), _p(self.right, C.c_int64),
                                 _p(self.start, C.c_int64), _p(self.count, C.c_int64),
@@ -187,6 +192,14 @@ def step_size(s1, s2, p, sigma):
 
 def opacity_correction(alpha, s, s1):
     return lib().orc_opacity_correction(alpha, s, s1)
+
+
+def tf_sample(table, lo, hi, v):
+    """K:74-90 -> (r, g, b, a)."""
+    table = np.ascontiguousarray(table, dtype=np.float64)
+    out = np.zeros(4)
+    lib().orc_tf_sample(_p(table, C.c_double), len(table), lo, hi, float(v), _p(out, C.c_double))
+    return tuple(out.tolist())
 
 
 def hash01(ix, iy):

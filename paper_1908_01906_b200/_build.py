@@ -67,8 +67,8 @@ def build_library(force: bool = False, verbose: bool = False) -> Path:
 def build_oracle(force: bool = False) -> Path:
     """The C parity oracle (test infrastructure; see oracle/oracle.c)."""
     target = ROOT / "oracle" / "liboracle.so"
-    src = ROOT / "oracle" / "oracle.c"
-    if force or _stale(target, [src]):
+    srcs = [ROOT / "oracle" / f for f in ("oracle.c", "build.c", "Makefile")]
+    if force or _stale(target, srcs):
         res = subprocess.run(["make", "-C", str(ROOT / "oracle"), "-B" if force else "-s"],
                              capture_output=True, text=True)
         if res.returncode != 0:

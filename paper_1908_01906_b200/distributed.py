@@ -1,12 +1,16 @@
 """Multi-GPU frame rendering: one process per GPU, the scene
 replicated in every GPU's HBM, the frame's 8x4 pixel tiles interleaved over
 the ranks (tile t -> rank t % world, slot t // world), so long and short rays
-spread evenly.  The merge is exactly the frame's data dependencies:
+spread evenly.  The merge is exactly the frame's data dependencies, and only
+rank 0 (the caller that returns the image) receives it:
 
-  * disjoint pixel tiles   -> NCCL all-gather of each rank's compact slots,
-                              then tr_scatter_tiles into image layout
-  * mergeable aggregates   -> NCCL all-reduce (int64 sum) of
+  * disjoint pixel tiles   -> NCCL gather of each rank's compact slots to
+                              rank 0, then tr_scatter_tiles into image layout
+  * mergeable aggregates   -> NCCL reduce (int64 sum) to rank 0 of
                               [total samples, visited sum, per-partition samples]
+
+With the gloo backend (CPU-side debugging, the 2-process one-GPU test) the
+same collectives run on host copies of the device tensors.
 
 Integer sums are order independent and tiles are disjoint, so an N-GPU frame
 is bit-identical to the 1-GPU frame (tests/test_distributed.py checks the
@@ -84,6 +88,35 @@ def merge_partials(rank_rgba, rank_samples, rank_visited, rank_counters, world, 
     return (*scatter(width, height, world, slots, g_rgba, g_samples, g_visited), counters)
 
 
+def _gloo() -> bool:
+    import torch.distributed as dist
+    return dist.get_backend() == "gloo"
+
+
+def _gather0(src, dst, rank: int, world: int) -> None:
+    """dst (rank 0: world equal chunks) <- every rank's src."""
+    import torch
+    import torch.distributed as dist
+    if _gloo():
+        h = src.cpu()
+        lst = [torch.empty_like(h) for _ in range(world)] if rank == 0 else None
+        dist.gather(h, lst, dst=0)
+        if rank == 0:
+            dst.copy_(torch.cat(lst))
+        return
+    dist.gather(src, list(dst.chunk(world)) if rank == 0 else None, dst=0)
+
+
+def _reduce0(t) -> None:
+    import torch.distributed as dist
+    if _gloo():
+        h = t.cpu()
+        dist.reduce(h, dst=0)
+        t.copy_(h)
+        return
+    dist.reduce(t, dst=0)
+
+
 class ShardedFrame:
     """One frame's launch plan on one rank: epoch, frame descriptor, buffers
     and (world > 1) the NCCL merge.  world == 1 renders straight into the
@@ -148,12 +181,13 @@ class ShardedFrame:
         if kernel_events is not None:
             kernel_events[1].record(stream)
         if self.compact:
-            import torch.distributed as dist
             self.local.copy_(fb.counters[:2])
-            dist.all_gather_into_tensor(self.g_rgba, fb.rgba)
-            dist.all_gather_into_tensor(self.g_samples, fb.samples)
-            dist.all_gather_into_tensor(self.g_visited, fb.visited)
-            dist.all_reduce(fb.counters)
+            _gather0(fb.rgba, self.g_rgba, self.rank, self.world)
+            _gather0(fb.samples, self.g_samples, self.rank, self.world)
+            _gather0(fb.visited, self.g_visited, self.rank, self.world)
+            _reduce0(fb.counters)
+            if self.rank != 0:
+                return
             _lib.check(_lib.lib().tr_scatter_tiles(
                 self.w, self.h, self.world, C.c_void_p(self.g_rgba.data_ptr()),
                 C.c_void_p(self.g_samples.data_ptr()), C.c_void_p(self.g_visited.data_ptr()),
@@ -183,28 +217,83 @@ class ShardedFrame:
                 self.fb.counters.cpu().numpy())
 
 
-def bench_e2e_sharded(runner: ShardedFrame, steps: int, rank: int, world: int) -> dict:
-    """End-to-end sharded frames: epoch re-upload (H2D) each step, image
-    read back (D2H) on rank 0; wall clock, max over ranks."""
+_FRAMES: dict = {}
+
+
+def render_sharded(scene, camera, mode: str, params, *, jitter: bool = False,
+                   track_per_partition: bool = True, device=None, flags: int = 0):
+    """render() over the ranks of the initialised torch.distributed group:
+    every rank calls it with the same arguments; rank 0 returns the
+    (Framebuffer, RenderStats) of the whole frame, bit-identical to the
+    one-GPU render(); the other ranks return (None, None)."""
     import torch
     import torch.distributed as dist
-    dev = runner.dscene.device
-    stream = torch.cuda.current_stream(dev)
+
+    from .device import device_scene_for
+    from .render import _MODE_IDS, Framebuffer, RenderStats
+    rank, world = dist.get_rank(), dist.get_world_size()
+    dscene = device_scene_for(scene, device)
+    track = track_per_partition and mode != "reference"
+    w, h = int(camera.width), int(camera.height)
+    key = (id(dscene), w, h, world, rank, _MODE_IDS[mode], track, bool(jitter), flags)
+    runner = _FRAMES.get(key)
+    if runner is None or runner.scene is not scene:
+        runner = ShardedFrame(dscene, scene, camera, _MODE_IDS[mode], params, track=track,
+                              rank=rank, world=world, flags=flags, jitter=jitter)
+        _FRAMES.clear()
+        _FRAMES[key] = runner
+    runner.camera, runner.params = camera, params
+    runner.frame = dscene.frame_desc(scene, camera, _MODE_IDS[mode], params, jitter, track,
+                                     flags, shard_rank=rank, shard_count=world, compact=True)
+    t0 = time.perf_counter()
+    with dscene.lock, torch.cuda.device(dscene.device):
+        stream = torch.cuda.current_stream(dscene.device)
+        runner.epoch = dscene.epoch(scene.meta_state(), params, stream)
+        runner.run(stream)
+        if rank != 0:
+            stream.synchronize()
+            return None, None
+        rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
+        samp_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
+        cnt_h = torch.empty(runner.fb.counters.numel(), dtype=torch.int64, pin_memory=True)
+        rgba_h.view(-1, 4).copy_(runner.rgba, non_blocking=True)
+        samp_h.view(-1).copy_(runner.samples, non_blocking=True)
+        cnt_h.copy_(runner.fb.counters, non_blocking=True)
+        stream.synchronize()
+    cnt = cnt_h.numpy()
+    samples = samp_h.numpy()
+    fb = Framebuffer(width=w, height=h, rgba=rgba_h.numpy(), samples=samples,
+                     background=np.asarray(scene.background, dtype=np.float64).copy())
+    st = RenderStats(total_samples=int(cnt[0]), wall_ms=(time.perf_counter() - t0) * 1e3,
+                     partitions_visited_mean=float(np.float64(cnt[1]) / np.float64(w * h)),
+                     per_partition_samples=cnt[3:].copy() if track else None, samples=samples,
+                     device_ms=0.0, gpu_launches=runner.launches_per_step())
+    return fb, st
+
+
+def bench_e2e_sharded(scene, camera, mode: str, params, steps: int, device) -> dict:
+    """End-to-end sharded frames through render_sharded: the epoch is
+    re-uploaded (H2D) every step on every rank and rank 0 reads the image
+    back (D2H); wall clock, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import device_scene_for
+    dscene = device_scene_for(scene, device)
+    for _ in range(3):
+        render_sharded(scene, camera, mode, params, device=device)
     dist.barrier()
     t0 = time.perf_counter()
+    fb = st = None
     for _ in range(steps):
-        runner.dscene._epochs.clear()
-        runner.epoch = runner.dscene.epoch(runner.scene.meta_state(), runner.params)
-        runner.run(stream)
-        if rank == 0:
-            rgba = runner.rgba.cpu()
-            samples = runner.samples.cpu()
-        else:
-            torch.cuda.synchronize(dev)
-    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+        dscene._epochs.clear()
+        fb, st = render_sharded(scene, camera, mode, params, device=device)
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dscene.device)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
-    total = runner.total_samples()
-    d2h = (runner.w * runner.h * 40 + 8 * runner.fb.counters.numel()) if rank == 0 else 0
-    return {"value": total * steps / float(dt[0]), "unit": "samples/s",
-            "h2d_bytes_per_step": int(runner.epoch.h2d_bytes), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": float(dt[0]) * 1000.0 / steps}
+    ep = next(iter(dscene._epochs.values()))
+    if dist.get_rank() != 0:
+        return None
+    d2h = fb.rgba.nbytes + fb.samples.nbytes + 8 * (3 + dscene.n_parts)
+    return {"value": st.total_samples * steps / float(dt[0]), "unit": "samples/s",
+            "h2d_bytes_per_step": int(ep.h2d_bytes), "d2h_bytes_per_step": int(d2h),
+            "ms_per_step": float(dt[0]) * 1000.0 / steps, "steps": steps}

@@ -54,6 +54,13 @@ def built_lib():
 
 
 @pytest.fixture(scope="session")
+def built_oracle():
+    from paper_1908_01906_b200 import _build
+    _build.build_oracle()
+    return True
+
+
+@pytest.fixture(scope="session")
 def B(built_lib):
     import paper_1908_01906_b200 as B
     return B
