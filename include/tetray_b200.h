@@ -57,13 +57,26 @@ typedef struct TrPNode {
     uint32_t minid[2];
 } TrPNode;
 
-/* Leaf header.  ex_lo/ex_hi: the leaf's EXCLUSIVE box (rounded inward to
- * f32): no other leaf's box meets its interior, so a point strictly inside
- * it can only be contained by this leaf's tets. */
+/* Leaf header, 64 B.  ex_lo/ex_hi: the leaf's EXCLUSIVE box (rounded
+ * inward to f32): no other leaf's box meets its interior, so a point
+ * strictly inside it can only be contained by this leaf's tets.
+ * walk: the leaf walk table (tr_leaf_walk; all zero = no walk, the leaf is
+ * scanned in id order).  For leaf-local tet i < 8, the 16-bit entry
+ * (walk[i / 2] >> (16 * (i % 2))): bits [3f, 3f+3) = the leaf-local tet
+ * across the face opposite vertex f (i itself: none in the leaf); bit 12 =
+ * CERTIFIED: a point whose barycentrics in tet i are all >= TR_WALK_TAU lies
+ * outside every lower-id tet of the leaf with the reference's -1e-9 slack
+ * (K:128), so tet i is the lowest-index containing tet (K:119) without
+ * testing them.  walk[4]: bits 0-2 = the walk's first tet (the largest),
+ * bit 31 = table valid. */
 typedef struct TrPLeaf {
     float ex_lo[3], ex_hi[3];
     uint32_t start, count;
+    uint32_t walk[8];
 } TrPLeaf;
+
+/* The walk's certification margin on the barycentrics (tr_leaf_walk). */
+#define TR_WALK_TAU 1e-6
 
 /* Partition BVH2 node: f64 child boxes (exact unions of partition boxes,
  * so node pruning is conservative for the exact f64 slab test).
@@ -115,6 +128,18 @@ int tr_pbvh_build(int64_t n_tets, const double *box_lo, const double *box_hi, in
 /* sizes: [0] = nodes, [1] = leaves, [2] = leaf ids, [3] = grid cells */
 int tr_pbvh_sizes(const TrHostBuf *b, int64_t *sizes4);
 int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids);
+/* Fill the walk tables of leaves[0, n_leaves) (in place) from the mesh:
+ * rec_ids[k] = tet id of record k (NULL: k), vertices (V,3), tets (T,4).
+ * Face neighbours are matched by shared vertex ids; the CERTIFIED bit of
+ * tet i is set only when, for every lower-id tet j of the leaf, a face plane
+ * of j separates tet i shrunk to barycentrics >= TR_WALK_TAU from j by more
+ * than the 1e-9 slack plus a 1e-8 margin, or a face plane of i separates j
+ * inflated by that slack from the shrunk tet (checked in long double at the
+ * shrunk/inflated vertices; leaves whose coordinates are too large for
+ * those margins to cover the device's rounding get no certificates).  Leaves
+ * of more than 8 tets get no table. */
+int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *rec_ids,
+                 const double *vertices, const int64_t *tets);
 /* Uniform-grid leaf index: cell (x,y,z) -> leaf whose exclusive box covers
  * most of it (-1: none).  cell = floor((p - org) * scale), row-major x,y,z. */
 int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
@@ -294,6 +319,7 @@ typedef struct TrFrame {
 /* flags bits 20-22: trace CTAs per SM (0 = occupancy maximum; tuning) */
 #define TR_FLAG_NO_CAND 0x800000 /* modes 1/2: intervals by the per-ray BSP walk, not the candidate raster (testing) */
 #define TR_FLAG_FORCE_CAND 0x1000000 /* the candidate raster also above 1M pixels (default there: the BSP walk) */
+#define TR_FLAG_NO_WALK 0x2000000 /* exclusive leaves scanned in id order, not walked (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */

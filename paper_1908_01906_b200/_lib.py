@@ -92,7 +92,7 @@ TET_RECORD_DTYPE = np.dtype([("inv", "<f8", 9), ("orig", "<f8", 3), ("f", "<f8",
 PNODE_DTYPE = np.dtype([("lo0", "<f4", 3), ("hi0", "<f4", 3), ("lo1", "<f4", 3),
                         ("hi1", "<f4", 3), ("child", "<i4", 2), ("minid", "<u4", 2)])
 PLEAF_DTYPE = np.dtype([("ex_lo", "<f4", 3), ("ex_hi", "<f4", 3), ("start", "<u4"),
-                        ("count", "<u4")])
+                        ("count", "<u4"), ("walk", "<u4", 8)])
 BNODE_DTYPE = np.dtype([("box", "<f8", (2, 6)), ("child", "<i4", 2), ("pad", "<i4", 2)])
 KNODE_DTYPE = np.dtype([("split", "<f8"), ("info", "<i4"), ("aux", "<i4")])
 
@@ -116,6 +116,7 @@ _SIGNATURES = [
     ("tr_pbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("tr_pbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_pbvh_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_leaf_walk", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_pbvh_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p]),
     ("tr_pbvh_coverage", C.c_double, [C.c_void_p]),
     ("tr_cells_build", C.c_int, [C.c_void_p, c_f64p, c_f64p, C.c_int32, C.c_int32,

@@ -269,7 +269,7 @@ struct PCtx {
 
 PRef p_make_leaf(PCtx &C, PBuf &O, int64_t b, int64_t e) {
     std::sort(C.idx.begin() + b, C.idx.begin() + e);
-    TrPLeaf L;
+    TrPLeaf L{};
     L.start = (uint32_t)O.ids.size();
     L.count = (uint32_t)(e - b);
     PRef r;
@@ -1093,6 +1093,191 @@ int tr_knodes_activity(int64_t n_nodes, const TrKNode *nodes, const int32_t *lea
             any = (out[i + 1] | out[N.info >> 2]) ? 1 : 0;
         }
         out[i] = any;
+    }
+    return TR_OK;
+}
+
+// ============================================================ leaf walk tables
+//
+// K:93-136 returns the LOWEST-index tet whose barycentrics are all >= -1e-9.
+// Inside a leaf's exclusive box only the leaf's tets can contain the point,
+// and the kernels used to test them in id order (a regular cube: 3.3 record
+// loads per sample, the central tet -- a third of the volume -- last).  The
+// walk starts at the largest tet and steps across the most violated face;
+// a tet that accepts the point with every barycentric >= TR_WALK_TAU is the
+// answer when it is CERTIFIED against every lower-id tet of the leaf (below);
+// anything else falls back to the id-order scan, so the result is always
+// the reference's.
+namespace {
+
+constexpr long double W_TOL = 1e-9L;     // K:15
+constexpr long double W_M1 = 1e-8L;      // margin beyond the slack
+constexpr long double W_TAU = (long double)TR_WALK_TAU;
+
+struct TetL {
+    long double v[4][3];
+    long double inv[3][3];
+    bool ok;
+};
+
+TetL tet_geo(const double *const vp[4]) {
+    TetL T;
+    for (int i = 0; i < 4; ++i)
+        for (int a = 0; a < 3; ++a) T.v[i][a] = vp[i][a];
+    long double e[3][3];   // columns: v1-v0, v2-v0, v3-v0 (mesh.py:253)
+    for (int a = 0; a < 3; ++a)
+        for (int c = 0; c < 3; ++c) e[a][c] = T.v[c + 1][a] - T.v[0][a];
+    const long double det = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                            e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                            e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+    T.ok = det != 0.0L && std::isfinite((double)det);
+    if (!T.ok) return T;
+    T.inv[0][0] = (e[1][1] * e[2][2] - e[1][2] * e[2][1]) / det;
+    T.inv[0][1] = (e[0][2] * e[2][1] - e[0][1] * e[2][2]) / det;
+    T.inv[0][2] = (e[0][1] * e[1][2] - e[0][2] * e[1][1]) / det;
+    T.inv[1][0] = (e[1][2] * e[2][0] - e[1][0] * e[2][2]) / det;
+    T.inv[1][1] = (e[0][0] * e[2][2] - e[0][2] * e[2][0]) / det;
+    T.inv[1][2] = (e[0][2] * e[1][0] - e[0][0] * e[1][2]) / det;
+    T.inv[2][0] = (e[1][0] * e[2][1] - e[1][1] * e[2][0]) / det;
+    T.inv[2][1] = (e[0][1] * e[2][0] - e[0][0] * e[2][1]) / det;
+    T.inv[2][2] = (e[0][0] * e[1][1] - e[0][1] * e[1][0]) / det;
+    return T;
+}
+
+void bary_l(const TetL &T, const long double p[3], long double l[4]) {
+    long double q[3];
+    for (int a = 0; a < 3; ++a) q[a] = p[a] - T.v[0][a];
+    for (int r = 0; r < 3; ++r) l[r + 1] = T.inv[r][0] * q[0] + T.inv[r][1] * q[1] + T.inv[r][2] * q[2];
+    l[0] = 1.0L - l[1] - l[2] - l[3];
+}
+
+// No point that tet K accepts with every barycentric >= TAU is accepted by
+// tet J (barycentrics >= -1e-9): (A) a face plane of J has K shrunk to
+// barycentrics >= TAU / 2 beyond -(slack + margin), or (B) a face plane of
+// K has J inflated by (slack + margin) below TAU / 2.  Convexity: checking
+// the 4 vertices of the shrunk / inflated tet covers it.  The device's
+// rounding of either tet's barycentrics (<= 1e-10, `certifiable` below) is
+// covered by the TAU / 2 and 1e-8 margins.
+bool separated(const TetL &J, const TetL &K) {
+    long double w[4][3], u[4][3], sk[3] = {0, 0, 0}, sj[3] = {0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+        for (int a = 0; a < 3; ++a) { sk[a] += K.v[i][a]; sj[a] += J.v[i][a]; }
+    const long double s = W_TOL + W_M1;
+    for (int i = 0; i < 4; ++i)
+        for (int a = 0; a < 3; ++a) {
+            w[i][a] = (1.0L - 2.0L * W_TAU) * K.v[i][a] + 0.5L * W_TAU * sk[a];
+            u[i][a] = (1.0L + 4.0L * s) * J.v[i][a] - s * sj[a];
+        }
+    long double lw[4][4], lu[4][4];
+    for (int i = 0; i < 4; ++i) { bary_l(J, w[i], lw[i]); bary_l(K, u[i], lu[i]); }
+    for (int f = 0; f < 4; ++f) {
+        bool a_ok = true, b_ok = true;
+        for (int i = 0; i < 4; ++i) {
+            a_ok = a_ok && lw[i][f] <= -(W_TOL + W_M1);
+            b_ok = b_ok && lu[i][f] <= 0.5L * W_TAU;
+        }
+        if (a_ok || b_ok) return true;
+    }
+    return false;
+}
+
+// The table of one leaf: n <= 8 tets, vertex ids vid[i][4], positions vp[i][4],
+// tet ids ids[i] (ascending or not).
+void walk_table(int n, const int64_t (*vid)[4], const double *const (*vp)[4], const int64_t *ids,
+                uint32_t walk[8]) {
+    for (int k = 0; k < 8; ++k) walk[k] = 0;
+    if (n < 1 || n > 8) return;
+    TetL geo[8];
+    long double vmax = 0.0L, imax = 0.0L, vol_best = -1.0L;
+    int first = 0;
+    for (int i = 0; i < n; ++i) {
+        geo[i] = tet_geo(vp[i]);
+        if (!geo[i].ok) return;
+        long double isum = 0.0L;
+        for (int r = 0; r < 3; ++r)
+            for (int c = 0; c < 3; ++c) isum += std::fabs(geo[i].inv[r][c]);
+        imax = std::max(imax, isum);
+        for (int q = 0; q < 4; ++q)
+            for (int a = 0; a < 3; ++a) vmax = std::max(vmax, (long double)std::fabs(vp[i][q][a]));
+        // volume ~ 1 / |det(inv)|: the largest tet has the smallest inverse
+        const long double (&m)[3][3] = geo[i].inv;
+        const long double dinv = std::fabs(m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) -
+                                           m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+                                           m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]));
+        const long double vol = 1.0L / dinv;
+        if (vol > vol_best) { vol_best = vol; first = i; }
+    }
+    // the device's barycentric rounding error is a few ulp of |inv| * |coords|;
+    // it must stay far below the 1e-8 and TAU / 2 margins
+    const bool certifiable = imax * (vmax + 1.0L) * 0x1p-51L < 1e-10L;
+    for (int i = 0; i < n; ++i) {
+        uint32_t e = 0;
+        for (int f = 0; f < 4; ++f) {
+            int64_t fa[3], m = 0;
+            for (int q = 0; q < 4; ++q)
+                if (q != f) fa[m++] = vid[i][q];
+            std::sort(fa, fa + 3);
+            int nb = i;
+            for (int j = 0; j < n && nb == i; ++j) {
+                if (j == i) continue;
+                int hits = 0;
+                for (int q = 0; q < 4; ++q)
+                    hits += (vid[j][q] == fa[0]) + (vid[j][q] == fa[1]) + (vid[j][q] == fa[2]);
+                if (hits == 3) nb = j;
+            }
+            e |= (uint32_t)nb << (3 * f);
+        }
+        bool cert = certifiable;
+        for (int j = 0; j < n && cert; ++j)
+            if (ids[j] < ids[i]) cert = separated(geo[j], geo[i]);
+        if (cert) e |= 1u << 12;
+        walk[i >> 1] |= e << (16 * (i & 1));
+    }
+    walk[4] = (uint32_t)first | (1u << 31);
+}
+
+}  // namespace
+
+void tr_walk_table_cube(int parity, uint32_t walk[8]) {
+    // mesh.py:151-163: corner c = 4x + 2y + z; odd cubes mirror x (c ^ 4)
+    static const int P[5][4] = {{0, 4, 2, 1}, {6, 2, 4, 7}, {5, 1, 7, 4}, {3, 7, 1, 2}, {4, 2, 1, 7}};
+    double pos[8][3];
+    for (int c = 0; c < 8; ++c) {
+        pos[c][0] = (c >> 2) & 1; pos[c][1] = (c >> 1) & 1; pos[c][2] = c & 1;
+    }
+    int64_t vid[5][4], ids[5];
+    const double *vp[5][4];
+    for (int k = 0; k < 5; ++k) {
+        ids[k] = k;
+        for (int q = 0; q < 4; ++q) {
+            const int c = parity ? (P[k][q] ^ 4) : P[k][q];
+            vid[k][q] = c;
+            vp[k][q] = pos[c];
+        }
+    }
+    walk_table(5, vid, vp, ids, walk);
+}
+
+extern "C" int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *rec_ids,
+                            const double *vertices, const int64_t *tets) {
+    if (n_leaves < 0 || (n_leaves > 0 && (!leaves || !vertices || !tets)))
+        return tr_fail(TR_EINVAL, "tr_leaf_walk: invalid arguments");
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t L = 0; L < n_leaves; ++L) {
+        TrPLeaf &lf = leaves[L];
+        const int n = (int)std::min<uint32_t>(lf.count, 9);
+        int64_t vid[8][4], ids[8];
+        const double *vp[8][4];
+        if (n > 8) { for (int k = 0; k < 8; ++k) lf.walk[k] = 0; continue; }
+        for (int i = 0; i < n; ++i) {
+            const int64_t t = rec_ids ? (int64_t)rec_ids[lf.start + i] : (int64_t)lf.start + i;
+            ids[i] = t;
+            for (int q = 0; q < 4; ++q) {
+                vid[i][q] = tets[4 * t + q];
+                vp[i][q] = vertices + 3 * vid[i][q];
+            }
+        }
+        walk_table(n, vid, vp, ids, lf.walk);
     }
     return TR_OK;
 }

@@ -277,6 +277,42 @@ __device__ __forceinline__ uint32_t scan_leaf_pairs(const SceneK &S, uint32_t st
     return UINT32_MAX;
 }
 
+// Leaf walk (TrPLeaf.walk, tr_leaf_walk): start at the leaf's largest tet,
+// step across the most violated face; a tet that accepts q with every
+// barycentric >= TR_WALK_TAU and carries the CERTIFIED bit is the lowest
+// index containing q (no lower-id tet of the leaf can accept it, and only
+// the leaf's tets can: q is strictly inside the exclusive box).  Anything
+// else -- an uncertified or marginal accept, a step out of the leaf, a
+// revisit -- ends in the id-order scan, so the result is always K:119's.
+// A regular cube: 1.67 record loads per sample instead of 3.33.
+__device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__restrict__ hdr,
+                                              uint32_t start, uint32_t count, const PQuery &q,
+                                              double l[4]) {
+    const uint32_t w4 = __ldg(&hdr->walk[4]);
+    if (w4 >> 31) {
+        uint32_t i = w4 & 7u, seen = 0;
+        for (uint32_t step = 0; step < count; ++step) {
+            seen |= 1u << i;
+            const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
+            if (bary_of(load_recm(S.tets, start + i), q, l)) {
+                if (((e >> 12) & 1u) && l[0] >= TR_WALK_TAU && l[1] >= TR_WALK_TAU &&
+                    l[2] >= TR_WALK_TAU && l[3] >= TR_WALK_TAU)
+                    return start + i;
+                break;
+            }
+            int f = 0;   // the most negative barycentric: q is beyond that face
+            double m = l[0];
+            if (l[1] < m) { m = l[1]; f = 1; }
+            if (l[2] < m) { m = l[2]; f = 2; }
+            if (l[3] < m) { f = 3; }
+            const uint32_t nb = (e >> (3 * f)) & 7u;
+            if (nb == i || ((seen >> nb) & 1u)) break;
+            i = nb;
+        }
+    }
+    return scan_leaf_first(S, start, count, q, l);
+}
+
 // Full-descent leaf scan: ids ascending; stop at the first id >= best.
 __device__ __forceinline__ void scan_leaf_ids(const SceneK &S, uint32_t start, uint32_t count,
                                               const PQuery &q, uint32_t &best, uint32_t &best_pos,
@@ -381,6 +417,7 @@ __device__ __forceinline__ bool locate_cells(const SceneK &S, const PQuery &q, d
 struct LeafHint {  // the ray's current leaf: exclusive box + record range, in registers
     float lo[3], hi[3];
     uint32_t start, count;
+    const TrPLeaf *hdr;   // the header (walk table)
     bool valid;
 };
 
@@ -391,6 +428,7 @@ __device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHin
     h.hi[0] = a.w; h.hi[1] = b.x; h.hi[2] = b.y;
     h.start = __float_as_uint(b.z);
     h.count = __float_as_uint(b.w);
+    h.hdr = S.pleaves + leaf;
     h.valid = true;
 }
 
@@ -415,6 +453,7 @@ __device__ __forceinline__ void load_leaf(const TrPLeaf *lf, LeafHint &h) {
     h.hi[1] = __int_as_float((int)w2); h.hi[2] = __int_as_float((int)(w2 >> 32));
     h.start = (uint32_t)w3;
     h.count = (uint32_t)((unsigned long long)w3 >> 32);
+    h.hdr = lf;
     h.valid = true;
 }
 
@@ -428,7 +467,7 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
     uint32_t pos;
     bool done = false;
     if (use_hint && hint.valid && strictly_in(q, hint.lo, hint.hi)) {
-        pos = scan_leaf_first(S, hint.start, hint.count, q, l);
+        pos = walk_leaf(S, hint.hdr, hint.start, hint.count, q, l);
         done = true;
     } else if (use_grid) {
         const int64_t gc = grid_cell(S, q);
@@ -443,7 +482,7 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
                 load_leaf(S.pgrid_leaf + gc, h);  // one load: the header is replicated per cell
             }
             if (strictly_in(q, h.lo, h.hi)) {
-                pos = scan_leaf_first(S, h.start, h.count, q, l);
+                pos = walk_leaf(S, h.hdr, h.start, h.count, q, l);
                 if (use_hint) hint = h;
                 done = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
@@ -1481,7 +1520,9 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
             load_leaf(S.pgrid_leaf + gc, hh);
             if (strictly_in(q, hh.lo, hh.hi)) {
                 pos = pair_scan ? scan_leaf_pairs(S, hh.start, hh.count, q, l)
-                                : scan_leaf_first(S, hh.start, hh.count, q, l);
+                      : (fr.flags & TR_FLAG_NO_WALK) ? scan_leaf_first(S, hh.start, hh.count, q, l)
+                                                     : walk_leaf(S, S.pgrid_leaf + gc, hh.start,
+                                                                 hh.count, q, l);
                 located = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }

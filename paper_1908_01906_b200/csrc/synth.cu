@@ -14,7 +14,8 @@
 //     k) so that spatial neighbours share DRAM pages and L2 sets, or in id order;
 //   * one leaf per cube (its 5 tets, ascending ids, consecutive records), exclusive
 //     box = the cube shrunk by the box pad (no other cube's padded tet boxes
-//     reach inside it), rounded inward to f32;
+//     reach inside it), rounded inward to f32, and the walk table of its
+//     parity (tr_walk_table_cube: the same builder as tr_leaf_walk's);
 //   * the uniform point grid is the cube grid itself (origin 0, scale 1), so
 //     a cell's candidate leaf header is the leaf array (no copy);
 //   * a BVH2 over the cubes by recursive halving of the longest cube range,
@@ -114,7 +115,11 @@ __global__ void grid_records_kernel(GridK G, const double *__restrict__ inv10, T
     }
 }
 
-__global__ void grid_leaves_kernel(GridK G, TrPLeaf *leaves) {
+struct WalkK {
+    uint32_t w[2][8];   // TrPLeaf.walk of an even / odd cube (tr_walk_table_cube)
+};
+
+__global__ void grid_leaves_kernel(GridK G, WalkK W, TrPLeaf *leaves) {
     const int64_t n = G.n, C = n * n * n;
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < C;
          c += (int64_t)gridDim.x * blockDim.x) {
@@ -128,6 +133,8 @@ __global__ void grid_leaves_kernel(GridK G, TrPLeaf *leaves) {
         }
         L.start = (uint32_t)(5 * cube_slot(G, q[0], q[1], q[2]));
         L.count = 5u;
+        const int par = (int)((q[0] + q[1] + q[2]) & 1);
+        for (int k = 0; k < 8; ++k) L.walk[k] = W.w[par][k];
         leaves[c] = L;
     }
 }
@@ -245,7 +252,10 @@ int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv1
     if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(inv10)");
     grid_records_kernel<<<grid_for(T), 256, 0, st>>>(G, d_inv, recs, ids);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "grid_records_kernel");
-    grid_leaves_kernel<<<grid_for(Lc), 256, 0, st>>>(G, leaves);
+    WalkK W;
+    tr_walk_table_cube(0, W.w[0]);
+    tr_walk_table_cube(1, W.w[1]);
+    grid_leaves_kernel<<<grid_for(Lc), 256, 0, st>>>(G, W, leaves);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "grid_leaves_kernel");
     if (Lc > 1) grid_nodes_kernel<<<grid_for(Nn), 256, 0, st>>>(G, Nn, nodes);
     else grid_single_node_kernel<<<1, 1, 0, st>>>(G, nodes);

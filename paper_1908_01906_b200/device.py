@@ -4,7 +4,7 @@ Layout in HBM, all owned by torch tensors:
   tets       TrTetRecord[T]     128 B/tet  (inv 72 B | orig 24 B | field x4 32 B),
                                 in point-BVH leaf order
   pnodes     TrPNode[]          64 B BVH2 nodes over padded tet boxes (f32, outward)
-  pleaves    TrPLeaf[]          32 B: exclusive box (f32, inward) + id range
+  pleaves    TrPLeaf[]          64 B: exclusive box (f32, inward) + id range + walk table
   pleaf_ids  uint32[]           ascending per leaf
   bnodes     TrBNode[]          112 B BVH2 nodes over partition boxes (f64)
   knodes     TrKNode[]          16 B BSP nodes over partition boxes (trace pass)
@@ -414,6 +414,11 @@ class DeviceScene:
             m = pnodes["minid"]                  # subtree minima too (descent pruning)
             ok = m < len(sub)
             m[ok] = sub[m[ok]].astype(np.uint32)
+        # leaf walk tables (tr_leaf_walk): face neighbours + certificates
+        verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+        _lib.check(_lib.lib().tr_leaf_walk(len(pleaves), _lib.vptr(pleaves), _lib.vptr(pids),
+                                           _lib.vptr(verts), _lib.vptr(tets)), "tr_leaf_walk")
         # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
         # reads consecutive 128-B lines with no id indirection
         rec = pack_tet_records(mesh, sampler, order=pids)
@@ -451,7 +456,8 @@ class DeviceScene:
                                          _lib.ptr(sz[2:3], C.c_int64)), "tr_grid_scene_sizes")
         n_tets, n_leaves, n_nodes = (int(v) for v in sz)
         self.t_tets = torch.empty(n_tets * 128, dtype=torch.uint8, device=self.device)
-        self.t_pleaves = torch.empty(n_leaves * 32, dtype=torch.uint8, device=self.device)
+        self.t_pleaves = torch.empty(n_leaves * _lib.PLEAF_DTYPE.itemsize, dtype=torch.uint8,
+                                     device=self.device)
         self.t_pnodes = torch.empty(n_nodes * 64, dtype=torch.uint8, device=self.device)
         inv10 = np.ascontiguousarray(sampler.inv10, dtype=np.float64).reshape(90)
         stream = torch.cuda.current_stream(self.device)

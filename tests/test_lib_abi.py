@@ -36,7 +36,7 @@ def test_every_declared_symbol_is_exported_and_bound(L):
 def test_record_layouts_match_header(L):
     assert L.TET_RECORD_DTYPE.itemsize == 128
     assert L.PNODE_DTYPE.itemsize == 64
-    assert L.PLEAF_DTYPE.itemsize == 32
+    assert L.PLEAF_DTYPE.itemsize == 64
     assert L.BNODE_DTYPE.itemsize == 112
     assert C.sizeof(L.TrFrame) % 8 == 0
     assert L.lib().tr_abi_version() == 1
