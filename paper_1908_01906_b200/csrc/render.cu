@@ -300,12 +300,12 @@ __device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__
                     return start + i;
                 break;
             }
-            int f = 0;   // the most negative barycentric: q is beyond that face
-            double m = l[0];
-            if (l[1] < m) { m = l[1]; f = 1; }
-            if (l[2] < m) { m = l[2]; f = 2; }
-            if (l[3] < m) { f = 3; }
-            const uint32_t nb = (e >> (3 * f)) & 7u;
+            int face = 0;   // the most negative barycentric: q is beyond that face
+            double lm = l[0];
+            if (l[1] < lm) { lm = l[1]; face = 1; }
+            if (l[2] < lm) { lm = l[2]; face = 2; }
+            if (l[3] < lm) { face = 3; }
+            const uint32_t nb = (e >> (3 * face)) & 7u;
             if (nb == i || ((seen >> nb) & 1u)) break;
             i = nb;
         }
@@ -1519,10 +1519,9 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
             LeafHint hh;
             load_leaf(S.pgrid_leaf + gc, hh);
             if (strictly_in(q, hh.lo, hh.hi)) {
-                pos = pair_scan ? scan_leaf_pairs(S, hh.start, hh.count, q, l)
-                      : (fr.flags & TR_FLAG_NO_WALK) ? scan_leaf_first(S, hh.start, hh.count, q, l)
-                                                     : walk_leaf(S, S.pgrid_leaf + gc, hh.start,
-                                                                 hh.count, q, l);
+                if (pair_scan) pos = scan_leaf_pairs(S, hh.start, hh.count, q, l);
+                else if (fr.flags & TR_FLAG_NO_WALK) pos = scan_leaf_first(S, hh.start, hh.count, q, l);
+                else pos = walk_leaf(S, S.pgrid_leaf + gc, hh.start, hh.count, q, l);
                 located = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
@@ -1829,6 +1828,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __shared__ long long s_out[NG], s_samples[NG];
     __shared__ uint32_t s_rr[NG], s_taken[NG], s_ctot[NG], s_cbefore[NG];
     __shared__ int32_t s_icur[NG], s_niv[NG], s_pix[NG], s_piy[NG];
+    __shared__ double s_ra[NG];                         // the cursor interval's record
+    __shared__ int32_t s_rpid[NG];                      // (rec[s_icur]: entry, partition,
+    __shared__ uint32_t s_rcum[NG];                     //  running sample count)
     __shared__ uint32_t s_cfull[BRICK ? NG : 1], s_tbegin[BRICK ? NG : 1];   // brick runs
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1898,6 +1900,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                             L.t_min = iv.tail[rr];
                             L.last = n_iv > 0 ? load_rec(rec + (n_iv - 1)).pid : -1;
                             L.visited = 0; L.started = 0; L.n = 0; L.k = 0;
+                        } else {
+                            const IvRec r0 = load_rec(rec + s_icur[g]);
+                            s_ra[g] = r0.a; s_rpid[g] = r0.pid; s_rcum[g] = r0.cum;
                         }
                     }
                     active = true;
@@ -1919,6 +1924,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         double a = 0.0;
         int32_t pid = -1, i_mine = 0;
         uint32_t c0_mine = 0;
+        IvRec r_mine = {0.0, 0, 0u};
         int64_t k = 0, remaining = 0;
         if (active && !idle) {
             if (!inline_mode) {
@@ -1929,8 +1935,10 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     const IvRec *rec = iv.rec + (int64_t)s_rr[g] * IV_CAP;
                     int32_t i = s_icur[g];
                     uint32_t c0 = s_cbefore[g];
-                    IvRec r = load_rec(rec + i);
+                    IvRec r;   // the cursor's record from shared memory, later ones from L2
+                    r.a = s_ra[g]; r.pid = s_rpid[g]; r.cum = s_rcum[g];
                     while (r.cum <= s) { c0 = r.cum; ++i; r = load_rec(rec + i); }
+                    r_mine = r;
                     a = r.a;
                     pid = r.pid;
                     // mode 0: one interval, or (bricks) its cuts, all from the entry
@@ -1991,6 +1999,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         const int src = gbase + ((taken_r > 0) ? taken_r - 1 : 0);
         const int32_t i_last = __shfl_sync(FULL, i_mine, src);
         const uint32_t c0_last = __shfl_sync(FULL, c0_mine, src);
+        const double ra_last = __shfl_sync(FULL, r_mine.a, src);
+        const int32_t rpid_last = __shfl_sync(FULL, r_mine.pid, src);
+        const uint32_t rcum_last = __shfl_sync(FULL, r_mine.cum, src);
         bool done = false, flush = false, suspend = false;
         int32_t flush_n = 0;
         uint32_t taken_now = 0;
@@ -2049,6 +2060,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 s_taken[g] = taken_now;
                 s_icur[g] = i_last;
                 s_cbefore[g] = c0_last;
+                s_ra[g] = ra_last; s_rpid[g] = rpid_last; s_rcum[g] = rcum_last;
             }
             if (done) {
                 int32_t visited = 0;
