@@ -78,6 +78,16 @@ typedef struct TrPLeaf {
 /* The walk's certification margin on the barycentrics (tr_leaf_walk). */
 #define TR_WALK_TAU 1e-6
 
+/* Walk-start predictor of a leaf (48 B): approximate barycentrics l1..l3 of
+ * the leaf's first tet, l_r ~ row[r][0]*(x - ex_lo[0]) + row[r][1]*(y - ex_lo[1])
+ * + row[r][2]*(z - ex_lo[2]) + row[r][3], in f32.  The march evaluates them
+ * (no record load) and starts the walk at the first tet's neighbour across
+ * the face it predicts the point is beyond; a wrong guess only costs a walk
+ * step -- acceptance is always the exact test + certificate. */
+typedef struct TrLeafPred {
+    float row[3][4];
+} TrLeafPred;
+
 /* Partition BVH2 node: f64 child boxes (exact unions of partition boxes,
  * so node pruning is conservative for the exact f64 slab test).
  * child >= 0: node; child < 0: partition ~child; INT32_MIN: none. */
@@ -139,7 +149,12 @@ int tr_pbvh_copy(const TrHostBuf *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *
  * those margins to cover the device's rounding get no certificates).  Leaves
  * of more than 8 tets get no table. */
 int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *rec_ids,
-                 const double *vertices, const int64_t *tets);
+                 const double *vertices, const int64_t *tets, TrLeafPred *pred);
+/* pred (n_leaves, may be NULL): the walk-start predictor of each leaf,
+ * relative to its ex_lo (set the exclusive boxes first). */
+/* The two predictors of tr_grid_scene_build's cubes (even, odd parity), for
+ * TrDeviceScene.pred_class (interior cubes; boundary cubes differ by the pad). */
+int tr_grid_walk_pred(double pad, TrLeafPred *pred2);
 /* Uniform-grid leaf index: cell (x,y,z) -> leaf whose exclusive box covers
  * most of it (-1: none).  cell = floor((p - org) * scale), row-major x,y,z. */
 int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
@@ -265,6 +280,13 @@ typedef struct TrDeviceScene {
     int32_t cdim[3];
     int32_t cells_first;   /* 1: skip the exclusive-leaf grid (it rarely proves a point) */
     double corg[3], cscale[3];
+    /* walk-start predictors: per grid cell (a copy of its leaf's, like
+     * pgrid_leaf), or -- pgrid_pred NULL, pred_classes 2 -- one per cube
+     * parity (tr_grid_scene_build's scenes); neither: no prediction */
+    const TrLeafPred *pgrid_pred;
+    int32_t pred_classes;
+    int32_t pad2;
+    TrLeafPred pred_class[2];
 } TrDeviceScene;
 
 /* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
@@ -320,6 +342,7 @@ typedef struct TrFrame {
 #define TR_FLAG_NO_CAND 0x800000 /* modes 1/2: intervals by the per-ray BSP walk, not the candidate raster (testing) */
 #define TR_FLAG_FORCE_CAND 0x1000000 /* the candidate raster also above 1M pixels (default there: the BSP walk) */
 #define TR_FLAG_NO_WALK 0x2000000 /* exclusive leaves scanned in id order, not walked (testing) */
+#define TR_FLAG_NO_PRED 0x4000000 /* leaf walks start at the first tet, no predictor (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */

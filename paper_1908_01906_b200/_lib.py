@@ -41,6 +41,8 @@ class TrDeviceScene(C.Structure):
         ("cell_off", C.c_void_p), ("cell_recs", C.c_void_p), ("tbox", C.c_void_p),
         ("cdim", C.c_int32 * 3), ("cells_first", C.c_int32),
         ("corg", C.c_double * 3), ("cscale", C.c_double * 3),
+        ("pgrid_pred", C.c_void_p), ("pred_classes", C.c_int32), ("pad2", C.c_int32),
+        ("pred_class", C.c_float * 24),
     ]
 
 
@@ -116,7 +118,9 @@ _SIGNATURES = [
     ("tr_pbvh_build", C.c_int, [C.c_int64, c_f64p, c_f64p, C.c_int32, C.POINTER(C.c_void_p)]),
     ("tr_pbvh_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_pbvh_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
-    ("tr_leaf_walk", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_leaf_walk", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p]),
+    ("tr_grid_walk_pred", C.c_int, [C.c_double, C.c_void_p]),
     ("tr_pbvh_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p]),
     ("tr_pbvh_coverage", C.c_double, [C.c_void_p]),
     ("tr_cells_build", C.c_int, [C.c_void_p, c_f64p, c_f64p, C.c_int32, C.c_int32,

@@ -15,7 +15,7 @@ int tr_fail(int code, const char *msg) {
 
 extern "C" const char *tr_last_error(void) { return g_last_error.c_str(); }
 
-extern "C" int tr_abi_version(void) { return 1; }
+extern "C" int tr_abi_version(void) { return 2; }   // 2: 64-B TrPLeaf (walk table), TrLeafPred
 
 extern "C" int tr_struct_sizes(int64_t *out, int32_t n) {
     if (!out || n < 0) return tr_fail(TR_EINVAL, "tr_struct_sizes: invalid arguments");

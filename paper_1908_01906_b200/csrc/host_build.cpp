@@ -1184,8 +1184,9 @@ bool separated(const TetL &J, const TetL &K) {
 // The table of one leaf: n <= 8 tets, vertex ids vid[i][4], positions vp[i][4],
 // tet ids ids[i] (ascending or not).
 void walk_table(int n, const int64_t (*vid)[4], const double *const (*vp)[4], const int64_t *ids,
-                uint32_t walk[8]) {
+                uint32_t walk[8], const float *ex_lo = nullptr, TrLeafPred *pred = nullptr) {
     for (int k = 0; k < 8; ++k) walk[k] = 0;
+    if (pred) std::memset(pred, 0, sizeof(TrLeafPred));
     if (n < 1 || n > 8) return;
     TetL geo[8];
     long double vmax = 0.0L, imax = 0.0L, vol_best = -1.0L;
@@ -1234,11 +1235,22 @@ void walk_table(int n, const int64_t (*vid)[4], const double *const (*vp)[4], co
         walk[i >> 1] |= e << (16 * (i & 1));
     }
     walk[4] = (uint32_t)first | (1u << 31);
+    if (pred && ex_lo) {   // l_r(p) = inv_r . (p - v0) = inv_r . (p - lo) + inv_r . (lo - v0)
+        const TetL &F = geo[first];
+        for (int r = 0; r < 3; ++r) {
+            long double d = 0.0L;
+            for (int c = 0; c < 3; ++c) {
+                pred->row[r][c] = (float)F.inv[r][c];
+                d += F.inv[r][c] * ((long double)ex_lo[c] - F.v[0][c]);
+            }
+            pred->row[r][3] = (float)d;
+        }
+    }
 }
 
 }  // namespace
 
-void tr_walk_table_cube(int parity, uint32_t walk[8]) {
+static void walk_table_cube(int parity, uint32_t walk[8], const float *ex_lo, TrLeafPred *pred) {
     // mesh.py:151-163: corner c = 4x + 2y + z; odd cubes mirror x (c ^ 4)
     static const int P[5][4] = {{0, 4, 2, 1}, {6, 2, 4, 7}, {5, 1, 7, 4}, {3, 7, 1, 2}, {4, 2, 1, 7}};
     double pos[8][3];
@@ -1255,11 +1267,22 @@ void tr_walk_table_cube(int parity, uint32_t walk[8]) {
             vp[k][q] = pos[c];
         }
     }
-    walk_table(5, vid, vp, ids, walk);
+    walk_table(5, vid, vp, ids, walk, ex_lo, pred);
+}
+
+void tr_walk_table_cube(int parity, uint32_t walk[8]) { walk_table_cube(parity, walk, nullptr, nullptr); }
+
+int tr_grid_walk_pred(double pad, TrLeafPred *pred2) {
+    if (!pred2 || !(pad >= 0.0)) return tr_fail(TR_EINVAL, "tr_grid_walk_pred: invalid arguments");
+    const float lo[3] = {(float)pad, (float)pad, (float)pad};   // an interior cube at the origin
+    uint32_t w[8];
+    walk_table_cube(0, w, lo, pred2);
+    walk_table_cube(1, w, lo, pred2 + 1);
+    return TR_OK;
 }
 
 extern "C" int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *rec_ids,
-                            const double *vertices, const int64_t *tets) {
+                            const double *vertices, const int64_t *tets, TrLeafPred *pred) {
     if (n_leaves < 0 || (n_leaves > 0 && (!leaves || !vertices || !tets)))
         return tr_fail(TR_EINVAL, "tr_leaf_walk: invalid arguments");
 #pragma omp parallel for schedule(dynamic, 4096)
@@ -1268,7 +1291,11 @@ extern "C" int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *r
         const int n = (int)std::min<uint32_t>(lf.count, 9);
         int64_t vid[8][4], ids[8];
         const double *vp[8][4];
-        if (n > 8) { for (int k = 0; k < 8; ++k) lf.walk[k] = 0; continue; }
+        if (n > 8) {
+            for (int k = 0; k < 8; ++k) lf.walk[k] = 0;
+            if (pred) std::memset(pred + L, 0, sizeof(TrLeafPred));
+            continue;
+        }
         for (int i = 0; i < n; ++i) {
             const int64_t t = rec_ids ? (int64_t)rec_ids[lf.start + i] : (int64_t)lf.start + i;
             ids[i] = t;
@@ -1277,7 +1304,7 @@ extern "C" int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *r
                 vp[i][q] = vertices + 3 * vid[i][q];
             }
         }
-        walk_table(n, vid, vp, ids, lf.walk);
+        walk_table(n, vid, vp, ids, lf.walk, lf.ex_lo, pred ? pred + L : nullptr);
     }
     return TR_OK;
 }

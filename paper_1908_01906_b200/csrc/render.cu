@@ -169,6 +169,10 @@ __device__ __forceinline__ double4 ldg256(const void *p) {
     return v;
 }
 
+#ifndef TR_PREFETCH_FIELD
+#define TR_PREFETCH_FIELD 0   // A/B knob: L1 prefetch of the walked tet's field values
+#endif
+
 // The 96 B of a record the barycentric test reads (inverse + origin).
 struct RecM {
     double2 a0, a1, a2, a3, a4, a5;
@@ -251,6 +255,9 @@ struct SceneK {  // kernel copy of TrDeviceScene
     int32_t cdim[3];
     int32_t cells_first;
     double corg[3], cscale[3];
+    const float4 *__restrict__ pgrid_pred;  // per cell: 3 float4 rows (TrLeafPred), or NULL
+    int32_t pred_classes;                   // 2: pred_class[cube parity] (grid scenes)
+    float pred_class[2][12];
 };
 
 // Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
@@ -285,12 +292,42 @@ __device__ __forceinline__ uint32_t scan_leaf_pairs(const SceneK &S, uint32_t st
 // else -- an uncertified or marginal accept, a step out of the leaf, a
 // revisit -- ends in the id-order scan, so the result is always K:119's.
 // A regular cube: 1.67 record loads per sample instead of 3.33.
+//
+// pred (TrLeafPred rows, or NULL): approximate f32 barycentrics of the first
+// tet relative to the exclusive box's corner `lo`; when they put q beyond a
+// face the walk starts at the neighbour across it instead -- one record load
+// for almost every sample (a wrong guess costs a step, never the result).
 __device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__restrict__ hdr,
                                               uint32_t start, uint32_t count, const PQuery &q,
-                                              double l[4]) {
+                                              double l[4], bool use_pred = false,
+                                              float4 r1 = float4(), float4 r2 = float4(),
+                                              float4 r3 = float4(), const float *lo = nullptr) {
     const uint32_t w4 = __ldg(&hdr->walk[4]);
     if (w4 >> 31) {
         uint32_t i = w4 & 7u, seen = 0;
+        if (use_pred) {
+            const float x = (float)(q.x - (double)lo[0]), y = (float)(q.y - (double)lo[1]);
+            const float z = (float)(q.z - (double)lo[2]);
+            const float p1 = r1.x * x + r1.y * y + r1.z * z + r1.w;
+            const float p2 = r2.x * x + r2.y * y + r2.z * z + r2.w;
+            const float p3 = r3.x * x + r3.y * y + r3.z * z + r3.w;
+            const float p0 = 1.0f - p1 - p2 - p3;
+            int face = 0;
+            float pm = p0;
+            if (p1 < pm) { pm = p1; face = 1; }
+            if (p2 < pm) { pm = p2; face = 2; }
+            if (p3 < pm) { pm = p3; face = 3; }
+            if (pm < -1e-4f) {
+                const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
+                const uint32_t nb = (e >> (3 * face)) & 7u;
+                if (nb < count) i = nb;
+            }
+        }
+#if TR_PREFETCH_FIELD
+        // the predicted tet's field chunk (K:149-151) into L1 with its barycentric
+        // data, so the interpolation after an accept does not wait on L2
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char *>(S.tets + start + i) + 96));
+#endif
         for (uint32_t step = 0; step < count; ++step) {
             seen |= 1u << i;
             const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
@@ -434,13 +471,15 @@ __device__ __forceinline__ void load_hint(const SceneK &S, int32_t leaf, LeafHin
 
 // Grid cell of q (-1: outside the grid).  The cell's candidate leaf is only a
 // hint: the caller accepts it after proving q strictly inside its exclusive box.
-__device__ __forceinline__ int64_t grid_cell(const SceneK &S, const PQuery &q) {
+__device__ __forceinline__ int64_t grid_cell(const SceneK &S, const PQuery &q,
+                                             int *parity = nullptr) {
     const double fx = (q.x - S.gorg[0]) * S.gscale[0];
     const double fy = (q.y - S.gorg[1]) * S.gscale[1];
     const double fz = (q.z - S.gorg[2]) * S.gscale[2];
     if (!(fx >= 0.0 && fy >= 0.0 && fz >= 0.0)) return -1;
     const int64_t cx = (int64_t)fx, cy = (int64_t)fy, cz = (int64_t)fz;
     if (cx >= S.gdim[0] || cy >= S.gdim[1] || cz >= S.gdim[2]) return -1;
+    if (parity) *parity = (int)((cx + cy + cz) & 1);
     return (cx * S.gdim[1] + cy) * S.gdim[2] + cz;
 }
 
@@ -1514,14 +1553,30 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
     uint32_t pos = UINT32_MAX;
     bool located = false;
     if (use_grid && !(use_cells && S.cells_first)) {
-        const int64_t gc = grid_cell(S, q);
+        int par = 0;
+        const int64_t gc = grid_cell(S, q, &par);
         if (gc >= 0) {
             LeafHint hh;
             load_leaf(S.pgrid_leaf + gc, hh);
+            float4 pr0 = float4(), pr1 = float4(), pr2 = float4();  // walk-start predictor
+            bool use_pred = false;
+            if (S.pgrid_pred) {
+                const float4 *src = S.pgrid_pred + 3 * gc;
+                pr0 = __ldg(src); pr1 = __ldg(src + 1); pr2 = __ldg(src + 2);
+                use_pred = true;
+            } else if (S.pred_classes == 2) {
+                const float *c = par ? S.pred_class[1] : S.pred_class[0];
+                pr0 = make_float4(c[0], c[1], c[2], c[3]);
+                pr1 = make_float4(c[4], c[5], c[6], c[7]);
+                pr2 = make_float4(c[8], c[9], c[10], c[11]);
+                use_pred = true;
+            }
+            if (fr.flags & TR_FLAG_NO_PRED) use_pred = false;
             if (strictly_in(q, hh.lo, hh.hi)) {
                 if (pair_scan) pos = scan_leaf_pairs(S, hh.start, hh.count, q, l);
                 else if (fr.flags & TR_FLAG_NO_WALK) pos = scan_leaf_first(S, hh.start, hh.count, q, l);
-                else pos = walk_leaf(S, S.pgrid_leaf + gc, hh.start, hh.count, q, l);
+                else pos = walk_leaf(S, S.pgrid_leaf + gc, hh.start, hh.count, q, l, use_pred, pr0,
+                                     pr1, pr2, hh.lo);
                 located = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
@@ -2190,6 +2245,10 @@ SceneK make_scene(const TrDeviceScene *s) {
     for (int a = 0; a < 3; ++a) { S.cdim[a] = s->cdim[a]; S.corg[a] = s->corg[a]; S.cscale[a] = s->cscale[a]; }
     S.cells_first = s->cells_first;
     if (!s->cell_recs || !s->tbox) S.cell_off = nullptr;
+    S.pgrid_pred = reinterpret_cast<const float4 *>(s->pgrid_pred);
+    S.pred_classes = s->pred_classes;
+    for (int c = 0; c < 2; ++c)
+        for (int k = 0; k < 12; ++k) S.pred_class[c][k] = (&s->pred_class[c].row[0][0])[k];
     return S;
 }
 

@@ -361,6 +361,7 @@ class DeviceScene:
         self.resident_bytes = sum(t.numel() for t in (self.t_tets, self.t_pnodes, self.t_pleaves,
                                                       self.t_pids, self.t_bnodes, self.t_plo,
                                                       self.t_phi, self.t_grid, self.t_grid_leaf,
+                                                      self.t_grid_pred,
                                                       self.t_knodes, self.t_kpids)
                                   if t is not None)
         ptr = lambda t: 0 if t is None else t.data_ptr()
@@ -378,6 +379,11 @@ class DeviceScene:
             gorg=(C.c_double * 3)(*grid.org), gscale=(C.c_double * 3)(*grid.scale),
             knodes=self.t_knodes.data_ptr(), kleaf_pids=self.t_kpids.data_ptr(),
             n_knodes=self.n_knodes, kroot=(C.c_double * 6)(*kroot))
+        if self.t_grid_pred is not None:
+            self.desc.pgrid_pred = self.t_grid_pred.data_ptr()
+        elif getattr(self, "grid_pred_class", None) is not None:
+            self.desc.pred_classes = 2
+            self.desc.pred_class = (C.c_float * 24)(*self.grid_pred_class)
         if self.cells is not None:
             cl = self.cells
             self.desc.cell_off = self.t_coff.data_ptr()
@@ -417,8 +423,10 @@ class DeviceScene:
         # leaf walk tables (tr_leaf_walk): face neighbours + certificates
         verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
         tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+        pred = np.zeros((len(pleaves), 12), np.float32)   # TrLeafPred per leaf
         _lib.check(_lib.lib().tr_leaf_walk(len(pleaves), _lib.vptr(pleaves), _lib.vptr(pids),
-                                           _lib.vptr(verts), _lib.vptr(tets)), "tr_leaf_walk")
+                                           _lib.vptr(verts), _lib.vptr(tets), _lib.vptr(pred)),
+                   "tr_leaf_walk")
         # records in LEAF order (record k = tet pleaf_ids[k]): a leaf scan
         # reads consecutive 128-B lines with no id indirection
         rec = pack_tet_records(mesh, sampler, order=pids)
@@ -435,6 +443,9 @@ class DeviceScene:
         has = grid.cells >= 0
         cell_leaf[has] = pleaves[grid.cells[has]]
         self.t_grid_leaf = _upload(cell_leaf, device)
+        cell_pred = np.zeros((len(grid.cells), 12), np.float32)
+        cell_pred[has] = pred[grid.cells[has]]
+        self.t_grid_pred = _upload(cell_pred, device)
         self.grid = grid
         self.cells = lists
         if lists is not None:
@@ -473,6 +484,10 @@ class DeviceScene:
         torch.cuda.synchronize(self.device)
         self.t_grid = None
         self.t_grid_leaf = None
+        self.t_grid_pred = None
+        self.grid_pred_class = np.zeros(24, np.float32)   # TrLeafPred of an even / odd cube
+        _lib.check(L.tr_grid_walk_pred(float(sampler.pad), _lib.vptr(self.grid_pred_class)),
+                   "tr_grid_walk_pred")
         self.cells = None
         self.pnodes_host = self.pleaves_host = None
         self.grid = PointGrid(np.full(3, n, np.int32), np.zeros(3), np.ones(3), None)

@@ -42,11 +42,31 @@ def scan(inv, orig, ids, p):
     return -1
 
 
-def walk(inv, orig, ids, w, p):
+def predict(w, pred, lo, p):
+    """render.cu walk_leaf's start: the first tet, or its neighbour across the
+    face the f32 predictor puts p beyond."""
+    i = int(w[4]) & 7
+    if pred is None:
+        return i
+    x = (p - lo.astype(np.float64)).astype(np.float32)
+    r = np.asarray(pred, np.float32).reshape(3, 4)
+    l123 = r[:, :3] @ x + r[:, 3]
+    l = np.concatenate([[np.float32(1.0) - l123.sum()], l123])
+    f = int(np.argmin(l))
+    if l[f] < -1e-4:
+        nb = (entry(w, i) >> (3 * f)) & 7
+        if nb < 8:
+            i = nb
+    return i
+
+
+def walk(inv, orig, ids, w, p, pred=None, lo=None):
     """render.cu walk_leaf."""
     n = len(ids)
     if int(w[4]) >> 31:
-        i, seen = int(w[4]) & 7, 0
+        i, seen = predict(w, pred, lo, p), 0
+        if i >= n:
+            i = int(w[4]) & 7
         for _ in range(n):
             seen |= 1 << i
             e = entry(w, i)
@@ -63,20 +83,24 @@ def walk(inv, orig, ids, w, p):
     return scan(inv, orig, ids, p), False
 
 
-def leaf_tables(B, verts, tets, leaf_sets):
-    """tr_leaf_walk over leaves given as lists of tet ids (ascending)."""
+def leaf_tables(B, verts, tets, leaf_sets, with_pred=False):
+    """tr_leaf_walk over leaves given as lists of tet ids (ascending); the
+    exclusive-box corner ex_lo is set to the leaf's vertex minimum."""
     from paper_1908_01906_b200 import _lib
     recs = np.concatenate([np.asarray(s, np.uint32) for s in leaf_sets])
     leaves = np.zeros(len(leaf_sets), dtype=_lib.PLEAF_DTYPE)
     off = 0
     for i, s in enumerate(leaf_sets):
         leaves[i]["start"], leaves[i]["count"] = off, len(s)
+        leaves[i]["ex_lo"] = verts[tets[s]].reshape(-1, 3).min(axis=0)
         off += len(s)
     verts = np.ascontiguousarray(verts, np.float64)
     tets = np.ascontiguousarray(tets, np.int64)
+    pred = np.zeros((len(leaves), 12), np.float32)
     _lib.check(_lib.lib().tr_leaf_walk(len(leaves), _lib.vptr(leaves), _lib.vptr(recs),
-                                       _lib.vptr(verts), _lib.vptr(tets)), "tr_leaf_walk")
-    return leaves, recs
+                                       _lib.vptr(verts), _lib.vptr(tets), _lib.vptr(pred)),
+               "tr_leaf_walk")
+    return (leaves, recs, pred) if with_pred else (leaves, recs)
 
 
 def inverses(verts, tets):
@@ -100,14 +124,23 @@ def test_generator_cubes_walk_from_the_central_tet(B):
             assert sum(((entry(w, i) >> (3 * f)) & 7) != i for f in range(4)) == 1
     # the device build of the generator's grid uses the same tables
     from paper_1908_01906_b200 import _lib
-    assert _lib.lib().tr_leaf_walk(0, None, None, None, None) == 0
+    assert _lib.lib().tr_leaf_walk(0, None, None, None, None, None) == 0
+    two = np.zeros(24, np.float32)
+    assert _lib.lib().tr_grid_walk_pred(1e-7, _lib.vptr(two)) == 0
+    _, _, preds = leaf_tables(B, m.vertices, m.tets, cubes, with_pred=True)
+    # an interior-cube class predictor = the per-leaf one up to the pad shift
+    assert np.allclose(two[:12], preds[0], atol=1e-5)
 
 
-def _check_points(inv, orig, ids, w, pts):
+def _check_points(inv, orig, ids, w, pts, pred=None, lo=None):
     certified = 0
     for p in pts:
+        want = scan(inv, orig, ids, p)
         got, cert = walk(inv, orig, ids, w, p)
-        assert got == scan(inv, orig, ids, p)
+        assert got == want
+        if pred is not None:
+            got_p, _ = walk(inv, orig, ids, w, p, pred, lo)
+            assert got_p == want
         certified += cert
     return certified
 
@@ -117,18 +150,21 @@ def test_walk_equals_lowest_index_scan_on_cubes(B):
     inv_all, orig_all = inverses(m.vertices, m.tets)
     rng = np.random.default_rng(3)
     cubes = [list(range(5 * c, 5 * c + 5)) for c in range(27)]
-    leaves, _ = leaf_tables(B, m.vertices, m.tets, cubes)
-    total = cert = 0
-    for c, lf in zip(cubes, leaves):
+    leaves, _, preds = leaf_tables(B, m.vertices, m.tets, cubes, with_pred=True)
+    total = cert = hit = 0
+    for c, lf, pr in zip(cubes, leaves, preds):
         lo = m.vertices[m.tets[c]].reshape(-1, 3).min(axis=0)
         pts = lo + rng.uniform(0, 1, (150, 3))
         # points on the cube's face diagonals and inner faces (ties)
         pts[:30, 1] = lo[1] + (pts[:30, 0] - lo[0])
         pts[30:50, 0] = lo[0] + np.round(pts[30:50, 0] - lo[0])
         ids = np.array(c)
-        cert += _check_points(inv_all[c], orig_all[c], ids, lf["walk"], pts)
+        cert += _check_points(inv_all[c], orig_all[c], ids, lf["walk"], pts, pr, lf["ex_lo"])
+        for p in pts[50:]:   # off the ties: the predicted start is the containing tet
+            hit += predict(lf["walk"], pr, lf["ex_lo"], p) == scan(inv_all[c], orig_all[c], ids, p)
         total += len(pts)
     assert cert > 0.5 * total   # most points end on a certified tet
+    assert hit > 0.98 * (total - 50 * len(cubes))
 
 
 def test_walk_equals_scan_on_unstructured_leaves(B):
@@ -142,19 +178,21 @@ def test_walk_equals_scan_on_unstructured_leaves(B):
     from paper_1908_01906_b200 import _lib
     verts = np.ascontiguousarray(sc.mesh.vertices)
     tets = np.ascontiguousarray(sc.mesh.tets)
+    pred = np.zeros((len(leaves), 12), np.float32)
     _lib.check(_lib.lib().tr_leaf_walk(len(leaves), _lib.vptr(leaves), _lib.vptr(pids),
-                                       _lib.vptr(verts), _lib.vptr(tets)), "tr_leaf_walk")
+                                       _lib.vptr(verts), _lib.vptr(tets), _lib.vptr(pred)),
+               "tr_leaf_walk")
     inv_all, orig_all = inverses(verts, tets)
     rng = np.random.default_rng(11)
     n_valid = 0
-    for lf in leaves[::3]:
+    for lf, pr in zip(leaves[::3], pred[::3]):
         s, n = int(lf["start"]), int(lf["count"])
         ids = pids[s:s + n].astype(np.int64)
         n_valid += int(lf["walk"][4]) >> 31
         pv = verts[tets[ids]]                       # (n, 4, 3)
         lam = rng.dirichlet(np.ones(4), size=(n, 12))
         pts = np.einsum("nkv,nva->nka", lam, pv).reshape(-1, 3)
-        _check_points(inv_all[ids], orig_all[ids], ids, lf["walk"], pts)
+        _check_points(inv_all[ids], orig_all[ids], ids, lf["walk"], pts, pr, lf["ex_lo"])
     assert n_valid > 0
 
 

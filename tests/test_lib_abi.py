@@ -39,7 +39,7 @@ def test_record_layouts_match_header(L):
     assert L.PLEAF_DTYPE.itemsize == 64
     assert L.BNODE_DTYPE.itemsize == 112
     assert C.sizeof(L.TrFrame) % 8 == 0
-    assert L.lib().tr_abi_version() == 1
+    assert L.lib().tr_abi_version() == 2
 
 
 def test_ctypes_structs_match_the_c_layouts(L):
