@@ -169,10 +169,6 @@ __device__ __forceinline__ double4 ldg256(const void *p) {
     return v;
 }
 
-#ifndef TR_PREFETCH_FIELD
-#define TR_PREFETCH_FIELD 0   // A/B knob: L1 prefetch of the walked tet's field values
-#endif
-
 // The 96 B of a record the barycentric test reads (inverse + origin).
 struct RecM {
     double2 a0, a1, a2, a3, a4, a5;
@@ -323,11 +319,6 @@ __device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__
                 if (nb < count) i = nb;
             }
         }
-#if TR_PREFETCH_FIELD
-        // the predicted tet's field chunk (K:149-151) into L1 with its barycentric
-        // data, so the interpolation after an accept does not wait on L2
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char *>(S.tets + start + i) + 96));
-#endif
         for (uint32_t step = 0; step < count; ++step) {
             seen |= 1u << i;
             const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
@@ -1451,12 +1442,20 @@ __global__ void __launch_bounds__(TRACE_BLOCK)
 order_rays_kernel(FrameK F, IvBuf iv) {
     __shared__ uint32_t start[N_BUCKETS];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        // lanes per ray: 4, unless the longest ray's rounds at 4 lanes
-        // (max / 4) exceed the average lane's share of the work (sum /
-        // resident lanes) -- then 16, so long rays stop setting the frame
-        // time (1e9-tet scenes: up to 3,600 samples on one ray)
+        // lanes per ray: 16 if the longest ray's rounds at 4 lanes (max / 4)
+        // exceed the average lane's share of the work (sum / resident lanes),
+        // so long rays stop setting the frame time (1e9-tet scenes: up to
+        // 3,600 samples on one ray); else 8 when the marching rays average
+        // >= 320 samples (fewer rounds per ray: radial272, ~390 samples per
+        // ray, -4%), else 4 (radial59 ~135 and radial128 ~270 samples per
+        // ray: 8 lanes +8%; measured, profiles/r02)
         const unsigned long long sum = iv.ray_stats[0], mx = iv.ray_stats[1];
-        *iv.gsel = (mx * (unsigned long long)F.march_lanes <= 4ull * sum) ? 4u : 16u;
+        unsigned long long n_march = 0;
+        for (int b = 1; b < N_BUCKETS; ++b) n_march += iv.hist[b];
+        uint32_t g = 4u;
+        if (mx * (unsigned long long)F.march_lanes > 4ull * sum) g = 16u;
+        else if (sum >= 320ull * n_march) g = 8u;
+        *iv.gsel = g;
     }
     if (threadIdx.x < N_BUCKETS) {
         uint32_t s = 0;
@@ -2588,15 +2587,17 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             e = cudaEventRecord((cudaEvent_t)out->ev_march_begin, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(begin)");
         }
-        // auto width: the G = 4 and 16 kernels are both launched and the one
-        // order_rays_kernel did not choose returns at once
-        void (*fns[2])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_fn, nullptr};
-        int gs[2] = {gsize, 0};
+        // auto width: the G = 4, 8 and 16 kernels are all launched and the
+        // ones order_rays_kernel did not choose return at once
+        void (*fns[3])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_fn, nullptr, nullptr};
+        int gs[3] = {gsize, 0, 0};
         int nf = 1;
         if (F.auto_g) {
-            fns[1] = march_sm_kernel<16, 3>;
-            gs[1] = 16;
-            nf = 2;
+            fns[1] = march_sm_kernel<8, 3>;
+            gs[1] = 8;
+            fns[2] = march_sm_kernel<16, 3>;
+            gs[2] = 16;
+            nf = 3;
         }
         for (int q = 0; q < nf; ++q) {
             int64_t grid = (int64_t)sm_count() * per_sm;
