@@ -347,7 +347,7 @@ typedef struct TrFrame {
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */
 /* flags bits 8-11: log2 of the lanes that march one ray together (0 = chosen
- * per ray chunk on the device, 4, 8 or 16, from the rays' sample counts);
+ * per ray chunk on the device, 4 or 16, from the rays' sample counts);
  * bits 12-13: register budget of the G = 4 kernel as minimum resident CTAs
  * per SM (0: 3, 1: 4, 2: 2, 3: 3); bits 14-15: CTAs per SM actually
  * launched (0: as many as fit).  Tuning knobs only:

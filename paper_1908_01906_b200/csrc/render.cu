@@ -1442,20 +1442,14 @@ __global__ void __launch_bounds__(TRACE_BLOCK)
 order_rays_kernel(FrameK F, IvBuf iv) {
     __shared__ uint32_t start[N_BUCKETS];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        // lanes per ray: 16 if the longest ray's rounds at 4 lanes (max / 4)
-        // exceed the average lane's share of the work (sum / resident lanes),
-        // so long rays stop setting the frame time (1e9-tet scenes: up to
-        // 3,600 samples on one ray); else 8 when the marching rays average
-        // >= 320 samples (fewer rounds per ray: radial272, ~390 samples per
-        // ray, -4%), else 4 (radial59 ~135 and radial128 ~270 samples per
-        // ray: 8 lanes +8%; measured, profiles/r02)
+        // lanes per ray: 4, unless the longest ray's rounds at 4 lanes
+        // (max / 4) exceed the average lane's share of the work (sum /
+        // resident lanes) -- then 16, so long rays stop setting the frame
+        // time (1e9-tet scenes: up to 3,600 samples on one ray).  8 lanes
+        // measured slower than 4 on radial59/128/272 in every mode except
+        // radial272 skip-adaptive (-2%; scripts/lane_sweep.py, profiles/r02)
         const unsigned long long sum = iv.ray_stats[0], mx = iv.ray_stats[1];
-        unsigned long long n_march = 0;
-        for (int b = 1; b < N_BUCKETS; ++b) n_march += iv.hist[b];
-        uint32_t g = 4u;
-        if (mx * (unsigned long long)F.march_lanes > 4ull * sum) g = 16u;
-        else if (sum >= 320ull * n_march) g = 8u;
-        *iv.gsel = g;
+        *iv.gsel = (mx * (unsigned long long)F.march_lanes <= 4ull * sum) ? 4u : 16u;
     }
     if (threadIdx.x < N_BUCKETS) {
         uint32_t s = 0;
@@ -2587,17 +2581,15 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             e = cudaEventRecord((cudaEvent_t)out->ev_march_begin, st);
             if (e != cudaSuccess) return cuda_fail(e, "cudaEventRecord(begin)");
         }
-        // auto width: the G = 4, 8 and 16 kernels are all launched and the
-        // ones order_rays_kernel did not choose return at once
-        void (*fns[3])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_fn, nullptr, nullptr};
-        int gs[3] = {gsize, 0, 0};
+        // auto width: the G = 4 and 16 kernels are both launched and the one
+        // order_rays_kernel did not choose returns at once
+        void (*fns[2])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_fn, nullptr};
+        int gs[2] = {gsize, 0};
         int nf = 1;
         if (F.auto_g) {
-            fns[1] = march_sm_kernel<8, 3>;
-            gs[1] = 8;
-            fns[2] = march_sm_kernel<16, 3>;
-            gs[2] = 16;
-            nf = 3;
+            fns[1] = march_sm_kernel<16, 3>;
+            gs[1] = 16;
+            nf = 2;
         }
         for (int q = 0; q < nf; ++q) {
             int64_t grid = (int64_t)sm_count() * per_sm;
