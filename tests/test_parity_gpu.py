@@ -86,9 +86,11 @@ def test_frame_matches_oracle_and_reference(B, golden, cid, recipe, modes, jitte
         # register-state kernel (0x80); lane groups of 2 / 8 / 16 (32 with
         # 0x80); register budgets of 4 / 2 / 3 CTAs per SM; the BSP walk
         # (0x800000) and the BVH next_interval (0x800008) instead of the
-        # raster -- every variant renders the same frame
+        # raster; the id-order leaf scan instead of the leaf walk (0x2000000)
+        # and the walk without its start predictor (0x4000000) -- every
+        # variant renders the same frame
         for flags in (0, 2, 0x40, 0x80, 0x100, 0x300, 0x400, 0x580, 0x1000, 0x2000, 0x3000,
-                      0x800000, 0x800008):
+                      0x800000, 0x800008, 0x2000000, 0x4000000):
             fb, st = B.render(sc, cam, mode, par, jitter=jitter, flags=flags)
             _compare(fb, st, ref, mode, golden["frames"][f"{cid}/{mode}"])
 
@@ -99,7 +101,7 @@ def test_radial59_benchmark_scene(B, golden, mode):
     sc, orc = scene_of(B, "radial59")
     cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
     g = golden["frames"][f"radial59/{mode}"]
-    for flags in (0, 0x80, 0x1000, 0x3000, 0x800000):
+    for flags in (0, 0x80, 0x1000, 0x3000, 0x800000, 0x2000000, 0x4000000):
         fb, st = B.render(sc, cam, mode, par, flags=flags)
         _check_radial59(fb, st, g, orc, cam, mode, par)
 
