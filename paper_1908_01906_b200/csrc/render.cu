@@ -122,30 +122,41 @@ __device__ __forceinline__ void slab(const RayD &r, const double *lo, const doub
 
 // ------------------------------------------------------------ point location
 
-struct PQuery {  // a point with f32 round-down / round-up copies for conservative box tests
+struct PQuery {  // a sample point
     double x, y, z;
-    float xd, yd, zd, xu, yu, zu;
 };
 
 __device__ __forceinline__ PQuery make_query(double x, double y, double z) {
     PQuery q;
     q.x = x; q.y = y; q.z = z;
-    q.xd = __double2float_rd(x); q.yd = __double2float_rd(y); q.zd = __double2float_rd(z);
-    q.xu = __double2float_ru(x); q.yu = __double2float_ru(y); q.zu = __double2float_ru(z);
     return q;
 }
 
+// f32 round-down / round-up copies of a point for conservative tests against
+// f32 boxes (the BVH descent and the cell lists; the grid path compares in f64)
+struct PQueryF {
+    float xd, yd, zd, xu, yu, zu;
+};
+
+__device__ __forceinline__ PQueryF make_qf(const PQuery &q) {
+    PQueryF f;
+    f.xd = __double2float_rd(q.x); f.yd = __double2float_rd(q.y); f.zd = __double2float_rd(q.z);
+    f.xu = __double2float_ru(q.x); f.yu = __double2float_ru(q.y); f.zu = __double2float_ru(q.z);
+    return f;
+}
+
 // conservative: true whenever the exact point lies in the closed box
-__device__ __forceinline__ bool in_box(const PQuery &q, float lx, float ly, float lz, float hx,
+__device__ __forceinline__ bool in_box(const PQueryF &q, float lx, float ly, float lz, float hx,
                                        float hy, float hz) {
     return !(q.xu < lx) && !(q.xd > hx) && !(q.yu < ly) && !(q.yd > hy) && !(q.zu < lz) &&
            !(q.zd > hz);
 }
 
-// strict and exact-safe: true only if the exact point is strictly inside
+// exact: true only if the point is strictly inside the f32 box (the floats
+// widen to double exactly, so these are exact comparisons)
 __device__ __forceinline__ bool strictly_in(const PQuery &q, const float *lo, const float *hi) {
-    return q.xd > lo[0] && q.xu < hi[0] && q.yd > lo[1] && q.yu < hi[1] && q.zd > lo[2] &&
-           q.zu < hi[2];
+    return q.x > (double)lo[0] && q.x < (double)hi[0] && q.y > (double)lo[1] &&
+           q.y < (double)hi[1] && q.z > (double)lo[2] && q.z < (double)hi[2];
 }
 
 // 32-B read-only loads (LDG.E.ENL2.256, sm_100): the march is bound by the
@@ -168,6 +179,10 @@ __device__ __forceinline__ double4 ldg256(const void *p) {
 #endif
     return v;
 }
+
+#ifndef TR_UNROLL_COMPOSITE
+#define TR_UNROLL_COMPOSITE 1   // A/B knob: the round's compositing loop unrolled over G
+#endif
 
 // The 96 B of a record the barycentric test reads (inverse + origin).
 struct RecM {
@@ -364,6 +379,7 @@ __device__ __forceinline__ void scan_leaf_ids(const SceneK &S, uint32_t start, u
 __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], int32_t &leaf_out) {
     uint32_t best = UINT32_MAX, best_pos = UINT32_MAX;
     int32_t best_leaf = -1;
+    const PQueryF qf = make_qf(q);
     int32_t st_node[PSTACK];
     uint32_t st_min[PSTACK];
     int sp = 0;
@@ -374,8 +390,8 @@ __device__ uint32_t locate_full(const SceneK &S, const PQuery &q, double l[4], i
         const int4 D = __ldg(reinterpret_cast<const int4 *>(np + 3));
         const int32_t c0 = D.x, c1 = D.y;
         const uint32_t m0 = (uint32_t)D.z, m1 = (uint32_t)D.w;
-        bool h0 = m0 < best && in_box(q, A.x, A.y, A.z, A.w, B.x, B.y);
-        bool h1 = c1 != CHILD_NONE && m1 < best && in_box(q, B.z, B.w, C.x, C.y, C.z, C.w);
+        bool h0 = m0 < best && in_box(qf, A.x, A.y, A.z, A.w, B.x, B.y);
+        bool h1 = c1 != CHILD_NONE && m1 < best && in_box(qf, B.z, B.w, C.x, C.y, C.z, C.w);
         if (h0 && c0 < 0) {
             const uint32_t before = best;
             const TrPLeaf *lf = S.pleaves + (~c0);
@@ -433,10 +449,11 @@ __device__ __forceinline__ bool locate_cells(const SceneK &S, const PQuery &q, d
     const int64_t cell = (c[0] * S.cdim[1] + c[1]) * S.cdim[2] + c[2];
     const uint32_t o0 = __ldg(S.cell_off + cell), o1 = __ldg(S.cell_off + cell + 1) & 0x7fffffffu;
     if (o0 & 0x80000000u) return false;
+    const PQueryF qf = make_qf(q);
     for (uint32_t k = o0; k < o1; ++k) {
         const uint32_t r = __ldg(S.cell_recs + k);
         const float4 b0 = __ldg(S.tbox + 2 * r), b1 = __ldg(S.tbox + 2 * r + 1);
-        if (!in_box(q, b0.x, b0.y, b0.z, b0.w, b1.x, b1.y)) continue;
+        if (!in_box(qf, b0.x, b0.y, b0.z, b0.w, b1.x, b1.y)) continue;
         if (bary_test(S.tets, r, q, l)) { pos = r; return true; }
     }
     return true;
@@ -2024,6 +2041,21 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         Acc acc = {0.0, 0.0, 0.0, 0.0};
         if (active && !idle) {
             acc.r = s_acc[0][g]; acc.g = s_acc[1][g]; acc.b = s_acc[2][g]; acc.a = s_acc[3][g];
+#if TR_UNROLL_COMPOSITE
+            // unrolled and predicated: no loop counter or exit branch per sample
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m < cnt && !term) {
+                    const double4 gg = shade[m][g];
+                    const double w = (1.0 - acc.a) * gg.x;
+                    acc.r += w * gg.y;
+                    acc.g += w * gg.z;
+                    acc.b += w * gg.w;
+                    acc.a += w;
+                    if (((fbits >> m) & 1u) && acc.a >= fr.term) { taken_r = m + 1; term = true; }
+                }
+            }
+#else
             for (int m = 0; m < cnt; ++m) {
                 const double4 gg = shade[m][g];
                 const double w = (1.0 - acc.a) * gg.x;
@@ -2033,6 +2065,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 acc.a += w;
                 if (((fbits >> m) & 1u) && acc.a >= fr.term) { taken_r = m + 1; term = true; break; }
             }
+#endif
             if (stats && j == 0) {
                 atomicAdd(&g_stats[ST_ROUNDS], 1ull);
                 if (cnt < G) atomicAdd(&g_stats[ST_PARTIAL], 1ull);

@@ -2,6 +2,7 @@
 build/ab/<name>/libtetray_b200.so (select one with TETRAY_B200_LIB=...).
 
     python scripts/ab_build.py name=-DTR_FIELD_PREFETCH=0 [name2=-DX=1,-DY=2 ...]
+    python scripts/ab_build.py head=@HEAD        # the committed sources of a git revision
 """
 import subprocess
 import sys
@@ -16,9 +17,24 @@ for spec in sys.argv[1:]:
     out = ROOT / "build" / "ab" / name / "libtetray_b200.so"
     out.parent.mkdir(parents=True, exist_ok=True)
     Bd.build_library()   # also refreshes the generated glibc pow header
+    csrc, inc = Bd.CSRC, ROOT / "include"
+    if defs.startswith("@"):   # sources of a git revision, into a scratch tree
+        rev, defs = defs[1:], ""
+        tmp = Path("/tmp/ab_src") / name
+        (tmp / "csrc").mkdir(parents=True, exist_ok=True)
+        (tmp / "include").mkdir(parents=True, exist_ok=True)
+        for f in list(Bd.SOURCES) + ["tr_internal.h", "glibc_pow.cuh"]:
+            (tmp / "csrc" / f).write_bytes(subprocess.run(
+                ["git", "-C", str(ROOT), "show", f"{rev}:paper_1908_01906_b200/csrc/{f}"],
+                capture_output=True, check=True).stdout)
+        (tmp / "include" / "tetray_b200.h").write_bytes(subprocess.run(
+            ["git", "-C", str(ROOT), "show", f"{rev}:include/tetray_b200.h"],
+            capture_output=True, check=True).stdout)
+        (tmp / "csrc" / "glibc_pow_data.h").write_bytes((Bd.CSRC / "glibc_pow_data.h").read_bytes())
+        csrc, inc = tmp / "csrc", tmp / "include"
     cmd = [Bd._nvcc(), *Bd.NVCC_FLAGS, *[d for d in defs.split(",") if d], "-ccbin", "/usr/bin/g++",
-           "-I", str(ROOT / "include"), "-I", str(Bd.CSRC),
-           *[str(Bd.CSRC / s) for s in Bd.SOURCES], "-o", str(out), "-lgomp"]
+           "-I", str(inc), "-I", str(csrc),
+           *[str(csrc / s) for s in Bd.SOURCES], "-o", str(out), "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode:
         sys.exit(res.stderr[-3000:])
