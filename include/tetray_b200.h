@@ -154,7 +154,8 @@ int tr_leaf_walk(int64_t n_leaves, TrPLeaf *leaves, const uint32_t *rec_ids,
  * relative to its ex_lo (set the exclusive boxes first). */
 /* The two predictors of tr_grid_scene_build's cubes (even, odd parity), for
  * TrDeviceScene.pred_class (interior cubes; boundary cubes differ by the pad). */
-int tr_grid_walk_pred(double pad, TrLeafPred *pred2);
+int tr_grid_walk_pred(double pad, TrLeafPred *pred2, uint32_t *walk16);
+/* walk16 (may be NULL): the two cubes' TrPLeaf.walk tables, 2 x 8 u32. */
 /* Uniform-grid leaf index: cell (x,y,z) -> leaf whose exclusive box covers
  * most of it (-1: none).  cell = floor((p - org) * scale), row-major x,y,z. */
 int tr_pbvh_grid(const TrHostBuf *b, int32_t *dims3, double *org3, double *scale3,
@@ -287,6 +288,16 @@ typedef struct TrDeviceScene {
     int32_t pred_classes;
     int32_t pad2;
     TrLeafPred pred_class[2];
+    /* analytic leaves of tr_grid_scene_build's n^3 cube grids (grid_n > 0):
+     * the march computes a sample's cube, its exclusive box and record range
+     * from the coordinates (the layout tr_grid_scene_build wrote; grid_brick:
+     * 8^3-cube brick order) and walks it with class_walk (device, 2 x 8 u32:
+     * the TrPLeaf.walk of an even / odd cube) -- no leaf header load */
+    int64_t grid_n;
+    double grid_pad;
+    int32_t grid_brick;
+    int32_t pad3;
+    const uint32_t *class_walk;
 } TrDeviceScene;
 
 /* One metadata epoch (scene.meta_state(), scene.py:48-50 / 78-82), device pointers. */
@@ -343,6 +354,7 @@ typedef struct TrFrame {
 #define TR_FLAG_FORCE_CAND 0x1000000 /* the candidate raster also above 1M pixels (default there: the BSP walk) */
 #define TR_FLAG_NO_WALK 0x2000000 /* exclusive leaves scanned in id order, not walked (testing) */
 #define TR_FLAG_NO_PRED 0x4000000 /* leaf walks start at the first tet, no predictor (testing) */
+#define TR_FLAG_NO_ANALYTIC 0x8000000 /* grid scenes: load leaf headers, not the analytic layout (testing) */
 #define TR_FLAG_NO_GRID 2      /* disable the uniform-grid leaf index (testing) */
 #define TR_FLAG_STATS 4        /* count kernel events (tr_kernel_stats); slows the frame */
 #define TR_FLAG_NO_BSP 8       /* where the BSP walk runs (TR_FLAG_NO_CAND, lists > 48): the partition BVH instead */

@@ -43,6 +43,8 @@ class TrDeviceScene(C.Structure):
         ("corg", C.c_double * 3), ("cscale", C.c_double * 3),
         ("pgrid_pred", C.c_void_p), ("pred_classes", C.c_int32), ("pad2", C.c_int32),
         ("pred_class", C.c_float * 24),
+        ("grid_n", C.c_int64), ("grid_pad", C.c_double), ("grid_brick", C.c_int32),
+        ("pad3", C.c_int32), ("class_walk", C.c_void_p),
     ]
 
 
@@ -120,7 +122,7 @@ _SIGNATURES = [
     ("tr_pbvh_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_leaf_walk", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                C.c_void_p]),
-    ("tr_grid_walk_pred", C.c_int, [C.c_double, C.c_void_p]),
+    ("tr_grid_walk_pred", C.c_int, [C.c_double, C.c_void_p, C.c_void_p]),
     ("tr_pbvh_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, C.c_void_p]),
     ("tr_pbvh_coverage", C.c_double, [C.c_void_p]),
     ("tr_cells_build", C.c_int, [C.c_void_p, c_f64p, c_f64p, C.c_int32, C.c_int32,

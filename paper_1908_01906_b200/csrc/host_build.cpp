@@ -1272,12 +1272,13 @@ static void walk_table_cube(int parity, uint32_t walk[8], const float *ex_lo, Tr
 
 void tr_walk_table_cube(int parity, uint32_t walk[8]) { walk_table_cube(parity, walk, nullptr, nullptr); }
 
-int tr_grid_walk_pred(double pad, TrLeafPred *pred2) {
+int tr_grid_walk_pred(double pad, TrLeafPred *pred2, uint32_t *walk16) {
     if (!pred2 || !(pad >= 0.0)) return tr_fail(TR_EINVAL, "tr_grid_walk_pred: invalid arguments");
     const float lo[3] = {(float)pad, (float)pad, (float)pad};   // an interior cube at the origin
-    uint32_t w[8];
-    walk_table_cube(0, w, lo, pred2);
-    walk_table_cube(1, w, lo, pred2 + 1);
+    uint32_t w[2][8];
+    walk_table_cube(0, w[0], lo, pred2);
+    walk_table_cube(1, w[1], lo, pred2 + 1);
+    if (walk16) std::memcpy(walk16, w, sizeof w);
     return TR_OK;
 }
 

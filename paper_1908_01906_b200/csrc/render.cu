@@ -38,6 +38,7 @@
 #include <string>
 
 #include "glibc_pow.cuh"
+#include "grid_layout.cuh"
 #include "tetray_b200.h"
 #include "tr_internal.h"
 
@@ -269,6 +270,10 @@ struct SceneK {  // kernel copy of TrDeviceScene
     const float4 *__restrict__ pgrid_pred;  // per cell: 3 float4 rows (TrLeafPred), or NULL
     int32_t pred_classes;                   // 2: pred_class[cube parity] (grid scenes)
     float pred_class[2][12];
+    int64_t grid_n;                         // > 0: analytic cube-grid leaves (grid_layout.cuh)
+    double grid_pad;
+    int32_t grid_brick;
+    const uint32_t *__restrict__ class_walk;   // 2 x 8 u32: walk tables of even / odd cubes
 };
 
 // Exclusive-leaf path: the records [start, start+count) are the leaf's tets in
@@ -308,12 +313,12 @@ __device__ __forceinline__ uint32_t scan_leaf_pairs(const SceneK &S, uint32_t st
 // tet relative to the exclusive box's corner `lo`; when they put q beyond a
 // face the walk starts at the neighbour across it instead -- one record load
 // for almost every sample (a wrong guess costs a step, never the result).
-__device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__restrict__ hdr,
+__device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const uint32_t *__restrict__ wt,
                                               uint32_t start, uint32_t count, const PQuery &q,
                                               double l[4], bool use_pred = false,
                                               float4 r1 = float4(), float4 r2 = float4(),
                                               float4 r3 = float4(), const float *lo = nullptr) {
-    const uint32_t w4 = __ldg(&hdr->walk[4]);
+    const uint32_t w4 = __ldg(wt + 4);
     if (w4 >> 31) {
         uint32_t i = w4 & 7u, seen = 0;
         if (use_pred) {
@@ -329,14 +334,14 @@ __device__ __forceinline__ uint32_t walk_leaf(const SceneK &S, const TrPLeaf *__
             if (p2 < pm) { pm = p2; face = 2; }
             if (p3 < pm) { pm = p3; face = 3; }
             if (pm < -1e-4f) {
-                const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
+                const uint32_t e = (__ldg(wt + (i >> 1)) >> (16 * (i & 1u))) & 0xffffu;
                 const uint32_t nb = (e >> (3 * face)) & 7u;
                 if (nb < count) i = nb;
             }
         }
         for (uint32_t step = 0; step < count; ++step) {
             seen |= 1u << i;
-            const uint32_t e = (__ldg(&hdr->walk[i >> 1]) >> (16 * (i & 1u))) & 0xffffu;
+            const uint32_t e = (__ldg(wt + (i >> 1)) >> (16 * (i & 1u))) & 0xffffu;
             if (bary_of(load_recm(S.tets, start + i), q, l)) {
                 if (((e >> 12) & 1u) && l[0] >= TR_WALK_TAU && l[1] >= TR_WALK_TAU &&
                     l[2] >= TR_WALK_TAU && l[3] >= TR_WALK_TAU)
@@ -514,7 +519,7 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
     uint32_t pos;
     bool done = false;
     if (use_hint && hint.valid && strictly_in(q, hint.lo, hint.hi)) {
-        pos = walk_leaf(S, hint.hdr, hint.start, hint.count, q, l);
+        pos = walk_leaf(S, hint.hdr->walk, hint.start, hint.count, q, l);
         done = true;
     } else if (use_grid) {
         const int64_t gc = grid_cell(S, q);
@@ -529,7 +534,7 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
                 load_leaf(S.pgrid_leaf + gc, h);  // one load: the header is replicated per cell
             }
             if (strictly_in(q, h.lo, h.hi)) {
-                pos = walk_leaf(S, h.hdr, h.start, h.count, q, l);
+                pos = walk_leaf(S, h.hdr->walk, h.start, h.count, q, l);
                 if (use_hint) hint = h;
                 done = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
@@ -1562,7 +1567,36 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
     double l[4];
     uint32_t pos = UINT32_MAX;
     bool located = false;
-    if (use_grid && !(use_cells && S.cells_first)) {
+    if (use_grid && S.grid_n > 0 && !(fr.flags & (TR_FLAG_NO_ANALYTIC | TR_FLAG_NO_WALK))) {
+        // analytic cube grid (tr_grid_scene_build): the cube, its exclusive box
+        // and records follow from the coordinates -- no leaf header load
+        const int64_t n = S.grid_n;
+        if (q.x >= 0.0 && q.y >= 0.0 && q.z >= 0.0) {
+            const int64_t cx = (int64_t)q.x, cy = (int64_t)q.y, cz = (int64_t)q.z;
+            if (cx < n && cy < n && cz < n) {
+                const float lo[3] = {__double2float_ru(tr_grid::ex_lo(cx, n, S.grid_pad)),
+                                     __double2float_ru(tr_grid::ex_lo(cy, n, S.grid_pad)),
+                                     __double2float_ru(tr_grid::ex_lo(cz, n, S.grid_pad))};
+                const float hi[3] = {__double2float_rd(tr_grid::ex_hi(cx, n, S.grid_pad)),
+                                     __double2float_rd(tr_grid::ex_hi(cy, n, S.grid_pad)),
+                                     __double2float_rd(tr_grid::ex_hi(cz, n, S.grid_pad))};
+                if (strictly_in(q, lo, hi)) {
+                    const int par = (int)((cx + cy + cz) & 1);
+                    const float *c = par ? S.pred_class[1] : S.pred_class[0];
+                    const uint32_t start =
+                        (uint32_t)(5 * tr_grid::cube_slot(n, S.grid_brick != 0, cx, cy, cz));
+                    pos = walk_leaf(S, S.class_walk + 8 * par, start, 5u, q, l,
+                                    !(fr.flags & TR_FLAG_NO_PRED),
+                                    make_float4(c[0], c[1], c[2], c[3]),
+                                    make_float4(c[4], c[5], c[6], c[7]),
+                                    make_float4(c[8], c[9], c[10], c[11]), lo);
+                    located = true;
+                    if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
+                }
+            }
+        }
+    }
+    if (!located && use_grid && !(use_cells && S.cells_first)) {
         int par = 0;
         const int64_t gc = grid_cell(S, q, &par);
         if (gc >= 0) {
@@ -1585,8 +1619,8 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
             if (strictly_in(q, hh.lo, hh.hi)) {
                 if (pair_scan) pos = scan_leaf_pairs(S, hh.start, hh.count, q, l);
                 else if (fr.flags & TR_FLAG_NO_WALK) pos = scan_leaf_first(S, hh.start, hh.count, q, l);
-                else pos = walk_leaf(S, S.pgrid_leaf + gc, hh.start, hh.count, q, l, use_pred, pr0,
-                                     pr1, pr2, hh.lo);
+                else pos = walk_leaf(S, S.pgrid_leaf[gc].walk, hh.start, hh.count, q, l, use_pred,
+                                     pr0, pr1, pr2, hh.lo);
                 located = true;
                 if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
@@ -2275,6 +2309,10 @@ SceneK make_scene(const TrDeviceScene *s) {
     S.pred_classes = s->pred_classes;
     for (int c = 0; c < 2; ++c)
         for (int k = 0; k < 12; ++k) S.pred_class[c][k] = (&s->pred_class[c].row[0][0])[k];
+    S.grid_n = s->class_walk ? s->grid_n : 0;
+    S.grid_pad = s->grid_pad;
+    S.grid_brick = s->grid_brick;
+    S.class_walk = s->class_walk;
     return S;
 }
 

@@ -31,6 +31,7 @@
 #include <cstdint>
 #include <string>
 
+#include "grid_layout.cuh"
 #include "tetray_b200.h"
 #include "tr_internal.h"
 
@@ -55,19 +56,9 @@ struct GridK {
     double pad;
 };
 
-constexpr int64_t BRICK = 8;
-
-// Record slot of cube (x, y, z): cube-major, or brick-major with the cubes of
-// a brick (8^3, clipped at the far faces) in x, y, z order -- dense, so the
-// 5 records of cube c start at 5 * cube_slot(c).
+// Record slot of cube (x, y, z): grid_layout.cuh (shared with the march).
 __device__ __forceinline__ int64_t cube_slot(const GridK &G, int64_t x, int64_t y, int64_t z) {
-    const int64_t n = G.n;
-    if (!G.brick) return (x * n + y) * n + z;
-    const int64_t bx = x / BRICK, by = y / BRICK, bz = z / BRICK;
-    const int64_t sx = min(BRICK, n - bx * BRICK), sy = min(BRICK, n - by * BRICK);
-    const int64_t sz = min(BRICK, n - bz * BRICK);
-    const int64_t before = BRICK * bx * n * n + sx * BRICK * by * n + sx * sy * BRICK * bz;
-    return before + ((x - bx * BRICK) * sy + (y - by * BRICK)) * sz + (z - bz * BRICK);
+    return tr_grid::cube_slot(G.n, G.brick != 0, x, y, z);
 }
 
 // mesh.py _ramp / _radial, then .astype(float32).astype(float64)
@@ -125,11 +116,9 @@ __global__ void grid_leaves_kernel(GridK G, WalkK W, TrPLeaf *leaves) {
          c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t q[3] = {c / (n * n), (c / n) % n, c % n};
         TrPLeaf L;
-        for (int a = 0; a < 3; ++a) {
-            const double lo = (q[a] == 0) ? -G.pad : (double)q[a] + G.pad;
-            const double hi = (q[a] == n - 1) ? (double)n + G.pad : (double)(q[a] + 1) - G.pad;
-            L.ex_lo[a] = __double2float_ru(lo);   // inward
-            L.ex_hi[a] = __double2float_rd(hi);
+        for (int a = 0; a < 3; ++a) {   // inward (grid_layout.cuh, shared with the march)
+            L.ex_lo[a] = __double2float_ru(tr_grid::ex_lo(q[a], n, G.pad));
+            L.ex_hi[a] = __double2float_rd(tr_grid::ex_hi(q[a], n, G.pad));
         }
         L.start = (uint32_t)(5 * cube_slot(G, q[0], q[1], q[2]));
         L.count = 5u;

@@ -384,6 +384,9 @@ class DeviceScene:
         elif getattr(self, "grid_pred_class", None) is not None:
             self.desc.pred_classes = 2
             self.desc.pred_class = (C.c_float * 24)(*self.grid_pred_class)
+            # the march derives leaves and records from the cube layout
+            self.desc.grid_n, self.desc.grid_pad, self.desc.grid_brick = self.grid_analytic
+            self.desc.class_walk = self.t_class_walk.data_ptr()
         if self.cells is not None:
             cl = self.cells
             self.desc.cell_off = self.t_coff.data_ptr()
@@ -486,8 +489,11 @@ class DeviceScene:
         self.t_grid_leaf = None
         self.t_grid_pred = None
         self.grid_pred_class = np.zeros(24, np.float32)   # TrLeafPred of an even / odd cube
-        _lib.check(L.tr_grid_walk_pred(float(sampler.pad), _lib.vptr(self.grid_pred_class)),
-                   "tr_grid_walk_pred")
+        walk16 = np.zeros(16, np.uint32)                   # their TrPLeaf.walk tables
+        _lib.check(L.tr_grid_walk_pred(float(sampler.pad), _lib.vptr(self.grid_pred_class),
+                                       _lib.vptr(walk16)), "tr_grid_walk_pred")
+        self.t_class_walk = _upload(walk16, self.device)
+        self.grid_analytic = (n, float(sampler.pad), 1 if brick else 0)
         self.cells = None
         self.pnodes_host = self.pleaves_host = None
         self.grid = PointGrid(np.full(3, n, np.int32), np.zeros(3), np.ones(3), None)

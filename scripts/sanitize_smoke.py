@@ -18,7 +18,7 @@ for recipe in ("golden_radial4", "conftest48", "inside", "axis", "a6fog", "jitte
                        fov_y_deg=cam.fov_y_deg, width=45, height=38)
     for mode in ("reference", "skip", "skip-adaptive"):
         ref = None
-        for flags in (0, 0x800000, 0x800008, 0x80, 0x400, 0x1000000):
+        for flags in (0, 0x800000, 0x800008, 0x80, 0x400, 0x1000000, 0x2000000, 0x4000000):
             for jitter in (False, True):
                 fb, st = B.render(sc, cam, mode, par, flags=flags, jitter=jitter)
                 if not jitter:
@@ -39,4 +39,12 @@ for recipe in ("golden_radial4", "conftest48", "inside", "axis", "a6fog", "jitte
         b = br.render(cam, mode, par)
         assert np.array_equal(a[0].rgba, b[0].rgba), (recipe, mode, "bricks")
     print(recipe, "ok", flush=True)
+# an HBM-generated grid: analytic cube leaves (default) and leaf headers
+sc = C.build_scene(B, "grid12")
+cam, par = C.camera(B, "radial16", scale=0.125), C.params(B, "radial16")
+for mode in ("reference", "skip", "skip-adaptive"):
+    a = B.render(sc, cam, mode, par)[0].rgba
+    for flags in (0x8000000, 0x4000000, 0x2000000):
+        assert np.array_equal(a, B.render(sc, cam, mode, par, flags=flags)[0].rgba), (mode, flags)
+print("grid12 ok", flush=True)
 print("sanitize smoke ok")

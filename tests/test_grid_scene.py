@@ -120,7 +120,9 @@ def test_grid_frames_equal_host_scene(B, n):
     g2 = cases.build_scene(B, f"grid{n}")
     g2.grid_id_order = True
     for mode in ("reference", "skip", "skip-adaptive"):
-        for gs, flags in ((g, 0), (g, 2), (g, 0x1000), (g2, 0)):
+        # default (analytic cube leaves), no grid, 4 CTAs/SM, headers instead
+        # of the analytic layout (0x8000000), id-order records (g2)
+        for gs, flags in ((g, 0), (g, 2), (g, 0x1000), (g, 0x8000000), (g, 0x4000000), (g2, 0)):
             fg, sg = B.render(gs, cam, mode, par, flags=flags)
             fr, sr = B.render(r, cam, mode, par)
             assert np.array_equal(fg.rgba, fr.rgba), (n, mode, flags)

@@ -126,10 +126,14 @@ def test_generator_cubes_walk_from_the_central_tet(B):
     from paper_1908_01906_b200 import _lib
     assert _lib.lib().tr_leaf_walk(0, None, None, None, None, None) == 0
     two = np.zeros(24, np.float32)
-    assert _lib.lib().tr_grid_walk_pred(1e-7, _lib.vptr(two)) == 0
-    _, _, preds = leaf_tables(B, m.vertices, m.tets, cubes, with_pred=True)
+    walk16 = np.zeros(16, np.uint32)
+    assert _lib.lib().tr_grid_walk_pred(1e-7, _lib.vptr(two), _lib.vptr(walk16)) == 0
+    lv, _, preds = leaf_tables(B, m.vertices, m.tets, cubes, with_pred=True)
     # an interior-cube class predictor = the per-leaf one up to the pad shift
     assert np.allclose(two[:12], preds[0], atol=1e-5)
+    # the class walk tables (the march's analytic grid path) = the per-leaf
+    # tables of an even and an odd cube
+    assert np.array_equal(walk16[:8], lv[0]["walk"]) and np.array_equal(walk16[8:], lv[1]["walk"])
 
 
 def _check_points(inv, orig, ids, w, pts, pred=None, lo=None):
