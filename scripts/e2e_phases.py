@@ -10,8 +10,9 @@ import paper_1908_01906_b200 as B
 from paper_1908_01906_b200 import device as DV
 from paper_1908_01906_b200.render import Framebuffer, RenderStats
 
-sc = C.build_scene(B, "radial59")
-cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
+SCENE = sys.argv[1] if len(sys.argv) > 1 else "radial59"
+sc = C.build_scene(B, SCENE)
+cam, par = C.camera(B, SCENE), C.params(B, SCENE)
 dev = DV.device_scene_for(sc)
 T = {}
 def render():
@@ -75,3 +76,13 @@ clock("h2d copy_ async", lambda: y.copy_(x, non_blocking=True))
 clock("torch.zeros(1) cuda", lambda: torch.zeros(1, dtype=torch.int32, device="cuda"))
 clock("current_stream", lambda: torch.cuda.current_stream(dev.device))
 clock("Epoch()", lambda: DV.Epoch(dev, sc.meta_state(), par))
+
+import cProfile, pstats, io
+pr = cProfile.Profile()
+pr.enable()
+for _ in range(200):
+    DV.Epoch(dev, sc.meta_state(), par)
+pr.disable()
+buf = io.StringIO()
+pstats.Stats(pr, stream=buf).sort_stats("tottime").print_stats(12)
+print(buf.getvalue())
