@@ -23,8 +23,26 @@ __host__ __device__ __forceinline__ int64_t cube_slot(int64_t n, bool brick, int
     return before + ((x - bx * BRICK) * sy + (y - by * BRICK)) * sz + (z - bz * BRICK);
 }
 
+// 32-bit cube_slot for the march (n <= 1024 and 5 n^3 < 2^32, checked by
+// tr_grid_scene_sizes, so every value fits).
+__host__ __device__ __forceinline__ uint32_t cube_slot32(uint32_t n, bool brick, uint32_t x, uint32_t y,
+                                                         uint32_t z) {
+    if (!brick) return (x * n + y) * n + z;
+    const uint32_t b = (uint32_t)BRICK;
+    const uint32_t bx = x / b, by = y / b, bz = z / b;
+    const uint32_t sx = n - bx * b < b ? n - bx * b : b;
+    const uint32_t sy = n - by * b < b ? n - by * b : b;
+    const uint32_t sz = n - bz * b < b ? n - bz * b : b;
+    const uint32_t before = b * bx * n * n + sx * b * by * n + sx * sy * b * bz;
+    return before + ((x - bx * b) * sy + (y - by * b)) * sz + (z - bz * b);
+}
+
 // The cube's exclusive box on one axis before f32 rounding (inward): the
 // cube shrunk by the box pad, reaching out by the pad at the grid's faces.
+// In f64 these are exactly the neighbouring cubes' padded tet box faces
+// (fl(c + pad), fl((c + 1) - pad): mesh.py:249-250 computes them the same
+// way), so the open interval between them meets no other cube's padded tet
+// box -- the march tests against them directly.
 __host__ __device__ __forceinline__ double ex_lo(int64_t c, int64_t n, double pad) {
     return (c == 0) ? -pad : (double)c + pad;
 }

@@ -1571,28 +1571,27 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
         // analytic cube grid (tr_grid_scene_build): the cube, its exclusive box
         // and records follow from the coordinates -- no leaf header load
         const int64_t n = S.grid_n;
-        if (q.x >= 0.0 && q.y >= 0.0 && q.z >= 0.0) {
-            const int64_t cx = (int64_t)q.x, cy = (int64_t)q.y, cz = (int64_t)q.z;
-            if (cx < n && cy < n && cz < n) {
-                const float lo[3] = {__double2float_ru(tr_grid::ex_lo(cx, n, S.grid_pad)),
-                                     __double2float_ru(tr_grid::ex_lo(cy, n, S.grid_pad)),
-                                     __double2float_ru(tr_grid::ex_lo(cz, n, S.grid_pad))};
-                const float hi[3] = {__double2float_rd(tr_grid::ex_hi(cx, n, S.grid_pad)),
-                                     __double2float_rd(tr_grid::ex_hi(cy, n, S.grid_pad)),
-                                     __double2float_rd(tr_grid::ex_hi(cz, n, S.grid_pad))};
-                if (strictly_in(q, lo, hi)) {
-                    const int par = (int)((cx + cy + cz) & 1);
-                    const float *c = par ? S.pred_class[1] : S.pred_class[0];
-                    const uint32_t start =
-                        (uint32_t)(5 * tr_grid::cube_slot(n, S.grid_brick != 0, cx, cy, cz));
-                    pos = walk_leaf(S, S.class_walk + 8 * par, start, 5u, q, l,
-                                    !(fr.flags & TR_FLAG_NO_PRED),
-                                    make_float4(c[0], c[1], c[2], c[3]),
-                                    make_float4(c[4], c[5], c[6], c[7]),
-                                    make_float4(c[8], c[9], c[10], c[11]), lo);
-                    located = true;
-                    if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
-                }
+        if (q.x >= 0.0 && q.y >= 0.0 && q.z >= 0.0 && q.x < (double)n && q.y < (double)n &&
+            q.z < (double)n) {
+            const int cx = (int)q.x, cy = (int)q.y, cz = (int)q.z;
+            if (q.x > tr_grid::ex_lo(cx, n, S.grid_pad) && q.x < tr_grid::ex_hi(cx, n, S.grid_pad) &&
+                q.y > tr_grid::ex_lo(cy, n, S.grid_pad) && q.y < tr_grid::ex_hi(cy, n, S.grid_pad) &&
+                q.z > tr_grid::ex_lo(cz, n, S.grid_pad) && q.z < tr_grid::ex_hi(cz, n, S.grid_pad)) {
+                const int par = (cx + cy + cz) & 1;
+                const float *c = par ? S.pred_class[1] : S.pred_class[0];
+                const uint32_t start = 5u * tr_grid::cube_slot32((uint32_t)n, S.grid_brick != 0,
+                                                                 (uint32_t)cx, (uint32_t)cy,
+                                                                 (uint32_t)cz);
+                // the predictor's rows are relative to an interior cube's box corner
+                const float lo[3] = {(float)cx + (float)S.grid_pad, (float)cy + (float)S.grid_pad,
+                                     (float)cz + (float)S.grid_pad};
+                pos = walk_leaf(S, S.class_walk + 8 * par, start, 5u, q, l,
+                                !(fr.flags & TR_FLAG_NO_PRED),
+                                make_float4(c[0], c[1], c[2], c[3]),
+                                make_float4(c[4], c[5], c[6], c[7]),
+                                make_float4(c[8], c[9], c[10], c[11]), lo);
+                located = true;
+                if (stats) atomicAdd(&g_stats[ST_GRID_HIT], 1ull);
             }
         }
     }

@@ -23,10 +23,13 @@ for spec in sys.argv[1:]:
         tmp = Path("/tmp/ab_src") / name
         (tmp / "csrc").mkdir(parents=True, exist_ok=True)
         (tmp / "include").mkdir(parents=True, exist_ok=True)
-        for f in list(Bd.SOURCES) + ["tr_internal.h", "glibc_pow.cuh"]:
-            (tmp / "csrc" / f).write_bytes(subprocess.run(
-                ["git", "-C", str(ROOT), "show", f"{rev}:paper_1908_01906_b200/csrc/{f}"],
-                capture_output=True, check=True).stdout)
+        listing = subprocess.run(["git", "-C", str(ROOT), "ls-tree", "--name-only", rev,
+                                  "paper_1908_01906_b200/csrc/"], capture_output=True, text=True,
+                                 check=True).stdout.split()
+        for path in listing:   # every source and header of that revision
+            (tmp / "csrc" / Path(path).name).write_bytes(subprocess.run(
+                ["git", "-C", str(ROOT), "show", f"{rev}:{path}"], capture_output=True,
+                check=True).stdout)
         (tmp / "include" / "tetray_b200.h").write_bytes(subprocess.run(
             ["git", "-C", str(ROOT), "show", f"{rev}:include/tetray_b200.h"],
             capture_output=True, check=True).stdout)
