@@ -1913,7 +1913,7 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
 // (SoA, one slot per group) instead of registers: the registers then hold a
 // sample's working set only, so more warps fit per SM.  Same
 // rounds, same exact compositing; lane 0 of a group writes the state.
-template <int G, int MINB, bool BRICK = false>
+template <int G, int MINB, bool BRICK = false, bool STATS = false>
 __global__ void __launch_bounds__(MARCH_BLOCK, MINB)
 march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
@@ -1939,7 +1939,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const bool track = fr.track_ppart && fr.mode != 0;
     const bool use_grid = !(fr.flags & TR_FLAG_NO_GRID);
     const bool use_cells = S.cell_off != nullptr && !(fr.flags & TR_FLAG_NO_CELLS);
-    const bool stats = (fr.flags & TR_FLAG_STATS) != 0;
+    constexpr bool stats = STATS;   // TR_FLAG_STATS selects the counting instantiation
     const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
     const bool timing = (fr.flags & TR_FLAG_TILE_TIMING) != 0;
     if (timing && threadIdx.x == 0) atomicMin(&g_stats[ST_MARCH_T0], globaltimer_ns());
@@ -2577,7 +2577,9 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         switch (gsize) {
             case 2: march_fn = march_sm_kernel<2, 3>; break;
             case 4: march_fn = minb == 2 ? march_sm_kernel<4, 2>
-                             : (minb == 1 ? march_sm_kernel<4, 4> : march_sm_kernel<4, 3>); break;
+                             : (minb == 1 ? march_sm_kernel<4, 4>
+                                : ((frame->flags & TR_FLAG_STATS) ? march_sm_kernel<4, 3, false, true>
+                                                                  : march_sm_kernel<4, 3>)); break;
             case 8: march_fn = march_sm_kernel<8, 3>; break;
             case 16: march_fn = march_sm_kernel<16, 3>; break;
             default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8 or 16");
