@@ -3,7 +3,7 @@
 
 Workload (BASELINE config 3: headline the >= 1e8-tet scene,
 where every sample's tet record is a DRAM miss): radial272 -- 100,618,240
-tets, default KD partitions (8,192), the radial16 TF scaled to N=272, camera
+tets, default KD partitions (4,096), the radial16 TF scaled to N=272, camera
 [40,26,34]*272/16 -> [136]^3, fov 35, 512x512, s1=0.08, s2=0.64, p=2,
 termination 0.9999, mode skip-adaptive (the paper's headline mode).
 `--scene radial59` is BASELINE config 2 (1e6 tets).  On the GPU arm a radialN
@@ -120,6 +120,19 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback"
+
+
+def mapped_repo_libs() -> list:
+    """Shared objects of this repository mapped into the process (/proc/self/maps)."""
+    libs = set()
+    try:
+        for line in Path("/proc/self/maps").read_text().splitlines():
+            path = line.split()[-1] if line.split() else ""
+            if path.endswith(".so") and str(ROOT) in path:
+                libs.add(str(Path(path).relative_to(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
 
 
 def cpu_model() -> str:
@@ -339,6 +352,7 @@ def run_reference(args, rank):
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "detail": {"scene_build_s": round(build_s, 2),
                        "render_wall_ms_median": statistics.median(walls),
+                       "repo_libs_mapped": mapped_repo_libs(),
                        "steps_requested": args.steps,
                        "scene": "stock tetray dataclasses around oracle/build.c arrays"
                                 if n >= 128 else "stock tetray Scene.build"}}
@@ -462,14 +476,14 @@ def main(argv=None):
         else:
             fb = None
             for _ in range(max(args.warmup, 3)):
-                dscene._epochs.clear()
+                dscene.mark_epochs_stale()
                 fb, st = B.render(scene, cam, args.mode, par, device=dev)
             per = []
             e2e_steps = max(args.steps, 20)   # wall-clock: more steps for a stable mean
             t0 = time.perf_counter()
             for _ in range(e2e_steps):
                 t1 = time.perf_counter()
-                dscene._epochs.clear()  # force the per-frame metadata upload
+                dscene.mark_epochs_stale()  # every step copies the metadata epoch again
                 fb, st = B.render(scene, cam, args.mode, par, device=dev)
                 per.append(time.perf_counter() - t1)
             dt = time.perf_counter() - t0
@@ -489,9 +503,12 @@ def main(argv=None):
                                f"frame {total_samples}")
 
     if rank == 0 and not args.no_traffic:
-        roof["traffic"], roof["traffic_source"] = ncu_traffic(args)
-        if roof["traffic"]:
-            roof["traffic_per_sample"] = roof["traffic"] / max(my_samples, 1)
+        if world > 1:   # the ncu pass profiles a one-GPU frame: N = 1 lines carry it
+            roof["traffic_source"] = "not measured at N > 1 (see the N = 1 line)"
+        else:
+            roof["traffic"], roof["traffic_source"] = ncu_traffic(args)
+            if roof["traffic"]:
+                roof["traffic_per_sample"] = roof["traffic"] / max(my_samples, 1)
 
     if rank == 0:
         line = {

@@ -399,6 +399,15 @@ int64_t tr_scratch_bytes(int64_t n_rays);
 /* Replaces _kernels.render_frame (K:312-398). stream: cudaStream_t. */
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                     const TrOutputs *out, void *stream);
+/* render()'s whole synchronous frame in one call (R:175-204 around K:312):
+ * zero the counters (out->totals: n_counters i64 = totals, work, per-partition
+ * samples), tr_render_frame, copy the counters to counters_host (page-locked)
+ * and the epoch's inexact word to *inexact_host (when epoch->inexact and
+ * inexact_host are set), synchronize `stream`; *device_ms = the frame's
+ * kernels (CUDA events).  rgba / samples land wherever `out` points. */
+int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrOutputs *out, int64_t n_counters, int64_t *counters_host,
+                   int32_t *inexact_host, void *stream, float *device_ms);
 
 /* ---- Exact record-sharded (KD-brick) rendering ----
  * The partitions are grouped into n_bricks convex bricks (KD subtrees); brick

@@ -166,6 +166,9 @@ _SIGNATURES = [
     ("tr_pow_glibc_available", C.c_int, []),
     ("tr_pow_glibc_host", C.c_double, [C.c_double, C.c_double, C.POINTER(C.c_int32)]),
     ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_render_sync", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),
+                                 C.POINTER(TrOutputs), C.c_int64, C.c_void_p, C.c_void_p,
+                                 C.c_void_p, C.POINTER(C.c_float)]),
     ("tr_render_frame", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch),
                                   C.POINTER(TrFrame), C.POINTER(TrOutputs), C.c_void_p]),
     ("tr_brick_trace", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),

@@ -2540,6 +2540,42 @@ static int prepare_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const
     return TR_OK;
 }
 
+// render()'s synchronous frame in one call (DeviceScene.render): counter
+// reset, the frame's kernels bracketed by events, the counters (and the
+// epoch's inexact word) copied to page-locked memory, stream synchronize.
+int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
+                   const TrOutputs *out, int64_t n_counters, int64_t *counters_host,
+                   int32_t *inexact_host, void *stream, float *device_ms) {
+    if (!out || !out->totals || n_counters < 3 || !counters_host)
+        return tr_fail(TR_EINVAL, "tr_render_sync: invalid arguments");
+    struct Ev { int dev = -1; cudaEvent_t a = nullptr, b = nullptr; };
+    thread_local Ev ev;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "tr_render_sync");
+    if (ev.dev != dev) {
+        if ((e = cudaEventCreate(&ev.a)) != cudaSuccess || (e = cudaEventCreate(&ev.b)) != cudaSuccess)
+            return cuda_fail(e, "tr_render_sync events");
+        ev.dev = dev;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if ((e = cudaMemsetAsync(out->totals, 0, 8 * n_counters, st)) != cudaSuccess ||
+        (e = cudaEventRecord(ev.a, st)) != cudaSuccess)
+        return cuda_fail(e, "tr_render_sync reset");
+    if (int rc = tr_render_frame(scene, epoch, frame, out, stream)) return rc;
+    if ((e = cudaEventRecord(ev.b, st)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(counters_host, out->totals, 8 * n_counters, cudaMemcpyDeviceToHost,
+                             st)) != cudaSuccess)
+        return cuda_fail(e, "tr_render_sync copy");
+    if (inexact_host && epoch->inexact &&
+        (e = cudaMemcpyAsync(inexact_host, epoch->inexact, 4, cudaMemcpyDeviceToHost, st)) != cudaSuccess)
+        return cuda_fail(e, "tr_render_sync copy");
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e, "tr_render_sync sync");
+    if (device_ms && (e = cudaEventElapsedTime(device_ms, ev.a, ev.b)) != cudaSuccess)
+        return cuda_fail(e, "tr_render_sync elapsed");
+    return TR_OK;
+}
+
 int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                     const TrOutputs *out, void *stream) {
     SceneK S;

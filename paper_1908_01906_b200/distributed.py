@@ -286,7 +286,7 @@ def bench_e2e_sharded(scene, camera, mode: str, params, steps: int, device) -> d
     t0 = time.perf_counter()
     fb = st = None
     for _ in range(steps):
-        dscene._epochs.clear()
+        dscene.mark_epochs_stale()   # every step copies the metadata epoch again
         fb, st = render_sharded(scene, camera, mode, params, device=device)
     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dscene.device)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)

@@ -20,7 +20,7 @@ def render():
     def tick(k):
         now = time.perf_counter(); T.setdefault(k, []).append(now - t[0]); t[0] = now
     w, h = cam.width, cam.height
-    dev._epochs.clear(); tick("clear")
+    dev.mark_epochs_stale(); tick("stale")
     with dev.lock, torch.cuda.device(dev.device):
         stream = torch.cuda.current_stream(dev.device)
         meta = sc.meta_state(); tick("stream+meta")

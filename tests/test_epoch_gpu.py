@@ -86,3 +86,19 @@ def test_concurrent_tf_updates_yield_whole_epoch_frames(B, device_meta):
         worker.join(timeout=60)
     assert not errors, errors[0]
     assert len(seen) >= 2   # frames really came from several epochs
+
+
+def test_stale_epoch_reupload_renders_the_same_frame(B):
+    """mark_epochs_stale (bench.py's end-to-end steps): the cached epoch is
+    packed and copied again in place; frames are unchanged."""
+    scene, cam, params, tfs = _setup(B, False)
+    from paper_1908_01906_b200.device import device_scene_for
+    fb0, st0 = B.render(scene, cam, "skip-adaptive", params)
+    dev = device_scene_for(scene)
+    ep = next(iter(dev._epochs.values()))
+    for _ in range(3):
+        dev.mark_epochs_stale()
+        assert ep.stale
+        fb, st = B.render(scene, cam, "skip-adaptive", params)
+        assert not ep.stale and next(iter(dev._epochs.values())) is ep
+        assert np.array_equal(fb.rgba, fb0.rgba) and st.total_samples == st0.total_samples
