@@ -88,6 +88,10 @@ def parse(argv=None):
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-budget-s", type=float, default=900.0,
                     help="reference arm: stop timing whole frames after this many seconds")
+    ap.add_argument("--shard", default="pixels", choices=["pixels", "records"],
+                    help="records: KD-brick record sharding (bricks.py; one brick per rank, "
+                         "or --bricks bricks emulated on one GPU)")
+    ap.add_argument("--bricks", type=int, default=2, help="--shard records on one GPU: bricks")
     ap.add_argument("--flags", type=lambda x: int(x, 0), default=0,
                     help="TR_FLAG_* bits (tuning experiments; bits 8-11 = log2 group size)")
     return ap.parse_args(argv)
@@ -360,6 +364,69 @@ def run_reference(args, rank):
     return 0
 
 
+# ------------------------------------------------- record-sharded GPU arm
+
+def run_records(args, world, rank, local):
+    """--shard records: the frame over KD bricks (bricks.py):
+    one brick per rank (NCCL state exchange per round, no host read between
+    the first n rounds), or args.bricks bricks emulated one after another on
+    one GPU.  value = samples / device time of the trace + rounds (max over
+    ranks); the frame is checked against the one-GPU render() (bit-exact)."""
+    import torch
+    import torch.distributed as dist
+
+    import cases as C
+    import paper_1908_01906_b200 as B
+    from paper_1908_01906_b200 import bricks as BR
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name = public_name(args.scene)
+    t0 = time.perf_counter()
+    scene = C.build_scene(B, name)           # host build: bricks need the mesh arrays
+    cam, par = C.camera(B, name, scale=args.scale), C.params(B, name)
+    n = world if world > 1 else args.bricks
+    br = BR.BrickRenderer(scene, n, max(par.s1, par.s2), device=dev,
+                          dist=dist if world > 1 else None)
+    setup_s = time.perf_counter() - t0
+    for _ in range(args.warmup):
+        br.render(cam, args.mode, par)
+    if world > 1:
+        dist.barrier()
+    ms, st = [], None
+    for _ in range(args.steps):
+        fb, st = br.render(cam, args.mode, par)
+        ms.append(st.device_ms)
+    t = torch.tensor([sum(ms) / 1000.0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    one = B.render(scene, cam, args.mode, par, device=dev) if rank == 0 else None
+    if rank == 0:
+        exact = bool(np.array_equal(one[0].rgba, fb.rgba) and
+                     np.array_equal(one[0].samples, fb.samples) and
+                     one[1].total_samples == st.total_samples)
+        value = st.total_samples * args.steps / float(t[0])
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": float(t[0]) * 1000.0 / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload_config(args, scene.mesh.n_tets, scene.n_partitions,
+                                          st.total_samples),
+                "detail": {"parallelism": f"records: {n} KD bricks over {world} GPU(s)"
+                                          + (" (emulated one after another)" if world == 1 else ""),
+                           "rounds": br.rounds, "tets_per_brick": br.tets_per_brick,
+                           "exact_vs_one_gpu_render": exact,
+                           "one_gpu_frame_ms": one[1].device_ms,
+                           "state_exchange_bytes_per_round": int(cam.width * cam.height * 64)
+                           if world > 1 else 0,
+                           "setup_s": round(setup_s, 2)}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 # ------------------------------------------------------------------ GPU arm
 
 def relaunch_distributed(argv) -> int:
@@ -384,6 +451,8 @@ def main(argv=None):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         return run_reference(args, rank)
+    if args.shard == "records":
+        return run_records(args, world, rank, local)
 
     import torch
     import torch.distributed as dist

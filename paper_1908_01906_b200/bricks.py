@@ -138,7 +138,13 @@ class BrickRenderer:
     max_step: the largest step any frame will use (s2 in skip-adaptive, else
     s1): it sets the halo, so frames with larger steps are refused."""
 
-    def __init__(self, scene, n_bricks: int, max_step: float, device=None, dist=None):
+    def __init__(self, scene, n_bricks: int, max_step: float, device=None, dist=None,
+                 sync_rounds: Optional[bool] = None):
+        """sync_rounds: read the active-ray count back after every round
+        (default for the one-device emulation) or run n_bricks rounds with no
+        host read first (default with `dist`: a ray's runs cross each convex
+        brick at most once, so n rounds finish every ray; one synchronized
+        round then confirms it -- and keeps going if ever needed)."""
         import torch
         self.scene = scene
         self.device = resolve_device(device)
@@ -156,6 +162,7 @@ class BrickRenderer:
                 raise ValueError("one brick per rank: world size must equal n_bricks")
             mine = [dist.get_rank()]
         self.mine = mine
+        self.sync_rounds = (dist is None) if sync_rounds is None else bool(sync_rounds)
         self.devs = {b: DeviceScene(scene, self.device, tet_subset=subsets[b]) for b in mine}
         d = self.device
         self.t_owner = torch.from_numpy(self.bricks.owner.copy()).to(d)
@@ -223,6 +230,21 @@ class BrickRenderer:
             _lib.check(L.tr_brick_trace(C.byref(dev0.desc), C.byref(ep.desc), C.byref(frame),
                                         C.byref(B), C.byref(out), s), "tr_brick_trace")
             rounds = 0
+            if profile and not self.sync_rounds:
+                ev.append((-1, -1, None, mark()))   # end of the trace
+            if not self.sync_rounds:
+                for _ in range(self.bricks.n):   # no host reads between these rounds
+                    for b in self.mine:
+                        B.rank = b
+                        e0 = mark() if profile else None
+                        _lib.check(L.tr_brick_round(C.byref(self.devs[b].desc), C.byref(ep.desc),
+                                                    C.byref(frame), C.byref(B), C.byref(out), s),
+                                   "tr_brick_round")
+                        if profile:
+                            ev.append((rounds, b, e0, mark()))
+                    rounds += 1
+                    if self.dist is not None:
+                        self.dist.all_reduce(state.view(torch.int64))
             while True:
                 active = None
                 if profile:

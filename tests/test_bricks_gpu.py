@@ -46,6 +46,18 @@ def test_bricks_equal_single_device(B, recipe, n_bricks):
         assert br.rounds >= 1
 
 
+@pytest.mark.parametrize("recipe,n_bricks", [("radial16", 4), ("a6fog", 3), ("sinus", 5)])
+def test_bricks_unsynchronized_rounds_equal_single_device(B, recipe, n_bricks):
+    """n_bricks rounds with no host read in between (the multi-rank default),
+    then the synchronized check round: the same frame."""
+    sc = cases.build_scene(B, recipe)
+    cam, par = cases.camera(B, recipe), cases.params(B, recipe)
+    br = BR.BrickRenderer(sc, n_bricks, max(par.s1, par.s2), sync_rounds=False)
+    for mode in ("reference", "skip", "skip-adaptive"):
+        _same(B.render(sc, cam, mode, par), br.render(cam, mode, par), mode != "reference")
+        assert br.rounds == n_bricks   # the check round found no active ray
+
+
 def test_bricks_radial59(B):
     """BASELINE config 2 scene split into 8 bricks; each brick holds a
     fraction of the tets."""
