@@ -14,6 +14,14 @@
 // (_glibc_pow.py -> glibc_pow_data.h).  Verified bit for bit against the live
 // libm on millions of arguments (tests/test_glibc_pow.py).
 //
+// Attribution and licence: the algorithm and its tables are the ARM
+// optimized-routines pow (Copyright (c) 2018-2023, Arm Limited; MIT OR
+// Apache-2.0 WITH LLVM-exception) as shipped in the GNU C Library 2.39
+// (sysdeps/ieee754/dbl-64/e_pow.c, e_pow_log_data.c, e_exp_data.c; LGPL-2.1+
+// in glibc).  No source file is copied: this is a restatement of the
+// instruction sequence, and the table values are extracted from the
+// installed libm at build time, not stored in this repository.
+//
 // Scope: the main path, i.e. x a positive normal double and 0x3be <=
 // top12(|y|) < 0x43e (|y| in [2^-65, 2^63)).  Callers handle x == 0 and x,
 // y outside that domain (tr_pow_glibc_supported()).  In the exp stage,
