@@ -1547,6 +1547,10 @@ __device__ bool inline_next(const SceneK &S, const EpochK &E, const TrFrame &fr,
 // exclusive box, else the full descent -- both exact), field
 // (K:149-153), TF (K:74-90) and opacity correction (K:27).  Returns
 // (ca, r, g, b); found = inside a tet (ca = c = 0 otherwise).
+#ifndef TR_RASTER_PX
+#define TR_RASTER_PX 262144   // A/B knob: band pixels per candidate-raster warp of a partition
+#endif
+
 __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E, const TrFrame &fr,
                                                 double ox, double oy, double oz, double dx,
                                                 double dy, double dz, double a, int64_t k,
@@ -2484,7 +2488,7 @@ static cudaError_t launch_cand_raster(const SceneK &S, const EpochK &E, const Fr
     // warps per partition rectangle ~ pixels of the chunk's band / 256K (1 at
     // 512^2; rectangles grow with the frame, so large frames spread wider)
     const int64_t rows = (F.n_rays / 32 + F.tiles_x - 1) / F.tiles_x * TILE_H;
-    G.raster_sub = (int32_t)std::min<int64_t>(std::max<int64_t>(F.f.width * rows / 262144, 1), 64);
+    G.raster_sub = (int32_t)std::min<int64_t>(std::max<int64_t>(F.f.width * rows / TR_RASTER_PX, 1), 64);
     int64_t grid = (F.n_parts * G.raster_sub + 7) / 8;
     if (grid > (int64_t)sm_count() * 8) grid = (int64_t)sm_count() * 8;
     if (grid < 1) grid = 1;
