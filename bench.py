@@ -378,10 +378,7 @@ def run_records(args, world, rank, local):
     import cases as C
     import paper_1908_01906_b200 as B
     from paper_1908_01906_b200 import bricks as BR
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dev = dist_setup(local, world)
     name = public_name(args.scene)
     t0 = time.perf_counter()
     scene = C.build_scene(B, name)           # host build: bricks need the mesh arrays
@@ -429,6 +426,24 @@ def run_records(args, world, rank, local):
 
 # ------------------------------------------------------------------ GPU arm
 
+def dist_setup(local: int, world: int):
+    """The rank's device and process group.  TETRAY_DIST_BACKEND=gloo with
+    TETRAY_ONE_DEVICE=1 runs every rank on cuda:0 (tests of the N > 1 path on
+    a one-GPU box: NCCL refuses two ranks on one device)."""
+    import torch
+    import torch.distributed as dist
+    one = os.environ.get("TETRAY_ONE_DEVICE") == "1"
+    dev = torch.device("cuda", 0 if one else local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        backend = os.environ.get("TETRAY_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    return dev
+
+
 def relaunch_distributed(argv) -> int:
     """`--gpus N` without a torchrun environment: run N ranks of this script."""
     args = parse(argv)
@@ -461,12 +476,8 @@ def main(argv=None):
     from paper_1908_01906_b200 import distributed as D
     from paper_1908_01906_b200.device import device_scene_for
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    nranks = 1
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-        nranks = dist.get_world_size()
+    dev = dist_setup(local, world)
+    nranks = dist.get_world_size() if world > 1 else 1
 
     scene, cam, par, build_s = build_gpu_workload(B, args)
     t0 = time.perf_counter()
@@ -494,7 +505,7 @@ def main(argv=None):
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with Clocks(local) as clk:
+    with Clocks(dev.index) as clk:
         time.sleep(0.25)
         for k in range(args.steps):
             flush.fill_(k & 0xFF)
