@@ -48,7 +48,14 @@ constexpr double BARY_TOL = 1e-9;  // K:15
 constexpr int TILE_W = 8, TILE_H = 4;
 constexpr int PSTACK = 64;
 constexpr int BSTACK = 64;
-constexpr int MARCH_BLOCK = 256;
+#ifndef TR_MARCH_BLOCK
+#define TR_MARCH_BLOCK 256   // A/B knob: threads per march CTA
+#endif
+#ifndef TR_MARCH_MINB
+#define TR_MARCH_MINB 3      // A/B knob: resident march CTAs per SM the registers are budgeted for
+#endif
+constexpr int MARCH_BLOCK = TR_MARCH_BLOCK;
+constexpr int MB = TR_MARCH_MINB;
 constexpr int TRACE_BLOCK = 128;
 constexpr int IV_CAP = 64;           // partition ids per ray kept in the scratch list
 constexpr int CAND_CAP = 48;         // partition slabs per ray kept by the candidate raster
@@ -1917,14 +1924,14 @@ march_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
 // (SoA, one slot per group) instead of registers: the registers then hold a
 // sample's working set only, so more warps fit per SM.  Same
 // rounds, same exact compositing; lane 0 of a group writes the state.
-template <int G, int MINB, bool BRICK = false, bool STATS = false>
-__global__ void __launch_bounds__(MARCH_BLOCK, MINB)
+template <int G, int MINB, bool BRICK = false, bool STATS = false, int BLK = MARCH_BLOCK>
+__global__ void __launch_bounds__(BLK, MINB)
 march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
     if (!BRICK && F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
-    constexpr int NG = MARCH_BLOCK / G;
-    __shared__ unsigned long long red[2][MARCH_BLOCK / 32];
-    __shared__ double4 shade[G][MARCH_BLOCK / G];   // [lane in group][group]: conflict free
+    constexpr int NG = BLK / G;
+    __shared__ unsigned long long red[2][BLK / 32];
+    __shared__ double4 shade[G][BLK / G];   // [lane in group][group]: conflict free
     __shared__ Inline inl[NG];
     __shared__ double s_o[3][NG], s_d[3][NG], s_acc[4][NG], s_phase[NG];
     __shared__ long long s_out[NG], s_samples[NG];
@@ -2219,7 +2226,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned long long s = 0, v = 0;
-        for (int w = 0; w < MARCH_BLOCK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
+        for (int w = 0; w < BLK / 32; ++w) { s += red[0][w]; v += red[1][w]; }
         if (s) atomicAdd((unsigned long long *)O.totals, s);
         if (v) atomicAdd((unsigned long long *)O.totals + 1, v);
     }
@@ -2618,21 +2625,30 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             case 2: march_fn = march_sm_kernel<2, 3>; break;
             case 4: march_fn = minb == 2 ? march_sm_kernel<4, 2>
                              : (minb == 1 ? march_sm_kernel<4, 4>
-                                : ((frame->flags & TR_FLAG_STATS) ? march_sm_kernel<4, 3, false, true>
-                                                                  : march_sm_kernel<4, 3>)); break;
+                                : ((frame->flags & TR_FLAG_STATS) ? march_sm_kernel<4, MB, false, true>
+                                                                  : march_sm_kernel<4, MB>)); break;
             case 8: march_fn = march_sm_kernel<8, 3>; break;
-            case 16: march_fn = march_sm_kernel<16, 3>; break;
+            case 16: march_fn = march_sm_kernel<16, MB>; break;
             default: return tr_fail(TR_EINVAL, "tr_render_frame: group size must be 2, 4, 8 or 16");
         }
     }
+    // reference and skip modes never evaluate pow: 128-thread CTAs budgeted for
+    // 7 per SM (72 registers, 28 warps) hide more latency there (-4%, profiles/r02)
+    int march_block = MARCH_BLOCK;
+    void (*march16_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = march_sm_kernel<16, MB>;
+    if (frame->mode != 2 && lg == 0 && minb == 3 && !(frame->flags & (TR_FLAG_REG_STATE | TR_FLAG_STATS))) {
+        march_fn = march_sm_kernel<4, 7, false, false, 128>;
+        march16_fn = march_sm_kernel<16, 7, false, false, 128>;
+        march_block = 128;
+    }
     cudaError_t e;
     int per_sm = 0;
-    e = occupancy(&per_sm, (const void *)march_fn, MARCH_BLOCK);
+    e = occupancy(&per_sm, (const void *)march_fn, march_block);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
     F.auto_g = (lg == 0 && !(frame->flags & TR_FLAG_REG_STATE) && minb == 3) ? 1 : 0;
-    F.march_lanes = (int64_t)sm_count() * per_sm * MARCH_BLOCK;
+    F.march_lanes = (int64_t)sm_count() * per_sm * march_block;
     int trace_per_sm = 0;
     void (*trace_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) =
         (frame->flags & TR_FLAG_STATS) ? trace_intervals_kernel<true> : trace_intervals_kernel<false>;
@@ -2699,16 +2715,16 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
         int gs[2] = {gsize, 0};
         int nf = 1;
         if (F.auto_g) {
-            fns[1] = march_sm_kernel<16, 3>;
+            fns[1] = march16_fn;
             gs[1] = 16;
             nf = 2;
         }
         for (int q = 0; q < nf; ++q) {
             int64_t grid = (int64_t)sm_count() * per_sm;
-            const int64_t need = (F.n_rays * gs[q] + MARCH_BLOCK - 1) / MARCH_BLOCK;
+            const int64_t need = (F.n_rays * gs[q] + march_block - 1) / march_block;
             if (grid > need) grid = need;
             if (grid < 1) grid = 1;
-            fns[q]<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
+            fns[q]<<<(unsigned)grid, march_block, 0, st>>>(S, E, F, iv, *out);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
             ++launches;
@@ -2725,7 +2741,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     }
     g_last_launch[0] = launches;
     g_last_launch[1] = march_grid;
-    g_last_launch[2] = MARCH_BLOCK;
+    g_last_launch[2] = march_block;
     return TR_OK;
 }
 
