@@ -225,3 +225,38 @@ def test_leaves_over_eight_tets_get_no_table(B):
     m = B.generate_synthetic(2, "radial", B.Centering.VERTEX)
     leaves, _ = leaf_tables(B, m.vertices, m.tets, [list(range(10))])
     assert int(leaves[0]["walk"][4]) == 0
+
+
+def test_walk_equals_scan_on_delaunay_leaves(B):
+    """Random Delaunay tetrahedralizations (scipy): conforming but irregular
+    meshes with slivers; leaves = 8 consecutive tets along a Morton-like sort
+    of their centroids.  The walk (with and without the predictor) must
+    return the lowest-index accepting tet for points in and around every
+    leaf's tets, including points on shared faces, edges and vertices."""
+    from scipy.spatial import Delaunay
+    rng = np.random.default_rng(17)
+    for trial in range(3):
+        pts = rng.uniform(0.0, 4.0, (120, 3))
+        tri = Delaunay(pts)
+        tets = tri.simplices.astype(np.int64)
+        p = pts[tets]
+        e = np.stack([p[:, 1] - p[:, 0], p[:, 2] - p[:, 0], p[:, 3] - p[:, 0]], axis=-1)
+        vol = np.abs(np.linalg.det(e))
+        keep = vol > 1e-6                       # the reference rejects degenerate tets
+        tets = tets[keep]
+        cen = pts[tets].mean(axis=1)
+        order = np.lexsort((cen[:, 2], cen[:, 1], np.floor(cen[:, 0])))
+        leaf_sets = [sorted(order[k:k + 8].tolist()) for k in range(0, len(order), 8)]
+        leaves, _, preds = leaf_tables(B, pts, tets, leaf_sets, with_pred=True)
+        inv_all, orig_all = inverses(pts, tets)
+        for lf, pr, ids in zip(leaves, preds, leaf_sets):
+            ids = np.array(ids)
+            pv = pts[tets[ids]]
+            lam = rng.dirichlet(np.ones(4), size=(len(ids), 10))
+            q = np.einsum("nkv,nva->nka", lam, pv).reshape(-1, 3)
+            faces = pv[:, :3].mean(axis=1)             # on a face
+            edges = 0.5 * (pv[:, 0] + pv[:, 1])         # on an edge
+            verts = pv[:, 3]                            # a vertex
+            out = q + rng.normal(0.0, 0.05, q.shape)    # near the leaf, maybe outside it
+            allp = np.concatenate([q, faces, edges, verts, out])
+            _check_points(inv_all[ids], orig_all[ids], ids, lf["walk"], allp, pr, lf["ex_lo"])
