@@ -123,14 +123,15 @@ class ShardedFrame:
     image layout with no collective."""
 
     def __init__(self, dscene, scene, camera, mode_id: int, params, *, track: bool, rank: int = 0,
-                 world: int = 1, flags: int = 0, jitter: bool = False):
+                 world: int = 1, flags: int = 0, jitter: bool = False, compact=None):
         import torch
         self.torch = torch
         self.dscene = dscene
         self.scene, self.camera, self.params = scene, camera, params
         self.world, self.rank = world, rank
         self.w, self.h = int(camera.width), int(camera.height)
-        self.compact = world > 1
+        # compact tile slots + the gather / reduce (default: world > 1)
+        self.compact = (world > 1) if compact is None else bool(compact)
         self.slots = slots_per_rank(self.w, self.h, world) if self.compact else 0
         self.epoch = dscene.epoch(scene.meta_state(), params)
         self.frame = dscene.frame_desc(scene, camera, mode_id, params, jitter, track, flags,
@@ -239,7 +240,7 @@ def render_sharded(scene, camera, mode: str, params, *, jitter: bool = False,
     runner = _FRAMES.get(key)
     if runner is None or runner.scene is not scene:
         runner = ShardedFrame(dscene, scene, camera, _MODE_IDS[mode], params, track=track,
-                              rank=rank, world=world, flags=flags, jitter=jitter)
+                              rank=rank, world=world, flags=flags, jitter=jitter, compact=True)
         _FRAMES.clear()
         _FRAMES[key] = runner
     runner.camera, runner.params = camera, params
