@@ -329,6 +329,24 @@ int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8_t *active,
                     void *host_buf, void *dev_buf, int64_t buf_bytes, TrEpoch *out,
                     int64_t *h2d_bytes, void *stream);
 
+/* tr_epoch_upload's arguments as one struct (a binding builds it once per
+ * epoch and re-uploads with a single call: tr_epoch_upload_s, or inside
+ * tr_render_sync). */
+typedef struct TrEpochUpload {
+    int64_t n_parts;
+    const double *sigma;
+    const uint8_t *active, *bnode_active, *knode_active;
+    int64_t n_bnodes, n_knodes;
+    const double *tf_table;
+    int64_t n_tf;
+    double tf_lo, tf_hi, s1, s2, p;
+    int32_t steps_on_device;
+    int32_t pad0;
+    void *host_buf, *dev_buf;
+    int64_t buf_bytes;
+} TrEpochUpload;
+int tr_epoch_upload_s(const TrEpochUpload *u, TrEpoch *out, int64_t *h2d_bytes, void *stream);
+
 /* Frame parameters: render_frame's scalars (K:313-316, R:183-188). */
 typedef struct TrFrame {
     double cam_pos[3], cam_right[3], cam_up[3], cam_fwd[3];
@@ -407,7 +425,10 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
  * kernels (CUDA events).  rgba / samples land wherever `out` points. */
 int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                    const TrOutputs *out, int64_t n_counters, int64_t *counters_host,
-                   int32_t *inexact_host, void *stream, float *device_ms);
+                   int32_t *inexact_host, void *stream, float *device_ms,
+                   const TrEpochUpload *reupload);
+/* reupload (may be NULL): copy the epoch again first (tr_epoch_upload_s into
+ * the same buffers, so `epoch` stays valid). */
 
 /* ---- Exact record-sharded (KD-brick) rendering ----
  * The partitions are grouped into n_bricks convex bricks (KD subtrees); brick

@@ -57,6 +57,17 @@ class TrEpoch(C.Structure):
     ]
 
 
+class TrEpochUpload(C.Structure):
+    _fields_ = [
+        ("n_parts", C.c_int64), ("sigma", C.c_void_p), ("active", C.c_void_p),
+        ("bnode_active", C.c_void_p), ("knode_active", C.c_void_p), ("n_bnodes", C.c_int64),
+        ("n_knodes", C.c_int64), ("tf_table", C.c_void_p), ("n_tf", C.c_int64),
+        ("tf_lo", C.c_double), ("tf_hi", C.c_double), ("s1", C.c_double), ("s2", C.c_double),
+        ("p", C.c_double), ("steps_on_device", C.c_int32), ("pad0", C.c_int32),
+        ("host_buf", C.c_void_p), ("dev_buf", C.c_void_p), ("buf_bytes", C.c_int64),
+    ]
+
+
 class TrFrame(C.Structure):
     _fields_ = [
         ("cam_pos", C.c_double * 3), ("cam_right", C.c_double * 3),
@@ -168,7 +179,9 @@ _SIGNATURES = [
     ("tr_pow_glibc_batch", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_render_sync", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),
                                  C.POINTER(TrOutputs), C.c_int64, C.c_void_p, C.c_void_p,
-                                 C.c_void_p, C.POINTER(C.c_float)]),
+                                 C.c_void_p, C.POINTER(C.c_float), C.c_void_p]),
+    ("tr_epoch_upload_s", C.c_int, [C.POINTER(TrEpochUpload), C.POINTER(TrEpoch),
+                                    C.POINTER(C.c_int64), C.c_void_p]),
     ("tr_render_frame", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch),
                                   C.POINTER(TrFrame), C.POINTER(TrOutputs), C.c_void_p]),
     ("tr_brick_trace", C.c_int, [C.POINTER(TrDeviceScene), C.POINTER(TrEpoch), C.POINTER(TrFrame),

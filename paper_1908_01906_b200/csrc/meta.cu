@@ -332,3 +332,12 @@ extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8
     out->inexact = steps_on_device ? inexact : nullptr;
     return TR_OK;
 }
+
+extern "C" int tr_epoch_upload_s(const TrEpochUpload *u, TrEpoch *out, int64_t *h2d_bytes,
+                                 void *stream) {
+    if (!u) return tr_fail(TR_EINVAL, "tr_epoch_upload_s: invalid arguments");
+    return tr_epoch_upload(u->n_parts, u->sigma, u->active, u->bnode_active, u->n_bnodes,
+                           u->knode_active, u->n_knodes, u->tf_table, u->n_tf, u->tf_lo, u->tf_hi,
+                           u->s1, u->s2, u->p, u->steps_on_device, u->host_buf, u->dev_buf,
+                           u->buf_bytes, out, h2d_bytes, stream);
+}

@@ -2556,7 +2556,8 @@ static int prepare_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const
 // epoch's inexact word) copied to page-locked memory, stream synchronize.
 int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFrame *frame,
                    const TrOutputs *out, int64_t n_counters, int64_t *counters_host,
-                   int32_t *inexact_host, void *stream, float *device_ms) {
+                   int32_t *inexact_host, void *stream, float *device_ms,
+                   const TrEpochUpload *reupload) {
     if (!out || !out->totals || n_counters < 3 || !counters_host)
         return tr_fail(TR_EINVAL, "tr_render_sync: invalid arguments");
     struct Ev { int dev = -1; cudaEvent_t a = nullptr, b = nullptr; };
@@ -2570,6 +2571,10 @@ int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
         ev.dev = dev;
     }
     cudaStream_t st = (cudaStream_t)stream;
+    if (reupload) {   // the same buffers: `epoch` stays valid
+        TrEpoch again;
+        if (int rc = tr_epoch_upload_s(reupload, &again, nullptr, stream)) return rc;
+    }
     if ((e = cudaMemsetAsync(out->totals, 0, 8 * n_counters, st)) != cudaSuccess ||
         (e = cudaEventRecord(ev.a, st)) != cudaSuccess)
         return cuda_fail(e, "tr_render_sync reset");

@@ -244,8 +244,16 @@ class Epoch:
         # |min(sigma, 1) - 1| ** p is on the restated glibc pow's path
         self._step_dev = _steps_on_device(sig, pw)
         self.desc = _lib.TrEpoch()
-        self._args = (P, sig, act, bact, dev.n_bnodes, kact, dev.n_knodes, table, s1, s2, pw)
+        self._keep = (sig, act, bact, kact, table)   # the arrays `up` points at
+        self.up = _lib.TrEpochUpload(
+            n_parts=P, sigma=sig.ctypes.data, active=act.ctypes.data,
+            bnode_active=bact.ctypes.data, knode_active=kact.ctypes.data,
+            n_bnodes=dev.n_bnodes, n_knodes=dev.n_knodes, tf_table=table.ctypes.data,
+            n_tf=self.n_tf, tf_lo=self.tf_lo, tf_hi=self.tf_hi, s1=s1, s2=s2, p=pw,
+            steps_on_device=1 if self._step_dev else 0, host_buf=self.host.data_ptr(),
+            dev_buf=self.buf.data_ptr(), buf_bytes=nbytes)
         self._dev = dev
+        self._P = P
         self.stale = False
         self._uploaded = torch.cuda.Event()   # recorded after each copy out of `host`
         self._recorded = False
@@ -253,26 +261,19 @@ class Epoch:
 
     def upload(self, stream=None, hold: bool = True) -> None:
         """Pack the epoch's host arrays into the page-locked staging buffer and
-        copy them to the device (tr_epoch_upload); device steps recomputed.
+        copy them to the device (tr_epoch_upload_s); device steps recomputed.
         A re-upload (a stale epoch: a caller asked for the copy again) first
         waits for the previous copy out of the staging buffer."""
         torch = _torch()
-        L = _lib.lib()
         dev = self._dev
         if stream is None:
             stream = torch.cuda.current_stream(dev.device)
         if self._recorded:
             self._uploaded.synchronize()
-        P, sig, act, bact, n_b, kact, n_k, table, s1, s2, pw = self._args
         h2d = C.c_int64(0)
-        _lib.check(L.tr_epoch_upload(
-            P, sig.ctypes.data, act.ctypes.data, bact.ctypes.data, n_b, kact.ctypes.data, n_k,
-            table.ctypes.data, self.n_tf, self.tf_lo, self.tf_hi, s1, s2, pw,
-            1 if self._step_dev else 0, self.host.data_ptr(), self.buf.data_ptr(),
-            self.host.numel(), C.byref(self.desc), C.byref(h2d), stream.cuda_stream),
-            "tr_epoch_upload")
+        _lib.check(_lib.lib().tr_epoch_upload_s(C.byref(self.up), C.byref(self.desc), C.byref(h2d),
+                                                stream.cuda_stream), "tr_epoch_upload_s")
         self.h2d_bytes = int(h2d.value)
-        self._P = P
         self.stale = False
         # device steps: the first frame reads back the epoch's inexact word
         self.verified = not self.desc.inexact
@@ -538,7 +539,11 @@ class DeviceScene:
         self._act_key, self._act_val = key, (kact, bact)
         return kact, bact
 
-    def epoch(self, meta_state, params, stream=None, hold: bool = True) -> Epoch:
+    def epoch(self, meta_state, params, stream=None, hold: bool = True,
+              defer_stale: bool = False) -> Epoch:
+        """The cached epoch of meta_state (uploaded on first use).  A stale
+        cached epoch is copied again here, or -- defer_stale -- left stale for
+        the caller to re-upload inside its frame call (render())."""
         key = (id(meta_state), float(params.s1), float(params.s2), float(params.p))
         ep = self._epochs.get(key)
         if ep is None or ep.meta_state is not meta_state:
@@ -547,7 +552,7 @@ class DeviceScene:
             while len(self._epochs) > 8:
                 self._epochs.popitem(last=False)
         else:
-            if ep.stale:
+            if ep.stale and not defer_stale:
                 ep.upload(stream, hold)
             self._epochs.move_to_end(key)
         return ep
@@ -628,12 +633,17 @@ class DeviceScene:
             t0 = time.perf_counter()
             stream = torch.cuda.current_stream(self.device)
             meta = scene.meta_state()
-            ep = self.epoch(meta, params, stream, hold=False)   # synchronized below
+            ep = self.epoch(meta, params, stream, hold=False, defer_stale=True)   # synchronized below
             frame = self.frame_desc(scene, camera, mode, params, jitter, track, flags)
             fb = self.frame_buffers(w, h)
-            rgba_h = torch.empty((h, w, 4), dtype=torch.float64, pin_memory=True)
-            samp_h = torch.empty((h, w), dtype=torch.int64, pin_memory=True)
-            cnt_h = torch.empty(4 + self.n_parts, dtype=torch.int64, pin_memory=True)
+            # one page-locked block: rgba | samples | counters (+ inexact word)
+            npx = h * w
+            blk = torch.empty(8 * (5 * npx + 4 + self.n_parts), dtype=torch.uint8, pin_memory=True)
+            rgba_h = blk[:32 * npx].view(torch.float64).view(h, w, 4)
+            samp_h = blk[32 * npx:40 * npx].view(torch.int64).view(h, w)
+            cnt_h = blk[40 * npx:].view(torch.int64)
+            if ep._recorded:
+                ep._uploaded.synchronize()   # a staging-buffer copy of its own upload()
             out = fb.outputs()
             if DIRECT_HOST_OUTPUTS:
                 # the kernels store each finished pixel straight into the
@@ -646,12 +656,15 @@ class DeviceScene:
                 cnt_h[-1] = 0
                 inexact = cnt_h.data_ptr() + 8 * (3 + self.n_parts)
             dms = C.c_float(0.0)
-            # counters reset, the frame, counters (+ inexact word) D2H, sync: one call
+            reup = C.byref(ep.up) if ep.stale else None
+            # (stale epoch re-upload,) counters reset, the frame, counters (+ inexact
+            # word) D2H, sync: one call
             _lib.check(_lib.lib().tr_render_sync(C.byref(self.desc), C.byref(ep.desc),
                                                  C.byref(frame), C.byref(out),
                                                  3 + self.n_parts, cnt_h.data_ptr(), inexact,
-                                                 stream.cuda_stream, C.byref(dms)),
+                                                 stream.cuda_stream, C.byref(dms), reup),
                        "tr_render_sync")
+            ep.stale = False
             if not DIRECT_HOST_OUTPUTS:
                 rgba_h.view(-1, 4).copy_(fb.rgba)
                 samp_h.view(-1).copy_(fb.samples)
