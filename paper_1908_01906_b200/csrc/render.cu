@@ -1928,7 +1928,7 @@ template <int G, int MINB, bool BRICK = false, bool STATS = false, int BLK = MAR
 __global__ void __launch_bounds__(BLK, MINB)
 march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     static_assert(G >= 2 && G <= 32 && (32 % G) == 0, "group size");
-    if (!BRICK && F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
+    if (F.auto_g && *(volatile const uint32_t *)iv.gsel != (uint32_t)G) return;   // not the chosen width
     constexpr int NG = BLK / G;
     __shared__ unsigned long long red[2][BLK / 32];
     __shared__ double4 shade[G][BLK / G];   // [lane in group][group]: conflict free
@@ -2400,6 +2400,7 @@ __global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
     for (int64_t r0 = blockIdx.x * (int64_t)blockDim.x; r0 < F.n_rays; r0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t rr = r0 + threadIdx.x;
         bool act = false, mine = false;
+        uint32_t bucket = 0;
         TrRayState st = {};
         if (rr < F.n_rays) {
             st = F.B_state[rr];
@@ -2427,6 +2428,7 @@ __global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
                 st.cbefore = c0;
                 st.stop = cend;
                 F.B_state[rr] = st;
+                bucket = cost_bucket((double)(cend - st.taken));
             }
         }
         if (rr < F.n_rays && !mine && F.B_zero_foreign) {
@@ -2438,7 +2440,57 @@ __global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
         unsigned base = 0;
         if (lane == 0 && mm) base = atomicAdd(F.B_ctr, (unsigned)__popc(mm));
         base = __shfl_sync(FULL, base, 0);
-        if (mine) F.B_queue[base + __popc(mm & ((1u << lane) - 1u))] = (uint32_t)rr;
+        unsigned long long run = mine ? (unsigned long long)(st.stop - st.taken) : 0ull, run_max = run;
+        for (int o = 16; o; o >>= 1) {
+            run += __shfl_xor_sync(FULL, run, o);
+            const unsigned long long m = __shfl_xor_sync(FULL, run_max, o);
+            run_max = m > run_max ? m : run_max;
+        }
+        if (lane == 0 && mm) {   // this round's work and longest run: the lane width
+            atomicAdd(iv.ray_stats, run);
+            atomicMax(iv.ray_stats + 1, run_max);
+        }
+        if (mine) {   // unsorted; brick_order_kernel sorts the runs longest first
+            iv.order[base + __popc(mm & ((1u << lane) - 1u))] = (uint32_t)rr;
+            const unsigned peers = __match_any_sync(mm, bucket);
+            if (lane == __ffs(peers) - 1) atomicAdd(iv.hist + bucket, (unsigned)__popc(peers));
+        }
+    }
+}
+
+// This round's queue in descending run-length buckets (the one-device
+// march's longest-first order, order_rays_kernel, applied to the runs): a
+// round ends with its longest run, so starting the long runs first shortens
+// the round's tail.  Order inside a bucket is arbitrary; outputs do not
+// depend on it.
+__global__ void __launch_bounds__(256) brick_order_kernel(FrameK F, IvBuf iv) {
+    __shared__ uint32_t start[N_BUCKETS];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // order_rays_kernel's lane-width rule on the runs
+        const unsigned long long sum = iv.ray_stats[0], mx = iv.ray_stats[1];
+        *iv.gsel = (mx * (unsigned long long)F.march_lanes <= 4ull * sum) ? 4u : 16u;
+    }
+    if (threadIdx.x < N_BUCKETS) {
+        uint32_t s = 0;
+        for (int b = N_BUCKETS - 1; b > (int)threadIdx.x; --b) s += iv.hist[b];
+        start[threadIdx.x] = s;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const uint32_t n = *F.B_ctr;
+    for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x; e0 < n; e0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = e0 + threadIdx.x;
+        const bool valid = e < n;
+        const unsigned vm = __ballot_sync(FULL, valid);
+        if (!valid) continue;
+        const uint32_t rr = iv.order[e];
+        const TrRayState &st = F.B_state[rr];
+        const uint32_t bucket = cost_bucket((double)(st.stop - st.taken));
+        const unsigned peers = __match_any_sync(vm, bucket);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(iv.cursor + bucket, (unsigned)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        F.B_queue[start[bucket] + base + __popc(peers & ((1u << lane) - 1u))] = rr;
     }
 }
 
@@ -2908,6 +2960,7 @@ int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e;
     if ((e = cudaMemsetAsync(bricks->counters, 0, 8, st)) != cudaSuccess ||
+        (e = cudaMemsetAsync(iv.hist, 0, 552, st)) != cudaSuccess ||   // hist .. gsel
         (e = cudaMemsetAsync(out->work, 0, sizeof(uint32_t), st)) != cudaSuccess)
         return cuda_fail(e, "tr_brick_round memset");
     if (F.n_rays == 0) return TR_OK;
@@ -2915,18 +2968,28 @@ int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
     if (pg > (int64_t)sm_count() * 8) pg = (int64_t)sm_count() * 8;
     brick_plan_kernel<<<(unsigned)pg, 256, 0, st>>>(F, iv);
     if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "brick_plan_kernel launch");
-    void (*march_fn)(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = march_sm_kernel<4, 3, true>;
+    // lanes per ray as in tr_render_frame (4, or 16 when the round's
+    // longest run would set its time): both widths launch, one returns
+    void (*fns[2])(SceneK, EpochK, FrameK, IvBuf, TrOutputs) = {march_sm_kernel<4, 3, true>,
+                                                                march_sm_kernel<16, 3, true>};
+    const int gs[2] = {4, 16};
     int per_sm = 0;
-    if ((e = occupancy(&per_sm, (const void *)march_fn, MARCH_BLOCK)) != cudaSuccess)
+    if ((e = occupancy(&per_sm, (const void *)fns[0], MARCH_BLOCK)) != cudaSuccess)
         return cuda_fail(e, "occupancy(march)");
     if (per_sm < 1) per_sm = 1;
-    int64_t grid = (int64_t)sm_count() * per_sm;
-    const int64_t need = (F.n_rays * 4 + MARCH_BLOCK - 1) / MARCH_BLOCK;
-    if (grid > need) grid = need;
-    if (grid < 1) grid = 1;
-    march_fn<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
-    e = cudaGetLastError();
-    return e == cudaSuccess ? TR_OK : cuda_fail(e, "march_sm_kernel launch (bricks)");
+    F.auto_g = 1;
+    F.march_lanes = (int64_t)sm_count() * per_sm * MARCH_BLOCK;
+    brick_order_kernel<<<(unsigned)pg, 256, 0, st>>>(F, iv);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "brick_order_kernel launch");
+    for (int q = 0; q < 2; ++q) {
+        int64_t grid = (int64_t)sm_count() * per_sm;
+        const int64_t need = (F.n_rays * gs[q] + MARCH_BLOCK - 1) / MARCH_BLOCK;
+        if (grid > need) grid = need;
+        if (grid < 1) grid = 1;
+        fns[q]<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "march_sm_kernel launch (bricks)");
+    }
+    return TR_OK;
 }
 
 }  // extern "C"
