@@ -341,7 +341,11 @@ typedef struct TrEpochUpload {
     int64_t n_tf;
     double tf_lo, tf_hi, s1, s2, p;
     int32_t steps_on_device;
-    int32_t pad0;
+    int32_t packed;            /* host_buf already holds this epoch's sections (an
+                                  earlier call packed them; the arrays are immutable):
+                                  re-upload without packing -- with steps_on_device,
+                                  ONE kernel reads the page-locked block over PCIe
+                                  and writes the sections and the steps */
     void *host_buf, *dev_buf;
     int64_t buf_bytes;
 } TrEpochUpload;

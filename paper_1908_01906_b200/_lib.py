@@ -63,7 +63,7 @@ class TrEpochUpload(C.Structure):
         ("bnode_active", C.c_void_p), ("knode_active", C.c_void_p), ("n_bnodes", C.c_int64),
         ("n_knodes", C.c_int64), ("tf_table", C.c_void_p), ("n_tf", C.c_int64),
         ("tf_lo", C.c_double), ("tf_hi", C.c_double), ("s1", C.c_double), ("s2", C.c_double),
-        ("p", C.c_double), ("steps_on_device", C.c_int32), ("pad0", C.c_int32),
+        ("p", C.c_double), ("steps_on_device", C.c_int32), ("packed", C.c_int32),
         ("host_buf", C.c_void_p), ("dev_buf", C.c_void_p), ("buf_bytes", C.c_int64),
     ]
 

@@ -37,10 +37,11 @@ __device__ const __align__(32) unsigned long long d_etab[] = TR_POW_EXP_TAB_INIT
 // tr_step_sizes wherever the restated path applies; elsewhere the entry is
 // NaN and *inexact is set (render() checks it and raises: the host precheck
 // admitted a sigma it should not have).  Also the K:27 exponent step / s1.
-__global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, double s1,
-                                   double s2, double p, double *step, double *ratio, int *inexact) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
+__device__ __forceinline__ void epoch_steps_body(int64_t t0, int64_t stride, int64_t n,
+                                                 const double *__restrict__ sigma, double s1,
+                                                 double s2, double p, double *step, double *ratio,
+                                                 int *inexact) {
+    for (int64_t i = t0; i < n; i += stride) {
         const double sg = sigma[i];
         const double m = (1.0 < sg) ? 1.0 : sg;   // Python min(sigma, 1.0)
         const double x = fabs(m - 1.0);
@@ -68,6 +69,12 @@ __global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, 
         ratio[2 * i] = st;
         ratio[2 * i + 1] = st / s1;
     }
+}
+
+__global__ void epoch_steps_kernel(int64_t n, const double *__restrict__ sigma, double s1,
+                                   double s2, double p, double *step, double *ratio, int *inexact) {
+    epoch_steps_body(blockIdx.x * (int64_t)blockDim.x + threadIdx.x,
+                     (int64_t)gridDim.x * blockDim.x, n, sigma, s1, s2, p, step, ratio, inexact);
 }
 
 struct Rows {  // the overlapping rows of one partition (transfer.py:96-110)
@@ -333,9 +340,62 @@ extern "C" int tr_epoch_upload(int64_t n_parts, const double *sigma, const uint8
     return TR_OK;
 }
 
+// A packed epoch's re-upload in one launch: the sections after the steps
+// (sigma, TF, activity bits) are read from the page-locked block over PCIe
+// (mapped host memory) and stored in HBM, and the steps are recomputed from
+// the sigma read (epoch_steps_kernel's arithmetic).  The inexact word is not
+// touched: the block is the one whose first upload zeroed and then checked it,
+// and the same sigma gives the same steps.
+__global__ void __launch_bounds__(256) epoch_refresh_kernel(const int4 *__restrict__ src, int4 *dst,
+                                                            int64_t n16, int64_t n,
+                                                            const double *sigma_h, double s1,
+                                                            double s2, double p, double *step,
+                                                            double *ratio, int *inexact) {
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = t0; i < n16; i += stride) dst[i] = src[i];
+    epoch_steps_body(t0, stride, n, sigma_h, s1, s2, p, step, ratio, inexact);
+}
+
 extern "C" int tr_epoch_upload_s(const TrEpochUpload *u, TrEpoch *out, int64_t *h2d_bytes,
                                  void *stream) {
     if (!u) return tr_fail(TR_EINVAL, "tr_epoch_upload_s: invalid arguments");
+    if (u->packed && u->steps_on_device) {
+        const int64_t n = u->n_parts;
+        if (n < 1 || !u->host_buf || !u->dev_buf || !out ||
+            u->buf_bytes < tr_epoch_bytes(n, u->n_tf, u->n_bnodes, u->n_knodes))
+            return tr_fail(TR_EINVAL, "tr_epoch_upload_s: packed re-upload of an epoch never uploaded");
+        const int64_t o_ratio = a64(8 * n), o_sigma = a64(o_ratio + 16 * n);
+        const int64_t o_tf = a64(o_sigma + 8 * n), o_act = a64(o_tf + 32 * u->n_tf);
+        const int64_t o_bact = a64(o_act + n), o_kact = a64(o_bact + u->n_bnodes);
+        const int64_t o_flag = a64(o_kact + u->n_knodes);
+        void *hd = nullptr;
+        cudaError_t e = cudaHostGetDevicePointer(&hd, u->host_buf, 0);
+        if (e != cudaSuccess) return cuda_fail(e, "tr_epoch_upload_s: host block not mapped");
+        const char *h = static_cast<const char *>(hd);
+        char *d = static_cast<char *>(u->dev_buf);
+        const int64_t n16 = (o_flag - o_sigma) / 16;   // offsets are 64-B aligned
+        int64_t blocks = (n16 + 255) / 256;
+        if (blocks > 148) blocks = 148;
+        epoch_refresh_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+            reinterpret_cast<const int4 *>(h + o_sigma), reinterpret_cast<int4 *>(d + o_sigma), n16, n,
+            reinterpret_cast<const double *>(h + o_sigma), u->s1, u->s2, u->p,
+            reinterpret_cast<double *>(d), reinterpret_cast<double *>(d + o_ratio),
+            reinterpret_cast<int *>(d + o_flag));
+        if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "epoch_refresh_kernel");
+        if (h2d_bytes) *h2d_bytes = o_flag - o_sigma;
+        out->active = reinterpret_cast<const uint8_t *>(d + o_act);
+        out->bnode_active = reinterpret_cast<const uint8_t *>(d + o_bact);
+        out->step = reinterpret_cast<const double *>(d);
+        out->tf_table = reinterpret_cast<const double *>(d + o_tf);
+        out->n_tf = u->n_tf;
+        out->tf_lo = u->tf_lo;
+        out->tf_hi = u->tf_hi;
+        out->knode_active = reinterpret_cast<const uint8_t *>(d + o_kact);
+        out->step_ratio = reinterpret_cast<const double *>(d + o_ratio);
+        out->inexact = reinterpret_cast<int32_t *>(d + o_flag);
+        return TR_OK;
+    }
     return tr_epoch_upload(u->n_parts, u->sigma, u->active, u->bnode_active, u->n_bnodes,
                            u->knode_active, u->n_knodes, u->tf_table, u->n_tf, u->tf_lo, u->tf_hi,
                            u->s1, u->s2, u->p, u->steps_on_device, u->host_buf, u->dev_buf,

@@ -20,9 +20,11 @@ mirroring the reference's TF decoupling (transfer.py:144-167, A7).
 
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import math
 import os
+import sys
 import threading
 import time
 import weakref
@@ -275,8 +277,12 @@ class Epoch:
                                                 stream.cuda_stream), "tr_epoch_upload_s")
         self.h2d_bytes = int(h2d.value)
         self.stale = False
-        # device steps: the first frame reads back the epoch's inexact word
-        self.verified = not self.desc.inexact
+        if not self.up.packed:
+            # device steps: the first frame reads back the epoch's inexact word
+            self.verified = not self.desc.inexact
+        # the staging block now holds the sections: a re-upload (stale) only
+        # moves it (one kernel over PCIe with device steps)
+        self.up.packed = 1
         self._uploaded.record(stream)
         self._recorded = True
         # the copy is not torch's: keep the staging buffer alive until it has run
@@ -422,6 +428,7 @@ class DeviceScene:
             self.resident_bytes += sum(t.numel() for t in (self.t_coff, self.t_crecs, self.t_tbox))
         self._epochs: OrderedDict = OrderedDict()
         self._frames: dict = {}
+        self._results = _ResultPool()
         self._act_key, self._act_val = None, None
         self._desc_key, self._desc_val = None, None
 
@@ -629,75 +636,109 @@ class DeviceScene:
         from .render import Framebuffer, RenderStats
         torch = _torch()
         w, h = int(camera.width), int(camera.height)
-        with self.lock, torch.cuda.device(self.device):
+        idx = self.device.index
+        ctx = (contextlib.nullcontext() if torch.cuda.current_device() == idx
+               else torch.cuda.device(self.device))
+        with self.lock, ctx:
             t0 = time.perf_counter()
-            stream = torch.cuda.current_stream(self.device)
-            meta = scene.meta_state()
-            ep = self.epoch(meta, params, stream, hold=False, defer_stale=True)   # synchronized below
+            raw_stream = torch._C._cuda_getCurrentRawStream(idx)
+            ep = self.epoch(scene.meta_state(), params, None, hold=False, defer_stale=True)
             frame = self.frame_desc(scene, camera, mode, params, jitter, track, flags)
             fb = self.frame_buffers(w, h)
             # one page-locked block: rgba | samples | counters (+ inexact word)
             npx = h * w
-            blk = torch.empty(8 * (5 * npx + 4 + self.n_parts), dtype=torch.uint8, pin_memory=True)
-            rgba_h = blk[:32 * npx].view(torch.float64).view(h, w, 4)
-            samp_h = blk[32 * npx:40 * npx].view(torch.int64).view(h, w)
-            cnt_h = blk[40 * npx:].view(torch.int64)
+            base, dptr = self._results.take(8 * (5 * npx + 4 + self.n_parts))
+            rgba_h = base[:32 * npx].view(np.float64).reshape(h, w, 4)
+            samp_h = base[32 * npx:40 * npx].view(np.int64).reshape(h, w)
+            cnt_h = base[40 * npx:].view(np.int64)
             if ep._recorded:
                 ep._uploaded.synchronize()   # a staging-buffer copy of its own upload()
+                ep._recorded = False
             out = fb.outputs()
             if DIRECT_HOST_OUTPUTS:
                 # the kernels store each finished pixel straight into the
                 # page-locked result arrays, overlapping the device->host
                 # transfer with the march (tr_host_device_pointer)
-                out.rgba = host_device_pointer(rgba_h)
-                out.samples = host_device_pointer(samp_h)
+                out.rgba = dptr
+                out.samples = dptr + 32 * npx
             inexact = None
             if not ep.verified:
                 cnt_h[-1] = 0
-                inexact = cnt_h.data_ptr() + 8 * (3 + self.n_parts)
+                inexact = cnt_h.ctypes.data + 8 * (3 + self.n_parts)
             dms = C.c_float(0.0)
             reup = C.byref(ep.up) if ep.stale else None
             # (stale epoch re-upload,) counters reset, the frame, counters (+ inexact
             # word) D2H, sync: one call
             _lib.check(_lib.lib().tr_render_sync(C.byref(self.desc), C.byref(ep.desc),
                                                  C.byref(frame), C.byref(out),
-                                                 3 + self.n_parts, cnt_h.data_ptr(), inexact,
-                                                 stream.cuda_stream, C.byref(dms), reup),
+                                                 3 + self.n_parts, cnt_h.ctypes.data, inexact,
+                                                 raw_stream, C.byref(dms), reup),
                        "tr_render_sync")
             ep.stale = False
             if not DIRECT_HOST_OUTPUTS:
-                rgba_h.view(-1, 4).copy_(fb.rgba)
-                samp_h.view(-1).copy_(fb.samples)
+                torch.from_numpy(rgba_h).view(-1, 4).copy_(fb.rgba)
+                torch.from_numpy(samp_h).view(-1).copy_(fb.samples)
             if not ep.verified:
                 if int(cnt_h[-1]) != 0:
                     raise RuntimeError("device step sizes of this epoch are inexact (sigma outside "
                                        "the restated glibc pow domain); frame discarded")
                 ep.verified = True
             wall_ms = (time.perf_counter() - t0) * 1000.0
-            dev_ms = dms.value
-        cnt = cnt_h.numpy()
-        rgba = rgba_h.numpy()
-        samples = samp_h.numpy()
-        fbuf = Framebuffer(width=w, height=h, rgba=rgba, samples=samples,
+        fbuf = Framebuffer(width=w, height=h, rgba=rgba_h, samples=samp_h,
                            background=np.asarray(scene.background, dtype=np.float64).copy())
         stats = RenderStats(
-            total_samples=int(cnt[0]), wall_ms=wall_ms,
-            partitions_visited_mean=float(np.float64(cnt[1]) / np.float64(w * h)),
-            per_partition_samples=cnt[3:3 + self.n_parts].copy() if track else None,
-            samples=samples, device_ms=float(dev_ms), gpu_launches=last_launches())
+            total_samples=int(cnt_h[0]), wall_ms=wall_ms,
+            partitions_visited_mean=float(np.float64(cnt_h[1]) / np.float64(w * h)),
+            per_partition_samples=cnt_h[3:3 + self.n_parts].copy() if track else None,
+            samples=samp_h, device_ms=float(dms.value), gpu_launches=last_launches())
         return fbuf, stats
+
+
+class _ResultPool:
+    """Page-locked result blocks for render(): a block is handed out again
+    once no array returned from it is alive (the returned arrays are numpy
+    views of the block's base array, so its reference count says when)."""
+
+    KEEP = 4
+
+    def __init__(self):
+        self.blocks = []   # [nbytes, tensor, base ndarray, device address]
+
+    def take(self, nbytes: int):
+        for b in self.blocks:
+            if b[0] == nbytes and sys.getrefcount(b[2]) == 2:   # the list + the argument
+                return b[2], b[3]
+        torch = _torch()
+        t = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        blk = [nbytes, t, t.numpy(), host_device_pointer(t)]
+        self.blocks.append(blk)
+        if len(self.blocks) > self.KEEP:   # a busy block leaves with its last view
+            for k, b in enumerate(self.blocks):
+                if b is not blk and sys.getrefcount(b[2]) > 2:
+                    del self.blocks[k]
+                    break
+            else:
+                del self.blocks[0]
+        return blk[2], blk[3]
+
+_LAST_LAUNCH = (C.c_int64 * 3)()
 
 
 def last_launches() -> int:
     """Kernels of ours the last tr_render_frame launched (tr_last_launch)."""
-    out = np.zeros(3, np.int64)
-    _lib.check(_lib.lib().tr_last_launch(_lib.ptr(out, C.c_int64)), "tr_last_launch")
-    return int(out[0])
+    _lib.check(_lib.lib().tr_last_launch(_LAST_LAUNCH), "tr_last_launch")
+    return int(_LAST_LAUNCH[0])
 
 
 def device_scene_for(scene, device=None) -> DeviceScene:
     """Cached DeviceScene of `scene` (rebuilt if its sampler or BVH changed)."""
-    device = resolve_device(device)
+    if device is None:   # the common case, without building a torch.device
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: the B200 render path has no CPU fallback")
+        idx = torch.cuda.current_device()
+    else:
+        idx = resolve_device(device).index
     cache = getattr(scene, _CACHE_ATTR, None)
     if cache is None:
         cache = {}
@@ -705,12 +746,12 @@ def device_scene_for(scene, device=None) -> DeviceScene:
             object.__setattr__(scene, _CACHE_ATTR, cache)
         except AttributeError:
             cache = _GLOBAL_CACHE.setdefault(id(scene), {})
-    key = (str(device), id(scene.sampler), id(scene.bvh))
+    key = (idx, id(scene.sampler), id(scene.bvh))
     ent = cache.get(key)
     if ent is None or ent[0]() is not scene.sampler or ent[1]() is not scene.bvh:
-        for k in [k for k in cache if k[0] == str(device)]:
+        for k in [k for k in cache if k[0] == idx]:
             del cache[k]
-        dev = DeviceScene(scene, device)
+        dev = DeviceScene(scene, _torch().device("cuda", idx))
         cache[key] = (weakref.ref(scene.sampler), weakref.ref(scene.bvh), dev)
         return dev
     return ent[2]

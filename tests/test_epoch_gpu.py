@@ -89,16 +89,46 @@ def test_concurrent_tf_updates_yield_whole_epoch_frames(B, device_meta):
 
 
 def test_stale_epoch_reupload_renders_the_same_frame(B):
-    """mark_epochs_stale (bench.py's end-to-end steps): the cached epoch is
-    packed and copied again in place; frames are unchanged."""
+    """mark_epochs_stale (bench.py's end-to-end steps): the cached epoch's
+    page-locked block is copied again in place (after the first upload: one
+    kernel reading it over PCIe and recomputing the steps); frames are
+    unchanged even when the device copy was wiped in between."""
     scene, cam, params, tfs = _setup(B, False)
     from paper_1908_01906_b200.device import device_scene_for
     fb0, st0 = B.render(scene, cam, "skip-adaptive", params)
     dev = device_scene_for(scene)
     ep = next(iter(dev._epochs.values()))
-    for _ in range(3):
+    for i in range(3):
         dev.mark_epochs_stale()
         assert ep.stale
+        if i:   # the re-upload really rewrites the device sections and steps
+            ep.buf.zero_()
         fb, st = B.render(scene, cam, "skip-adaptive", params)
         assert not ep.stale and next(iter(dev._epochs.values())) is ep
         assert np.array_equal(fb.rgba, fb0.rgba) and st.total_samples == st0.total_samples
+
+
+def test_held_frames_are_not_reused(B):
+    """render() hands out page-locked result blocks again only once no
+    returned array views them: frames (or slices of them) a caller keeps are
+    never overwritten by later frames."""
+    scene, cam, params, tfs = _setup(B, False)
+    kept, copies = [], []
+    for i in range(7):
+        scene.set_transfer_function(tfs[i])
+        fb, st = B.render(scene, cam, "skip-adaptive", params)
+        keep = fb.rgba if i % 2 == 0 else fb.samples[3:9]   # a whole frame, or a slice
+        kept.append(keep)
+        copies.append(keep.copy())
+        del fb, st
+    for _ in range(6):   # more frames while the kept ones are alive
+        B.render(scene, cam, "skip-adaptive", params)
+    for k, c in zip(kept, copies):
+        assert np.array_equal(k, c)
+    from paper_1908_01906_b200.device import device_scene_for
+    pool = device_scene_for(scene)._results
+    kept.clear()
+    n = len(pool.blocks)
+    for _ in range(4):   # freed blocks are reused, not multiplied
+        B.render(scene, cam, "skip-adaptive", params)
+    assert len(pool.blocks) <= max(n, pool.KEEP)
