@@ -1139,14 +1139,31 @@ __global__ void __launch_bounds__(256, 4) cand_raster_kernel(SceneK S, EpochK E,
         iy1 = min(iy1, (t_last / F.tiles_x) * TILE_H + TILE_H - 1);
         iy0 += sub;   // this warp's rows: iy0 + sub, iy0 + sub + nsub, ...
         if (iy0 > iy1) continue;
-        const uint32_t rw = (uint32_t)(ix1 - ix0 + 1);
+        // columns enumerated per row: every column of the rectangle, or
+        // (sharded frame) only this rank's tiles -- tile ty * tiles_x + tx is
+        // the rank's when it is == rank (mod shard_count), so on one tile row
+        // its tile columns step by shard_count: ceil(span / count) + 1 of them
+        // (8 columns each) cover the rectangle, and the raster's work shrinks
+        // with the rank count like the rest of the frame's
+        const uint32_t shards = (uint32_t)cnt;
+        const uint32_t tc0 = (uint32_t)ix0 / TILE_W;
+        uint32_t rw = (uint32_t)(ix1 - ix0 + 1);
+        if (shards > 1) rw = TILE_W * (((uint32_t)ix1 / TILE_W - tc0 + shards) / shards + 1);
         const uint32_t nrow = (uint32_t)((iy1 - iy0) / nsub + 1), npx = rw * nrow;
         // (row, column) of pixel k stepped incrementally: no division per pixel
         const uint32_t dcol = 32u % rw, drow = 32u / rw;
         uint32_t col = (uint32_t)lane % rw, row = (uint32_t)lane / rw;
         for (uint32_t k = lane; k < npx; k += 32, col += dcol, row += drow) {
             if (col >= rw) { col -= rw; ++row; }
-            const uint32_t ix = (uint32_t)ix0 + col, iy = (uint32_t)iy0 + row * (uint32_t)nsub;
+            const uint32_t iy = (uint32_t)iy0 + row * (uint32_t)nsub;
+            uint32_t ix = (uint32_t)ix0 + col;
+            if (shards > 1) {   // the col / 8-th tile of the rank's on this tile row
+                const uint32_t first = (iy / TILE_H * (uint32_t)F.tiles_x + tc0) % shards;
+                const uint32_t tx = tc0 + ((uint32_t)fr.shard_rank + shards - first) % shards +
+                                    col / TILE_W * shards;
+                ix = tx * TILE_W + col % TILE_W;
+                if (ix < (uint32_t)ix0 || ix > (uint32_t)ix1) continue;
+            }
             const int64_t rr = pixel_ray(F, ix, iy);
             if (rr < 0) continue;
             RayD ray;   // the trace's make_ray, from the per-ray table (slab needs o, 1/d)
