@@ -27,9 +27,13 @@ One step = one frame.  Items = samples (point queries, RenderStats.total_samples
             numba kernel) on its own scene build, all host cores, a bounded
             sample of whole frames
 N > 1 (`--gpus N` re-launches itself under torch.distributed.run when
-WORLD_SIZE is unset): strong scaling of the one frame -- 8x4 pixel tiles
-interleaved over the ranks, each rank's tiles gathered to rank 0 and the
-counters reduced there over NCCL (paper_1908_01906_b200/distributed.py).
+WORLD_SIZE is unset): one frame's 8x4 pixel tiles interleaved over the
+ranks, each rank's tiles gathered to rank 0 and the counters reduced there
+over NCCL (paper_1908_01906_b200/distributed.py).  Default `--scaling weak`:
+the frame side grows with sqrt(N) (512, 728, 1024, 1448 px at N = 1, 2, 4,
+8; same camera), so every GPU keeps ~512^2 rays -- a 512^2 frame split 8
+ways leaves 32k rays per B200, under one wave of its march lanes.
+`--scaling strong` splits the 512^2 frame itself.
 
 --impl reference: the reference's own render() (pkg/src/tetray/render.py:161-205,
 numba, installed under baseline/_ref) with all host threads, on whole frames
@@ -45,6 +49,7 @@ from __future__ import annotations
 
 import argparse
 import csv
+import math
 import io
 import json
 import os
@@ -80,13 +85,16 @@ def parse(argv=None):
     ap.add_argument("--scene", default="radial272")
     ap.add_argument("--mode", default="skip-adaptive", choices=MODES)
     ap.add_argument("--scale", type=float, default=1.0, help="image size multiplier (512*scale)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = frame side x sqrt(N) (fixed rays per GPU), strong = "
+                         "the same frame split N ways")
     ap.add_argument("--host-build", action="store_true",
                     help="build radialN through the general host path, not GridScene")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-budget-s", type=float, default=900.0,
+    ap.add_argument("--ref-budget-s", type=float, default=180.0,
                     help="reference arm: stop timing whole frames after this many seconds")
     ap.add_argument("--shard", default="pixels", choices=["pixels", "records"],
                     help="records: KD-brick record sharding (bricks.py; one brick per rank, "
@@ -95,6 +103,14 @@ def parse(argv=None):
     ap.add_argument("--flags", type=lambda x: int(x, 0), default=0,
                     help="TR_FLAG_* bits (tuning experiments; bits 8-11 = log2 group size)")
     return ap.parse_args(argv)
+
+
+def weak_scale(args, world: int) -> None:
+    """--scaling weak at N > 1: the frame side x sqrt(N), rounded to whole
+    8-pixel tiles, so the rays per GPU stay those of the N = 1 frame."""
+    if world > 1 and args.scaling == "weak":
+        side = int(round(512 * args.scale * math.sqrt(world) / 8.0)) * 8
+        args.scale = side / 512.0
 
 
 def scene_n(name: str) -> int:
@@ -300,8 +316,9 @@ def ncu_traffic(args):
 
 # ------------------------------------------------------------ reference arm
 
-def run_reference(args, rank):
-    """The stock reference render() on whole frames of the workload."""
+def run_reference(args, rank, base_scale=None):
+    """The stock reference render() on whole frames of the workload (the
+    warm-up frames -- numba JIT, page-in -- at the N = 1 frame size)."""
     if rank != 0:
         return 0
     os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/tetray_bench_numba")
@@ -325,8 +342,10 @@ def run_reference(args, rank):
     cam = C.camera(tetray, public_name(args.scene), scale=args.scale)
     par = C.params(tetray, public_name(args.scene))
     threads = os.cpu_count() or 1
+    cam_w = C.camera(tetray, public_name(args.scene),
+                     scale=args.scale if base_scale is None else base_scale)
     for _ in range(args.warmup):   # the first frame also JIT-compiles the numba kernels
-        tetray.render(scene, cam, args.mode, par, threads=threads)
+        tetray.render(scene, cam_w, args.mode, par, threads=threads)
     times, walls, samples = [], [], None
     t_start = time.perf_counter()
     for _ in range(args.steps):
@@ -347,7 +366,8 @@ def run_reference(args, rank):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": len(times), "warmup": args.warmup,
             "ms_per_step": tot * 1000.0 / len(times), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak" if args.gpus > 1 and args.scaling == "weak" else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, scene.mesh.n_tets, len(scene.partitions), samples),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "reference",
                              "cpu_model": cpu_model(), "numba_num_threads": nthreads,
@@ -464,8 +484,11 @@ def main(argv=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    base_scale = args.scale
+    if args.shard == "pixels":
+        weak_scale(args, world)
     if args.impl == "reference":
-        return run_reference(args, rank)
+        return run_reference(args, rank, base_scale)
     if args.shard == "records":
         return run_records(args, world, rank, local)
 
@@ -595,7 +618,8 @@ def main(argv=None):
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t_max * 1000.0 / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak" if world > 1 and args.scaling == "weak" else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, scene.mesh.n_tets, scene.n_partitions,
                                       total_samples),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -605,6 +629,8 @@ def main(argv=None):
                        "rays_per_s": cam.width * cam.height * args.steps / t_max,
                        "n_active": int(scene.meta_state()[0].sum()),
                        "parallelism": f"pixel tiles interleaved over {world} GPU(s)",
+                       "scaling_rule": "frame side x sqrt(N) (--scaling weak)"
+                       if world > 1 and args.scaling == "weak" else "one frame split N ways",
                        "comm_nranks": nranks, "flags": hex(args.flags),
                        "scene_path": type(scene).__name__,
                        "scene_build_s": round(build_s, 3), "upload_s": round(upload_s, 3),

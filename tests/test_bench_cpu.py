@@ -42,3 +42,19 @@ def test_workload_config_names_grid_scenes_by_their_radial_recipe():
     a = bench.workload_config(args, 100618240, 4096, 34935023)
     b = bench.workload_config(bench.parse(["--scene", "radial272"]), 100618240, 4096, 34935023)
     assert a == b and a["workload"] == "radial272 512x512 skip-adaptive"
+
+
+def test_weak_scaling_grows_the_frame_side_with_sqrt_n():
+    sys.path.insert(0, str(ROOT))
+    import bench
+    sides = {}
+    for n in (1, 2, 4, 8):
+        args = bench.parse(["--gpus", str(n)])
+        bench.weak_scale(args, n)
+        sides[n] = bench.workload_config(args, 1, 1, 1)["width"]
+    assert sides == {1: 512, 2: 728, 4: 1024, 8: 1448}
+    for n in (1, 2, 4, 8):   # rays per GPU within 1% of the 512^2 frame
+        assert abs(sides[n] ** 2 / n / 512 ** 2 - 1.0) < 0.011
+    args = bench.parse(["--gpus", "8", "--scaling", "strong"])
+    bench.weak_scale(args, 8)
+    assert bench.workload_config(args, 1, 1, 1)["width"] == 512
