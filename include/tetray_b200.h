@@ -409,6 +409,12 @@ typedef struct TrOutputs {
  * pixel straight into the caller's host framebuffer over PCIe while it runs
  * (render() does this; no separate device->host copy after the frame). */
 int tr_host_device_pointer(void *host, void **dev);
+/* Page-lock and map existing host memory (cudaHostRegister, mapped +
+ * portable) and return its device address; render(distributed=True) maps one
+ * node-shared result block (a /dev/shm file every rank has mapped) this way,
+ * so each GPU writes its own pixel tiles into the frame rank 0 returns. */
+int tr_host_register(void *host, int64_t bytes, void **dev);
+int tr_host_unregister(void *host);
 /* Stream-ordered memset / copy (cudaMemsetAsync, cudaMemcpyAsync with
  * cudaMemcpyDefault): the per-frame counter reset and read-back without a
  * framework dispatcher in between. */

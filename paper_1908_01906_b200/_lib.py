@@ -172,6 +172,8 @@ _SIGNATURES = [
     ("tr_step_size", C.c_double, [C.c_double, C.c_double, C.c_double, C.c_double]),
     ("tr_opacity_correction", C.c_double, [C.c_double, C.c_double, C.c_double]),
     ("tr_host_device_pointer", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tr_host_register", C.c_int, [C.c_void_p, C.c_int64, C.POINTER(C.c_void_p)]),
+    ("tr_host_unregister", C.c_int, [C.c_void_p]),
     ("tr_memset_async", C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p]),
     ("tr_copy_async", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("tr_pow_glibc_available", C.c_int, []),

@@ -2902,6 +2902,24 @@ int tr_host_device_pointer(void *host, void **dev) {
     return TR_OK;
 }
 
+int tr_host_register(void *host, int64_t bytes, void **dev) {
+    if (!host || bytes <= 0 || !dev) return tr_fail(TR_EINVAL, "tr_host_register: invalid arguments");
+    cudaError_t e = cudaHostRegister(host, (size_t)bytes, cudaHostRegisterMapped | cudaHostRegisterPortable);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaHostRegister");
+    e = cudaHostGetDevicePointer(dev, host, 0);
+    if (e != cudaSuccess) {
+        cudaHostUnregister(host);
+        return cuda_fail(e, "cudaHostGetDevicePointer");
+    }
+    return TR_OK;
+}
+
+int tr_host_unregister(void *host) {
+    if (!host) return tr_fail(TR_EINVAL, "tr_host_unregister: null");
+    cudaError_t e = cudaHostUnregister(host);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "cudaHostUnregister");
+}
+
 int tr_last_launch(int64_t *out3) {
     if (!out3) return tr_fail(TR_EINVAL, "tr_last_launch: null");
     for (int i = 0; i < 3; ++i) out3[i] = g_last_launch[i];

@@ -19,12 +19,18 @@ host-side logic with gloo on CPU; tests/test_parity_gpu.py the kernels).
 
 from __future__ import annotations
 
+import atexit
 import ctypes as C
+import mmap
+import os
+import secrets
+import sys
 import time
 
 import numpy as np
 
 from . import _lib
+from .device import last_launches
 
 TILE_W, TILE_H = 8, 4
 TILE_PIXELS = TILE_W * TILE_H
@@ -221,12 +227,192 @@ class ShardedFrame:
 _FRAMES: dict = {}
 
 
+def _all_reduce(t) -> None:
+    import torch.distributed as dist
+    if _gloo():
+        h = t.cpu()
+        dist.all_reduce(h)
+        t.copy_(h)
+        return
+    dist.all_reduce(t)
+
+
+class SharedBlocks:
+    """Frame result blocks (rgba f64 | samples i64, image layout) in
+    page-locked host memory shared by the ranks of one node: /dev/shm files
+    that every rank maps and registers with CUDA (tr_host_register).  Each
+    rank's kernels store its own pixel tiles straight into the block over its
+    own PCIe link, so rank 0 returns the frame with no gather and no
+    device->host copy of the image.
+
+    A block is handed out again only once no array rank 0 returned views it
+    (the views' base is the block's array: its reference count says so).
+    Rank 0 picks the NEXT frame's block while a frame runs and every rank
+    learns it from that frame's counter all-reduce, so no extra collective
+    is needed; a new block is created by rank 0 before it is announced."""
+
+    MAX_BLOCKS = 64
+
+    def __init__(self, token: str, nbytes: int, rank: int):
+        self.token, self.nbytes, self.rank = token, nbytes, rank
+        self.blocks = []   # [base uint8 array over the mapping, device address]
+        self.cur = 0
+        if rank == 0:
+            self._create(0)
+
+    def _path(self, i: int) -> str:
+        return f"/dev/shm/tetray_b200_{self.token}_{self.nbytes}_{i}"
+
+    def _create(self, i: int) -> None:
+        fd = os.open(self._path(i), os.O_CREAT | os.O_EXCL | os.O_RDWR, 0o600)
+        try:
+            os.ftruncate(fd, self.nbytes)
+        finally:
+            os.close(fd)
+
+    def block(self, i: int):
+        """(base array, device address) of block i, mapped on first use."""
+        while len(self.blocks) <= i:
+            k = len(self.blocks)
+            fd = os.open(self._path(k), os.O_RDWR)
+            try:
+                mm = mmap.mmap(fd, self.nbytes)
+            finally:
+                os.close(fd)
+            base = np.frombuffer(mm, dtype=np.uint8)
+            dptr = C.c_void_p()
+            _lib.check(_lib.lib().tr_host_register(C.c_void_p(base.ctypes.data), self.nbytes,
+                                                   C.byref(dptr)), "tr_host_register")
+            self.blocks.append([base, int(dptr.value)])
+        return self.blocks[i][0], self.blocks[i][1]
+
+    def pick_next(self) -> int:
+        """Rank 0: a block no returned frame views, other than the current one."""
+        for i, b in enumerate(self.blocks):
+            if i != self.cur and sys.getrefcount(b[0]) == 2:   # the list entry + the argument
+                return i
+        k = len(self.blocks)
+        if k >= self.MAX_BLOCKS:
+            raise RuntimeError(f"render(distributed=True): {k} frames still referenced")
+        self._create(k)
+        self.block(k)
+        return k
+
+    def close(self) -> None:
+        for base, _ in self.blocks:
+            _lib.lib().tr_host_unregister(C.c_void_p(base.ctypes.data))
+        if self.rank == 0:
+            for i in range(len(self.blocks)):
+                try:
+                    os.unlink(self._path(i))
+                except OSError:
+                    pass
+        self.blocks = []
+
+
+_SHARED: dict = {}
+_TOKEN: list = []
+
+
+def _shared_blocks(nbytes: int, rank: int) -> SharedBlocks:
+    """The node-shared block pool of one frame size (collective on first use)."""
+    import torch.distributed as dist
+    pool = _SHARED.get(nbytes)
+    if pool is None:
+        if not _TOKEN:   # one name prefix per process group, from rank 0
+            obj = [f"{os.getpid()}_{secrets.token_hex(4)}" if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            _TOKEN.append(obj[0])
+            atexit.register(release_shared_frames)
+        pool = SharedBlocks(_TOKEN[0], nbytes, rank)
+        dist.barrier()   # block 0 exists before the other ranks map it
+        _SHARED[nbytes] = pool
+    return pool
+
+
+def release_shared_frames() -> None:
+    """Unmap the node-shared result blocks (rank 0 also removes their
+    /dev/shm files; arrays rank 0 returned stay valid).  Runs at exit; call it
+    where processes end without atexit (multiprocessing workers)."""
+    for pool in _SHARED.values():
+        pool.close()
+    _SHARED.clear()
+
+
+def _node_local(world: int) -> bool:
+    """Every rank on this host (torchrun exports LOCAL_WORLD_SIZE)."""
+    return int(os.environ.get("LOCAL_WORLD_SIZE", world)) == world
+
+
 def render_sharded(scene, camera, mode: str, params, *, jitter: bool = False,
                    track_per_partition: bool = True, device=None, flags: int = 0):
     """render() over the ranks of the initialised torch.distributed group:
     every rank calls it with the same arguments; rank 0 returns the
     (Framebuffer, RenderStats) of the whole frame, bit-identical to the
-    one-GPU render(); the other ranks return (None, None)."""
+    one-GPU render(); the other ranks return (None, None).
+
+    Ranks of one node write their tiles into a node-shared page-locked
+    frame (SharedBlocks) and all-reduce the counters; across nodes the
+    tiles are gathered to rank 0 over NCCL (render_sharded_gather)."""
+    import torch
+    import torch.distributed as dist
+
+    from .device import device_scene_for
+    from .render import _MODE_IDS, Framebuffer, RenderStats
+    rank, world = dist.get_rank(), dist.get_world_size()
+    if not _node_local(world):
+        return render_sharded_gather(scene, camera, mode, params, jitter=jitter,
+                                     track_per_partition=track_per_partition, device=device,
+                                     flags=flags)
+    dscene = device_scene_for(scene, device)
+    track = track_per_partition and mode != "reference"
+    w, h = int(camera.width), int(camera.height)
+    npx = w * h
+    P = dscene.n_parts
+    frame = dscene.frame_desc(scene, camera, _MODE_IDS[mode], params, jitter, track, flags,
+                              shard_rank=rank, shard_count=world, compact=False)
+    pool = _shared_blocks(40 * npx, rank)
+    t0 = time.perf_counter()
+    with dscene.lock, torch.cuda.device(dscene.device):
+        stream = torch.cuda.current_stream(dscene.device)
+        ep = dscene.epoch(scene.meta_state(), params, stream)
+        fb = dscene.frame_buffers(w, h)
+        base, dptr = pool.block(pool.cur)
+        nxt = pool.pick_next() if rank == 0 else 0
+        out = fb.outputs()
+        out.rgba, out.samples = dptr, dptr + 32 * npx   # this rank's tiles, in place
+        fb.counters.zero_()
+        _lib.check(_lib.lib().tr_render_frame(C.byref(dscene.desc), C.byref(ep.desc),
+                                              C.byref(frame), C.byref(out),
+                                              C.c_void_p(stream.cuda_stream)), "tr_render_frame")
+        # [totals | work | per-partition samples | next block]: one all-reduce;
+        # it runs after every rank's frame, so rank 0 then sees every tile
+        red = torch.empty(4 + P, dtype=torch.int64, device=dscene.device)
+        red[:3 + P].copy_(fb.counters)
+        red[3 + P:].fill_(nxt)
+        _all_reduce(red)
+        cnt_h = torch.empty(4 + P, dtype=torch.int64, pin_memory=True)
+        cnt_h.copy_(red, non_blocking=True)
+        stream.synchronize()
+    cnt = cnt_h.numpy()
+    pool.cur = int(cnt[3 + P])
+    if rank != 0:
+        return None, None
+    rgba = base[:32 * npx].view(np.float64).reshape(h, w, 4)
+    samples = base[32 * npx:40 * npx].view(np.int64).reshape(h, w)
+    fbuf = Framebuffer(width=w, height=h, rgba=rgba, samples=samples,
+                       background=np.asarray(scene.background, dtype=np.float64).copy())
+    st = RenderStats(total_samples=int(cnt[0]), wall_ms=(time.perf_counter() - t0) * 1e3,
+                     partitions_visited_mean=float(np.float64(cnt[1]) / np.float64(w * h)),
+                     per_partition_samples=cnt[3:3 + P].copy() if track else None,
+                     samples=samples, device_ms=0.0, gpu_launches=last_launches())
+    return fbuf, st
+
+
+def render_sharded_gather(scene, camera, mode: str, params, *, jitter: bool = False,
+                          track_per_partition: bool = True, device=None, flags: int = 0):
+    """render_sharded across nodes: each rank's compact tiles gathered to
+    rank 0 over NCCL, counters reduced there, rank 0 reads the frame back."""
     import torch
     import torch.distributed as dist
 

@@ -1,8 +1,9 @@
 """Multi-process sharded frames through the public render(distributed=True):
 N processes (sharing the one GPU of this run, gloo transport: NCCL refuses two
-ranks on one device) each render their interleaved 8x4 pixel tiles
-(distributed.ShardedFrame, compact slot-major outputs), rank 0 gathers the
-tiles and reduces the counters and returns the frame.  It must be
+ranks on one device) each render their interleaved 8x4 pixel tiles straight
+into the node-shared page-locked frame (distributed.SharedBlocks), the
+counters are all-reduced and rank 0 returns the frame; the cross-node
+variant (compact tiles gathered to rank 0, render_sharded_gather) too.  It must be
 bit-identical to the one-process frame -- rows are independent
 (pkg/src/tetray/_kernels.py:323-328), integer sums are order-free."""
 
@@ -24,11 +25,13 @@ def B(built_lib):
     return B
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, path):
     import os
     import sys
     sys.path[:0] = [str(cases.ROOT), str(cases.ROOT / "tests")]
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    # "gather": as if every rank were on its own node (render_sharded_gather)
+    os.environ["LOCAL_WORLD_SIZE"] = "1" if path == "gather" else str(world)
     import torch
     import torch.distributed as dist
 
@@ -49,18 +52,20 @@ def _worker(rank, world, port, q):
                     assert fb is None and st is None
         q.put((rank, out))
     finally:
+        from paper_1908_01906_b200.distributed import release_shared_frames
+        release_shared_frames()
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_distributed_render_equals_one_gpu_frame(B, world):
+@pytest.mark.parametrize("world,path", [(2, "shared"), (3, "shared"), (2, "gather")])
+def test_distributed_render_equals_one_gpu_frame(B, world, path):
     import torch.multiprocessing as mp
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, path)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
