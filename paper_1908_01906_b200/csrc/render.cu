@@ -188,6 +188,9 @@ __device__ __forceinline__ double4 ldg256(const void *p) {
     return v;
 }
 
+#ifndef TR_RAY_TIMES
+#define TR_RAY_TIMES 0
+#endif
 #ifndef TR_UNROLL_COMPOSITE
 #define TR_UNROLL_COMPOSITE 1   // A/B knob: the round's compositing loop unrolled over G
 #endif
@@ -1958,6 +1961,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __shared__ int32_t s_rpid[NG];                      // (rec[s_icur]: entry, partition,
     __shared__ uint32_t s_rcum[NG];                     //  running sample count)
     __shared__ uint32_t s_cfull[BRICK ? NG : 1], s_tbegin[BRICK ? NG : 1];   // brick runs
+#if TR_RAY_TIMES   // diagnostics build: each ray's (start, end) globaltimer in rgba.r / .g
+    __shared__ unsigned long long s_tstart[NG];
+#endif
     const TrFrame &fr = F.f;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int j = lane % G;
@@ -2004,6 +2010,9 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         const Pixel px = ray_pixel(F, rr);
                         const RayD ray = make_ray(fr, px.ix, px.iy);
                         s_rr[g] = rr; s_out[g] = px.out;
+#if TR_RAY_TIMES
+                        s_tstart[g] = globaltimer_ns();
+#endif
                         s_pix[g] = (int32_t)px.ix; s_piy[g] = (int32_t)px.iy;
                         s_o[0][g] = ray.ox; s_o[1][g] = ray.oy; s_o[2][g] = ray.oz;
                         s_d[0][g] = ray.dx; s_d[1][g] = ray.dy; s_d[2][g] = ray.dz;
@@ -2210,7 +2219,11 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     if (!inline_mode) visited = term ? i_last + 1 : s_niv[g];
                     else visited = s_niv[g] + L.visited;
                 }
+#if TR_RAY_TIMES
+                const Acc acc = {(double)s_tstart[g], (double)globaltimer_ns(), 0.0, 1.0};
+#else
                 const Acc acc = {s_acc[0][g], s_acc[1][g], s_acc[2][g], s_acc[3][g]};
+#endif
                 write_pixel(fr, O, s_out[g], acc, samples, visited);
                 my_samples += (unsigned long long)samples;
                 my_visited += (unsigned long long)visited;
