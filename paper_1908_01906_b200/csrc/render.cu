@@ -191,6 +191,9 @@ __device__ __forceinline__ double4 ldg256(const void *p) {
 #ifndef TR_RAY_TIMES
 #define TR_RAY_TIMES 0
 #endif
+#ifndef TR_ROUND_TIMES
+#define TR_ROUND_TIMES 0
+#endif
 #ifndef TR_UNROLL_COMPOSITE
 #define TR_UNROLL_COMPOSITE 1   // A/B knob: the round's compositing loop unrolled over G
 #endif
@@ -569,7 +572,8 @@ __device__ __forceinline__ uint32_t field_at(const SceneK &S, const PQuery &q, L
     return pos;
 }
 
-// K:74-90
+// K:74-90.  SHARED: T is the march's shared-memory copy of the table.
+template <bool SHARED = false>
 __device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t n, double lo,
                                           double hi, double v, double c[4]) {
     const double u = (v - lo) / (hi - lo) * (double)(n - 1);
@@ -579,10 +583,11 @@ __device__ __forceinline__ void tf_sample(const double *__restrict__ T, int64_t 
     if (u <= 0.0) { j = 0; interp = false; }
     else if (u >= (double)(n - 1)) { j = n - 1; interp = false; }
     else { j = (int64_t)floor(u); }
-    const double4 a = ldg256(T + 4 * j);
+    const double4 a = SHARED ? *reinterpret_cast<const double4 *>(T + 4 * j) : ldg256(T + 4 * j);
     if (!interp) { c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; return; }
     f = u - (double)j;
-    const double4 b = ldg256(T + 4 * j + 4);
+    const double4 b = SHARED ? *reinterpret_cast<const double4 *>(T + 4 * j + 4)
+                             : ldg256(T + 4 * j + 4);
     c[0] = a.x + f * (b.x - a.x);
     c[1] = a.y + f * (b.y - a.y);
     c[2] = a.z + f * (b.z - a.z);
@@ -1578,12 +1583,43 @@ __device__ bool inline_next(const SceneK &S, const EpochK &E, const TrFrame &fr,
 #define TR_RASTER_PX 262144   // A/B knob: band pixels per candidate-raster warp of a partition
 #endif
 
+#if TR_ROUND_TIMES   // diagnostics build: per-thread cycle sums of the march's phases
+constexpr int DBG_THREADS = 148 * 8 * 256, DBG_PH = 8;
+__device__ unsigned long long g_dbg[DBG_THREADS * DBG_PH];
+__device__ __forceinline__ void dbg_add(int ph, long long dt) {
+    const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < DBG_THREADS) g_dbg[t * DBG_PH + ph] += (unsigned long long)dt;
+}
+#define DBG_T(v) const long long v = clock64()
+#else
+#define DBG_T(v)
+#endif
+
+// The transfer function staged in shared memory once per march CTA: a
+// sample's TF lookup (K:74-90) then costs a shared-memory load instead of an
+// L1/L2 round trip on its dependent chain.  Only in the 128-thread march of
+// reference / skip modes (2-4% faster there; with it the 256-thread
+// skip-adaptive march measured 2% slower, so its instantiation has no TF code).
+struct MarchTabs {
+    const double *tf;   // TF table copy, or NULL (global)
+};
+constexpr int TABS_TF_MAX = 16384;   // TF tables up to 512 entries are staged
+#ifndef TR_TABS_TF   // A/B knob
+#define TR_TABS_TF 1
+#endif
+
+// dynamic shared memory of a march launch with `block` threads per CTA
+__host__ __device__ inline int march_tabs_bytes(int block, int64_t n_tf) {
+    return (TR_TABS_TF && block == 128 && n_tf * 32 <= TABS_TF_MAX) ? (int)(n_tf * 32) : 0;
+}
+
+template <bool TABS = false>
 __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E, const TrFrame &fr,
                                                 double ox, double oy, double oz, double dx,
                                                 double dy, double dz, double a, int64_t k,
                                                 double phase, int32_t pid, bool stats,
                                                 bool pair_scan, bool use_grid, bool use_cells,
-                                                bool &found) {
+                                                bool &found, const MarchTabs *T = nullptr) {
     double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
     found = false;
     double step = fr.s1, e = 1.0;
@@ -1592,6 +1628,7 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
         step = se.x;
         e = se.y;
     }
+    DBG_T(d0);
     const double t = a + ((double)k + phase) * step;
     const PQuery q = make_query(ox + t * dx, oy + t * dy, oz + t * dz);
     if (stats) atomicAdd(&g_stats[ST_SLOTS], 1ull);
@@ -1663,6 +1700,7 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
         pos = locate_full(S, q, l, leaf);
     }
     if (pos == UINT32_MAX) return sh;
+    DBG_T(d1);
     double v;
     const double2 *rp = reinterpret_cast<const double2 *>(S.tets + pos);
     if (S.centering == 0) {   // K:149-151
@@ -1672,11 +1710,26 @@ __device__ __forceinline__ double4 shade_sample(const SceneK &S, const EpochK &E
         v = __ldg(rp + 6).x;
     }
     double c[4];
-    tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+#if TR_ROUND_TIMES
+    asm volatile("" :: "d"(v));
+#endif
+    DBG_T(d2);
+    if (TABS && T->tf) tf_sample<true>(T->tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
+    else tf_sample(E.tf, E.n_tf, E.tf_lo, E.tf_hi, v, c);
     const double x = 1.0 - c[3];
+#if TR_ROUND_TIMES
+    asm volatile("" :: "d"(x));
+#endif
+    DBG_T(d3);
     // K:27; glibc's pow(x, 1) and pow(1, y) are exactly x and 1
     const bool need_pow = e != 1.0 && x != 1.0;
     sh.x = 1.0 - (need_pow ? ref_pow(x, e) : x);
+#if TR_ROUND_TIMES
+    asm volatile("" :: "d"(sh.x));
+    DBG_T(d4);
+    dbg_add(0, d1 - d0); dbg_add(1, d2 - d1); dbg_add(2, d3 - d2); dbg_add(3, d4 - d3);
+    dbg_add(7, 1);
+#endif
     if (stats) {
         atomicAdd(&g_stats[ST_FOUND], 1ull);
         if (need_pow) atomicAdd(&g_stats[ST_POW], 1ull);
@@ -1953,7 +2006,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     __shared__ unsigned long long red[2][BLK / 32];
     __shared__ double4 shade[G][BLK / G];   // [lane in group][group]: conflict free
     __shared__ Inline inl[NG];
-    __shared__ double s_o[3][NG], s_d[3][NG], s_acc[4][NG], s_phase[NG];
+    __shared__ double s_d[3][NG], s_acc[4][NG], s_phase[NG];   // origin: the camera (make_ray)
     __shared__ long long s_out[NG], s_samples[NG];
     __shared__ uint32_t s_rr[NG], s_taken[NG], s_ctot[NG], s_cbefore[NG];
     __shared__ int32_t s_icur[NG], s_niv[NG], s_pix[NG], s_piy[NG];
@@ -1977,6 +2030,16 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     const bool pair_scan = (fr.flags & TR_FLAG_PAIR_SCAN) != 0;
     const bool timing = (fr.flags & TR_FLAG_TILE_TIMING) != 0;
     if (timing && threadIdx.x == 0) atomicMin(&g_stats[ST_MARCH_T0], globaltimer_ns());
+    // the TF table into shared memory (MarchTabs)
+    extern __shared__ __align__(16) unsigned char s_tabs[];
+    MarchTabs tabs;
+    tabs.tf = nullptr;
+    if (march_tabs_bytes(BLK, E.n_tf)) {   // compile-time false unless BLK == 128
+        double *tf = reinterpret_cast<double *>(s_tabs);
+        for (int k2 = threadIdx.x; k2 < 4 * E.n_tf; k2 += BLK) tf[k2] = E.tf[k2];
+        tabs.tf = tf;
+        __syncthreads();
+    }
     uint32_t n_queue = 0;
     if (BRICK) n_queue = *(volatile const uint32_t *)F.B_ctr;
     else
@@ -1985,6 +2048,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
     bool active = false, exhausted = false, inline_mode = false, more = false;
 
     while (true) {
+        DBG_T(r0);
         // ---- refill: one queue slot per group that needs a ray
         const bool want = !active && !exhausted;
         const unsigned lm = __ballot_sync(FULL, want && j == 0);
@@ -2014,7 +2078,6 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                         s_tstart[g] = globaltimer_ns();
 #endif
                         s_pix[g] = (int32_t)px.ix; s_piy[g] = (int32_t)px.iy;
-                        s_o[0][g] = ray.ox; s_o[1][g] = ray.oy; s_o[2][g] = ray.oz;
                         s_d[0][g] = ray.dx; s_d[1][g] = ray.dy; s_d[2][g] = ray.dz;
                         s_phase[g] = fr.jitter ? hash01(px.ix, px.iy) : 0.5;
                         s_acc[0][g] = s_acc[1][g] = s_acc[2][g] = s_acc[3][g] = 0.0;
@@ -2094,15 +2157,18 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         }
 
         // ---- shade my sample (K:277-290)
+        DBG_T(r1);
         double4 sh = make_double4(0.0, 0.0, 0.0, 0.0);
         bool found = false;
         if (has)
-            sh = shade_sample(S, E, fr, s_o[0][g], s_o[1][g], s_o[2][g], s_d[0][g], s_d[1][g],
-                              s_d[2][g], a, k, s_phase[g], pid, stats, pair_scan, use_grid, use_cells,
-                              found);
+            sh = shade_sample<BLK == 128 && TR_TABS_TF>(
+                S, E, fr, fr.cam_pos[0], fr.cam_pos[1], fr.cam_pos[2], s_d[0][g], s_d[1][g],
+                s_d[2][g], a, k, s_phase[g], pid, stats, pair_scan, use_grid, use_cells, found,
+                &tabs);
         shade[j][threadIdx.x / G] = sh;
         const unsigned fbits = __ballot_sync(FULL, found) >> gbase;
         __syncwarp();
+        DBG_T(r2);
 
         // ---- composite the round in sample order (K:285-295)
         const int cnt = (int)((remaining < G) ? remaining : G);
@@ -2244,6 +2310,12 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
         }
         if (done || suspend) active = false;
         __syncwarp();
+#if TR_ROUND_TIMES
+        if (lane == 0) {
+            DBG_T(r3);
+            dbg_add(4, r1 - r0); dbg_add(5, r2 - r1); dbg_add(6, r3 - r2);
+        }
+#endif
     }
     if (timing && threadIdx.x == 0) atomicMax(&g_stats[ST_MARCH_T1], globaltimer_ns());
     // block reduction of the frame totals (R:198-201)
@@ -2369,8 +2441,8 @@ int sm_count() {
 
 // Resident CTAs per SM of a kernel, cached per (device, kernel): the query
 // costs several microseconds of host time on every frame otherwise.
-static cudaError_t occupancy(int *out, const void *fn, int block) {
-    struct Ent { int dev; const void *fn; int block, n; };
+static cudaError_t occupancy(int *out, const void *fn, int block, int smem = 0) {
+    struct Ent { int dev; const void *fn; int block, smem, n; };
     static Ent cache[64];
     static int n_cache = 0;
     static std::mutex mu;
@@ -2379,12 +2451,13 @@ static cudaError_t occupancy(int *out, const void *fn, int block) {
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(mu);
     for (int i = 0; i < n_cache; ++i)
-        if (cache[i].dev == dev && cache[i].fn == fn && cache[i].block == block) {
+        if (cache[i].dev == dev && cache[i].fn == fn && cache[i].block == block &&
+            cache[i].smem == smem) {
             *out = cache[i].n;
             return cudaSuccess;
         }
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, block, 0);
-    if (e == cudaSuccess && n_cache < 64) cache[n_cache++] = {dev, fn, block, *out};
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(out, fn, block, (size_t)smem);
+    if (e == cudaSuccess && n_cache < 64) cache[n_cache++] = {dev, fn, block, smem, *out};
     return e;
 }
 
@@ -2730,7 +2803,8 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
     }
     cudaError_t e;
     int per_sm = 0;
-    e = occupancy(&per_sm, (const void *)march_fn, march_block);
+    const int tabs_smem = march_tabs_bytes(march_block, epoch->n_tf);   // MarchTabs (dynamic smem)
+    e = occupancy(&per_sm, (const void *)march_fn, march_block, tabs_smem);
     if (e != cudaSuccess) return cuda_fail(e, "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
     if (per_sm < 1) per_sm = 1;
     if ((frame->flags >> 14) & 0x3) per_sm = (frame->flags >> 14) & 0x3;  // tuning: CTAs per SM
@@ -2811,7 +2885,7 @@ int tr_render_frame(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFr
             const int64_t need = (F.n_rays * gs[q] + march_block - 1) / march_block;
             if (grid > need) grid = need;
             if (grid < 1) grid = 1;
-            fns[q]<<<(unsigned)grid, march_block, 0, st>>>(S, E, F, iv, *out);
+            fns[q]<<<(unsigned)grid, march_block, tabs_smem, st>>>(S, E, F, iv, *out);
             e = cudaGetLastError();
             if (e != cudaSuccess) return cuda_fail(e, "march_kernel launch");
             ++launches;
@@ -2874,6 +2948,23 @@ int tr_kernel_stats(int64_t *out, int32_t n, int32_t reset) {
     e = cudaMemcpyFromSymbol(h, g_stats, sizeof h);
     if (e != cudaSuccess) return cuda_fail(e, "tr_kernel_stats copy");
     for (int i = 0; i < n && i < 32; ++i) out[i] = (int64_t)h[i];
+#if TR_ROUND_TIMES   // slots 24-31: the phase sums over every thread
+    {
+        static unsigned long long dbg[DBG_THREADS * DBG_PH];
+        if ((e = cudaMemcpyFromSymbol(dbg, g_dbg, sizeof dbg)) != cudaSuccess)
+            return cuda_fail(e, "tr_kernel_stats dbg");
+        for (int ph = 0; ph < DBG_PH && 24 + ph < n; ++ph) {
+            unsigned long long t = 0;
+            for (int i = 0; i < DBG_THREADS; ++i) t += dbg[i * DBG_PH + ph];
+            out[24 + ph] = (int64_t)t;
+        }
+        if (reset) {
+            for (int i = 0; i < DBG_THREADS * DBG_PH; ++i) dbg[i] = 0;
+            if ((e = cudaMemcpyToSymbol(g_dbg, dbg, sizeof dbg)) != cudaSuccess)
+                return cuda_fail(e, "tr_kernel_stats dbg reset");
+        }
+    }
+#endif
     if (reset) {
         for (int i = 0; i < 32; ++i) h[i] = 0;
         h[ST_MARCH_T0] = h[ST_MARCH_TQ] = ~0ull;   // atomicMin slots
@@ -3022,7 +3113,8 @@ int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
                                                                 march_sm_kernel<16, 3, true>};
     const int gs[2] = {4, 16};
     int per_sm = 0;
-    if ((e = occupancy(&per_sm, (const void *)fns[0], MARCH_BLOCK)) != cudaSuccess)
+    const int tabs_smem = march_tabs_bytes(MARCH_BLOCK, epoch->n_tf);
+    if ((e = occupancy(&per_sm, (const void *)fns[0], MARCH_BLOCK, tabs_smem)) != cudaSuccess)
         return cuda_fail(e, "occupancy(march)");
     if (per_sm < 1) per_sm = 1;
     F.auto_g = 1;
@@ -3034,7 +3126,7 @@ int tr_brick_round(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
         const int64_t need = (F.n_rays * gs[q] + MARCH_BLOCK - 1) / MARCH_BLOCK;
         if (grid > need) grid = need;
         if (grid < 1) grid = 1;
-        fns[q]<<<(unsigned)grid, MARCH_BLOCK, 0, st>>>(S, E, F, iv, *out);
+        fns[q]<<<(unsigned)grid, MARCH_BLOCK, tabs_smem, st>>>(S, E, F, iv, *out);
         if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e, "march_sm_kernel launch (bricks)");
     }
     return TR_OK;
