@@ -36,6 +36,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"tra
 timeout 1500 ncu --set full --clock-control none --import-source on -k regex:march_sm -s 2 -c 2 \
   -o gpurun_out/prof_march585_$TAG python bench.py --scene grid585 --steps 1 --warmup 1 --no-e2e --no-cpu --no-traffic > /dev/null 2>&1
 for sc in radial59 grid272; do timeout 300 python scripts/gpu_stats.py $sc >> gpurun_out/stats_$TAG.log 2>&1; done
+timeout 900 python scripts/brick_bench.py radial59 radial128 > gpurun_out/bricks_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
+timeout 600 python scripts/shard_timing.py grid272 skip-adaptive > gpurun_out/shard_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
+timeout 600 python scripts/shard_timing.py grid272 reference >> gpurun_out/shard_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
+timeout 600 python scripts/e2e_phases.py radial59 radial128 > gpurun_out/e2e_phases_$TAG.txt 2>&1
 timeout 1200 compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py > gpurun_out/sanitizer_$TAG.log 2>&1
 timeout 1200 compute-sanitizer --tool racecheck python scripts/sanitize_smoke.py >> gpurun_out/sanitizer_$TAG.log 2>&1
 echo done

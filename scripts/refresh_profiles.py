@@ -23,7 +23,9 @@ def last(f):
 for src, dst in ((f"modes_{tag}.jsonl", "bench_modes.jsonl"), (f"configs_{tag}.jsonl", "configs.jsonl"),
                  (f"stats_{tag}.log", "kernel_stats.txt"), (f"pytest_{tag}.log", "pytest.log"),
                  (f"smoke_{tag}.log", "smoke.log"), (f"box_{tag}.txt", "box.txt"),
-                 (f"sanitizer_{tag}.log", "sanitizer.log"), (f"launches_{tag}.csv", "launches.csv")):
+                 (f"sanitizer_{tag}.log", "sanitizer.log"), (f"launches_{tag}.csv", "launches.csv"),
+                 (f"bricks_{tag}.jsonl", "bricks.jsonl"), (f"shard_{tag}.jsonl", "shard_timing.jsonl"),
+                 (f"e2e_phases_{tag}.txt", "e2e_phases.txt")):
     if (g / src).exists():
         shutil.copy(g / src, p / dst)
 if (g / f"launches_{tag}.csv").exists():
