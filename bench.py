@@ -578,11 +578,13 @@ def main(argv=None):
             e2e = D.bench_e2e_sharded(scene, cam, args.mode, par, args.steps, dev)
         else:
             fb = None
-            for _ in range(max(args.warmup, 3)):
+            for _ in range(max(args.warmup, 10)):
                 dscene.mark_epochs_stale()
                 fb, st = B.render(scene, cam, args.mode, par, device=dev)
             per = []
-            e2e_steps = max(args.steps, 20)   # wall-clock: more steps for a stable mean
+            # wall clock: enough steps for a stable mean (~1 s of frames, 20-200)
+            frame_s = t_max / args.steps
+            e2e_steps = max(args.steps, 20, min(200, int(1.0 / max(frame_s, 1e-6))))
             t0 = time.perf_counter()
             for _ in range(e2e_steps):
                 t1 = time.perf_counter()

@@ -460,8 +460,10 @@ def render_sharded_gather(scene, camera, mode: str, params, *, jitter: bool = Fa
 
 def bench_e2e_sharded(scene, camera, mode: str, params, steps: int, device) -> dict:
     """End-to-end sharded frames through render_sharded: the epoch is
-    re-uploaded (H2D) every step on every rank and rank 0 reads the image
-    back (D2H); wall clock, max over ranks."""
+    re-uploaded (H2D) every step on every rank and the image reaches host
+    memory every step (one node: each rank's tiles stored into the shared
+    page-locked frame; across nodes: gathered to rank 0 and read back);
+    wall clock, max over ranks."""
     import torch
     import torch.distributed as dist
 
