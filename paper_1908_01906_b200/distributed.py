@@ -314,19 +314,36 @@ _SHARED: dict = {}
 _TOKEN: list = []
 
 
-def _shared_blocks(nbytes: int, rank: int) -> SharedBlocks:
-    """The node-shared block pool of one frame size (collective on first use)."""
+def _shared_blocks(nbytes: int, rank: int, device):
+    """The node-shared block pool of one frame size (collective on first
+    use), or None when any rank could not create / map / page-lock it (the
+    frame then takes the gather path; every rank agrees)."""
+    import torch
     import torch.distributed as dist
-    pool = _SHARED.get(nbytes)
-    if pool is None:
-        if not _TOKEN:   # one name prefix per process group, from rank 0
-            obj = [f"{os.getpid()}_{secrets.token_hex(4)}" if rank == 0 else None]
-            dist.broadcast_object_list(obj, src=0)
-            _TOKEN.append(obj[0])
-            atexit.register(release_shared_frames)
+    if nbytes in _SHARED:
+        return _SHARED[nbytes]
+    if not _TOKEN:   # one name prefix per process group, from rank 0
+        obj = [f"{os.getpid()}_{secrets.token_hex(4)}" if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        _TOKEN.append(obj[0])
+        atexit.register(release_shared_frames)
+    pool, ok = None, 1
+    try:
         pool = SharedBlocks(_TOKEN[0], nbytes, rank)
-        dist.barrier()   # block 0 exists before the other ranks map it
-        _SHARED[nbytes] = pool
+    except OSError:
+        ok = 0
+    dist.barrier()   # block 0 exists before the other ranks map it
+    if pool is not None:
+        try:
+            pool.block(0)
+        except (OSError, RuntimeError):
+            ok = 0
+    flag = torch.tensor([ok], dtype=torch.int32, device="cpu" if _gloo() else device)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) == 0 and pool is not None:
+        pool.close()
+        pool = None
+    _SHARED[nbytes] = pool
     return pool
 
 
@@ -335,7 +352,8 @@ def release_shared_frames() -> None:
     /dev/shm files; arrays rank 0 returned stay valid).  Runs at exit; call it
     where processes end without atexit (multiprocessing workers)."""
     for pool in _SHARED.values():
-        pool.close()
+        if pool is not None:
+            pool.close()
     _SHARED.clear()
 
 
@@ -369,9 +387,13 @@ def render_sharded(scene, camera, mode: str, params, *, jitter: bool = False,
     w, h = int(camera.width), int(camera.height)
     npx = w * h
     P = dscene.n_parts
+    pool = _shared_blocks(40 * npx, rank, dscene.device)
+    if pool is None:
+        return render_sharded_gather(scene, camera, mode, params, jitter=jitter,
+                                     track_per_partition=track_per_partition, device=device,
+                                     flags=flags)
     frame = dscene.frame_desc(scene, camera, _MODE_IDS[mode], params, jitter, track, flags,
                               shard_rank=rank, shard_count=world, compact=False)
-    pool = _shared_blocks(40 * npx, rank)
     t0 = time.perf_counter()
     with dscene.lock, torch.cuda.device(dscene.device):
         stream = torch.cuda.current_stream(dscene.device)
