@@ -2112,10 +2112,12 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
 
         // ---- inline mode: lane 0 fetches the next interval with samples when needed
         bool idle = false;
-        if (active && inline_mode && j == 0 && L.k >= L.n)
-            idle = !inline_next(S, E, fr, s_pix[g], s_piy[g], s_phase[g], L);
-        __syncwarp();
-        idle = __shfl_sync(FULL, idle, gbase);
+        if (__any_sync(FULL, active && inline_mode)) {   // rare: skip the sync otherwise
+            if (active && inline_mode && j == 0 && L.k >= L.n)
+                idle = !inline_next(S, E, fr, s_pix[g], s_piy[g], s_phase[g], L);
+            __syncwarp();
+            idle = __shfl_sync(FULL, idle, gbase);
+        }
 
         // ---- my sample
         bool has = false;
