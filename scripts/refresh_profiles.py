@@ -18,9 +18,11 @@ def last(f):
     return (g / f).read_text().strip().splitlines()[-1] + "\n"
 
 
+full = (g / f"bench_ref_{tag}.json").exists()   # gpu_final_r02.sh (else the short refresh)
 (p / "bench.json").write_text(last(f"bench_{tag}.json"))
-(p / "bench_reference.json").write_text(last(f"bench_ref_{tag}.json"))
-for src, dst in ((f"modes_{tag}.jsonl", "bench_modes.jsonl"), (f"configs_{tag}.jsonl", "configs.jsonl"),
+if full:
+    (p / "bench_reference.json").write_text(last(f"bench_ref_{tag}.json"))
+for src, dst in ((f"modes_{tag}.jsonl", "bench_modes.jsonl"), (f"configs_{tag}.jsonl", "configs.jsonl" if full else f"configs_{tag}.jsonl"),
                  (f"stats_{tag}.log", "kernel_stats.txt"), (f"pytest_{tag}.log", "pytest.log"),
                  (f"smoke_{tag}.log", "smoke.log"), (f"box_{tag}.txt", "box.txt"),
                  (f"sanitizer_{tag}.log", "sanitizer.log"), (f"launches_{tag}.csv", "launches.csv"),
