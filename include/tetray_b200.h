@@ -505,6 +505,37 @@ int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv1
 /* ids: NULL -> records in id order (pleaf_ids = NULL); else records in
  * 8^3-cube brick order and ids[k] (n_tets u32) = tet id of record k. */
 
+/* Device build of the point-location structures of an ARBITRARY mesh
+ * (csrc/pbuild.cu; replaces MeshSampler's host BVH build,
+ * mesh.py:246-254 / bvh.py:41-98, and this library's host builders
+ * tr_tet_boxes + tr_pbvh_build + tr_pbvh_grid + tr_cells_build): Morton
+ * codes of the padded tet boxes' centres, a Karras radix tree collapsed to
+ * leaves of <= leaf_max tets, bottom-up refit, exclusive boxes, the leaf grid
+ * and -- when the grid's coverage is below cells_below -- the cell candidate
+ * lists.  vertices (V,3) f64 and tets (T,4) i64 are DEVICE pointers; leaves
+ * carry no walk tables.  The handle owns device buffers until tr_dpb_free. */
+typedef struct TrDevPointBuild TrDevPointBuild;
+int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_tets,
+                         const int64_t *tets, double pad, int32_t leaf_max, double cells_below,
+                         int32_t refine, int32_t max_list, void *stream, TrDevPointBuild **out);
+/* sizes6: n_nodes, n_leaves, n_ids (= n_tets), grid cells, cell-list cells (0: none),
+ * cell-list entries. */
+int tr_dpb_sizes(const TrDevPointBuild *b, int64_t *sizes6);
+int tr_dpb_grid(const TrDevPointBuild *b, int32_t *gdim3, double *gorg3, double *gscale3,
+                double *coverage, int32_t *cdim3, double *corg3, double *cscale3);
+/* Device-to-device copy into caller buffers (any may be NULL); grid_leaf: one
+ * TrPLeaf per grid cell (its candidate's header, an empty box for -1). */
+int tr_dpb_copy(const TrDevPointBuild *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids,
+                int32_t *grid, TrPLeaf *grid_leaf, uint32_t *cell_off, uint32_t *cell_recs,
+                float *tbox, void *stream);
+void tr_dpb_free(TrDevPointBuild *b);
+/* tr_pack_tets on the device: every pointer a device pointer. */
+int tr_pack_tets_device(int64_t n, const int64_t *tets, const double *tet_orig,
+                        const double *tet_inv, const double *field, int32_t centering,
+                        const uint32_t *order, TrTetRecord *out, void *stream);
+/* Host (pageable) -> device copy through page-locked staging (synchronous). */
+int tr_upload(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Replaces _kernels.field_at_many (K:157-170): pts (n,3) f64 device;
  * found (n,) u8, vals (n,) f64, tet (n,) i64 (may be NULL) device. */
 int tr_field_at_many(const TrDeviceScene *scene, int64_t n, const double *pts, uint8_t *found,

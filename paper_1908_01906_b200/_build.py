@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libtetray_b200.so"
-SOURCES = ["render.cu", "synth.cu", "meta.cu", "epilogue.cu", "host_build.cpp", "common.cpp"]
+SOURCES = ["render.cu", "synth.cu", "pbuild.cu", "meta.cu", "epilogue.cu", "host_build.cpp", "common.cpp"]
 HEADERS = [ROOT / "include" / "tetray_b200.h", CSRC / "tr_internal.h", CSRC / "glibc_pow.cuh"]
 
 NVCC_FLAGS = [

@@ -193,6 +193,18 @@ _SIGNATURES = [
     ("tr_grid_scene_sizes", C.c_int, [C.c_int64, c_i64p, c_i64p, c_i64p]),
     ("tr_grid_scene_build", C.c_int, [C.c_int64, C.c_int32, C.c_double, c_f64p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_pbvh_build_device", C.c_int, [C.c_int64, C.c_void_p, C.c_int64, C.c_void_p, C.c_double,
+                                       C.c_int32, C.c_double, C.c_int32, C.c_int32, C.c_void_p,
+                                       C.POINTER(C.c_void_p)]),
+    ("tr_dpb_sizes", C.c_int, [C.c_void_p, c_i64p]),
+    ("tr_dpb_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, c_f64p, C.c_void_p, c_f64p,
+                              c_f64p]),
+    ("tr_dpb_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_dpb_free", None, [C.c_void_p]),
+    ("tr_pack_tets_device", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_upload", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("tr_quantize_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("tr_heatmap_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p]),

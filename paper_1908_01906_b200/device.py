@@ -99,6 +99,19 @@ CELL_COVERAGE_MIN = 0.9   # below this mean grid coverage the cell lists are bui
 CELL_REFINE = 2           # cell-list grid: the point grid refined 2x per axis
 CELL_MAX_LIST = 96        # longer lists fall back to the BVH descent
 
+POINT_BUILD_ENV = "TETRAY_POINT_BUILD"
+
+
+def point_build_mode(scene) -> str:
+    """Where a general mesh's point-location structures are built:
+    "host" (host_build.cpp, with the leaf walk tables: the fastest march) or
+    "device" (csrc/pbuild.cu: Morton LBVH in HBM, no walk tables).  From
+    scene.point_build, else $TETRAY_POINT_BUILD, else "host"."""
+    m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "host"
+    if m not in ("host", "device"):
+        raise ValueError(f"point_build must be 'host' or 'device', not {m!r}")
+    return m if scene.mesh.n_tets > _LEAF_MAX else "host"
+
 
 def build_point_bvh(box_lo: np.ndarray, box_hi: np.ndarray, leaf_max: int = _LEAF_MAX,
                     cells=None):
@@ -376,6 +389,8 @@ class DeviceScene:
             self.n_tets = int(mesh.n_tets if self.tet_subset is None else len(self.tet_subset))
             if getattr(mesh, "device_generated", False):
                 point = self._point_structures_grid(scene)
+            elif point_build_mode(scene) == "device" and self.tet_subset is None:
+                point = self._point_structures_device(scene)
             else:
                 point = self._point_structures_host(scene)
             self.build_s = time.perf_counter() - t0
@@ -485,6 +500,86 @@ class DeviceScene:
             self.t_crecs = _upload(lists.recs, device)
             self.t_tbox = _upload(lists.tbox, device)
         return len(pnodes), len(pleaves)
+
+    def _point_structures_device(self, scene):
+        """The same structures built in HBM (csrc/pbuild.cu):
+        mesh arrays uploaded once through page-locked staging, then Morton
+        LBVH, exclusive boxes, leaf grid, cell lists and the records in leaf
+        order on the device.  No walk tables (leaves scanned in id order)."""
+        torch = _torch()
+        device = self.device
+        L = _lib.lib()
+        mesh, sampler = scene.mesh, scene.sampler
+        stream = torch.cuda.current_stream(device)
+        sp = C.c_void_p(stream.cuda_stream)
+
+        def up(arr, dtype):
+            a = np.ascontiguousarray(arr, dtype=dtype)
+            t = torch.empty(a.nbytes, dtype=torch.uint8, device=device)
+            _lib.check(L.tr_upload(C.c_void_p(t.data_ptr()), _lib.vptr(a), a.nbytes, sp), "tr_upload")
+            return t
+
+        t0 = time.perf_counter()
+        t_verts, t_tets = up(mesh.vertices, np.float64), up(mesh.tets, np.int64)
+        t_up = time.perf_counter() - t0
+        pad = BOX_PAD_REL * max(mesh.bounds.diagonal(), 1e-30)
+        cells = getattr(scene, "cell_lists", None)
+        below = CELL_COVERAGE_MIN if cells is None else (2.0 if cells else -1.0)
+        h = C.c_void_p()
+        _lib.check(L.tr_pbvh_build_device(len(mesh.vertices), C.c_void_p(t_verts.data_ptr()), mesh.n_tets,
+                                          C.c_void_p(t_tets.data_ptr()), pad, _LEAF_MAX, below,
+                                          CELL_REFINE, CELL_MAX_LIST, sp, C.byref(h)),
+                   "tr_pbvh_build_device")
+        try:
+            sz = np.zeros(6, np.int64)
+            _lib.check(L.tr_dpb_sizes(h, _lib.ptr(sz, C.c_int64)), "tr_dpb_sizes")
+            n_nodes, n_leaves, n_ids, n_grid, n_cc, n_cr = (int(x) for x in sz)
+            grid = PointGrid(np.zeros(3, np.int32), np.zeros(3), np.zeros(3), None)
+            cdim, corg, cscale, cov = np.zeros(3, np.int32), np.zeros(3), np.zeros(3), np.zeros(1)
+            _lib.check(L.tr_dpb_grid(h, _lib.vptr(grid.dims), _lib.ptr(grid.org, C.c_double),
+                                     _lib.ptr(grid.scale, C.c_double), _lib.ptr(cov, C.c_double),
+                                     _lib.vptr(cdim), _lib.ptr(corg, C.c_double),
+                                     _lib.ptr(cscale, C.c_double)), "tr_dpb_grid")
+            grid.coverage = float(cov[0])
+            u8 = lambda n: torch.empty(max(int(n), 1), dtype=torch.uint8, device=device)
+            self.t_pnodes = u8(n_nodes * _lib.PNODE_DTYPE.itemsize)
+            self.t_pleaves = u8(n_leaves * _lib.PLEAF_DTYPE.itemsize)
+            self.t_pids = u8(n_ids * 4)
+            self.t_grid = u8(n_grid * 4)
+            self.t_grid_leaf = u8(n_grid * _lib.PLEAF_DTYPE.itemsize)
+            self.t_grid_pred = None          # no walk tables -> no walk-start predictor
+            lists = None
+            if n_cc:
+                lists = CellLists(cdim, corg, cscale, None, None, None)
+                self.t_coff = u8((n_cc + 1) * 4)
+                self.t_crecs = u8(n_cr * 4)
+                self.t_tbox = u8(n_ids * 32)
+            dp = lambda t: C.c_void_p(t.data_ptr())
+            _lib.check(L.tr_dpb_copy(h, dp(self.t_pnodes), dp(self.t_pleaves), dp(self.t_pids),
+                                     dp(self.t_grid), dp(self.t_grid_leaf),
+                                     dp(self.t_coff) if lists else None,
+                                     dp(self.t_crecs) if lists else None,
+                                     dp(self.t_tbox) if lists else None, sp), "tr_dpb_copy")
+        finally:
+            L.tr_dpb_free(h)
+        del t_verts
+        # records in leaf order, packed on the device
+        t1 = time.perf_counter()
+        t_orig = up(sampler.tet_orig, np.float64)
+        t_inv = up(sampler.tet_inv, np.float64)
+        t_field = up(mesh.field, np.float64)
+        t_up += time.perf_counter() - t1
+        self.t_tets = u8(n_ids * _lib.TET_RECORD_DTYPE.itemsize)
+        _lib.check(L.tr_pack_tets_device(n_ids, dp(t_tets), dp(t_orig), dp(t_inv), dp(t_field),
+                                         int(mesh.centering), dp(self.t_pids), dp(self.t_tets), sp),
+                   "tr_pack_tets_device")
+        stream.synchronize()
+        del t_tets, t_orig, t_inv, t_field
+        self.pnodes_host = self.pleaves_host = None
+        self.grid = grid
+        self.cells = lists
+        self.upload_s = t_up
+        return n_nodes, n_leaves
 
     def _point_structures_grid(self, scene):
         """Synthetic cube-grid scene generated in HBM (tr_grid_scene_build,
