@@ -100,6 +100,9 @@ def parse(argv=None):
                     help="records: KD-brick record sharding (bricks.py; one brick per rank, "
                          "or --bricks bricks emulated on one GPU)")
     ap.add_argument("--bricks", type=int, default=2, help="--shard records on one GPU: bricks")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "sum"],
+                    help="--shard records, N > 1: ray states pushed to peer inboxes over NVLink "
+                         "(CUDA IPC) or a SUM all-reduce of the state array per round")
     ap.add_argument("--flags", type=lambda x: int(x, 0), default=0,
                     help="TR_FLAG_* bits (tuning experiments; bits 8-11 = log2 group size)")
     return ap.parse_args(argv)
@@ -405,7 +408,7 @@ def run_records(args, world, rank, local):
     cam, par = C.camera(B, name, scale=args.scale), C.params(B, name)
     n = world if world > 1 else args.bricks
     br = BR.BrickRenderer(scene, n, max(par.s1, par.s2), device=dev,
-                          dist=dist if world > 1 else None)
+                          dist=dist if world > 1 else None, exchange=args.exchange)
     setup_s = time.perf_counter() - t0
     for _ in range(args.warmup):
         br.render(cam, args.mode, par)
@@ -435,11 +438,13 @@ def run_records(args, world, rank, local):
                            "rounds": br.rounds, "tets_per_brick": br.tets_per_brick,
                            "exact_vs_one_gpu_render": exact,
                            "one_gpu_frame_ms": one[1].device_ms,
+                           "exchange": br.exchange if world > 1 else None,
                            "state_exchange_bytes_per_round": int(cam.width * cam.height * 64)
-                           if world > 1 else 0,
+                           if world > 1 and br.exchange == "sum" else None,
                            "setup_s": round(setup_s, 2)}}
         print(json.dumps(line), flush=True)
     if world > 1:
+        br.close()
         dist.destroy_process_group()
     return 0
 

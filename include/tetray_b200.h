@@ -452,8 +452,15 @@ int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
  * count are exactly the single-GPU frame's.  Mode 0's one mesh-box interval
  * is cut at the brick boxes (records keep its entry: sample k stays
  * entry + (k + phase) s1).  Rounds repeat until no ray is active; between
- * rounds the ranks exchange states (each active ray was advanced by exactly
- * one rank: an int64 SUM all-reduce of the states, zero elsewhere, is exact).
+ * rounds the ranks exchange states.  Two exchanges: (a) SUM -- each active
+ * ray was advanced by exactly one rank, so an int64 SUM all-reduce of the
+ * states (zero elsewhere, zero_foreign = 1) is exact; (b) PEER (n_peers > 0)
+ * -- the march stores each state it finishes straight into every peer's
+ * inbox over NVLink (peer_inbox: CUDA IPC mappings), tagged with the round;
+ * the next round's plan takes the inbox entries of the previous round (an
+ * inbox per round parity, so a round's stores never meet a reader of the
+ * round before).  Only the rays a rank advanced cross the link, and the
+ * ranks need no more than a barrier between rounds (no SUM, no host read).
  * The frame must fit one ray chunk (tr_scratch_bytes(W*H)). */
 typedef struct TrRayState {   /* 64 B per ray */
     double acc[4];
@@ -463,7 +470,7 @@ typedef struct TrRayState {   /* 64 B per ray */
     uint32_t cbefore;          /* cum before interval icur */
     uint32_t stop;             /* end of the current run (set by the plan) */
     uint32_t flags;            /* 1 active, 2 done */
-    uint32_t pad;
+    uint32_t tag;              /* PEER exchange: exchange_tag of the round that wrote it + 1 */
 } TrRayState;
 
 typedef struct TrBricks {
@@ -477,6 +484,14 @@ typedef struct TrBricks {
     uint32_t *counters;        /* [4] device: rays queued, rays active, error bits, spare */
     int32_t zero_foreign;      /* 1: zero the states of rays another brick advances (SUM exchange) */
     int32_t write_background;  /* 1: the trace writes the background pixels (one rank only) */
+    /* PEER exchange (n_peers = 0: off).  exchange_tag = 256 * frame number
+     * (>= 1, the same on every rank) + round; inbox = this rank's [2][rays]
+     * states (device, zeroed once); peer_inbox[2 r + p] = rank r's inbox of
+     * round parity p mapped here (device array of 2 n_bricks pointers). */
+    uint32_t exchange_tag;
+    int32_t n_peers;
+    TrRayState *const *peer_inbox;
+    TrRayState *inbox;
 } TrBricks;
 
 /* Trace + state init of a brick-sharded frame (any brick's scene: the
@@ -533,6 +548,12 @@ void tr_dpb_free(TrDevPointBuild *b);
 int tr_pack_tets_device(int64_t n, const int64_t *tets, const double *tet_orig,
                         const double *tet_inv, const double *field, int32_t centering,
                         const uint32_t *order, TrTetRecord *out, void *stream);
+/* CUDA IPC for the PEER brick exchange: a zeroed device allocation and its
+ * 64-B handle; open a peer's handle (peer access enabled lazily); close; free. */
+int tr_ipc_alloc(int64_t bytes, void **dptr, void *handle64);
+int tr_ipc_open(const void *handle64, void **dptr);
+int tr_ipc_close(void *dptr);
+int tr_dev_free(void *dptr);
 /* Host (pageable) -> device copy through page-locked staging (synchronous). */
 int tr_upload(void *dst, const void *src, int64_t bytes, void *stream);
 

@@ -97,6 +97,8 @@ class TrBricks(C.Structure):
         ("owner", C.c_void_p), ("brick_lo", C.c_void_p), ("brick_hi", C.c_void_p),
         ("state", C.c_void_p), ("queue", C.c_void_p), ("counters", C.c_void_p),
         ("zero_foreign", C.c_int32), ("write_background", C.c_int32),
+        ("exchange_tag", C.c_uint32), ("n_peers", C.c_int32),
+        ("peer_inbox", C.c_void_p), ("inbox", C.c_void_p),
     ]
 
 
@@ -204,6 +206,10 @@ _SIGNATURES = [
     ("tr_dpb_free", None, [C.c_void_p]),
     ("tr_pack_tets_device", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("tr_ipc_alloc", C.c_int, [C.c_int64, C.POINTER(C.c_void_p), C.c_void_p]),
+    ("tr_ipc_open", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
+    ("tr_ipc_close", C.c_int, [C.c_void_p]),
+    ("tr_dev_free", C.c_int, [C.c_void_p]),
     ("tr_upload", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("tr_quantize_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     ("tr_heatmap_rgb", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p,

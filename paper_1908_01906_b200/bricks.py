@@ -139,13 +139,24 @@ class BrickRenderer:
     s1): it sets the halo, so frames with larger steps are refused."""
 
     def __init__(self, scene, n_bricks: int, max_step: float, device=None, dist=None,
-                 sync_rounds: Optional[bool] = None):
+                 sync_rounds: Optional[bool] = None, exchange: str = "sum"):
         """sync_rounds: read the active-ray count back after every round
         (default for the one-device emulation) or run n_bricks rounds with no
         host read first (default with `dist`: a ray's runs cross each convex
         brick at most once, so n rounds finish every ray; one synchronized
-        round then confirms it -- and keeps going if ever needed)."""
+        round then confirms it -- and keeps going if ever needed).
+
+        exchange (with `dist`): "sum" -- an int64 SUM all-reduce of the whole
+        state array per round; "peer" -- the march stores each state it
+        finishes into the other ranks' inboxes through CUDA IPC mappings
+        (NVLink on one node), so only the rays a rank advanced move and a
+        round needs just a barrier (the ranks must share a node)."""
         import torch
+        if exchange not in ("sum", "peer"):
+            raise ValueError(f"exchange must be 'sum' or 'peer', not {exchange!r}")
+        self.exchange = exchange if dist is not None else "sum"
+        self._frame_no = 0
+        self._ipc = []   # (own inbox pointer, opened peer pointers)
         self.scene = scene
         self.device = resolve_device(device)
         self.dist = dist
@@ -185,8 +196,61 @@ class BrickRenderer:
             fb.scratch = torch.empty(fb.scratch_bytes, dtype=torch.uint8, device=self.device)
             state = torch.empty(rays * _lib.RAY_STATE_BYTES, dtype=torch.uint8, device=self.device)
             queue = torch.empty(rays, dtype=torch.int32, device=self.device)
-            self._bufs[key] = (fb, state, queue)
+            peer = self._peer_inboxes(rays) if self.exchange == "peer" else None
+            self._bufs[key] = (fb, state, queue, peer)
         return self._bufs[key]
+
+    def _peer_inboxes(self, rays: int):
+        """PEER exchange: this rank's [2][rays] inbox (CUDA IPC allocation)
+        and the device table of every rank's inbox mapped here."""
+        import torch
+        L = _lib.lib()
+        nbytes = 2 * rays * _lib.RAY_STATE_BYTES
+        own, h = C.c_void_p(), (C.c_ubyte * 64)()
+        with torch.cuda.device(self.device):
+            _lib.check(L.tr_ipc_alloc(nbytes, C.byref(own), h), "tr_ipc_alloc")
+            handles = [None] * self.dist.get_world_size()
+            self.dist.all_gather_object(handles, bytes(h))
+            table, opened = [], []
+            for r, hr in enumerate(handles):
+                if r == self.dist.get_rank():
+                    table += [0, 0]
+                    continue
+                buf = C.create_string_buffer(hr, 64)
+                p = C.c_void_p()
+                _lib.check(L.tr_ipc_open(C.cast(buf, C.c_void_p), C.byref(p)), "tr_ipc_open")
+                opened.append(p.value)
+                table += [p.value, p.value + rays * _lib.RAY_STATE_BYTES]
+            t_table = torch.tensor(table, dtype=torch.int64, device=self.device)
+        self._ipc.append((own.value, opened))
+        self._token = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return own.value, t_table
+
+    def _round_barrier(self, stream) -> None:
+        """PEER exchange: every rank's round (and its NVLink stores) is done
+        before any rank plans the next one."""
+        if self.dist.get_backend() == "nccl":
+            self.dist.all_reduce(self._token)   # stream-ordered, no host wait
+        else:
+            stream.synchronize()
+            self.dist.barrier()
+
+    def close(self) -> None:
+        """Release the PEER inboxes (collective: every rank calls it)."""
+        if not self._ipc:
+            return
+        import torch
+        torch.cuda.synchronize(self.device)
+        self.dist.barrier()
+        L = _lib.lib()
+        for own, opened in self._ipc:
+            for p in opened:
+                L.tr_ipc_close(C.c_void_p(p))
+        self.dist.barrier()
+        for own, _ in self._ipc:
+            L.tr_dev_free(C.c_void_p(own))
+        self._ipc = []
+        self._bufs.clear()
 
     def render(self, camera, mode: str, params, *, jitter: bool = False,
                track_per_partition: bool = True, flags: int = 0, profile: bool = False):
@@ -208,7 +272,8 @@ class BrickRenderer:
         with torch.cuda.device(self.device):
             ep = dev0.epoch(sc.meta_state(), params)   # partition data is global
             frame = dev0._frame_desc(sc, camera, mid, params, jitter, track, flags, 0, 1, False)
-            fb, state, queue = self._buffers(w, h)
+            fb, state, queue, peer = self._buffers(w, h)
+            self._frame_no += 1
             fb.counters.zero_()
             if self.dist is not None:
                 fb.rgba.zero_(); fb.samples.zero_(); fb.visited.zero_()
@@ -217,8 +282,19 @@ class BrickRenderer:
                               owner=self.t_owner.data_ptr(), brick_lo=self.t_lo.data_ptr(),
                               brick_hi=self.t_hi.data_ptr(), state=state.data_ptr(),
                               queue=queue.data_ptr(), counters=self.counters.data_ptr(),
-                              zero_foreign=1 if self.dist is not None else 0,
+                              zero_foreign=1 if self.exchange == "sum" and self.dist is not None else 0,
                               write_background=1 if self.mine[0] == 0 else 0)
+            if peer is not None:
+                B.n_peers = self.bricks.n - 1
+                B.inbox, B.peer_inbox = peer[0], peer[1].data_ptr()
+
+            def exchange():
+                if self.dist is None:
+                    return
+                if peer is None:   # exactly one rank advanced each active ray
+                    self.dist.all_reduce(state.view(torch.int64))
+                else:
+                    self._round_barrier(stream)
             L = _lib.lib()
             s = C.c_void_p(stream.cuda_stream)
             ev = []   # profile: (round, brick, start event, end event)
@@ -234,6 +310,7 @@ class BrickRenderer:
                 ev.append((-1, -1, None, mark()))   # end of the trace
             if not self.sync_rounds:
                 for _ in range(self.bricks.n):   # no host reads between these rounds
+                    B.exchange_tag = 256 * self._frame_no + rounds
                     for b in self.mine:
                         B.rank = b
                         e0 = mark() if profile else None
@@ -243,12 +320,14 @@ class BrickRenderer:
                         if profile:
                             ev.append((rounds, b, e0, mark()))
                     rounds += 1
-                    if self.dist is not None:
-                        self.dist.all_reduce(state.view(torch.int64))
+                    exchange()
             while True:
                 active = None
                 if profile:
                     ev.append((-1, -1, None, mark()))   # end of the trace / previous round
+                if rounds >= 255:
+                    raise RuntimeError("brick frame did not finish in 255 rounds")
+                B.exchange_tag = 256 * self._frame_no + rounds
                 for b in self.mine:
                     B.rank = b
                     e0 = mark() if profile else None
@@ -267,8 +346,7 @@ class BrickRenderer:
                 if active == 0:
                     break
                 rounds += 1
-                if self.dist is not None:   # exactly one rank advanced each active ray
-                    self.dist.all_reduce(state.view(torch.int64))
+                exchange()
             fb.end.record(stream)
             if self.dist is not None:
                 # every pixel and count was written by exactly one rank

@@ -649,12 +649,13 @@ __global__ void pack_kernel(int64_t n, const int64_t *__restrict__ tets, const d
 // Scratch of one build (freed on every exit path).
 struct Scratch {
     cudaStream_t st;
-    void *p[32] = {};
+    void *p[64] = {};
     int n = 0;
     cudaError_t err = cudaSuccess;
     template <class T>
     T *get(size_t count) {
         void *q = nullptr;
+        if (n == (int)(sizeof p / sizeof p[0])) err = cudaErrorMemoryAllocation;   // table full
         if (err == cudaSuccess) err = cudaMallocAsync(&q, count * sizeof(T) + 16, st);
         if (err != cudaSuccess) return nullptr;
         p[n++] = q;
@@ -956,4 +957,34 @@ extern "C" int tr_upload(void *dst, const void *src, int64_t bytes, void *stream
         if (stage[i]) cudaFreeHost(stage[i]);
     }
     return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_upload");
+}
+
+extern "C" int tr_ipc_alloc(int64_t bytes, void **dptr, void *handle64) {
+    if (bytes <= 0 || !dptr || !handle64) return tr_fail(TR_EINVAL, "tr_ipc_alloc: invalid arguments");
+    cudaError_t e = cudaMalloc(dptr, (size_t)bytes);
+    if (e == cudaSuccess) e = cudaMemset(*dptr, 0, (size_t)bytes);
+    cudaIpcMemHandle_t h;
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, *dptr);
+    if (e != cudaSuccess) return cuda_fail(e, "tr_ipc_alloc");
+    static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+    memcpy(handle64, &h, sizeof h);
+    return TR_OK;
+}
+
+extern "C" int tr_ipc_open(const void *handle64, void **dptr) {
+    if (!handle64 || !dptr) return tr_fail(TR_EINVAL, "tr_ipc_open: invalid arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle64, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_ipc_open");
+}
+
+extern "C" int tr_ipc_close(void *dptr) {
+    cudaError_t e = cudaIpcCloseMemHandle(dptr);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_ipc_close");
+}
+
+extern "C" int tr_dev_free(void *dptr) {
+    cudaError_t e = cudaFree(dptr);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_dev_free");
 }

@@ -851,6 +851,11 @@ struct FrameK {
     const double *B_lo, *B_hi;
     TrRayState *B_state;
     uint32_t *B_queue, *B_ctr;
+    // PEER exchange (B_npeers > 0): states pushed to the peers' inboxes
+    uint32_t B_tag;
+    int32_t B_npeers;
+    TrRayState *const *B_peer_inbox;
+    TrRayState *B_inbox;
 };
 
 // One stored interval of a ray (16 B): next_interval's clamped entry, the
@@ -2299,6 +2304,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     TrRayState st = {};
                     st.flags = 2u;
                     F.B_state[s_rr[g]] = st;
+                    if (F.B_npeers) push_state(F, s_rr[g], st);
                 }
             } else if (BRICK && suspend) {
                 TrRayState st = {};
@@ -2308,6 +2314,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 st.taken = s_taken[g]; st.icur = s_icur[g]; st.cbefore = s_cbefore[g];
                 st.flags = 1u;
                 F.B_state[s_rr[g]] = st;
+                if (F.B_npeers) push_state(F, s_rr[g], st);
             }
         }
         if (done || suspend) active = false;
@@ -2492,6 +2499,20 @@ constexpr int64_t IV_FIXED_BYTES = 1024;
 
 // ---- brick-sharded frames (tr_brick_*)
 
+// PEER exchange: the state a run leaves goes into every other rank's inbox
+// of this round's parity (NVLink stores through CUDA IPC mappings), tagged so
+// that the next round's plan takes exactly this round's entries.
+__device__ __noinline__ void push_state(const FrameK &F, int64_t rr, TrRayState st) {
+    st.tag = F.B_tag + 1u;
+    const int par = (int)(F.B_tag & 1u);
+    for (int r = 0; r < F.B_n; ++r) {
+        if (r == F.B_rank) continue;
+        TrRayState *dst = F.B_peer_inbox[2 * r + par];
+        if (dst) dst[rr] = st;   // already rank r's parity-par inbox
+    }
+    __threadfence_system();
+}
+
 __device__ __forceinline__ int brick_of(const FrameK &F, int32_t pid) {
     return pid >= 0 ? (int)__ldg(F.B_owner + pid) : (-1 - pid);
 }
@@ -2509,6 +2530,13 @@ __global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
         TrRayState st = {};
         if (rr < F.n_rays) {
             st = F.B_state[rr];
+            if (F.B_npeers) {   // a peer advanced this ray last round: its state is in my inbox
+                const TrRayState in = F.B_inbox[(int64_t)((F.B_tag - 1u) & 1u) * F.n_rays + rr];
+                if (in.tag == F.B_tag) {
+                    st = in;
+                    F.B_state[rr] = in;
+                }
+            }
             act = st.flags == 1u;
         }
         if (act) {
@@ -3058,6 +3086,13 @@ static int brick_setup(const TrDeviceScene *scene, const TrEpoch *epoch, const T
     F.B_state = bricks->state;
     F.B_queue = bricks->queue;
     F.B_ctr = bricks->counters;
+    F.B_tag = bricks->exchange_tag;
+    F.B_npeers = bricks->n_peers;
+    F.B_peer_inbox = bricks->peer_inbox;
+    F.B_inbox = bricks->inbox;
+    if (F.B_npeers && (!F.B_peer_inbox || !F.B_inbox || F.B_zero_foreign || bricks->exchange_tag < 256))
+        return tr_fail(TR_EINVAL, "tr_brick: PEER exchange needs peer_inbox, inbox, zero_foreign = 0 "
+                                  "and exchange_tag >= 256");
     iv = make_iv(out, F.n_rays);
     return TR_OK;
 }

@@ -78,7 +78,7 @@ def test_bricks_refuse_steps_beyond_the_halo(B):
         br.render(cam, "skip-adaptive", par)
 
 
-def _dist_worker(rank, world, port, q):
+def _dist_worker(rank, world, port, q, exchange="sum"):
     import os
     import sys
     sys.path[:0] = [str(cases.ROOT), str(cases.ROOT / "tests")]
@@ -89,20 +89,25 @@ def _dist_worker(rank, world, port, q):
     try:
         sc = cases.build_scene(B, "radial16")
         cam, par = cases.camera(B, "radial16", scale=0.25), cases.params(B, "radial16")
-        br = BR.BrickRenderer(sc, world, par.s2, dist=dist)
+        br = BR.BrickRenderer(sc, world, par.s2, dist=dist, exchange=exchange)
         out = {}
-        for mode in ("reference", "skip-adaptive"):
-            fb, st = br.render(cam, mode, par)
-            out[mode] = (fb.rgba, fb.samples, st.total_samples, st.partitions_visited_mean,
-                         st.per_partition_samples, br.rounds)
+        for rep in range(2):   # the second frame reuses the inboxes (frame-tagged states)
+            for mode in ("reference", "skip-adaptive"):
+                fb, st = br.render(cam, mode, par)
+                out[mode] = (fb.rgba, fb.samples, st.total_samples, st.partitions_visited_mean,
+                             st.per_partition_samples, br.rounds)
+        br.close()
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
 
 
-def test_bricks_dist_gpu(B):
-    """Two ranks (processes sharing the GPU, gloo all-reduces of CUDA
-    tensors) each hold one brick; both assemble the one-device frame."""
+@pytest.mark.parametrize("exchange", ["sum", "peer"])
+def test_bricks_dist_gpu(B, exchange):
+    """Two ranks (processes sharing the GPU) each hold one brick; both
+    assemble the one-device frame.  sum: gloo all-reduces of the CUDA state
+    array; peer: the march stores finished states into the other rank's
+    inbox through a CUDA IPC mapping (the NVLink path), gloo barriers."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
@@ -110,7 +115,7 @@ def test_bricks_dist_gpu(B):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q, exchange)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
