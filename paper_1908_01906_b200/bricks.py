@@ -284,6 +284,7 @@ class BrickRenderer:
                               queue=queue.data_ptr(), counters=self.counters.data_ptr(),
                               zero_foreign=1 if self.exchange == "sum" and self.dist is not None else 0,
                               write_background=1 if self.mine[0] == 0 else 0)
+            B.exchange_tag = 256 * self._frame_no
             if peer is not None:
                 B.n_peers = self.bricks.n - 1
                 B.inbox, B.peer_inbox = peer[0], peer[1].data_ptr()

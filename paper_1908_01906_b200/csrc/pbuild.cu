@@ -927,6 +927,11 @@ extern "C" int tr_upload(void *dst, const void *src, int64_t bytes, void *stream
     if (bytes < 0 || (bytes > 0 && (!dst || !src))) return tr_fail(TR_EINVAL, "tr_upload: invalid arguments");
     if (bytes == 0) return TR_OK;
     cudaStream_t st = (cudaStream_t)stream;
+    if (bytes <= ((int64_t)1 << 20)) {   // small: the driver's own staging
+        cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_upload");
+    }
     const int64_t CH = (int64_t)64 << 20;
     const int nbuf = bytes > CH ? 2 : 1;
     void *stage[2] = {nullptr, nullptr};

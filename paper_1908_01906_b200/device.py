@@ -60,9 +60,17 @@ def resolve_device(device=None):
 
 
 def _upload(arr: np.ndarray, device):
+    """Host array -> new device byte tensor, synchronously, through the
+    library's page-locked staging (tr_upload: a pageable copy of a fresh
+    numpy array runs at a fraction of PCIe speed)."""
     torch = _torch()
     raw = np.ascontiguousarray(arr).view(np.uint8).reshape(-1)
-    return torch.from_numpy(raw).to(device)  # synchronous copy; `arr` outlives it
+    t = torch.empty(raw.nbytes, dtype=torch.uint8, device=device)
+    if raw.nbytes:
+        stream = torch.cuda.current_stream(t.device)
+        _lib.check(_lib.lib().tr_upload(C.c_void_p(t.data_ptr()), _lib.vptr(raw), raw.nbytes,
+                                        C.c_void_p(stream.cuda_stream)), "tr_upload")
+    return t
 
 
 def _padded_boxes(scene) -> tuple[np.ndarray, np.ndarray]:
@@ -104,12 +112,14 @@ POINT_BUILD_ENV = "TETRAY_POINT_BUILD"
 
 def point_build_mode(scene) -> str:
     """Where a general mesh's point-location structures are built:
-    "host" (host_build.cpp, with the leaf walk tables: the fastest march) or
-    "device" (csrc/pbuild.cu: Morton LBVH in HBM, no walk tables).  From
-    scene.point_build, else $TETRAY_POINT_BUILD, else "host"."""
+    "host" (host_build.cpp, with the leaf walk tables: the fastest march),
+    "device" (csrc/pbuild.cu: Morton LBVH in HBM, no walk tables) or
+    "device-walk" (the device build, then the host's leaf walk tables and
+    walk-start predictors attached to its leaves: the host build's march).
+    From scene.point_build, else $TETRAY_POINT_BUILD, else "host"."""
     m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "host"
-    if m not in ("host", "device"):
-        raise ValueError(f"point_build must be 'host' or 'device', not {m!r}")
+    if m not in ("host", "device", "device-walk"):
+        raise ValueError(f"point_build must be 'host', 'device' or 'device-walk', not {m!r}")
     return m if scene.mesh.n_tets > _LEAF_MAX else "host"
 
 
@@ -389,8 +399,10 @@ class DeviceScene:
             self.n_tets = int(mesh.n_tets if self.tet_subset is None else len(self.tet_subset))
             if getattr(mesh, "device_generated", False):
                 point = self._point_structures_grid(scene)
-            elif point_build_mode(scene) == "device" and self.tet_subset is None:
+            elif point_build_mode(scene) != "host" and self.tet_subset is None:
                 point = self._point_structures_device(scene)
+                if point_build_mode(scene) == "device-walk":
+                    self._attach_walk_tables(scene)
             else:
                 point = self._point_structures_host(scene)
             self.build_s = time.perf_counter() - t0
@@ -580,6 +592,31 @@ class DeviceScene:
         self.cells = lists
         self.upload_s = t_up
         return n_nodes, n_leaves
+
+    def _attach_walk_tables(self, scene):
+        """tr_leaf_walk (host, long-double certificates) over the device-built
+        leaves: walk tables into the leaf headers and the per-cell copies,
+        walk-start predictors per grid cell (as _point_structures_host)."""
+        mesh = scene.mesh
+        pleaves = self.t_pleaves.cpu().numpy().view(_lib.PLEAF_DTYPE).copy()
+        pids = np.ascontiguousarray(self.t_pids.cpu().numpy().view(np.uint32))
+        verts = np.ascontiguousarray(mesh.vertices, dtype=np.float64)
+        tets = np.ascontiguousarray(mesh.tets, dtype=np.int64)
+        pred = np.zeros((len(pleaves), 12), np.float32)
+        _lib.check(_lib.lib().tr_leaf_walk(len(pleaves), _lib.vptr(pleaves), _lib.vptr(pids),
+                                           _lib.vptr(verts), _lib.vptr(tets), _lib.vptr(pred)),
+                   "tr_leaf_walk")
+        cells = self.t_grid.cpu().numpy().view(np.int32)
+        has = cells >= 0
+        cell_leaf = np.zeros(len(cells), dtype=_lib.PLEAF_DTYPE)
+        cell_leaf["ex_lo"] = 1.0
+        cell_leaf["ex_hi"] = 0.0
+        cell_leaf[has] = pleaves[cells[has]]
+        cell_pred = np.zeros((len(cells), 12), np.float32)
+        cell_pred[has] = pred[cells[has]]
+        self.t_pleaves = _upload(pleaves, self.device)
+        self.t_grid_leaf = _upload(cell_leaf, self.device)
+        self.t_grid_pred = _upload(cell_pred, self.device)
 
     def _point_structures_grid(self, scene):
         """Synthetic cube-grid scene generated in HBM (tr_grid_scene_build,

@@ -36,7 +36,7 @@ for recipe in sys.argv[1:]:
     sc = C.build_scene(B, recipe)
     scene_s = time.perf_counter() - t0
     res = {}
-    for build in ("device", "host"):
+    for build in ("device", "device-walk", "host"):
         getattr(sc, _CACHE_ATTR, {}).clear()
         gc.collect()
         torch.cuda.empty_cache()
@@ -59,7 +59,8 @@ for recipe in sys.argv[1:]:
         res[build] = row
         print(json.dumps(row), flush=True)
     for mode in ("skip-adaptive", "reference"):
-        assert res["device"][f"{mode}_samples"] == res["host"][f"{mode}_samples"], (recipe, mode)
+        for b in ("device", "device-walk"):
+            assert res[b][f"{mode}_samples"] == res["host"][f"{mode}_samples"], (recipe, b, mode)
     del sc
     gc.collect()
     torch.cuda.empty_cache()

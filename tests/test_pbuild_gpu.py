@@ -32,14 +32,14 @@ def B(built_lib):
 _SCENES = {}
 
 
-def device_built(B, recipe):
-    """(scene with point_build = "device", oracle scene)."""
-    if recipe not in _SCENES:
+def device_built(B, recipe, mode="device"):
+    """(scene with point_build = mode, oracle scene)."""
+    if (recipe, mode) not in _SCENES:
         from oracle.oracle import OracleScene
         sc = C.build_scene(B, recipe)
-        sc.point_build = "device"
-        _SCENES[recipe] = (sc, OracleScene(sc))
-    return _SCENES[recipe]
+        sc.point_build = mode
+        _SCENES[(recipe, mode)] = (sc, OracleScene(sc))
+    return _SCENES[(recipe, mode)]
 
 
 def dev_of(sc):
@@ -75,6 +75,25 @@ def test_device_built_radial59(B, golden, mode):
     for flags in (0, 0x80):
         fb, st = B.render(sc, cam, mode, par, flags=flags)
         _check_radial59(fb, st, g, orc, cam, mode, par)
+
+
+@pytest.mark.parametrize("recipe", ["radial16", "radial59"])
+def test_device_walk_frames(B, golden, recipe):
+    """point_build = "device-walk": the device build plus the host's walk
+    tables and predictors on its leaves -- the reference's frames, and the
+    walk really is used (predictors present)."""
+    sc, orc = device_built(B, recipe, "device-walk")
+    dev = dev_of(sc)
+    assert dev.t_grid_pred is not None
+    _, leaves, _ = _download(dev)
+    assert (leaves["walk"][:, 4] >> 31).any(), "no valid walk table attached"
+    cam, par = C.camera(B, recipe), C.params(B, recipe)
+    for mode in ("reference", "skip", "skip-adaptive"):
+        ref = orc.render(cam, mode, par)
+        g = golden["frames"][f"{recipe}/{mode}"]
+        for flags in (0, 0x2000000):
+            fb, st = B.render(sc, cam, mode, par, flags=flags)
+            _compare(fb, st, ref, mode, g if recipe != "radial59" else None)
 
 
 @pytest.mark.parametrize("recipe", ["jitter8", "jitter16", "jitter32"])
