@@ -116,8 +116,10 @@ def point_build_mode(scene) -> str:
     "device" (csrc/pbuild.cu: Morton LBVH in HBM, no walk tables) or
     "device-walk" (the device build, then the host's leaf walk tables and
     walk-start predictors attached to its leaves: the host build's march).
-    From scene.point_build, else $TETRAY_POINT_BUILD, else "host"."""
-    m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "host"
+    From scene.point_build, else $TETRAY_POINT_BUILD, else "device-walk"
+    (measured at or below the host build's frame time on every scene, ready
+    2-4x sooner: DESIGN.md §8a)."""
+    m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "device-walk"
     if m not in ("host", "device", "device-walk"):
         raise ValueError(f"point_build must be 'host', 'device' or 'device-walk', not {m!r}")
     return m if scene.mesh.n_tets > _LEAF_MAX else "host"
@@ -402,7 +404,9 @@ class DeviceScene:
             elif point_build_mode(scene) != "host" and self.tet_subset is None:
                 point = self._point_structures_device(scene)
                 if point_build_mode(scene) == "device-walk":
+                    tw = time.perf_counter()
                     self._attach_walk_tables(scene)
+                    self.build_phases["walk_s"] = time.perf_counter() - tw
             else:
                 point = self._point_structures_host(scene)
             self.build_s = time.perf_counter() - t0
@@ -538,6 +542,7 @@ class DeviceScene:
         cells = getattr(scene, "cell_lists", None)
         below = CELL_COVERAGE_MIN if cells is None else (2.0 if cells else -1.0)
         h = C.c_void_p()
+        tb = time.perf_counter()
         _lib.check(L.tr_pbvh_build_device(len(mesh.vertices), C.c_void_p(t_verts.data_ptr()), mesh.n_tets,
                                           C.c_void_p(t_tets.data_ptr()), pad, _LEAF_MAX, below,
                                           CELL_REFINE, CELL_MAX_LIST, sp, C.byref(h)),
@@ -574,9 +579,10 @@ class DeviceScene:
                                      dp(self.t_tbox) if lists else None, sp), "tr_dpb_copy")
         finally:
             L.tr_dpb_free(h)
+        t_build = time.perf_counter() - tb
         del t_verts
         # records in leaf order, packed on the device
-        t1 = time.perf_counter()
+        t1, t_up0 = time.perf_counter(), t_up
         t_orig = up(sampler.tet_orig, np.float64)
         t_inv = up(sampler.tet_inv, np.float64)
         t_field = up(mesh.field, np.float64)
@@ -586,6 +592,8 @@ class DeviceScene:
                                          int(mesh.centering), dp(self.t_pids), dp(self.t_tets), sp),
                    "tr_pack_tets_device")
         stream.synchronize()
+        self.build_phases = {"upload_s": t_up, "lbvh_s": t_build,
+                             "pack_s": time.perf_counter() - t1 - (t_up - t_up0)}
         del t_tets, t_orig, t_inv, t_field
         self.pnodes_host = self.pleaves_host = None
         self.grid = grid

@@ -51,7 +51,8 @@ for recipe in sys.argv[1:]:
                "upload_s": round(getattr(dev, "upload_s", float("nan")), 3),
                "n_leaves": int(dev.desc.n_pleaves), "n_nodes": int(dev.desc.n_pnodes),
                "grid_coverage": round(float(getattr(dev.grid, "coverage", float("nan"))), 4),
-               "cell_lists": dev.cells is not None}
+               "cell_lists": dev.cells is not None,
+               "phases": {k: round(v, 3) for k, v in getattr(dev, "build_phases", {}).items()}}
         for mode in ("skip-adaptive", "reference"):
             ms, tot = frame_ms(sc, recipe, mode)
             row[f"{mode}_ms"] = round(ms, 4)

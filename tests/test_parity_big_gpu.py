@@ -5,7 +5,8 @@ samples):
 
   config 3  radial128 (10.5M tets) and radial272 (100.6M tets), 512^2, all
             three modes -- both through the general host build
-            (Scene.build -> csrc/host_build.cpp) and through the HBM-generated
+            (Scene.build; point location built by the default device build,
+            csrc/pbuild.cu + host walk tables) and through the HBM-generated
             GridScene the benchmark uses
   config 5  radial59 at 1536^2 (three ray chunks), all three modes
 

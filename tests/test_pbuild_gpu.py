@@ -225,3 +225,20 @@ def test_device_built_config3_matches_reference(B, recipe):
         sc.point_build = None
         for k in list(getattr(sc, _CACHE_ATTR, {}) or {}):
             del getattr(sc, _CACHE_ATTR)[k]
+
+
+@pytest.mark.parametrize("recipe", ["radial16", "jitter16", "radial59"])
+def test_host_point_build_still_matches(B, golden, recipe):
+    """point_build = "host" (host_build.cpp; the default is the device
+    build): the same frames."""
+    sc, orc = device_built(B, recipe, "host")
+    dev = dev_of(sc)
+    assert not hasattr(dev, "build_phases"), "expected the host build"
+    cam, par = C.camera(B, recipe), C.params(B, recipe)
+    if cam.width > 256:
+        cam = B.Camera(position=cam.position, look_at=cam.look_at, up=cam.up,
+                       fov_y_deg=cam.fov_y_deg, width=192, height=160)
+    for mode in ("reference", "skip", "skip-adaptive"):
+        ref = orc.render(cam, mode, par)
+        fb, st = B.render(sc, cam, mode, par)
+        _compare(fb, st, ref, mode)
