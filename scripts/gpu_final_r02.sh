@@ -39,6 +39,8 @@ for sc in radial59 grid272; do timeout 300 python scripts/gpu_stats.py $sc >> gp
 timeout 900 python scripts/brick_bench.py radial59 radial128 > gpurun_out/bricks_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
 timeout 600 python scripts/shard_timing.py grid272 skip-adaptive > gpurun_out/shard_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
 timeout 600 python scripts/shard_timing.py grid272 reference >> gpurun_out/shard_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
+timeout 900 python scripts/pbuild_timing.py radial272 > gpurun_out/pbuild_timing_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
+timeout 900 python scripts/pbuild_timing.py jitter59 radial128 >> gpurun_out/pbuild_timing_$TAG.jsonl 2>>gpurun_out/configs_$TAG.err
 timeout 600 python scripts/e2e_phases.py radial59 radial128 > gpurun_out/e2e_phases_$TAG.txt 2>&1
 timeout 1200 compute-sanitizer --tool memcheck python scripts/sanitize_smoke.py > gpurun_out/sanitizer_$TAG.log 2>&1
 timeout 1200 compute-sanitizer --tool racecheck python scripts/sanitize_smoke.py >> gpurun_out/sanitizer_$TAG.log 2>&1

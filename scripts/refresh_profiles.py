@@ -27,7 +27,8 @@ for src, dst in ((f"modes_{tag}.jsonl", "bench_modes.jsonl"), (f"configs_{tag}.j
                  (f"smoke_{tag}.log", "smoke.log"), (f"box_{tag}.txt", "box.txt"),
                  (f"sanitizer_{tag}.log", "sanitizer.log"), (f"launches_{tag}.csv", "launches.csv"),
                  (f"bricks_{tag}.jsonl", "bricks.jsonl"), (f"shard_{tag}.jsonl", "shard_timing.jsonl"),
-                 (f"e2e_phases_{tag}.txt", "e2e_phases.txt")):
+                 (f"e2e_phases_{tag}.txt", "e2e_phases.txt"),
+                 (f"pbuild_timing_{tag}.jsonl", "pbuild_timing.jsonl")):
     if (g / src).exists():
         shutil.copy(g / src, p / dst)
 if (g / f"launches_{tag}.csv").exists():

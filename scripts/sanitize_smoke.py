@@ -1,5 +1,5 @@
 """Small frames through every kernel path, for compute-sanitizer runs:
-candidate raster / BSP walk / BVH, all modes, jitter, ragged frame, shards,
+the point-location builds (device / device-walk / host), candidate raster / BSP walk / BVH, all modes, jitter, ragged frame, shards,
 bricks, direct host framebuffer and staged outputs, chunked frames."""
 import sys
 from pathlib import Path
@@ -39,6 +39,17 @@ for recipe in ("golden_radial4", "conftest48", "inside", "axis", "a6fog", "jitte
         b = br.render(cam, mode, par)
         assert np.array_equal(a[0].rgba, b[0].rgba), (recipe, mode, "bricks")
     print(recipe, "ok", flush=True)
+# the point-location builds (default: device LBVH + host walk tables): the
+# device build alone (cell lists on the unstructured mesh) and the host build
+for recipe in ("golden_radial4", "jitter8"):
+    cam, par = C.camera(B, recipe), C.params(B, recipe)
+    ref = {m: B.render(C.build_scene(B, recipe), cam, m, par)[0].rgba for m in ("reference", "skip-adaptive")}
+    for build in ("device", "host"):
+        sc = C.build_scene(B, recipe)
+        sc.point_build = build
+        for mode in ("reference", "skip-adaptive"):
+            assert np.array_equal(ref[mode], B.render(sc, cam, mode, par)[0].rgba), (recipe, build, mode)
+    print(recipe, "point builds ok", flush=True)
 # an HBM-generated grid: analytic cube leaves (default) and leaf headers
 sc = C.build_scene(B, "grid12")
 cam, par = C.camera(B, "radial16", scale=0.125), C.params(B, "radial16")
