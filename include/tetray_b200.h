@@ -538,11 +538,17 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
 int tr_dpb_sizes(const TrDevPointBuild *b, int64_t *sizes6);
 int tr_dpb_grid(const TrDevPointBuild *b, int32_t *gdim3, double *gorg3, double *gscale3,
                 double *coverage, int32_t *cdim3, double *corg3, double *cscale3);
-/* Device-to-device copy into caller buffers (any may be NULL); grid_leaf: one
- * TrPLeaf per grid cell (its candidate's header, an empty box for -1). */
+/* The leaves' walk tables and walk-start predictors on the device
+ * (tr_leaf_walk's tables; a CERTIFIED bit only where the orientation
+ * determinants prove the separation with their error bounds, so a subset of
+ * the host's long-double certificates).  vertices/tets: device pointers. */
+int tr_dpb_walk(TrDevPointBuild *b, const double *vertices, const int64_t *tets, void *stream);
+/* Device-to-device copy into caller buffers (any may be NULL); grid_leaf /
+ * grid_pred: per grid cell, its candidate's header / predictor (an empty box
+ * / zeros for -1; predictors only after tr_dpb_walk). */
 int tr_dpb_copy(const TrDevPointBuild *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids,
-                int32_t *grid, TrPLeaf *grid_leaf, uint32_t *cell_off, uint32_t *cell_recs,
-                float *tbox, void *stream);
+                int32_t *grid, TrPLeaf *grid_leaf, TrLeafPred *grid_pred, uint32_t *cell_off,
+                uint32_t *cell_recs, float *tbox, void *stream);
 void tr_dpb_free(TrDevPointBuild *b);
 /* tr_pack_tets on the device: every pointer a device pointer. */
 int tr_pack_tets_device(int64_t n, const int64_t *tets, const double *tet_orig,

@@ -201,8 +201,10 @@ _SIGNATURES = [
     ("tr_dpb_sizes", C.c_int, [C.c_void_p, c_i64p]),
     ("tr_dpb_grid", C.c_int, [C.c_void_p, C.c_void_p, c_f64p, c_f64p, c_f64p, C.c_void_p, c_f64p,
                               c_f64p]),
+    ("tr_dpb_walk", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("tr_dpb_copy", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
-                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                              C.c_void_p]),
     ("tr_dpb_free", None, [C.c_void_p]),
     ("tr_pack_tets_device", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),

@@ -57,6 +57,7 @@ struct TrDevPointBuild {
     int32_t *grid = nullptr;
     uint32_t *coff = nullptr, *crecs = nullptr;
     float *tbox = nullptr;
+    TrLeafPred *pred = nullptr;   // tr_dpb_walk: walk-start predictor per leaf
 };
 
 namespace {
@@ -608,9 +609,15 @@ __global__ void tbox_kernel(int64_t nrec, const uint32_t *__restrict__ ids, cons
 }
 
 __global__ void grid_leaf_kernel(int64_t n, const int32_t *__restrict__ grid, const TrPLeaf *__restrict__ leaves,
-                                 TrPLeaf *__restrict__ out) {
+                                 TrPLeaf *__restrict__ out, const TrLeafPred *__restrict__ pred,
+                                 TrLeafPred *__restrict__ pred_out) {
     GRID_STRIDE(c, n) {
         const int32_t L = grid[c];
+        if (pred_out) {
+            TrLeafPred p = {};
+            if (L >= 0 && pred) p = pred[L];
+            pred_out[c] = p;
+        }
         TrPLeaf lf;
         if (L >= 0) {
             lf = leaves[L];
@@ -668,7 +675,7 @@ struct Scratch {
 
 void free_build(TrDevPointBuild *B) {
     if (!B) return;
-    void *ps[] = {B->nodes, B->leaves, B->ids, B->grid, B->coff, B->crecs, B->tbox};
+    void *ps[] = {B->nodes, B->leaves, B->ids, B->grid, B->coff, B->crecs, B->tbox, B->pred};
     for (void *q : ps)
         if (q) cudaFreeAsync(q, B->st);
     cudaStreamSynchronize(B->st);
@@ -881,7 +888,8 @@ int tr_dpb_grid(const TrDevPointBuild *b, int32_t *gdim3, double *gorg3, double 
 }
 
 int tr_dpb_copy(const TrDevPointBuild *b, TrPNode *nodes, TrPLeaf *leaves, uint32_t *ids, int32_t *grid,
-                TrPLeaf *grid_leaf, uint32_t *cell_off, uint32_t *cell_recs, float *tbox, void *stream) {
+                TrPLeaf *grid_leaf, TrLeafPred *grid_pred, uint32_t *cell_off, uint32_t *cell_recs, float *tbox,
+                void *stream) {
     if (!b) return tr_fail(TR_EINVAL, "tr_dpb_copy: invalid arguments");
     cudaStream_t st = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
@@ -898,7 +906,8 @@ int tr_dpb_copy(const TrDevPointBuild *b, TrPNode *nodes, TrPLeaf *leaves, uint3
         cp(tbox, b->tbox, b->n_tets * 8 * sizeof(float));
     }
     if (e == cudaSuccess && grid_leaf)
-        grid_leaf_kernel<<<grid_for(b->n_grid), 256, 0, st>>>(b->n_grid, b->grid, b->leaves, grid_leaf);
+        grid_leaf_kernel<<<grid_for(b->n_grid), 256, 0, st>>>(b->n_grid, b->grid, b->leaves, grid_leaf, b->pred,
+                                                              grid_pred);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_dpb_copy");
@@ -962,6 +971,176 @@ extern "C" int tr_upload(void *dst, const void *src, int64_t bytes, void *stream
         if (stage[i]) cudaFreeHost(stage[i]);
     }
     return e == cudaSuccess ? TR_OK : cuda_fail(e, "tr_upload");
+}
+
+// ---------------------------------------------------------------- walk tables
+// tr_leaf_walk's tables (host_build.cpp walk_table) on the device: face
+// neighbours by shared vertex ids, the walk's first tet (largest volume),
+// the walk-start predictor, and the CERTIFIED bit of tet i when every
+// lower-id tet j of the leaf is separated from it (host `separated`: a face
+// plane of j has i shrunk to barycentrics >= TAU / 2 beyond -(1e-9 + 1e-8),
+// or a face plane of i has j inflated by that slack below TAU / 2).  The host
+// evaluates the barycentrics in long double; here each one is a ratio of
+// orientation determinants, and a face test passes only if it passes with
+// the determinants' forward error bound (Shewchuk's orient3d bound, taken as
+// 1e-15 x the permanent) added against it -- so a device certificate implies
+// the exact one (tests compare the device tables with tr_leaf_walk's).
+namespace {
+
+constexpr double W_TOL = 1e-9, W_M1 = 1e-8, W_TAU = TR_WALK_TAU;
+
+__device__ __forceinline__ double orient_eb(const double *a, const double *b, const double *c, const double *x,
+                                            double &eb) {
+    const double ad0 = a[0] - x[0], ad1 = a[1] - x[1], ad2 = a[2] - x[2];
+    const double bd0 = b[0] - x[0], bd1 = b[1] - x[1], bd2 = b[2] - x[2];
+    const double cd0 = c[0] - x[0], cd1 = c[1] - x[1], cd2 = c[2] - x[2];
+    const double det = ad0 * (bd1 * cd2 - bd2 * cd1) + ad1 * (bd2 * cd0 - bd0 * cd2) + ad2 * (bd0 * cd1 - bd1 * cd0);
+    const double perm = fabs(ad0) * (fabs(bd1 * cd2) + fabs(bd2 * cd1)) +
+                        fabs(ad1) * (fabs(bd2 * cd0) + fabs(bd0 * cd2)) +
+                        fabs(ad2) * (fabs(bd0 * cd1) + fabs(bd1 * cd0));
+    eb = 1e-15 * perm;
+    return det;
+}
+
+__device__ __forceinline__ void face_of(int f, int o[3]) {
+    int m = 0;
+    for (int q = 0; q < 4; ++q)
+        if (q != f) o[m++] = q;
+}
+
+// For every point x in pts[4]: sign(D) O_f(x) + off |D| <= 0 with the error
+// bounds against it, where l_f(x) = O_f(x) / D (tet T's barycentric of f).
+__device__ bool face_rejects(const double (*T)[3], int f, const double (*pts)[3], double off) {
+    int o[3];
+    face_of(f, o);
+    double eD;
+    const double D = orient_eb(T[o[0]], T[o[1]], T[o[2]], T[f], eD);
+    if (!(fabs(D) > eD)) return false;
+    const double sg = D > 0.0 ? 1.0 : -1.0;
+    for (int i = 0; i < 4; ++i) {
+        double eO;
+        const double O = orient_eb(T[o[0]], T[o[1]], T[o[2]], pts[i], eO);
+        if (!(sg * O + off * fabs(D) + eO + fabs(off) * eD <= 0.0)) return false;
+    }
+    return true;
+}
+
+__device__ bool separated_dev(const double (*J)[3], const double (*K)[3]) {
+    double sk[3] = {0, 0, 0}, sj[3] = {0, 0, 0};
+    for (int i = 0; i < 4; ++i)
+        for (int a = 0; a < 3; ++a) { sk[a] += K[i][a]; sj[a] += J[i][a]; }
+    const double s = W_TOL + W_M1;
+    double w[4][3], u[4][3];
+    for (int i = 0; i < 4; ++i)
+        for (int a = 0; a < 3; ++a) {
+            w[i][a] = (1.0 - 2.0 * W_TAU) * K[i][a] + 0.5 * W_TAU * sk[a];
+            u[i][a] = (1.0 + 4.0 * s) * J[i][a] - s * sj[a];
+        }
+    for (int f = 0; f < 4; ++f) {
+        if (face_rejects(J, f, w, s)) return true;              // l_f^J(w) <= -(slack + margin)
+        if (face_rejects(K, f, u, -0.5 * W_TAU)) return true;   // l_f^K(u) <= TAU / 2
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(128) walk_kernel(int64_t n_leaves, TrPLeaf *__restrict__ leaves,
+                                                   const uint32_t *__restrict__ ids, const double *__restrict__ V,
+                                                   const int64_t *__restrict__ tets, TrLeafPred *__restrict__ pred) {
+    GRID_STRIDE(L, n_leaves) {
+        TrPLeaf &lf = leaves[L];
+        uint32_t walk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        TrLeafPred pr = {};
+        const int n = (int)min(lf.count, 9u);
+        bool ok = n >= 1 && n <= 8;
+        double P[8][4][3];
+        int64_t vid[8][4], tid[8];
+        double inv[8][3][3];
+        double vmax = 0.0, imax = 0.0, vol_best = -1.0;
+        int first = 0;
+        for (int i = 0; ok && i < n; ++i) {
+            tid[i] = ids[lf.start + i];
+            for (int q = 0; q < 4; ++q) {
+                vid[i][q] = tets[4 * tid[i] + q];
+                for (int a = 0; a < 3; ++a) {
+                    P[i][q][a] = V[3 * vid[i][q] + a];
+                    vmax = fmax(vmax, fabs(P[i][q][a]));
+                }
+            }
+            double e[3][3];   // columns v1-v0, v2-v0, v3-v0
+            for (int a = 0; a < 3; ++a)
+                for (int c = 0; c < 3; ++c) e[a][c] = P[i][c + 1][a] - P[i][0][a];
+            const double det = e[0][0] * (e[1][1] * e[2][2] - e[1][2] * e[2][1]) -
+                               e[0][1] * (e[1][0] * e[2][2] - e[1][2] * e[2][0]) +
+                               e[0][2] * (e[1][0] * e[2][1] - e[1][1] * e[2][0]);
+            if (!(det != 0.0 && isfinite(det))) { ok = false; break; }
+            double (&m)[3][3] = inv[i];
+            m[0][0] = (e[1][1] * e[2][2] - e[1][2] * e[2][1]) / det;
+            m[0][1] = (e[0][2] * e[2][1] - e[0][1] * e[2][2]) / det;
+            m[0][2] = (e[0][1] * e[1][2] - e[0][2] * e[1][1]) / det;
+            m[1][0] = (e[1][2] * e[2][0] - e[1][0] * e[2][2]) / det;
+            m[1][1] = (e[0][0] * e[2][2] - e[0][2] * e[2][0]) / det;
+            m[1][2] = (e[0][2] * e[1][0] - e[0][0] * e[1][2]) / det;
+            m[2][0] = (e[1][0] * e[2][1] - e[1][1] * e[2][0]) / det;
+            m[2][1] = (e[0][1] * e[2][0] - e[0][0] * e[2][1]) / det;
+            m[2][2] = (e[0][0] * e[1][1] - e[0][1] * e[1][0]) / det;
+            double isum = 0.0;
+            for (int r = 0; r < 3; ++r)
+                for (int c = 0; c < 3; ++c) isum += fabs(m[r][c]);
+            imax = fmax(imax, isum);
+            const double vol = fabs(det);
+            if (vol > vol_best) { vol_best = vol; first = i; }
+        }
+        if (ok) {
+            const bool certifiable = imax * (vmax + 1.0) * 0x1p-51 < 1e-10;
+            for (int i = 0; i < n; ++i) {
+                uint32_t e = 0;
+                for (int f = 0; f < 4; ++f) {
+                    int64_t fa[3];
+                    int m = 0;
+                    for (int q = 0; q < 4; ++q)
+                        if (q != f) fa[m++] = vid[i][q];
+                    int nb = i;
+                    for (int j = 0; j < n && nb == i; ++j) {
+                        if (j == i) continue;
+                        int hits = 0;
+                        for (int q = 0; q < 4; ++q)
+                            hits += (vid[j][q] == fa[0]) + (vid[j][q] == fa[1]) + (vid[j][q] == fa[2]);
+                        if (hits == 3) nb = j;
+                    }
+                    e |= (uint32_t)nb << (3 * f);
+                }
+                bool cert = certifiable;
+                for (int j = 0; j < n && cert; ++j)
+                    if (tid[j] < tid[i]) cert = separated_dev(P[j], P[i]);
+                if (cert) e |= 1u << 12;
+                walk[i >> 1] |= e << (16 * (i & 1));
+            }
+            walk[4] = (uint32_t)first | (1u << 31);
+            for (int r = 0; r < 3; ++r) {
+                double d = 0.0;
+                for (int c = 0; c < 3; ++c) {
+                    pr.row[r][c] = (float)inv[first][r][c];
+                    d += inv[first][r][c] * ((double)lf.ex_lo[c] - P[first][0][c]);
+                }
+                pr.row[r][3] = (float)d;
+            }
+        }
+        for (int k = 0; k < 8; ++k) lf.walk[k] = walk[k];
+        if (pred) pred[L] = pr;
+    }
+}
+
+}  // namespace
+
+extern "C" int tr_dpb_walk(TrDevPointBuild *b, const double *vertices, const int64_t *tets, void *stream) {
+    if (!b || !vertices || !tets) return tr_fail(TR_EINVAL, "tr_dpb_walk: invalid arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (!b->pred) e = cudaMallocAsync(&b->pred, std::max<int64_t>(b->n_leaves, 1) * sizeof(TrLeafPred), st);
+    if (e != cudaSuccess) return cuda_fail(e, "tr_dpb_walk: allocation");
+    walk_kernel<<<grid_for(b->n_leaves) * 2, 128, 0, st>>>(b->n_leaves, b->leaves, b->ids, vertices, tets, b->pred);
+    if ((e = cudaGetLastError()) == cudaSuccess) e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? TR_OK : cuda_fail(e, "walk_kernel");
 }
 
 extern "C" int tr_ipc_alloc(int64_t bytes, void **dptr, void *handle64) {

@@ -108,20 +108,19 @@ CELL_REFINE = 2           # cell-list grid: the point grid refined 2x per axis
 CELL_MAX_LIST = 96        # longer lists fall back to the BVH descent
 
 POINT_BUILD_ENV = "TETRAY_POINT_BUILD"
+POINT_BUILDS = ("device", "device-nowalk", "device-hostwalk", "host")
 
 
 def point_build_mode(scene) -> str:
     """Where a general mesh's point-location structures are built:
-    "host" (host_build.cpp, with the leaf walk tables: the fastest march),
-    "device" (csrc/pbuild.cu: Morton LBVH in HBM, no walk tables) or
-    "device-walk" (the device build, then the host's leaf walk tables and
-    walk-start predictors attached to its leaves: the host build's march).
-    From scene.point_build, else $TETRAY_POINT_BUILD, else "device-walk"
-    (measured at or below the host build's frame time on every scene, ready
-    2-4x sooner: DESIGN.md §8a)."""
-    m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "device-walk"
-    if m not in ("host", "device", "device-walk"):
-        raise ValueError(f"point_build must be 'host', 'device' or 'device-walk', not {m!r}")
+    "device" (csrc/pbuild.cu: Morton LBVH, exclusive boxes, grid, cell lists
+    and the leaf walk tables, all in HBM), "device-nowalk" (the same without
+    walk tables), "device-hostwalk" (the device build with the host's
+    long-double walk tables, tr_leaf_walk) or "host" (host_build.cpp).  From
+    scene.point_build, else $TETRAY_POINT_BUILD, else "device"."""
+    m = getattr(scene, "point_build", None) or os.environ.get(POINT_BUILD_ENV) or "device"
+    if m not in POINT_BUILDS:
+        raise ValueError(f"point_build must be one of {POINT_BUILDS}, not {m!r}")
     return m if scene.mesh.n_tets > _LEAF_MAX else "host"
 
 
@@ -402,8 +401,8 @@ class DeviceScene:
             if getattr(mesh, "device_generated", False):
                 point = self._point_structures_grid(scene)
             elif point_build_mode(scene) != "host" and self.tet_subset is None:
-                point = self._point_structures_device(scene)
-                if point_build_mode(scene) == "device-walk":
+                point = self._point_structures_device(scene, point_build_mode(scene) == "device")
+                if point_build_mode(scene) == "device-hostwalk":
                     tw = time.perf_counter()
                     self._attach_walk_tables(scene)
                     self.build_phases["walk_s"] = time.perf_counter() - tw
@@ -517,7 +516,7 @@ class DeviceScene:
             self.t_tbox = _upload(lists.tbox, device)
         return len(pnodes), len(pleaves)
 
-    def _point_structures_device(self, scene):
+    def _point_structures_device(self, scene, walk: bool = True):
         """The same structures built in HBM (csrc/pbuild.cu):
         mesh arrays uploaded once through page-locked staging, then Morton
         LBVH, exclusive boxes, leaf grid, cell lists and the records in leaf
@@ -548,6 +547,9 @@ class DeviceScene:
                                           CELL_REFINE, CELL_MAX_LIST, sp, C.byref(h)),
                    "tr_pbvh_build_device")
         try:
+            if walk:   # walk tables + predictors on the device
+                _lib.check(L.tr_dpb_walk(h, C.c_void_p(t_verts.data_ptr()), C.c_void_p(t_tets.data_ptr()),
+                                         sp), "tr_dpb_walk")
             sz = np.zeros(6, np.int64)
             _lib.check(L.tr_dpb_sizes(h, _lib.ptr(sz, C.c_int64)), "tr_dpb_sizes")
             n_nodes, n_leaves, n_ids, n_grid, n_cc, n_cr = (int(x) for x in sz)
@@ -564,7 +566,7 @@ class DeviceScene:
             self.t_pids = u8(n_ids * 4)
             self.t_grid = u8(n_grid * 4)
             self.t_grid_leaf = u8(n_grid * _lib.PLEAF_DTYPE.itemsize)
-            self.t_grid_pred = None          # no walk tables -> no walk-start predictor
+            self.t_grid_pred = u8(n_grid * 48) if walk else None   # TrLeafPred per cell
             lists = None
             if n_cc:
                 lists = CellLists(cdim, corg, cscale, None, None, None)
@@ -574,6 +576,7 @@ class DeviceScene:
             dp = lambda t: C.c_void_p(t.data_ptr())
             _lib.check(L.tr_dpb_copy(h, dp(self.t_pnodes), dp(self.t_pleaves), dp(self.t_pids),
                                      dp(self.t_grid), dp(self.t_grid_leaf),
+                                     dp(self.t_grid_pred) if walk else None,
                                      dp(self.t_coff) if lists else None,
                                      dp(self.t_crecs) if lists else None,
                                      dp(self.t_tbox) if lists else None, sp), "tr_dpb_copy")

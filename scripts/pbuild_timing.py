@@ -36,7 +36,7 @@ for recipe in sys.argv[1:]:
     sc = C.build_scene(B, recipe)
     scene_s = time.perf_counter() - t0
     res = {}
-    for build in ("device", "device-walk", "host"):
+    for build in ("device", "device-nowalk", "device-hostwalk", "host"):
         getattr(sc, _CACHE_ATTR, {}).clear()
         gc.collect()
         torch.cuda.empty_cache()
@@ -60,7 +60,7 @@ for recipe in sys.argv[1:]:
         res[build] = row
         print(json.dumps(row), flush=True)
     for mode in ("skip-adaptive", "reference"):
-        for b in ("device", "device-walk"):
+        for b in ("device", "device-nowalk", "device-hostwalk"):
             assert res[b][f"{mode}_samples"] == res["host"][f"{mode}_samples"], (recipe, b, mode)
     del sc
     gc.collect()

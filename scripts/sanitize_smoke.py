@@ -1,5 +1,5 @@
 """Small frames through every kernel path, for compute-sanitizer runs:
-the point-location builds (device / device-walk / host), candidate raster / BSP walk / BVH, all modes, jitter, ragged frame, shards,
+the point-location builds (device / device-nowalk / host), candidate raster / BSP walk / BVH, all modes, jitter, ragged frame, shards,
 bricks, direct host framebuffer and staged outputs, chunked frames."""
 import sys
 from pathlib import Path
@@ -44,7 +44,7 @@ for recipe in ("golden_radial4", "conftest48", "inside", "axis", "a6fog", "jitte
 for recipe in ("golden_radial4", "jitter8"):
     cam, par = C.camera(B, recipe), C.params(B, recipe)
     ref = {m: B.render(C.build_scene(B, recipe), cam, m, par)[0].rgba for m in ("reference", "skip-adaptive")}
-    for build in ("device", "host"):
+    for build in ("device-nowalk", "host"):
         sc = C.build_scene(B, recipe)
         sc.point_build = build
         for mode in ("reference", "skip-adaptive"):

@@ -52,7 +52,9 @@ FRAME_CASES = [c for c in C.FRAME_CASES if c[1] not in ("single",)]
 
 @pytest.mark.parametrize("cid,recipe,modes,jitter", FRAME_CASES, ids=[c[0] for c in FRAME_CASES])
 def test_device_built_frames_match_reference(B, golden, cid, recipe, modes, jitter):
-    sc, orc = device_built(B, recipe)
+    """The device build without walk tables (the default, with device walk
+    tables, runs every other GPU test)."""
+    sc, orc = device_built(B, recipe, "device-nowalk")
     if sc.mesh.n_tets <= 8:
         pytest.skip("one-leaf mesh: host build")
     dev = dev_of(sc)
@@ -69,7 +71,7 @@ def test_device_built_frames_match_reference(B, golden, cid, recipe, modes, jitt
 def test_device_built_radial59(B, golden, mode):
     """BASELINE config 2 through the device build: the reference's frame."""
     from test_parity_gpu import _check_radial59
-    sc, orc = device_built(B, "radial59")
+    sc, orc = device_built(B, "radial59", "device-nowalk")
     cam, par = C.camera(B, "radial59"), C.params(B, "radial59")
     g = golden["frames"][f"radial59/{mode}"]
     for flags in (0, 0x80):
@@ -79,10 +81,10 @@ def test_device_built_radial59(B, golden, mode):
 
 @pytest.mark.parametrize("recipe", ["radial16", "radial59"])
 def test_device_walk_frames(B, golden, recipe):
-    """point_build = "device-walk": the device build plus the host's walk
+    """point_build = "device-hostwalk": the device build plus the host's walk
     tables and predictors on its leaves -- the reference's frames, and the
     walk really is used (predictors present)."""
-    sc, orc = device_built(B, recipe, "device-walk")
+    sc, orc = device_built(B, recipe, "device-hostwalk")
     dev = dev_of(sc)
     assert dev.t_grid_pred is not None
     _, leaves, _ = _download(dev)
@@ -100,7 +102,7 @@ def test_device_walk_frames(B, golden, recipe):
 def test_device_built_unstructured(B, recipe):
     """Unstructured meshes: low grid coverage -> the device builds the cell
     candidate lists; every mode bit-identical to the oracle."""
-    sc, orc = device_built(B, recipe)
+    sc, orc = device_built(B, recipe, "device-nowalk")
     dev = dev_of(sc)
     assert dev.cells is not None, "unstructured mesh should get cell lists"
     cam, par = C.camera(B, recipe), C.params(B, recipe)
@@ -141,7 +143,7 @@ def _download(dev):
 @pytest.mark.parametrize("recipe", ["radial16", "jitter16"])
 def test_device_built_structure_invariants(B, recipe):
     from paper_1908_01906_b200 import device as DV
-    sc, _ = device_built(B, recipe)
+    sc, _ = device_built(B, recipe, "device-nowalk")
     dev = dev_of(sc)
     nodes, leaves, ids = _download(dev)
     T = sc.mesh.n_tets
@@ -242,3 +244,35 @@ def test_host_point_build_still_matches(B, golden, recipe):
         ref = orc.render(cam, mode, par)
         fb, st = B.render(sc, cam, mode, par)
         _compare(fb, st, ref, mode)
+
+
+@pytest.mark.parametrize("recipe", ["radial16", "jitter16", "radial59", "jitter32"])
+def test_device_walk_tables_vs_host(B, recipe):
+    """tr_dpb_walk against tr_leaf_walk on the same device-built leaves:
+    identical face neighbours and walk start, and every device certificate
+    is a host (long-double) certificate; on the generator's meshes the two
+    sets are equal.  Predictors agree to f32 rounding."""
+    import ctypes
+    from paper_1908_01906_b200 import _lib
+    sc, _ = device_built(B, recipe, "device")
+    dev = dev_of(sc)
+    _, leaves, ids = _download(dev)
+    host = leaves.copy()
+    pred = np.zeros((len(host), 12), np.float32)
+    verts = np.ascontiguousarray(sc.mesh.vertices, dtype=np.float64)
+    tets = np.ascontiguousarray(sc.mesh.tets, dtype=np.int64)
+    ids = np.ascontiguousarray(ids)
+    _lib.check(_lib.lib().tr_leaf_walk(len(host), _lib.vptr(host), _lib.vptr(ids), _lib.vptr(verts),
+                                       _lib.vptr(tets), _lib.vptr(pred)), "tr_leaf_walk")
+    dw, hw = leaves["walk"].astype(np.uint32), host["walk"].astype(np.uint32)
+    assert np.array_equal(dw[:, 4], hw[:, 4]), "walk start / validity differ"
+    ent = lambda w: np.stack([(w[:, i >> 1] >> (16 * (i & 1))) & 0xffff for i in range(8)], 1)
+    de, he = ent(dw), ent(hw)
+    assert np.array_equal(de & 0xfff, he & 0xfff), "face neighbours differ"
+    dc, hc = (de >> 12) & 1, (he >> 12) & 1
+    assert not np.any(dc & ~hc), "a device certificate the host does not give"
+    n_dev, n_host = int(dc.sum()), int(hc.sum())
+    print(recipe, "certificates device / host:", n_dev, n_host)
+    if recipe.startswith("radial"):
+        assert n_dev == n_host
+    assert n_dev >= 0.9 * n_host
