@@ -528,7 +528,8 @@ int tr_grid_scene_build(int64_t n, int32_t field, double pad, const double *inv1
  * leaves of <= leaf_max tets, bottom-up refit, exclusive boxes, the leaf grid
  * and -- when the grid's coverage is below cells_below -- the cell candidate
  * lists.  vertices (V,3) f64 and tets (T,4) i64 are DEVICE pointers; leaves
- * carry no walk tables.  The handle owns device buffers until tr_dpb_free. */
+ * carry no walk tables until tr_dpb_walk.  The handle owns device buffers
+ * until tr_dpb_free. */
 typedef struct TrDevPointBuild TrDevPointBuild;
 int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_tets,
                          const int64_t *tets, double pad, int32_t leaf_max, double cells_below,

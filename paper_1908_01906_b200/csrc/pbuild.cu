@@ -30,8 +30,10 @@
 //   8. when coverage is low (unstructured meshes), the cell candidate lists
 //      (host tr_cells_build): counts, prefix sum, fill, per-cell sort by tet id,
 //      overflow bit, f32 record boxes.
-// Walk tables (tr_leaf_walk's long-double certificates) are not built here:
-// leaves carry walk = 0, which the march reads as "scan the leaf in id order".
+//   9. (tr_dpb_walk, below) the leaf walk tables: neighbours, start,
+//      predictors and certificates proved with orientation-determinant error
+//      bounds.  Without it leaves carry walk = 0, which the march reads as
+//      "scan the leaf in id order".
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
