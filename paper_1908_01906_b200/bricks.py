@@ -299,6 +299,7 @@ class BrickRenderer:
             L = _lib.lib()
             s = C.c_void_p(stream.cuda_stream)
             ev = []   # profile: (round, brick, start event, end event)
+            queued = []   # profile: (round, brick, rays that brick marched: its PEER pushes)
             def mark():
                 e = torch.cuda.Event(enable_timing=True)
                 e.record(stream)
@@ -320,6 +321,7 @@ class BrickRenderer:
                                    "tr_brick_round")
                         if profile:
                             ev.append((rounds, b, e0, mark()))
+                            queued.append((rounds, b, int(self.counters[0].item())))
                     rounds += 1
                     exchange()
             while True:
@@ -337,6 +339,7 @@ class BrickRenderer:
                                "tr_brick_round")
                     if profile:
                         ev.append((rounds, b, e0, mark()))
+                        queued.append((rounds, b, int(self.counters[0].item())))
                     if active is None:
                         ctr = self.counters.cpu().numpy()
                         if ctr[2] & 1:
@@ -362,7 +365,8 @@ class BrickRenderer:
             self.profile = {"frame_ms": float(dev_ms),
                             "trace_ms": float(fb.start.elapsed_time(ev[0][3])),
                             "runs": [(r, b, float(e0.elapsed_time(e1))) for r, b, e0, e1 in ev
-                                     if e0 is not None]}
+                                     if e0 is not None],
+                            "queued": queued}
         fbuf = Framebuffer(width=w, height=h, rgba=rgba, samples=samples,
                            background=np.asarray(sc.background, dtype=np.float64).copy())
         stats = RenderStats(
