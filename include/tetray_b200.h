@@ -455,12 +455,14 @@ int tr_render_sync(const TrDeviceScene *scene, const TrEpoch *epoch, const TrFra
  * rounds the ranks exchange states.  Two exchanges: (a) SUM -- each active
  * ray was advanced by exactly one rank, so an int64 SUM all-reduce of the
  * states (zero elsewhere, zero_foreign = 1) is exact; (b) PEER (n_peers > 0)
- * -- the march stores each state it finishes straight into every peer's
- * inbox over NVLink (peer_inbox: CUDA IPC mappings), tagged with the round;
- * the next round's plan takes the inbox entries of the previous round (an
- * inbox per round parity, so a round's stores never meet a reader of the
- * round before).  Only the rays a rank advanced cross the link, and the
- * ranks need no more than a barrier between rounds (no SUM, no host read).
+ * -- when a run suspends, the march stores the ray's state straight into the
+ * inbox of the one rank that owns its next run, over NVLink (peer_inbox: CUDA
+ * IPC mappings), tagged with the round; after round 0 a rank plans only the
+ * rays its inbox received in the previous round (an inbox per round parity,
+ * so a round's stores never meet a reader of the round before).  Each
+ * suspended ray crosses the link once, finished rays not at all, and the
+ * ranks need no more than a barrier between rounds (no SUM, no host read;
+ * counters[1] is then the rank's own active rays).
  * The frame must fit one ray chunk (tr_scratch_bytes(W*H)). */
 typedef struct TrRayState {   /* 64 B per ray */
     double acc[4];

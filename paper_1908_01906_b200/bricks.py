@@ -345,6 +345,10 @@ class BrickRenderer:
                         if ctr[2] & 1:
                             raise RuntimeError("a ray needs more intervals than the stored list")
                         active = int(ctr[1])
+                        if peer is not None and rounds > 0:   # each rank planned only its own rays
+                            t = self.counters[1:2].clone()
+                            self.dist.all_reduce(t)
+                            active = int(t.item())
                         if active == 0:
                             break
                 if active == 0:

@@ -2304,7 +2304,6 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                     TrRayState st = {};
                     st.flags = 2u;
                     F.B_state[s_rr[g]] = st;
-                    if (F.B_npeers) push_state(F, s_rr[g], st);
                 }
             } else if (BRICK && suspend) {
                 TrRayState st = {};
@@ -2314,7 +2313,7 @@ march_sm_kernel(SceneK S, EpochK E, FrameK F, IvBuf iv, TrOutputs O) {
                 st.taken = s_taken[g]; st.icur = s_icur[g]; st.cbefore = s_cbefore[g];
                 st.flags = 1u;
                 F.B_state[s_rr[g]] = st;
-                if (F.B_npeers) push_state(F, s_rr[g], st);
+                if (F.B_npeers) push_state(F, iv, s_rr[g], st);
             }
         }
         if (done || suspend) active = false;
@@ -2499,17 +2498,27 @@ constexpr int64_t IV_FIXED_BYTES = 1024;
 
 // ---- brick-sharded frames (tr_brick_*)
 
-// PEER exchange: the state a run leaves goes into every other rank's inbox
-// of this round's parity (NVLink stores through CUDA IPC mappings), tagged so
-// that the next round's plan takes exactly this round's entries.
-__device__ __noinline__ void push_state(const FrameK &F, int64_t rr, TrRayState st) {
+// PEER exchange: a suspended ray's state goes to the inbox of the ONE rank
+// that owns its next run (the brick of the interval holding sample `taken`,
+// found as the plan finds it), in this round's parity slot, tagged so that
+// the next round's plan takes exactly this round's entries.  Finished rays
+// are not sent: their pixel is written here and no other rank plans a ray
+// it was not sent.
+__device__ __forceinline__ int brick_of(const FrameK &F, int32_t pid);
+__device__ __noinline__ void push_state(const FrameK &F, const IvBuf &iv, int64_t rr, TrRayState st) {
     st.tag = F.B_tag + 1u;
     const int par = (int)(F.B_tag & 1u);
-    for (int r = 0; r < F.B_n; ++r) {
-        if (r == F.B_rank) continue;
-        TrRayState *dst = F.B_peer_inbox[2 * r + par];
-        if (dst) dst[rr] = st;   // already rank r's parity-par inbox
+    const uint32_t n_iv = iv.cnt[rr] & 0xffffu;
+    const IvRec *rec = iv.rec + rr * IV_CAP;
+    int32_t i = st.icur;
+    int nb = F.B_rank;   // no further interval (not expected): keep it here
+    while (i < (int32_t)n_iv) {
+        const IvRec r = load_rec(rec + i);
+        if (r.cum > st.taken) { nb = brick_of(F, r.pid); break; }
+        ++i;
     }
+    TrRayState *dst = nb == F.B_rank ? F.B_inbox + (int64_t)par * F.n_rays : F.B_peer_inbox[2 * nb + par];
+    if (dst) dst[rr] = st;
     __threadfence_system();
 }
 
@@ -2530,11 +2539,14 @@ __global__ void __launch_bounds__(256) brick_plan_kernel(FrameK F, IvBuf iv) {
         TrRayState st = {};
         if (rr < F.n_rays) {
             st = F.B_state[rr];
-            if (F.B_npeers) {   // a peer advanced this ray last round: its state is in my inbox
+            if (F.B_npeers && (F.B_tag & 255u) != 0u) {
+                // after round 0 a rank plans only the rays sent to it last round
                 const TrRayState in = F.B_inbox[(int64_t)((F.B_tag - 1u) & 1u) * F.n_rays + rr];
                 if (in.tag == F.B_tag) {
                     st = in;
                     F.B_state[rr] = in;
+                } else {
+                    st.flags = 0u;
                 }
             }
             act = st.flags == 1u;

@@ -4,8 +4,9 @@ one after another), rounds, per-brick resident bytes, and the n-GPU critical
 path estimate = trace + sum over rounds of the slowest brick's run (plus the
 state exchange: rays x 64 B int64 all-reduce per round, not timed here), and
 the PEER-exchange estimate: per round the slowest brick's run plus its pushes
-(rays it marched x 64 B x (n - 1) at NVLINK_GBS) plus one barrier (BARRIER_MS)
--- an upper bound, the stores overlap the march.
+(rays it marched x 64 B, each to the one rank of the ray's next run, at
+NVLINK_GBS) plus one barrier (BARRIER_MS) -- an upper bound, the stores
+overlap the march.
 Usage: python scripts/brick_bench.py [scene ...] -> JSON lines."""
 import json, sys, time
 from pathlib import Path
@@ -45,7 +46,7 @@ for name in (sys.argv[1:] or ["radial59"]):
                 per_round.setdefault(r, []).append(ms)
             crit = prof["trace_ms"] + sum(max(v) for v in per_round.values())
             runs = {(r, b): ms for r, b, ms in prof["runs"]}
-            push = {(r, b): q * 64 * (n - 1) for r, b, q in prof["queued"]}
+            push = {(r, b): q * 64 for r, b, q in prof["queued"]}
             rounds_peer = {}
             for (r, b), ms in runs.items():
                 t = ms + push.get((r, b), 0) / (NVLINK_GBS * 1e6)
