@@ -16,9 +16,12 @@ A frame (csrc/render.cu, tr_brick_trace / tr_brick_round):
    from the ray state the previous run left (acc rgba, samples taken,
    position in the interval list).  A run ends at the brick's last interval or
    at early termination (K:285-295, K:388-389), where the pixel is written;
-3. between rounds the ranks exchange the states.  Each active ray was advanced
-   by exactly one rank, so an int64 SUM all-reduce of the state array with
-   every other entry zeroed reproduces it bit for bit.
+3. between rounds the ranks exchange the states: either (SUM) each active
+   ray was advanced by exactly one rank, so an int64 SUM all-reduce of the
+   state array with every other entry zeroed reproduces it bit for bit, or
+   (PEER, one node) the march stores a suspended ray's state straight into
+   the inbox of the rank owning its next run (CUDA IPC over NVLink) and the
+   ranks only meet at a barrier.
 
 Compositing order, sample positions (entry + (k + phase) * step with the
 ray's own k), per-partition counts and `visited` are the one-GPU frame's, so
@@ -147,10 +150,11 @@ class BrickRenderer:
         round then confirms it -- and keeps going if ever needed).
 
         exchange (with `dist`): "sum" -- an int64 SUM all-reduce of the whole
-        state array per round; "peer" -- the march stores each state it
-        finishes into the other ranks' inboxes through CUDA IPC mappings
-        (NVLink on one node), so only the rays a rank advanced move and a
-        round needs just a barrier (the ranks must share a node)."""
+        state array per round; "peer" -- when a run suspends, the march
+        stores the ray's state into the inbox of the one rank owning its next
+        run through CUDA IPC mappings (NVLink on one node), so each suspended
+        ray moves once and a round needs just a barrier (the ranks must share
+        a node)."""
         import torch
         if exchange not in ("sum", "peer"):
             raise ValueError(f"exchange must be 'sum' or 'peer', not {exchange!r}")
