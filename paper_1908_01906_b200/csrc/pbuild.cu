@@ -700,7 +700,8 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
     TrDevPointBuild *B = new TrDevPointBuild();
     B->st = st;
     B->n_tets = T;
-    cudaError_t e = cudaSuccess;
+    cudaError_t e = cudaSuccess, ce = cudaSuccess;   // ce: first CUB error
+    auto ck = [&ce](cudaError_t x) { if (x != cudaSuccess && ce == cudaSuccess) ce = x; };
     int rc = TR_OK;
     {
         Scratch S{st};
@@ -723,21 +724,22 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
         morton_kernel<<<grid_for(T), 256, 0, st>>>(T, box, bnd, code, id);
         // radix sort (code, id): stable, ids ascending within equal codes
         size_t tmp_bytes = 0, tb2 = 0;
-        cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, id, B->ids, (int)T, 0,
-                                        3 * MORTON_BITS, st);
-        cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, cidx, (int)T, st);
+        ck(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, code, code2, id, B->ids, (int)T, 0,
+                                        3 * MORTON_BITS, st));
+        ck(cub::DeviceScan::ExclusiveSum(nullptr, tb2, flag, cidx, (int)T, st));
         if (tb2 > tmp_bytes) tmp_bytes = tb2;
         void *tmp = S.get<uint8_t>(tmp_bytes + 1024);
         if ((e = S.err) != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: allocation"); }
         size_t tsz = tmp_bytes;
-        cub::DeviceRadixSort::SortPairs(tmp, tsz, code, code2, id, B->ids, (int)T, 0, 3 * MORTON_BITS, st);
+        ck(cub::DeviceRadixSort::SortPairs(tmp, tsz, code, code2, id, B->ids, (int)T, 0, 3 * MORTON_BITS, st));
         heads_kernel<<<grid_for(T), 256, 0, st>>>(T, code2, flag);
         tsz = tmp_bytes;
-        cub::DeviceScan::ExclusiveSum(tmp, tsz, flag, cidx, (int)T, st);
+        ck(cub::DeviceScan::ExclusiveSum(tmp, tsz, flag, cidx, (int)T, st));
         uint32_t last_c = 0, last_f = 0;
         cudaMemcpyAsync(&last_c, cidx + T - 1, 4, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(&last_f, flag + T - 1, 4, cudaMemcpyDeviceToHost, st);
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: sort"); }
+        if ((e = cudaStreamSynchronize(st)) == cudaSuccess) e = ce;
+        if (e != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: sort"); }
         const int64_t n_u = (int64_t)last_c + last_f;
         if (n_u < 2) { free_build(B); return tr_fail(TR_EINVAL, "tr_pbvh_build_device: every tet box has the same centre"); }
         uint32_t *cstart = S.get<uint32_t>(n_u + 1);
@@ -754,16 +756,17 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
         Tree Tr{first, last, left, right, cstart, leaf_max};
         keep_kernel<<<grid_for(n_int), 256, 0, st>>>(n_int, Tr, keep, lhead, err);
         tsz = tmp_bytes;
-        cub::DeviceScan::ExclusiveSum(tmp, tsz, keep, nidx, (int)n_int, st);
+        ck(cub::DeviceScan::ExclusiveSum(tmp, tsz, keep, nidx, (int)n_int, st));
         tsz = tmp_bytes;
-        cub::DeviceScan::ExclusiveSum(tmp, tsz, lhead, lidx, (int)n_u, st);
+        ck(cub::DeviceScan::ExclusiveSum(tmp, tsz, lhead, lidx, (int)n_u, st));
         uint32_t h4[5] = {0, 0, 0, 0, 0};
         cudaMemcpyAsync(h4 + 0, nidx + n_int - 1, 4, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(h4 + 1, keep + n_int - 1, 4, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(h4 + 2, lidx + n_u - 1, 4, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(h4 + 3, lhead + n_u - 1, 4, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(h4 + 4, err, 4, cudaMemcpyDeviceToHost, st);
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: tree"); }
+        if ((e = cudaStreamSynchronize(st)) == cudaSuccess) e = ce;
+        if (e != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: tree"); }
         if (h4[4]) { free_build(B); return tr_fail(TR_EINVAL, "tr_pbvh_build_device: more than 64 tets share a Morton cell"); }
         B->n_nodes = (int64_t)h4[0] + h4[1];
         B->n_leaves = (int64_t)h4[2] + h4[3];
@@ -831,7 +834,7 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
             uint32_t *cnt = S.get<uint32_t>(nc), *fill = S.get<uint32_t>(nc);
             uint64_t *eff = S.get<uint64_t>(nc + 1), *off = S.get<uint64_t>(nc + 1);
             size_t tb3 = 0;
-            cub::DeviceScan::ExclusiveSum(nullptr, tb3, eff, off, (int)(nc + 1), st);
+            ck(cub::DeviceScan::ExclusiveSum(nullptr, tb3, eff, off, (int)(nc + 1), st));
             void *tmp3 = S.get<uint8_t>(tb3 + 16);
             if ((e = S.err) == cudaSuccess) e = cudaMallocAsync(&B->coff, (nc + 1) * sizeof(uint32_t), st);
             if (e == cudaSuccess) e = cudaMallocAsync(&B->tbox, T * 8 * sizeof(float), st);
@@ -841,10 +844,11 @@ int tr_pbvh_build_device(int64_t n_vertices, const double *vertices, int64_t n_t
             cudaMemsetAsync(eff + nc, 0, sizeof(uint64_t), st);
             cells_count_kernel<<<grid_for(T), 256, 0, st>>>(T, B->ids, box, Cp, cnt);
             cells_eff_kernel<<<grid_for(nc), 256, 0, st>>>(nc, cnt, (uint32_t)max_list, eff);
-            cub::DeviceScan::ExclusiveSum(tmp3, tb3, eff, off, (int)(nc + 1), st);
+            ck(cub::DeviceScan::ExclusiveSum(tmp3, tb3, eff, off, (int)(nc + 1), st));
             uint64_t total = 0;
             cudaMemcpyAsync(&total, off + nc, 8, cudaMemcpyDeviceToHost, st);
-            if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: cells"); }
+            if ((e = cudaStreamSynchronize(st)) == cudaSuccess) e = ce;
+            if (e != cudaSuccess) { free_build(B); return cuda_fail(e, "tr_pbvh_build_device: cells"); }
             if (total >= 0x7fffffffull) { free_build(B); return tr_fail(TR_ENOMEM, "tr_pbvh_build_device: cell lists too large"); }
             B->n_crecs = (int64_t)total;
             e = cudaMallocAsync(&B->crecs, std::max<uint64_t>(total, 1) * sizeof(uint32_t), st);
