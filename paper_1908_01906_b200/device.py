@@ -546,6 +546,7 @@ class DeviceScene:
                                           C.c_void_p(t_tets.data_ptr()), pad, _LEAF_MAX, below,
                                           CELL_REFINE, CELL_MAX_LIST, sp, C.byref(h)),
                    "tr_pbvh_build_device")
+        t_call = time.perf_counter() - tb
         try:
             if walk:   # walk tables + predictors on the device
                 _lib.check(L.tr_dpb_walk(h, C.c_void_p(t_verts.data_ptr()), C.c_void_p(t_tets.data_ptr()),
@@ -581,7 +582,9 @@ class DeviceScene:
                                      dp(self.t_crecs) if lists else None,
                                      dp(self.t_tbox) if lists else None, sp), "tr_dpb_copy")
         finally:
+            tf = time.perf_counter()
             L.tr_dpb_free(h)
+            t_free = time.perf_counter() - tf
         t_build = time.perf_counter() - tb
         del t_verts
         # records in leaf order, packed on the device
@@ -595,7 +598,8 @@ class DeviceScene:
                                          int(mesh.centering), dp(self.t_pids), dp(self.t_tets), sp),
                    "tr_pack_tets_device")
         stream.synchronize()
-        self.build_phases = {"upload_s": t_up, "lbvh_s": t_build,
+        self.build_phases = {"upload_s": t_up, "lbvh_s": t_build, "lbvh_call_s": t_call,
+                             "lbvh_free_s": t_free,
                              "pack_s": time.perf_counter() - t1 - (t_up - t_up0)}
         del t_tets, t_orig, t_inv, t_field
         self.pnodes_host = self.pleaves_host = None
