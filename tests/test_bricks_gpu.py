@@ -102,9 +102,9 @@ def _dist_worker(rank, world, port, q, exchange="sum"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("exchange", ["sum", "peer"])
-def test_bricks_dist_gpu(B, exchange):
-    """Two ranks (processes sharing the GPU) each hold one brick; both
+@pytest.mark.parametrize("exchange,world", [("sum", 2), ("peer", 2), ("peer", 3)])
+def test_bricks_dist_gpu(B, exchange, world):
+    """Two or three ranks (processes sharing the GPU) each hold one brick; all
     assemble the one-device frame.  sum: gloo all-reduces of the CUDA state
     array; peer: the march stores finished states into the other rank's
     inbox through a CUDA IPC mapping (the NVLink path), gloo barriers."""
@@ -115,7 +115,7 @@ def test_bricks_dist_gpu(B, exchange):
         port = s.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_dist_worker, args=(r, 2, port, q, exchange)) for r in range(2)]
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, q, exchange)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=600) for _ in procs)
@@ -126,7 +126,7 @@ def test_bricks_dist_gpu(B, exchange):
     cam, par = cases.camera(B, "radial16", scale=0.25), cases.params(B, "radial16")
     for mode in ("reference", "skip-adaptive"):
         fb, st = B.render(sc, cam, mode, par)
-        for r in (0, 1):
+        for r in range(world):
             rgba, samples, tot, vis, ppart, rounds = res[r][mode]
             assert np.array_equal(rgba, fb.rgba)
             assert np.array_equal(samples, fb.samples)
