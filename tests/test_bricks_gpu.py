@@ -106,8 +106,9 @@ def _dist_worker(rank, world, port, q, exchange="sum"):
 def test_bricks_dist_gpu(B, exchange, world):
     """Two or three ranks (processes sharing the GPU) each hold one brick; all
     assemble the one-device frame.  sum: gloo all-reduces of the CUDA state
-    array; peer: the march stores finished states into the other rank's
-    inbox through a CUDA IPC mapping (the NVLink path), gloo barriers."""
+    array; peer: the march stores each suspended ray's state into the inbox
+    of the rank owning its next run through a CUDA IPC mapping (the NVLink
+    path), gloo barriers; two frames reuse the inboxes."""
     import socket
     import torch.multiprocessing as mp
     with socket.socket() as s:
